@@ -1,0 +1,911 @@
+/* TEST INFRASTRUCTURE ONLY -- the CPU oracle.
+ *
+ * A plain-C restatement of the batched elementwise math path, used solely by
+ * tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+ * reference leg, as the checker.  The product (libvem.so, CUDA sm_100a) never
+ * links or calls anything here, and there is no CPU fallback in the product.
+ *
+ * Every function follows the same operation order as the CUDA kernel of the
+ * same name, so GPU results must be BIT-IDENTICAL to this file (the
+ * "deterministic variant" of the north star).  Independently of that, each
+ * function is checked against MPFR 4.2.1 for its ULP bound (tests/), and:
+ *   - the reduction (cw1 / cw2 / ph / trig_reduce) is checked bit-for-bit
+ *     against the reference's own code compiled from /root/reference
+ *     (oracle/_ref, see ref_build.py): reduction.hpp:147-212, ddarith.hpp;
+ *   - fmod is checked bit-for-bit against glibc fmod/fmodf (exact);
+ *   - the Payne-Hanek table digests are pinned (tests/golden).
+ *
+ * Build: gcc -O2 -ffp-contract=off -mfma -fopenmp (oracle/Makefile).
+ * Contraction MUST stay off: every fused op below is an explicit fma().
+ *
+ * Citations: backend.hpp / ddarith.hpp / reduction.hpp / constants.hpp are
+ * /root/reference/proj/core/include/vem/; SPEC.md / PAPER.md at the root of
+ * /root/reference.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stddef.h>
+#include <string.h>
+
+#include "vem_coeffs.h"
+#include "vem_ph_tables.h"
+
+typedef struct { double hi, lo; } dd_t;
+
+/* ------------------------------------------------------------------ bits */
+static inline uint64_t bits_d(double x) { uint64_t u; memcpy(&u, &x, 8); return u; }
+static inline double from_bits_d(uint64_t u) { double x; memcpy(&x, &u, 8); return x; }
+static inline uint32_t bits_f(float x) { uint32_t u; memcpy(&u, &x, 4); return u; }
+static inline float from_bits_f(uint32_t u) { float x; memcpy(&x, &u, 4); return x; }
+
+#define CANON_NAN_D 0x7ff8000000000000ull
+#define CANON_NAN_F 0x7fc00000u
+static inline double canon_d(double y) { return (y != y) ? from_bits_d(CANON_NAN_D) : y; }
+static inline float canon_f(float y) { return (y != y) ? from_bits_f(CANON_NAN_F) : y; }
+
+/* constants.hpp:14-58 (values reused; they are the reference's frozen limbs) */
+#define K_PIO2_QD0 0x1.921fb54442d18p+0
+#define K_PIO2_QD1 0x1.1a62633145c07p-54
+#define K_PIO2_QD2 -0x1.f1976b7ed8fbcp-110
+#define K_PIO2_QD3 0x1.4cf98e804177dp-164
+#define K_TWO_OVER_PI 0x1.45f306dc9c883p-1
+#define K_CW1_P0 0x1.921fb54442d20p+0
+#define K_CW1_T1 -0x1.ee59d9cceba40p-50
+#define K_CW1_T2 0x1.b839a252049c1p-104
+#define K_CW2_A 0x1.921fb58000000p+0
+#define K_CW2_B -0x1.dde9740000000p-27
+#define K_CW2_C 0x1.1a62630000000p-54
+#define K_CW2_D1 0x1.8a2e03707344ap-81
+#define K_CW2_D2 0x1.024e088a67cc7p-135
+#define K_INV_LN2 0x1.71547652b82fep+0
+#define K_EXP_L1 0x1.62e42fefa3800p-1
+#define K_EXP_L2 0x1.ef35793c76730p-45
+#define K_LN2_HI 0x1.62e42fefa39efp-1
+#define K_LN2_LO 0x1.abc9e3b39803fp-56
+#define K_EXP_OVF 0x1.62e42fefa39efp+9
+#define K_EXP_UNF -0x1.74910d52d3051p+9
+#define K_CW1_MAX 15.0
+#define K_CW2_MAX 1e14
+#define K_FOUR_THIRDS 0x1.5555555555555p+0
+
+static const double PH_D[4 * VEM_PH_D_ENTRIES] = {VEM_PH_D_INIT};
+static const double PH_F[3 * VEM_PH_F_ENTRIES] = {VEM_PH_F_INIT};
+
+/* ------------------------------------------- primitives (backend.hpp) */
+/* backend.hpp:47-52 round_ta: nearest integer, ties away from zero */
+static inline double round_ta(double x) {
+  double t = trunc(x);
+  double f = x - t;
+  double up = t + (x < 0 ? -1.0 : 1.0);
+  return (f >= 0.5 || f <= -0.5) ? up : t;
+}
+/* backend.hpp:133-138 ldexp2 (two half-step power-of-two multiplies) */
+static inline double pow2_bits(int64_t e) { return from_bits_d((uint64_t)(e + 1023) << 52); }
+static inline double ldexp2(double x, int64_t e) {
+  e = e > 2046 ? 2046 : (e < -2044 ? -2044 : e);
+  int64_t h = e >> 1;
+  return (x * pow2_bits(h)) * pow2_bits(e - h);
+}
+/* backend.hpp:381-384 mulsign */
+static inline double mulsign(double x, double s) {
+  return from_bits_d(bits_d(x) ^ (bits_d(s) & 0x8000000000000000ull));
+}
+static inline double copysign_b(double m, double s) {
+  return from_bits_d((bits_d(m) & 0x7fffffffffffffffull) | (bits_d(s) & 0x8000000000000000ull));
+}
+static inline double neg_if(double y, int c) {
+  return from_bits_d(bits_d(y) ^ ((uint64_t)(c != 0) << 63));
+}
+/* backend.hpp:418-423 toward_zero for positive finite x */
+static inline double toward0_pos(double x) { return from_bits_d(bits_d(x) - 1); }
+
+/* ------------------------------------------------- DD (ddarith.hpp) */
+static inline dd_t two_sum(double a, double b) { /* ddarith.hpp:29-35 */
+  double s = a + b, v = s - a;
+  dd_t r = {s, (a - (s - v)) + (b - v)};
+  return r;
+}
+static inline dd_t two_sum_fast(double a, double b) { /* ddarith.hpp:39-44 */
+  double s = a + b;
+  dd_t r = {s, b - (s - a)};
+  return r;
+}
+static inline dd_t two_prod(double a, double b) { /* ddarith.hpp:51-56 (FMA) */
+  double p = a * b;
+  dd_t r = {p, fma(a, b, -p)};
+  return r;
+}
+static inline dd_t dd_add2(dd_t x, dd_t y) { /* ddarith.hpp:111-117 */
+  double s = x.hi + y.hi, v = s - x.hi;
+  double e = (x.hi - (s - v)) + (y.hi - v);
+  dd_t r = {s, e + (x.lo + y.lo)};
+  return r;
+}
+static inline dd_t dd_add2_d(dd_t x, double y) { /* ddarith.hpp:120-126 */
+  double s = x.hi + y, v = s - x.hi;
+  double e = (x.hi - (s - v)) + (y - v);
+  dd_t r = {s, e + x.lo};
+  return r;
+}
+static inline dd_t dd_mul(dd_t x, dd_t y) { /* ddarith.hpp:163-170 (FMA) */
+  double p = x.hi * y.hi;
+  double e = fma(x.hi, y.hi, -p);
+  e = fma(x.hi, y.lo, e);
+  e = fma(x.lo, y.hi, e);
+  dd_t r = {p, e};
+  return r;
+}
+static inline dd_t dd_mul_d(dd_t x, double y) { /* ddarith.hpp:178-184 (FMA) */
+  double p = x.hi * y;
+  double e = fma(x.hi, y, -p);
+  e = fma(x.lo, y, e);
+  dd_t r = {p, e};
+  return r;
+}
+static inline dd_t dd_squ(dd_t x) { /* ddarith.hpp:197-203 (FMA) */
+  double p = x.hi * x.hi;
+  double e = fma(x.hi, x.hi, -p);
+  e = fma(x.hi + x.hi, x.lo, e);
+  dd_t r = {p, e};
+  return r;
+}
+static inline dd_t dd_div(dd_t x, dd_t y) { /* ddarith.hpp:220-228 (FMA) */
+  double t = 1.0 / y.hi;
+  double q = x.hi * t;
+  double u = fma(t, x.hi, -q);
+  double v = fma(y.lo, -t, fma(y.hi, -t, 1.0));
+  dd_t r = {q, fma(q, v, fma(x.lo, t, u))};
+  return r;
+}
+static inline dd_t dd_normalize(dd_t x) { return two_sum_fast(x.hi, x.lo); } /* ddarith.hpp:103 */
+
+/* Estrin evaluation with fixed bracketing; the CUDA
+ * kernels (vem_math.cuh: vem_estrin) apply the identical pairing. */
+static inline double estrin(const double* c, int n, double x) {
+  double t[24];
+  for (int i = 0; i < n; i++) t[i] = c[i];
+  double p = x;
+  while (n > 1) {
+    int m = 0;
+    for (int i = 0; i + 1 < n; i += 2) t[m++] = fma(t[i + 1], p, t[i]);
+    if (n & 1) t[m++] = t[n - 1];
+    n = m;
+    if (n > 1) p = p * p;
+  }
+  return t[0];
+}
+
+/* ============================================ trig reduction (f64) */
+typedef struct { double hi, lo; int q; } red_t;
+
+/* reduction.hpp:148-159 -- Cody-Waite level 1, |x| <= 15 */
+static red_t cw1(double x) {
+  double qd = round_ta(x * K_TWO_OVER_PI);
+  double r0 = fma(qd, -K_CW1_P0, x);
+  dd_t tail = two_prod(qd, -K_CW1_T1);
+  tail.lo = fma(qd, -K_CW1_T2, tail.lo);
+  dd_t r0d = {r0, 0.0};
+  dd_t r = dd_normalize(dd_add2(r0d, tail));
+  red_t o = {r.hi, r.lo, (int)((int64_t)qd & 3)};
+  return o;
+}
+
+/* reduction.hpp:163-178 -- Cody-Waite level 2, |x| <= 1e14 */
+static red_t cw2(double x) {
+  double t = x * K_TWO_OVER_PI;
+  double qh = trunc(t * 0x1p-24);
+  qh = qh * 0x1p24;
+  double ql = round_ta(t - qh);
+  double r = x;
+  r = fma(qh, -K_CW2_A, r);
+  r = fma(ql, -K_CW2_A, r);
+  r = fma(qh, -K_CW2_B, r);
+  r = fma(ql, -K_CW2_B, r);
+  dd_t rd = {r, 0.0};
+  dd_t acc = dd_add2(rd, two_prod(qh, -K_CW2_C));
+  acc = dd_add2(acc, two_prod(ql, -K_CW2_C));
+  double qs = qh + ql;
+  dd_t dtail = two_prod(qs, -K_CW2_D1);
+  dtail.lo = fma(qs, -K_CW2_D2, dtail.lo);
+  acc = dd_add2(acc, dtail);
+  acc = dd_normalize(acc);
+  red_t o = {acc.hi, acc.lo, (int)((int64_t)ql & 3)};
+  return o;
+}
+
+/* reduction.hpp:35-43 rfrac with quadrant accumulation */
+static inline dd_t rfrac_q(dd_t a, int64_t* q) {
+  double rh = round_ta(a.hi);
+  a.hi = a.hi - rh;
+  *q += (int64_t)rh;
+  double rl = round_ta(a.lo);
+  a.lo = a.lo - rl;
+  *q += (int64_t)rl;
+  return a;
+}
+
+/* reduction.hpp:89-137 Payne-Hanek, REPAIRED:
+ * mod-4 table (tools/genphtable.py) + two_sum renormalisation after each
+ * rfrac.  Non-finite x are computed on a sanitised 0 and replaced by NaN at
+ * the end (the reference's `bad` select, reduction.hpp:131-135). */
+static red_t ph(double x_in) {
+  int bad = !(fabs(x_in) <= 1.7976931348623157e308);
+  double x = bad ? 0.0 : x_in;
+  double a = fabs(x);
+  int64_t er = (int64_t)((bits_d(a) >> 52) & 0x7ff);
+  int64_t idx = er - 1023;
+  idx = (0 > idx) ? 0 : idx;
+  idx = (idx > 1023) ? 1023 : idx;
+  double m = ldexp2(a, 52 - idx);
+  const double* f = PH_D + (idx << 2);
+  int64_t q = 0;
+  dd_t u = two_prod(m, f[0]);
+  u = rfrac_q(u, &q);
+  u = two_sum(u.hi, u.lo);
+  u = dd_add2(u, two_prod(m, f[1]));
+  u = rfrac_q(u, &q);
+  u = two_sum(u.hi, u.lo);
+  u = dd_add2(u, two_prod(m, f[2]));
+  u = rfrac_q(u, &q);
+  u = two_sum(u.hi, u.lo);
+  u = dd_add2(u, two_prod(m, f[3]));
+  double qv = round_ta(u.hi + u.lo);
+  u.hi = u.hi - qv;
+  q += (int64_t)qv;
+  double ql = round_ta(u.lo);
+  u.lo = u.lo - ql;
+  q += (int64_t)ql;
+  u = dd_normalize(u);
+  /* reduction.hpp:57-69 mul_pio2_qd */
+  double p = u.hi * K_PIO2_QD0;
+  double e = fma(u.hi, K_PIO2_QD0, -p);
+  e = fma(u.hi, K_PIO2_QD1, e);
+  e = fma(u.lo, K_PIO2_QD0, e);
+  e = fma(u.hi, K_PIO2_QD2, e);
+  e = fma(u.lo, K_PIO2_QD1, e);
+  e = fma(u.hi, K_PIO2_QD3, e);
+  e = fma(u.lo, K_PIO2_QD2, e);
+  double rh = mulsign(p, x), rl = mulsign(e, x);
+  if (x < 0.0) q = 0 - q;
+  red_t o;
+  if (bad) {
+    o.hi = from_bits_d(CANON_NAN_D);
+    o.lo = from_bits_d(CANON_NAN_D);
+    o.q = 0;
+  } else {
+    o.hi = rh;
+    o.lo = rl;
+    o.q = (int)(q & 3);
+  }
+  return o;
+}
+
+/* reduction.hpp:189-206, deterministic policy, per lane */
+static red_t trig_reduce(double x) {
+  double ax = fabs(x);
+  if (ax <= K_CW1_MAX) return cw1(x);
+  if (ax <= K_CW2_MAX) return cw2(x);
+  return ph(x);
+}
+
+/* ======================================================= f64 kernels */
+static const double C_SIN_D[] = VEM_SIN_D_ARR;
+static const double C_COS_D[] = VEM_COS_D_ARR;
+static const double C_TAN_D[] = VEM_TAN_D_ARR;
+static const double C_ATAN_D[] = VEM_ATAN_D_ARR;
+static const double C_EXP_D[] = VEM_EXP_D_ARR;
+static const double C_EXP_D_U35[] = VEM_EXP_D_U35_ARR;
+static const double C_LOG_D[] = VEM_LOG_D_ARR;
+static const double C_POWLOG_D[] = VEM_POWLOG_D_ARR;
+static const double C_POWEXP_D[] = VEM_POWEXP_D_ARR;
+static const double C_POWLOG_D_U35[] = VEM_POWLOG_D_U35_ARR;
+static const double C_POWEXP_D_U35[] = VEM_POWEXP_D_U35_ARR;
+
+/* sin/cos core on the reduced argument r = rh + rl, |r| <= 0.80, using a
+ * per-lane SELECTED polynomial (sin form for even effective quadrant, cos
+ * form for odd) -- branch-free on the GPU (SPEC.md:470 leaves the cos
+ * recipe open).  `cosform` picks the cos polynomial. */
+static double sincos_core_d(double rh, double rl, int cosform) {
+  double c[VEM_SIN_D_N];
+  for (int i = 0; i < VEM_SIN_D_N; i++) c[i] = cosform ? C_COS_D[i] : C_SIN_D[i];
+  double z = rh * rh;
+  double P = estrin(c, VEM_SIN_D_N, z);
+  /* sin form: rh + (rl - rl*z/2 + rh*z*P) */
+  double As = rh, Bs = 0.0, Ms = rh * z, Ts = fma(-0.5 * z, rl, rl);
+  /* cos form: w + (((1-w) - z/2) + (z^2*P - (zl/2 + rh*rl))), w = 1 - z/2 */
+  double zl = fma(rh, rh, -z);
+  double hz = 0.5 * z;
+  double w = 1.0 - hz;
+  double Ac = w, Bc = (1.0 - w) - hz, Mc = z * z, Tc = -fma(0.5, zl, rh * rl);
+  double A = cosform ? Ac : As, B = cosform ? Bc : Bs, M = cosform ? Mc : Ms, T = cosform ? Tc : Ts;
+  return A + (B + fma(M, P, T));
+}
+
+double vo_sin_d_u10(double x) {
+  red_t r = trig_reduce(x);
+  double y = sincos_core_d(r.hi, r.lo, r.q & 1);
+  y = neg_if(y, r.q & 2);
+  y = (x == 0.0) ? x : y;
+  return canon_d(y);
+}
+double vo_cos_d_u10(double x) {
+  red_t r = trig_reduce(x);
+  double y = sincos_core_d(r.hi, r.lo, (r.q & 1) ^ 1);
+  y = neg_if(y, (r.q + 1) & 2);
+  return canon_d(y);
+}
+double vo_sin_d_u10_ph(double x) {
+  red_t r = ph(x);
+  double y = sincos_core_d(r.hi, r.lo, r.q & 1);
+  y = neg_if(y, r.q & 2);
+  y = (x == 0.0) ? x : y;
+  return canon_d(y);
+}
+double vo_cos_d_u10_ph(double x) {
+  red_t r = ph(x);
+  double y = sincos_core_d(r.hi, r.lo, (r.q & 1) ^ 1);
+  y = neg_if(y, (r.q + 1) & 2);
+  return canon_d(y);
+}
+
+/* tan: half-angle: t = tan(r/2), tan r = 2t/(1-t^2),
+ * -cot r = -(1-t^2)/(2t); one DD division for both quadrant parities. */
+static double tan_core_d(double rh, double rl, int odd) {
+  double hh = rh * 0.5, hl = rl * 0.5;
+  double z = hh * hh;
+  double P = estrin(C_TAN_D, VEM_TAN_D_N, z);
+  double corr = fma(hh * z, P, fma(hl, z, hl));
+  dd_t t = two_sum_fast(hh, corr);
+  dd_t t2 = dd_squ(t);
+  dd_t den = two_sum(1.0, -t2.hi);
+  den.lo = den.lo - t2.lo;
+  dd_t num = {t.hi * 2.0, t.lo * 2.0};
+  dd_t X, Y;
+  if (odd) {
+    X.hi = -den.hi; X.lo = -den.lo; Y = num;
+  } else {
+    X = num; Y = den;
+  }
+  dd_t q = dd_div(X, Y);
+  return q.hi + q.lo;
+}
+double vo_tan_d_u10(double x) {
+  red_t r = trig_reduce(x);
+  double y = tan_core_d(r.hi, r.lo, r.q & 1);
+  y = (fabs(x) < 0x1p-27) ? x : y;
+  return canon_d(y);
+}
+double vo_tan_d_u10_ph(double x) {
+  red_t r = ph(x);
+  double y = tan_core_d(r.hi, r.lo, r.q & 1);
+  y = (fabs(x) < 0x1p-27) ? x : y;
+  return canon_d(y);
+}
+
+/* atan (restructured for one division): fold |x| into
+ * |b| <= tan(pi/8) with b = x, (x-1)/(x+1) or -1/x (offsets 0, pi/4, pi/2),
+ * one DD division (ddarith.hpp:220-228) covers all three cases, 12-term odd
+ * polynomial, offset added in DD.  The paper's single 1/x fold with a
+ * 20-term polynomial on [0,1] measured 1.29 ulp with a binary64 assembly;
+ * see DESIGN.md §4. */
+#define K_TAN_PI8 0x1.a827999fcef32p-2
+#define K_TAN_3PI8 0x1.3504f333f9de6p+1
+#define K_PIO4_HI 0x1.921fb54442d18p-1
+#define K_PIO4_LO 0x1.1a62633145c07p-55
+double vo_atan_d_u10(double x) {
+  double a = fabs(x);
+  int c1 = a > K_TAN_PI8;
+  int c2 = a > K_TAN_3PI8;
+  dd_t ns = two_sum(a, -1.0), ds = two_sum(a, 1.0);
+  dd_t nn, dn;
+  nn.hi = c2 ? -1.0 : (c1 ? ns.hi : a);
+  nn.lo = c2 ? 0.0 : (c1 ? ns.lo : 0.0);
+  dn.hi = c2 ? a : (c1 ? ds.hi : 1.0);
+  dn.lo = c2 ? 0.0 : (c1 ? ds.lo : 0.0);
+  dd_t b = dd_div(nn, dn);
+  double z = b.hi * b.hi;
+  double P = estrin(C_ATAN_D, VEM_ATAN_D_N, z);
+  double corr = fma(b.hi * z, P, fma(-b.lo, z, b.lo));
+  double offh = c2 ? K_PIO2_QD0 : (c1 ? K_PIO4_HI : 0.0);
+  double offl = c2 ? K_PIO2_QD1 : (c1 ? K_PIO4_LO : 0.0);
+  dd_t s = two_sum(offh, b.hi);
+  double y = s.hi + (s.lo + (offl + corr));
+  y = (a == INFINITY) ? K_PIO2_QD0 : y;
+  y = copysign_b(y, x);
+  return canon_d(y);
+}
+
+/* exp: k = rint(x/ln2), r = x - k*L1 - k*L2
+ * (constants.hpp:44-46), 13-term polynomial (u10) / 12-term (u35), no DD
+ * (SPEC.md:406), ldexp2 reconstruction, saturation (constants.hpp:53-54). */
+static double exp_core_d(double x, const double* c, int n, int u10) {
+  int ok = (x >= K_EXP_UNF) && (x <= K_EXP_OVF);
+  double xs = ok ? x : 0.0;
+  double kd = rint(xs * K_INV_LN2);
+  double r1 = fma(kd, -K_EXP_L1, xs);
+  double r = fma(kd, -K_EXP_L2, r1);
+  double P = estrin(c, n, r);
+  double y;
+  if (u10) {
+    /* r = rh + rl exactly-ish; exp(r) = (1 + rh) + (rl + rh^2 P) */
+    double rl = fma(-kd, K_EXP_L2, r1 - r);
+    double s = 1.0 + r;
+    double se = (1.0 - s) + r;
+    y = s + (se + fma(r * r, P, rl));
+  } else {
+    y = 1.0 + fma(r * r, P, r);
+  }
+  y = ldexp2(y, (int64_t)kd);
+  y = (x > K_EXP_OVF) ? INFINITY : y;
+  y = (x < K_EXP_UNF) ? 0.0 : y;
+  y = (x != x) ? x : y;
+  return canon_d(y);
+}
+double vo_exp_d_u10(double x) { return exp_core_d(x, C_EXP_D, VEM_EXP_D_N, 1); }
+double vo_exp_d_u35(double x) { return exp_core_d(x, C_EXP_D_U35, VEM_EXP_D_U35_N, 0); }
+
+/* log decomposition: denormals x 2^64, e = ilogb(RN(4a/3)),
+ * m = a*2^-e in [0.75, 1.5). */
+static inline void log_split(double a, double* m, double* E) {
+  int sub = a < 0x1p-1022;
+  double as = sub ? a * 0x1p64 : a;
+  int64_t eb = (int64_t)((bits_d(as * K_FOUR_THIRDS) >> 52) & 0x7ff) - 1023;
+  *m = from_bits_d(bits_d(as) - ((uint64_t)eb << 52));
+  *E = (double)(eb - (sub ? 64 : 0));
+}
+
+static double log_core_d(double x, int u10) {
+  int ok = (x > 0.0) && (x < INFINITY);
+  double a = ok ? x : 1.0;
+  double m, E;
+  log_split(a, &m, &E);
+  double xn = m - 1.0;
+  double dh = m + 1.0;
+  double dl = m - (dh - 1.0);
+  double t = 1.0 / dh;
+  double sh = xn * t;
+  double u = fma(t, xn, -sh);
+  double v = fma(dl, -t, fma(dh, -t, 1.0));
+  double sl = fma(sh, v, u);
+  double z = sh * sh;
+  double P = estrin(C_LOG_D, VEM_LOG_D_N, z);
+  double w = fma(sh * z, P, 2.0 * sl);
+  double ph_ = E * K_LN2_HI;
+  double pl = fma(E, K_LN2_HI, -ph_);
+  pl = fma(E, K_LN2_LO, pl);
+  double vv = 2.0 * sh;
+  double y;
+  if (u10) {
+    dd_t S = two_sum(ph_, vv);
+    y = S.hi + (S.lo + (pl + w));
+  } else {
+    y = ph_ + (vv + (pl + w));
+  }
+  y = (x == 0.0) ? -INFINITY : y;
+  y = (x < 0.0) ? from_bits_d(CANON_NAN_D) : y;
+  y = (x == INFINITY) ? x : y;
+  y = (x != x) ? x : y;
+  return canon_d(y);
+}
+double vo_log_d_u10(double x) { return log_core_d(x, 1); }
+double vo_log_d_u35(double x) { return log_core_d(x, 0); }
+
+/* pow internals: DD log (11 terms) x y -> DD exp. */
+static dd_t log_dd_full(double a, const double* c, int n, double c0l, double c1l) {
+  double m, E;
+  log_split(a, &m, &E);
+  double xn = m - 1.0;
+  double dh = m + 1.0;
+  double dl = m - (dh - 1.0);
+  double t = 1.0 / dh;
+  double sh = xn * t;
+  double u = fma(t, xn, -sh);
+  double v = fma(dl, -t, fma(dh, -t, 1.0));
+  dd_t s = {sh, fma(sh, v, u)};
+  dd_t z = dd_squ(s);
+  double Phi = estrin(c + 2, n - 2, z.hi);
+  dd_t c1 = {c[1], c1l}, c0 = {c[0], c0l};
+  dd_t T = dd_add2_d(c1, z.hi * Phi);
+  T = dd_add2(c0, dd_mul(z, T));
+  dd_t w = dd_mul(dd_mul(s, z), T);
+  dd_t s2 = {s.hi * 2.0, s.lo * 2.0};
+  dd_t lm = dd_add2(s2, w);
+  dd_t el = two_prod(E, K_LN2_HI);
+  el.lo = fma(E, K_LN2_LO, el.lo);
+  return dd_add2(el, lm);
+}
+
+/* DD exp of t = th + tl; returns exp(t) rounded, with ldexp2 scaling. */
+static double exp_dd(dd_t t, const double* c, int n, double c0l, double c1l) {
+  int ok = (t.hi >= -760.0) && (t.hi <= 720.0);
+  double th = ok ? t.hi : 0.0, tl = ok ? t.lo : 0.0;
+  double kd = rint(th * K_INV_LN2);
+  double rh0 = fma(kd, -K_EXP_L1, th);
+  dd_t r0 = {rh0, tl};
+  dd_t r = dd_normalize(dd_add2(r0, two_prod(kd, -K_EXP_L2)));
+  double Ehi = estrin(c + 2, n - 2, r.hi);
+  dd_t c1 = {c[1], c1l}, c0 = {c[0], c0l};
+  dd_t U = dd_add2_d(c1, r.hi * Ehi);
+  U = dd_add2(c0, dd_mul(r, U));
+  dd_t V = dd_mul(dd_squ(r), U);
+  dd_t W = dd_add2(r, V);
+  dd_t Y = dd_add2_d(W, 1.0);
+  double y = ldexp2(Y.hi + Y.lo, (int64_t)kd);
+  y = (t.hi > K_EXP_OVF) ? INFINITY : y;
+  y = (t.hi < K_EXP_UNF) ? 0.0 : y;
+  return y;
+}
+
+/* C99 Annex F pow special cases, applied at the end. */
+static inline int is_int_d(double y) { return (fabs(y) < INFINITY) && (trunc(y) == y); }
+static inline int is_odd_d(double y) {
+  return is_int_d(y) && (fabs(y) < 0x1p53) && (trunc(y * 0.5) * 2.0 != y);
+}
+
+static double pow_core_d(double x, double y, const double* cl, int nl, double cl0, double cl1,
+                         const double* ce, int ne, double ce0, double ce1) {
+  double ax = fabs(x);
+  int fin = (ax > 0.0) && (ax < INFINITY) && (fabs(y) < INFINITY);
+  double axs = fin ? ax : 1.0;
+  double ys = fin ? y : 0.0;
+  dd_t L = log_dd_full(axs, cl, nl, cl0, cl1);
+  dd_t T = dd_mul_d(L, ys);
+  double R = exp_dd(T, ce, ne, ce0, ce1);
+  int yint = is_int_d(y), yodd = is_odd_d(y);
+  double res = (x < 0.0 && yodd) ? -R : R;
+  res = (x < 0.0 && !yint && fabs(y) < INFINITY) ? from_bits_d(CANON_NAN_D) : res;
+  /* x = +-0 */
+  if (x == 0.0) {
+    if (y < 0.0) res = yodd ? copysign_b(INFINITY, x) : INFINITY;
+    else res = yodd ? x : 0.0;
+  }
+  /* x = +-inf */
+  if (ax == INFINITY) {
+    if (y < 0.0) res = (yodd && x < 0.0) ? -0.0 : 0.0;
+    else res = (yodd && x < 0.0) ? -INFINITY : INFINITY;
+  }
+  /* y = +-inf */
+  if (fabs(y) == INFINITY) {
+    if (ax == 1.0) res = 1.0;
+    else res = ((ax < 1.0) == (y < 0.0)) ? INFINITY : 0.0;
+  }
+  if (x != x || y != y) res = from_bits_d(CANON_NAN_D);
+  if (y == 0.0 || x == 1.0) res = 1.0;
+  return canon_d(res);
+}
+double vo_pow_d_u10(double x, double y) {
+  return pow_core_d(x, y, C_POWLOG_D, VEM_POWLOG_D_N, VEM_POWLOG_D_C0L, VEM_POWLOG_D_C1L,
+                    C_POWEXP_D, VEM_POWEXP_D_N, VEM_POWEXP_D_C0L, VEM_POWEXP_D_C1L);
+}
+double vo_pow_d_u35(double x, double y) {
+  return pow_core_d(x, y, C_POWLOG_D_U35, VEM_POWLOG_D_U35_N, VEM_POWLOG_D_U35_C0L,
+                    VEM_POWLOG_D_U35_C1L, C_POWEXP_D_U35, VEM_POWEXP_D_U35_N,
+                    VEM_POWEXP_D_U35_C0L, VEM_POWEXP_D_U35_C1L);
+}
+
+/* fmod -- exact remainder by FP long division (Alg. 1, PAPER.md:958-975,
+ * 1445-1469) restated for unbounded quotient ratios: each step divides by a
+ * staged divisor D = d*2^k with r/D < 2^51, so the ratio never overflows
+ * (SLEEF/the paper return NaN when |x/y| > DBL_MAX).
+ * One division per call (1/ds, ds = d scaled into [1,2)); the quotient
+ * estimate is forced low with nextafter-toward-zero steps and
+ * the off-by-one resolved exactly with two candidate remainders. */
+static inline int64_t ilogb_pos(double x) { /* x > 0 finite, subnormals exact */
+  uint64_t b = bits_d(x);
+  int64_t e = (int64_t)(b >> 52);
+  if (e != 0) return e - 1023;
+  return (int64_t)(63 - __builtin_clzll(b)) - 1074;
+}
+
+static double fmod_core(double x, double y) {
+  double n = fabs(x), d = fabs(y);
+  int ok = (n < INFINITY) && (d > 0.0) && (d < INFINITY);
+  double ns = ok ? n : 0.0, ds0 = ok ? d : 1.0;
+  int64_t ed = ilogb_pos(ds0);
+  double ds = ldexp2(ds0, -ed);
+  double rds = toward0_pos(1.0 / ds);
+  double r = ns;
+  while (r >= ds0) {
+    int64_t er = ilogb_pos(r);
+    int64_t k = er - ed - 50;
+    k = k > 0 ? k : 0;
+    double D = ldexp2(ds0, k);
+    double rs = ldexp2(r, -ed - k);
+    double Q = trunc(toward0_pos(rs * rds));
+    double Q2 = Q + 1.0;
+    double p1 = Q * D, e1 = fma(Q, D, -p1);
+    double V1 = (r - p1) - e1;
+    double p2 = Q2 * D, e2 = fma(Q2, D, -p2);
+    double V2 = (r - p2) - e2;
+    r = (V2 >= 0.0) ? V2 : V1;
+  }
+  double res = copysign_b(r, x);
+  res = (n < d) ? x : res;
+  res = (d == INFINITY && n < INFINITY) ? x : res;
+  res = (!(n < INFINITY) || d == 0.0 || x != x || y != y) ? from_bits_d(CANON_NAN_D) : res;
+  return canon_d(res);
+}
+double vo_fmod_d(double x, double y) { return fmod_core(x, y); }
+
+/* ================================ f32 kernels (binary64 internals) */
+static const double C_SIN_F[] = VEM_SIN_F_ARR;
+static const double C_COS_F[] = VEM_COS_F_ARR;
+static const double C_TAN_F[] = VEM_TAN_F_ARR;
+static const double C_EXP_F[] = VEM_EXP_F_ARR;
+static const double C_EXP_F_U35[] = VEM_EXP_F_U35_ARR;
+static const double C_LOG_F[] = VEM_LOG_F_ARR;
+static const double C_LOG_F_U35[] = VEM_LOG_F_U35_ARR;
+static const double C_POWLOG_F[] = VEM_POWLOG_F_ARR;
+static const double C_POWEXP_F[] = VEM_POWEXP_F_ARR;
+static const double C_POWLOG_F_U35[] = VEM_POWLOG_F_U35_ARR;
+static const double C_POWEXP_F_U35[] = VEM_POWEXP_F_U35_ARR;
+
+/* f32 Payne-Hanek in binary64 (new; the reference is double-only):
+ * |x| = M*2^E, M < 2^24; table T(E) = centred 2^E*2/pi mod 4, 3 limbs.
+ * Every f32 trig lane takes this path (no selector, no divergence). */
+typedef struct { double r; int q; } redf_t;
+static redf_t ph_f(float xf) {
+  int bad = !(fabsf(xf) <= 3.4028234663852886e38f);
+  float xs = bad ? 0.0f : xf;
+  uint32_t b = bits_f(xs) & 0x7fffffffu;
+  int32_t fe = (int32_t)(b >> 23);
+  int32_t E = (fe == 0 ? 1 : fe) - 150;
+  int32_t idx = E + 23;
+  idx = idx < 0 ? 0 : idx;
+  double ax = (double)from_bits_f(b);
+  double Mp = ax * pow2_bits(23 - idx);
+  const double* T = PH_F + 3 * idx;
+  double p0 = Mp * T[0];
+  double e0 = fma(Mp, T[0], -p0);
+  double q0 = rint(p0);
+  double f0 = p0 - q0;
+  dd_t s = two_sum_fast(f0, e0);
+  double p1 = Mp * T[1];
+  double e1 = fma(Mp, T[1], -p1);
+  double tt = e1 + Mp * T[2];
+  dd_t p1d = {p1, tt};
+  dd_t u = dd_add2(s, p1d);
+  double q1 = rint(u.hi);
+  u.hi = u.hi - q1;
+  dd_t fr = two_sum_fast(u.hi, u.lo);
+  double r = fma(fr.hi, K_PIO2_QD0, fma(fr.hi, K_PIO2_QD1, fr.lo * K_PIO2_QD0));
+  int q = (int)q0 + (int)q1;
+  if (xs < 0.0f) {
+    r = -r;
+    q = -q;
+  }
+  redf_t o = {r, q & 3};
+  return o;
+}
+
+static double sincos_core_f(double r, int cosform) {
+  /* sin: r + (r z) S(z);  cos: 1 + z (-1/2 + z C(z))  -> A + (A z) P(z) */
+  double c[5];
+  for (int i = 0; i < 4; i++) c[i] = cosform ? (i == 0 ? -0.5 : C_COS_F[i - 1]) : C_SIN_F[i];
+  c[4] = cosform ? C_COS_F[3] : 0.0;
+  double z = r * r;
+  double P = estrin(c, 5, z);
+  double A = cosform ? 1.0 : r;
+  return fma(A * z, P, A);
+}
+
+float vo_sin_f_u10(float x) {
+  redf_t r = ph_f(x);
+  double y = sincos_core_f(r.r, r.q & 1);
+  y = neg_if(y, r.q & 2);
+  float o = (float)y;
+  o = (x == 0.0f) ? x : o;
+  return canon_f(isinf(x) ? (float)NAN : (x != x ? x : o));
+}
+float vo_cos_f_u10(float x) {
+  redf_t r = ph_f(x);
+  double y = sincos_core_f(r.r, (r.q & 1) ^ 1);
+  y = neg_if(y, (r.q + 1) & 2);
+  float o = (float)y;
+  return canon_f(isinf(x) ? (float)NAN : (x != x ? x : o));
+}
+float vo_tan_f_u10(float x) {
+  redf_t r = ph_f(x);
+  double z = r.r * r.r;
+  double P = estrin(C_TAN_F, VEM_TAN_F_N, z);
+  double t = fma(r.r * z, P, r.r);
+  double y = (r.q & 1) ? -1.0 / t : t;
+  float o = (float)y;
+  o = (x == 0.0f) ? x : o;
+  return canon_f(isinf(x) ? (float)NAN : (x != x ? x : o));
+}
+
+static float exp_core_f(float x, const double* c, int n) {
+  float xc = fminf(fmaxf(x, -150.0f), 130.0f);
+  double xd = (double)xc;
+  double kd = rint(xd * K_INV_LN2);
+  double r = fma(kd, -K_EXP_L1, xd);
+  r = fma(kd, -K_EXP_L2, r);
+  double P = estrin(c, n, r);
+  double y = fma(r, P, 1.0);
+  y = y * pow2_bits((int64_t)kd);
+  float o = (float)y;
+  return canon_f((x != x) ? x : o);
+}
+float vo_exp_f_u10(float x) { return exp_core_f(x, C_EXP_F, VEM_EXP_F_N); }
+float vo_exp_f_u35(float x) { return exp_core_f(x, C_EXP_F_U35, VEM_EXP_F_U35_N); }
+
+/* f32 log in binary64: e, m from the exact double; s = (m-1)/(m+1) with a
+ * float-seeded reciprocal refined once in binary64 (the seed 1/(float)(m+1) is
+ * an IEEE-rounded division, identical on host and device). */
+static inline double log_f_internal(double a, const double* c, int n) {
+  int64_t eb = (int64_t)((bits_d(a * K_FOUR_THIRDS) >> 52) & 0x7ff) - 1023;
+  double m = from_bits_d(bits_d(a) - ((uint64_t)eb << 52));
+  double E = (double)eb;
+  double xn = m - 1.0;
+  double dh = m + 1.0;
+  double t0 = (double)(1.0f / (float)dh);
+  double t = fma(t0, fma(-dh, t0, 1.0), t0);
+  double s = xn * t;
+  double z = s * s;
+  double P = estrin(c, n, z);
+  return fma(E, K_LN2_HI, fma(s * z, P, fma(E, K_LN2_LO, 2.0 * s)));
+}
+static float log_core_f(float x, const double* c, int n) {
+  int ok = (x > 0.0f) && (x < INFINITY);
+  double a = ok ? (double)x : 1.0;
+  double y = log_f_internal(a, c, n);
+  float o = (float)y;
+  o = (x == 0.0f) ? -INFINITY : o;
+  o = (x < 0.0f) ? from_bits_f(CANON_NAN_F) : o;
+  o = (x == INFINITY) ? x : o;
+  o = (x != x) ? x : o;
+  return canon_f(o);
+}
+float vo_log_f_u10(float x) { return log_core_f(x, C_LOG_F, VEM_LOG_F_N); }
+float vo_log_f_u35(float x) { return log_core_f(x, C_LOG_F_U35, VEM_LOG_F_U35_N); }
+
+static inline int is_int_f(float y) { return (fabsf(y) < INFINITY) && (truncf(y) == y); }
+static inline int is_odd_f(float y) {
+  return is_int_f(y) && (fabsf(y) < 0x1p24f) && (truncf(y * 0.5f) * 2.0f != y);
+}
+static float pow_core_f(float x, float y, const double* cl, int nl, const double* ce, int ne) {
+  float ax = fabsf(x);
+  int fin = (ax > 0.0f) && (ax < INFINITY) && (fabsf(y) < INFINITY);
+  double a = fin ? (double)ax : 1.0;
+  double yd = fin ? (double)y : 0.0;
+  double t = yd * log_f_internal(a, cl, nl);
+  double tc = fmin(fmax(t, -200.0), 200.0);
+  double kd = rint(tc * K_INV_LN2);
+  double r = fma(kd, -K_EXP_L1, tc);
+  r = fma(kd, -K_EXP_L2, r);
+  double P = estrin(ce, ne, r);
+  double R = fma(r, P, 1.0) * pow2_bits((int64_t)kd);
+  float Rf = (float)R;
+  int yint = is_int_f(y), yodd = is_odd_f(y);
+  float res = (x < 0.0f && yodd) ? -Rf : Rf;
+  res = (x < 0.0f && !yint && fabsf(y) < INFINITY) ? from_bits_f(CANON_NAN_F) : res;
+  if (x == 0.0f) {
+    if (y < 0.0f) res = yodd ? copysignf(INFINITY, x) : INFINITY;
+    else res = yodd ? x : 0.0f;
+  }
+  if (ax == INFINITY) {
+    if (y < 0.0f) res = (yodd && x < 0.0f) ? -0.0f : 0.0f;
+    else res = (yodd && x < 0.0f) ? -INFINITY : INFINITY;
+  }
+  if (fabsf(y) == INFINITY) {
+    if (ax == 1.0f) res = 1.0f;
+    else res = ((ax < 1.0f) == (y < 0.0f)) ? INFINITY : 0.0f;
+  }
+  if (x != x || y != y) res = from_bits_f(CANON_NAN_F);
+  if (y == 0.0f || x == 1.0f) res = 1.0f;
+  return canon_f(res);
+}
+float vo_pow_f_u10(float x, float y) { return pow_core_f(x, y, C_POWLOG_F, VEM_POWLOG_F_N, C_POWEXP_F, VEM_POWEXP_F_N); }
+float vo_pow_f_u35(float x, float y) {
+  return pow_core_f(x, y, C_POWLOG_F_U35, VEM_POWLOG_F_U35_N, C_POWEXP_F_U35, VEM_POWEXP_F_U35_N);
+}
+
+float vo_fmod_f(float x, float y) {
+  /* fmodf(x,y) == (float)fmod((double)x,(double)y) exactly: the remainder is
+   * representable in binary32. NaN canonicalised in the float domain. */
+  double r = fmod_core((double)x, (double)y);
+  return canon_f((float)r);
+}
+
+/* ============================================ exported array API */
+void vo_trig_reduce_d(const double* x, double* hi, double* lo, int* q, size_t n) {
+  for (size_t i = 0; i < n; i++) {
+    red_t r = trig_reduce(x[i]);
+    hi[i] = r.hi; lo[i] = r.lo; q[i] = r.q;
+  }
+}
+void vo_ph_reduce_d(const double* x, double* hi, double* lo, int* q, size_t n) {
+  for (size_t i = 0; i < n; i++) {
+    red_t r = ph(x[i]);
+    hi[i] = r.hi; lo[i] = r.lo; q[i] = r.q;
+  }
+}
+void vo_cw_reduce_d(const double* x, double* hi, double* lo, int* q, size_t n, int level) {
+  for (size_t i = 0; i < n; i++) {
+    red_t r = level == 1 ? cw1(x[i]) : cw2(x[i]);
+    hi[i] = r.hi; lo[i] = r.lo; q[i] = r.q;
+  }
+}
+void vo_ph_reduce_f(const float* x, double* r, int* q, size_t n) {
+  for (size_t i = 0; i < n; i++) {
+    redf_t o = ph_f(x[i]);
+    r[i] = o.r; q[i] = o.q;
+  }
+}
+const double* vo_ph_table_d(void) { return PH_D; }
+const double* vo_ph_table_f(void) { return PH_F; }
+double vo_round_ta(double x) { return round_ta(x); }
+
+#define UNARY_ARR(name, T)                                             \
+  void name##_arr(const T* x, T* y, size_t n) {                        \
+    _Pragma("omp parallel for schedule(static)")                       \
+    for (size_t i = 0; i < n; i++) y[i] = name(x[i]);                  \
+  }
+#define BINARY_ARR(name, T)                                            \
+  void name##_arr(const T* x, const T* y2, T* y, size_t n) {           \
+    _Pragma("omp parallel for schedule(static)")                       \
+    for (size_t i = 0; i < n; i++) y[i] = name(x[i], y2[i]);           \
+  }
+
+UNARY_ARR(vo_sin_d_u10, double)
+UNARY_ARR(vo_cos_d_u10, double)
+UNARY_ARR(vo_tan_d_u10, double)
+UNARY_ARR(vo_sin_d_u10_ph, double)
+UNARY_ARR(vo_cos_d_u10_ph, double)
+UNARY_ARR(vo_tan_d_u10_ph, double)
+UNARY_ARR(vo_atan_d_u10, double)
+UNARY_ARR(vo_exp_d_u10, double)
+UNARY_ARR(vo_exp_d_u35, double)
+UNARY_ARR(vo_log_d_u10, double)
+UNARY_ARR(vo_log_d_u35, double)
+BINARY_ARR(vo_pow_d_u10, double)
+BINARY_ARR(vo_pow_d_u35, double)
+BINARY_ARR(vo_fmod_d, double)
+UNARY_ARR(vo_sin_f_u10, float)
+UNARY_ARR(vo_cos_f_u10, float)
+UNARY_ARR(vo_tan_f_u10, float)
+UNARY_ARR(vo_exp_f_u10, float)
+UNARY_ARR(vo_exp_f_u35, float)
+UNARY_ARR(vo_log_f_u10, float)
+UNARY_ARR(vo_log_f_u35, float)
+BINARY_ARR(vo_pow_f_u10, float)
+BINARY_ARR(vo_pow_f_u35, float)
+BINARY_ARR(vo_fmod_f, float)
+
+/* fmod iteration count (for the step-curve property) */
+int vo_fmod_d_iters(double x, double y) {
+  double n = fabs(x), d = fabs(y);
+  if (!(n < INFINITY) || !(d > 0.0) || !(d < INFINITY)) return 0;
+  int64_t ed = ilogb_pos(d);
+  double ds = ldexp2(d, -ed);
+  double rds = toward0_pos(1.0 / ds);
+  double r = n;
+  int it = 0;
+  while (r >= d) {
+    int64_t er = ilogb_pos(r);
+    int64_t k = er - ed - 50;
+    k = k > 0 ? k : 0;
+    double D = ldexp2(d, k);
+    double rs = ldexp2(r, -ed - k);
+    double Q = trunc(toward0_pos(rs * rds));
+    double Q2 = Q + 1.0;
+    double p1 = Q * D, e1 = fma(Q, D, -p1);
+    double V1 = (r - p1) - e1;
+    double p2 = Q2 * D, e2 = fma(Q2, D, -p2);
+    double V2 = (r - p2) - e2;
+    r = (V2 >= 0.0) ? V2 : V1;
+    it++;
+  }
+  return it;
+}
+
+/* debug hooks (tests only) */
+void vo_dbg_log_dd(double a, double* hi, double* lo) {
+  dd_t r = log_dd_full(a, C_POWLOG_D, VEM_POWLOG_D_N, VEM_POWLOG_D_C0L, VEM_POWLOG_D_C1L);
+  *hi = r.hi; *lo = r.lo;
+}
+double vo_dbg_exp_dd(double th, double tl) {
+  dd_t t = {th, tl};
+  return exp_dd(t, C_POWEXP_D, VEM_POWEXP_D_N, VEM_POWEXP_D_C0L, VEM_POWEXP_D_C1L);
+}
