@@ -1,0 +1,125 @@
+"""Host-side mirror of the reference's function interface over device arrays.
+
+The reference exposes each function as `name`, `name_u35`, `name_det`
+ on one lane vector (backend.hpp:294-305).  Here each name
+takes a CUDA tensor (torch is only the device-memory/stream plumbing) and
+calls the matching C-ABI entry point (include/vem.h) on the current torch
+stream.  The u10 kernels ARE the deterministic variants (bit-identical to the
+CPU oracle), so `name_det` aliases `name`.  Errors are in-band (NaN/Inf), as
+in the reference; misuse (CPU tensor, wrong dtype, non-contiguous) raises.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+
+_SUFFIX = {torch.float64: "d", torch.float32: "f"}
+
+
+def _entry(fn: str, acc: str, x: torch.Tensor, ph: bool = False) -> str:
+    if not isinstance(x, torch.Tensor) or not x.is_cuda:
+        raise TypeError(f"vem.{fn}: expected a CUDA tensor (no CPU fallback)")
+    if x.dtype not in _SUFFIX:
+        raise TypeError(f"vem.{fn}: dtype {x.dtype} unsupported (float32/float64)")
+    p = _SUFFIX[x.dtype]
+    name = f"{fn}_{p}" if fn == "fmod" else f"{fn}_{p}_{acc}"
+    if ph:
+        name += "_ph"
+    if name not in _lib.ALL:
+        raise TypeError(f"vem: no entry point {name}")
+    return name
+
+
+def _stream_ptr() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def call(name: str, x: torch.Tensor, y: torch.Tensor | None = None, out: torch.Tensor | None = None):
+    """Launch vem_<name> on tensors (asynchronous on the current stream)."""
+    L = _lib.lib()
+    if not x.is_contiguous() or (y is not None and not y.is_contiguous()):
+        raise ValueError("vem: inputs must be contiguous")
+    if out is None:
+        out = torch.empty_like(x)
+    n = x.numel()
+    if name in _lib.BINARY:
+        if y is None or y.shape != x.shape or y.dtype != x.dtype:
+            raise ValueError(f"vem.{name}: second operand must match the first")
+        rc = getattr(L, "vem_" + name)(x.data_ptr(), y.data_ptr(), out.data_ptr(), n, _stream_ptr())
+    else:
+        rc = getattr(L, "vem_" + name)(x.data_ptr(), out.data_ptr(), n, _stream_ptr())
+    _lib.check(rc, "vem_" + name)
+    return out
+
+
+def _u(fn, acc="u10", ph=False):
+    def f(x, out=None):
+        return call(_entry(fn, acc, x, ph), x, out=out)
+    f.__name__ = fn if acc == "u10" else f"{fn}_{acc}"
+    return f
+
+
+def _b(fn, acc="u10"):
+    def f(x, y, out=None):
+        return call(_entry(fn, acc, x), x, y, out=out)
+    f.__name__ = fn if acc == "u10" else f"{fn}_{acc}"
+    return f
+
+
+sin = sin_det = _u("sin")
+cos = cos_det = _u("cos")
+tan = tan_det = _u("tan")
+sin_ph = _u("sin", ph=True)
+cos_ph = _u("cos", ph=True)
+tan_ph = _u("tan", ph=True)
+atan = atan_det = _u("atan")
+exp = exp_det = _u("exp")
+exp_u35 = _u("exp", "u35")
+log = log_det = _u("log")
+log_u35 = _u("log", "u35")
+pow = pow_det = _b("pow")  # noqa: A001
+pow_u35 = _b("pow", "u35")
+fmod = fmod_det = _b("fmod")
+
+
+def trig_reduce(x: torch.Tensor, kind: str = "trig", level: int = 1):
+    """Device trig_reduce / cody_waite_reduce / payne_hanek_reduce -> (hi, lo, q)."""
+    L = _lib.lib()
+    if x.dtype == torch.float32:
+        r = torch.empty(x.shape, dtype=torch.float64, device=x.device)
+        q = torch.empty(x.shape, dtype=torch.int32, device=x.device)
+        _lib.check(L.vem_ph_reduce_f(x.data_ptr(), r.data_ptr(), q.data_ptr(), x.numel(), _stream_ptr()),
+                   "vem_ph_reduce_f")
+        return r, q
+    hi = torch.empty_like(x)
+    lo = torch.empty_like(x)
+    q = torch.empty(x.shape, dtype=torch.int32, device=x.device)
+    if kind == "trig":
+        rc = L.vem_trig_reduce_d(x.data_ptr(), hi.data_ptr(), lo.data_ptr(), q.data_ptr(), x.numel(), _stream_ptr())
+    elif kind == "ph":
+        rc = L.vem_ph_reduce_d(x.data_ptr(), hi.data_ptr(), lo.data_ptr(), q.data_ptr(), x.numel(), _stream_ptr())
+    else:
+        rc = L.vem_cw_reduce_d(x.data_ptr(), hi.data_ptr(), lo.data_ptr(), q.data_ptr(), x.numel(), level,
+                               _stream_ptr())
+    _lib.check(rc, "vem reduce")
+    return hi, lo, q
+
+
+def run_sharded(name: str, x: np.ndarray, y: np.ndarray | None = None, ngpu: int = 1):
+    """Host arrays in, host array out, sharded over `ngpu` devices by the C++
+    driver (vem_run_sharded).  Returns (out, max-over-devices kernel ms)."""
+    L = _lib.lib()
+    x = np.ascontiguousarray(x)
+    out = np.empty_like(x)
+    ms = ctypes.c_double(0.0)
+    yp = None
+    if y is not None:
+        y = np.ascontiguousarray(y)
+        yp = y.ctypes.data
+    rc = L.vem_run_sharded(name.encode(), x.ctypes.data, yp, out.ctypes.data, x.size, ngpu, ctypes.byref(ms))
+    _lib.check(rc, "vem_run_sharded")
+    return out, ms.value

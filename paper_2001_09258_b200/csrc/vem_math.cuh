@@ -1,0 +1,760 @@
+// Per-lane device math for the vem kernels (sm_100a).
+//
+// One CUDA thread = one lane of the reference's Backend<1, Fma=true, Det=true>
+// (backend.hpp:62-144, ScalarFmaDet backend.hpp:430): opmask `select` becomes a
+// predicated SEL, `all/any` skips become plain per-lane branches that a warp
+// only pays for when its lanes disagree.  Every floating-point operation is
+// written out explicitly (the library is compiled with --fmad=false; fused
+// operations are explicit fma()), in exactly the order of the CPU oracle
+// (oracle/vem_oracle.c), so results are bit-identical to it.
+//
+// DD arithmetic follows ddarith.hpp (FMA paths); the reduction follows
+// reduction.hpp:31-212 with the Payne-Hanek repairs of SURVEY.md §0 item 4.
+#pragma once
+
+#include <cstdint>
+
+#include "vem_coeffs.h"
+#include "vem_ph_tables.h"
+
+namespace vem {
+
+struct dd { double hi, lo; };
+
+// ---------------------------------------------------------------- bits
+__device__ __forceinline__ uint64_t bits_d(double x) { return (uint64_t)__double_as_longlong(x); }
+__device__ __forceinline__ double from_bits_d(uint64_t u) { return __longlong_as_double((long long)u); }
+__device__ __forceinline__ uint32_t bits_f(float x) { return (uint32_t)__float_as_uint(x); }
+__device__ __forceinline__ float from_bits_f(uint32_t u) { return __uint_as_float(u); }
+
+constexpr uint64_t kCanonNanD = 0x7ff8000000000000ull;
+constexpr uint32_t kCanonNanF = 0x7fc00000u;
+__device__ __forceinline__ double canon_d(double y) { return (y != y) ? from_bits_d(kCanonNanD) : y; }
+__device__ __forceinline__ float canon_f(float y) { return (y != y) ? from_bits_f(kCanonNanF) : y; }
+
+// constants.hpp:14-58
+constexpr double kPio2Qd0 = 0x1.921fb54442d18p+0;
+constexpr double kPio2Qd1 = 0x1.1a62633145c07p-54;
+constexpr double kPio2Qd2 = -0x1.f1976b7ed8fbcp-110;
+constexpr double kPio2Qd3 = 0x1.4cf98e804177dp-164;
+constexpr double kTwoOverPi = 0x1.45f306dc9c883p-1;
+constexpr double kCw1P0 = 0x1.921fb54442d20p+0;
+constexpr double kCw1T1 = -0x1.ee59d9cceba40p-50;
+constexpr double kCw1T2 = 0x1.b839a252049c1p-104;
+constexpr double kCw2A = 0x1.921fb58000000p+0;
+constexpr double kCw2B = -0x1.dde9740000000p-27;
+constexpr double kCw2C = 0x1.1a62630000000p-54;
+constexpr double kCw2D1 = 0x1.8a2e03707344ap-81;
+constexpr double kCw2D2 = 0x1.024e088a67cc7p-135;
+constexpr double kInvLn2 = 0x1.71547652b82fep+0;
+constexpr double kExpL1 = 0x1.62e42fefa3800p-1;
+constexpr double kExpL2 = 0x1.ef35793c76730p-45;
+constexpr double kLn2Hi = 0x1.62e42fefa39efp-1;
+constexpr double kLn2Lo = 0x1.abc9e3b39803fp-56;
+constexpr double kExpOvf = 0x1.62e42fefa39efp+9;
+constexpr double kExpUnf = -0x1.74910d52d3051p+9;
+constexpr double kCw1Max = 15.0;
+constexpr double kCw2Max = 1e14;
+constexpr double kFourThirds = 0x1.5555555555555p+0;
+constexpr double kTanPi8 = 0x1.a827999fcef32p-2;
+constexpr double kTan3Pi8 = 0x1.3504f333f9de6p+1;
+constexpr double kPio4Hi = 0x1.921fb54442d18p-1;
+constexpr double kPio4Lo = 0x1.1a62633145c07p-55;
+constexpr double kDblMax = 1.7976931348623157e308;
+constexpr double kInf = __builtin_huge_val();
+constexpr float kInfF = __builtin_huge_valf();
+
+// Coefficients live in the constant bank: uniform operands of DFMA.
+__constant__ double cSinD[] = VEM_SIN_D_ARR;
+__constant__ double cCosD[] = VEM_COS_D_ARR;
+__constant__ double cTanD[] = VEM_TAN_D_ARR;
+__constant__ double cAtanD[] = VEM_ATAN_D_ARR;
+__constant__ double cExpD[] = VEM_EXP_D_ARR;
+__constant__ double cExpDU35[] = VEM_EXP_D_U35_ARR;
+__constant__ double cLogD[] = VEM_LOG_D_ARR;
+__constant__ double cPowLogD[] = VEM_POWLOG_D_ARR;
+__constant__ double cPowExpD[] = VEM_POWEXP_D_ARR;
+__constant__ double cPowLogDU35[] = VEM_POWLOG_D_U35_ARR;
+__constant__ double cPowExpDU35[] = VEM_POWEXP_D_U35_ARR;
+__constant__ double cSinF[] = VEM_SIN_F_ARR;
+__constant__ double cCosF[] = VEM_COS_F_ARR;
+__constant__ double cTanF[] = VEM_TAN_F_ARR;
+__constant__ double cExpF[] = VEM_EXP_F_ARR;
+__constant__ double cExpFU35[] = VEM_EXP_F_U35_ARR;
+__constant__ double cLogF[] = VEM_LOG_F_ARR;
+__constant__ double cLogFU35[] = VEM_LOG_F_U35_ARR;
+__constant__ double cPowLogF[] = VEM_POWLOG_F_ARR;
+__constant__ double cPowExpF[] = VEM_POWEXP_F_ARR;
+__constant__ double cPowLogFU35[] = VEM_POWLOG_F_U35_ARR;
+__constant__ double cPowExpFU35[] = VEM_POWEXP_F_U35_ARR;
+
+// Payne-Hanek tables (global copy; kernels stage them into shared memory).
+__device__ const double gPhD[4 * VEM_PH_D_ENTRIES] = {VEM_PH_D_INIT};
+__device__ const double gPhF[3 * VEM_PH_F_ENTRIES] = {VEM_PH_F_INIT};
+
+// ---------------------------------------------------- primitives
+// backend.hpp:47-52 round_ta == CUDA round() (ties away from zero) for every
+// binary64 input incl. signed zeros; tests/test_gpu_parity.py pins it.
+__device__ __forceinline__ double round_ta(double x) { return round(x); }
+__device__ __forceinline__ double pow2_bits(int64_t e) { return from_bits_d((uint64_t)(e + 1023) << 52); }
+// backend.hpp:133-138
+__device__ __forceinline__ double ldexp2(double x, int64_t e) {
+  e = e > 2046 ? 2046 : (e < -2044 ? -2044 : e);
+  int64_t h = e >> 1;
+  return (x * pow2_bits(h)) * pow2_bits(e - h);
+}
+__device__ __forceinline__ double mulsign(double x, double s) {  // backend.hpp:381-384
+  return from_bits_d(bits_d(x) ^ (bits_d(s) & 0x8000000000000000ull));
+}
+__device__ __forceinline__ double copysign_b(double m, double s) {
+  return from_bits_d((bits_d(m) & 0x7fffffffffffffffull) | (bits_d(s) & 0x8000000000000000ull));
+}
+__device__ __forceinline__ double neg_if(double y, int c) {
+  return from_bits_d(bits_d(y) ^ ((uint64_t)(c != 0) << 63));
+}
+__device__ __forceinline__ double toward0_pos(double x) { return from_bits_d(bits_d(x) - 1); }
+
+// ------------------------------------------------------ DD (ddarith.hpp)
+__device__ __forceinline__ dd two_sum(double a, double b) {
+  double s = a + b, v = s - a;
+  return {s, (a - (s - v)) + (b - v)};
+}
+__device__ __forceinline__ dd two_sum_fast(double a, double b) {
+  double s = a + b;
+  return {s, b - (s - a)};
+}
+__device__ __forceinline__ dd two_prod(double a, double b) {
+  double p = a * b;
+  return {p, fma(a, b, -p)};
+}
+__device__ __forceinline__ dd dd_add2(dd x, dd y) {
+  double s = x.hi + y.hi, v = s - x.hi;
+  double e = (x.hi - (s - v)) + (y.hi - v);
+  return {s, e + (x.lo + y.lo)};
+}
+__device__ __forceinline__ dd dd_add2_d(dd x, double y) {
+  double s = x.hi + y, v = s - x.hi;
+  double e = (x.hi - (s - v)) + (y - v);
+  return {s, e + x.lo};
+}
+__device__ __forceinline__ dd dd_mul(dd x, dd y) {
+  double p = x.hi * y.hi;
+  double e = fma(x.hi, y.hi, -p);
+  e = fma(x.hi, y.lo, e);
+  e = fma(x.lo, y.hi, e);
+  return {p, e};
+}
+__device__ __forceinline__ dd dd_mul_d(dd x, double y) {
+  double p = x.hi * y;
+  double e = fma(x.hi, y, -p);
+  e = fma(x.lo, y, e);
+  return {p, e};
+}
+__device__ __forceinline__ dd dd_squ(dd x) {
+  double p = x.hi * x.hi;
+  double e = fma(x.hi, x.hi, -p);
+  e = fma(x.hi + x.hi, x.lo, e);
+  return {p, e};
+}
+__device__ __forceinline__ dd dd_div(dd x, dd y) {
+  double t = 1.0 / y.hi;
+  double q = x.hi * t;
+  double u = fma(t, x.hi, -q);
+  double v = fma(y.lo, -t, fma(y.hi, -t, 1.0));
+  return {q, fma(q, v, fma(x.lo, t, u))};
+}
+__device__ __forceinline__ dd dd_normalize(dd x) { return two_sum_fast(x.hi, x.lo); }
+
+// Estrin with the oracle's fixed bracketing (oracle/vem_oracle.c: estrin).
+template <int N>
+__device__ __forceinline__ double estrin(const double* c, double x) {
+  double t[N];
+#pragma unroll
+  for (int i = 0; i < N; i++) t[i] = c[i];
+  double p = x;
+  int n = N;
+#pragma unroll
+  for (int lvl = 0; lvl < 6; lvl++) {
+    if (n > 1) {
+      int m = 0;
+#pragma unroll
+      for (int i = 0; i + 1 < N; i += 2)
+        if (i + 1 < n) t[m++] = fma(t[i + 1], p, t[i]);
+      if (n & 1) t[m++] = t[n - 1];
+      n = m;
+      if (n > 1) p = p * p;
+    }
+  }
+  return t[0];
+}
+// Same with per-lane selected coefficients (a ? ca[i] : cb[i]).
+template <int N>
+__device__ __forceinline__ double estrin_sel(const double* ca, const double* cb, bool a, double x) {
+  double t[N];
+#pragma unroll
+  for (int i = 0; i < N; i++) t[i] = a ? ca[i] : cb[i];
+  double p = x;
+  int n = N;
+#pragma unroll
+  for (int lvl = 0; lvl < 6; lvl++) {
+    if (n > 1) {
+      int m = 0;
+#pragma unroll
+      for (int i = 0; i + 1 < N; i += 2)
+        if (i + 1 < n) t[m++] = fma(t[i + 1], p, t[i]);
+      if (n & 1) t[m++] = t[n - 1];
+      n = m;
+      if (n > 1) p = p * p;
+    }
+  }
+  return t[0];
+}
+
+// ===================================================== reduction (f64)
+struct red { double hi, lo; int q; };
+
+// reduction.hpp:148-159
+__device__ __forceinline__ red cw1(double x) {
+  double qd = round_ta(x * kTwoOverPi);
+  double r0 = fma(qd, -kCw1P0, x);
+  dd tail = two_prod(qd, -kCw1T1);
+  tail.lo = fma(qd, -kCw1T2, tail.lo);
+  dd r = dd_normalize(dd_add2(dd{r0, 0.0}, tail));
+  return {r.hi, r.lo, (int)((long long)qd & 3)};
+}
+
+// reduction.hpp:163-178
+__device__ __forceinline__ red cw2(double x) {
+  double t = x * kTwoOverPi;
+  double qh = trunc(t * 0x1p-24);
+  qh = qh * 0x1p24;
+  double ql = round_ta(t - qh);
+  double r = x;
+  r = fma(qh, -kCw2A, r);
+  r = fma(ql, -kCw2A, r);
+  r = fma(qh, -kCw2B, r);
+  r = fma(ql, -kCw2B, r);
+  dd acc = dd_add2(dd{r, 0.0}, two_prod(qh, -kCw2C));
+  acc = dd_add2(acc, two_prod(ql, -kCw2C));
+  double qs = qh + ql;
+  dd dtail = two_prod(qs, -kCw2D1);
+  dtail.lo = fma(qs, -kCw2D2, dtail.lo);
+  acc = dd_add2(acc, dtail);
+  acc = dd_normalize(acc);
+  return {acc.hi, acc.lo, (int)((long long)ql & 3)};
+}
+
+// reduction.hpp:35-43
+__device__ __forceinline__ dd rfrac_q(dd a, long long& q) {
+  double rh = round_ta(a.hi);
+  a.hi = a.hi - rh;
+  q += (long long)rh;
+  double rl = round_ta(a.lo);
+  a.lo = a.lo - rl;
+  q += (long long)rl;
+  return a;
+}
+
+// reduction.hpp:89-137, repaired (mod-4 table in `tab`, two_sum renorm).
+__device__ __forceinline__ red ph(double x_in, const double* __restrict__ tab) {
+  bool bad = !(fabs(x_in) <= kDblMax);
+  double x = bad ? 0.0 : x_in;
+  double a = fabs(x);
+  long long er = (long long)((bits_d(a) >> 52) & 0x7ff);
+  long long idx = er - 1023;
+  idx = (0 > idx) ? 0 : idx;
+  idx = (idx > 1023) ? 1023 : idx;
+  double m = ldexp2(a, 52 - idx);
+  const double2* f2 = reinterpret_cast<const double2*>(tab + (idx << 2));
+  double2 fa = f2[0], fb = f2[1];
+  long long q = 0;
+  dd u = two_prod(m, fa.x);
+  u = rfrac_q(u, q);
+  u = two_sum(u.hi, u.lo);
+  u = dd_add2(u, two_prod(m, fa.y));
+  u = rfrac_q(u, q);
+  u = two_sum(u.hi, u.lo);
+  u = dd_add2(u, two_prod(m, fb.x));
+  u = rfrac_q(u, q);
+  u = two_sum(u.hi, u.lo);
+  u = dd_add2(u, two_prod(m, fb.y));
+  double qv = round_ta(u.hi + u.lo);
+  u.hi = u.hi - qv;
+  q += (long long)qv;
+  double ql = round_ta(u.lo);
+  u.lo = u.lo - ql;
+  q += (long long)ql;
+  u = dd_normalize(u);
+  double p = u.hi * kPio2Qd0;  // reduction.hpp:57-69 mul_pio2_qd
+  double e = fma(u.hi, kPio2Qd0, -p);
+  e = fma(u.hi, kPio2Qd1, e);
+  e = fma(u.lo, kPio2Qd0, e);
+  e = fma(u.hi, kPio2Qd2, e);
+  e = fma(u.lo, kPio2Qd1, e);
+  e = fma(u.hi, kPio2Qd3, e);
+  e = fma(u.lo, kPio2Qd2, e);
+  double rh = mulsign(p, x), rl = mulsign(e, x);
+  if (x < 0.0) q = 0 - q;
+  red o;
+  o.hi = bad ? from_bits_d(kCanonNanD) : rh;
+  o.lo = bad ? from_bits_d(kCanonNanD) : rl;
+  o.q = bad ? 0 : (int)(q & 3);
+  return o;
+}
+
+// reduction.hpp:189-206 (deterministic, per lane).  Lanes of one warp that
+// agree skip the heavier paths; disagreeing warps run both (SIMT divergence).
+__device__ __forceinline__ red trig_reduce(double x, const double* __restrict__ tab) {
+  double ax = fabs(x);
+  red r;
+  if (ax <= kCw1Max) {
+    r = cw1(x);
+  } else if (ax <= kCw2Max) {
+    r = cw2(x);
+  } else {
+    r = ph(x, tab);
+  }
+  return r;
+}
+
+// ===================================================== f64 functions
+__device__ __forceinline__ double sincos_core_d(double rh, double rl, int cosform) {
+  bool cf = cosform != 0;
+  double z = rh * rh;
+  double P = estrin_sel<VEM_SIN_D_N>(cCosD, cSinD, cf, z);
+  double As = rh, Bs = 0.0, Ms = rh * z, Ts = fma(-0.5 * z, rl, rl);
+  double zl = fma(rh, rh, -z);
+  double hz = 0.5 * z;
+  double w = 1.0 - hz;
+  double Ac = w, Bc = (1.0 - w) - hz, Mc = z * z, Tc = -fma(0.5, zl, rh * rl);
+  double A = cf ? Ac : As, B = cf ? Bc : Bs, M = cf ? Mc : Ms, T = cf ? Tc : Ts;
+  return A + (B + fma(M, P, T));
+}
+
+template <bool kForcePh>
+__device__ __forceinline__ double sin_d_u10(double x, const double* tab) {
+  red r = kForcePh ? ph(x, tab) : trig_reduce(x, tab);
+  double y = sincos_core_d(r.hi, r.lo, r.q & 1);
+  y = neg_if(y, r.q & 2);
+  y = (x == 0.0) ? x : y;
+  return canon_d(y);
+}
+template <bool kForcePh>
+__device__ __forceinline__ double cos_d_u10(double x, const double* tab) {
+  red r = kForcePh ? ph(x, tab) : trig_reduce(x, tab);
+  double y = sincos_core_d(r.hi, r.lo, (r.q & 1) ^ 1);
+  y = neg_if(y, (r.q + 1) & 2);
+  return canon_d(y);
+}
+
+__device__ __forceinline__ double tan_core_d(double rh, double rl, int odd) {
+  double hh = rh * 0.5, hl = rl * 0.5;
+  double z = hh * hh;
+  double P = estrin<VEM_TAN_D_N>(cTanD, z);
+  double corr = fma(hh * z, P, fma(hl, z, hl));
+  dd t = two_sum_fast(hh, corr);
+  dd t2 = dd_squ(t);
+  dd den = two_sum(1.0, -t2.hi);
+  den.lo = den.lo - t2.lo;
+  dd num = {t.hi * 2.0, t.lo * 2.0};
+  bool o = odd != 0;
+  dd X = {o ? -den.hi : num.hi, o ? -den.lo : num.lo};
+  dd Y = {o ? num.hi : den.hi, o ? num.lo : den.lo};
+  dd q = dd_div(X, Y);
+  return q.hi + q.lo;
+}
+template <bool kForcePh>
+__device__ __forceinline__ double tan_d_u10(double x, const double* tab) {
+  red r = kForcePh ? ph(x, tab) : trig_reduce(x, tab);
+  double y = tan_core_d(r.hi, r.lo, r.q & 1);
+  y = (fabs(x) < 0x1p-27) ? x : y;
+  return canon_d(y);
+}
+
+__device__ __forceinline__ double atan_d_u10(double x) {
+  double a = fabs(x);
+  bool c1 = a > kTanPi8;
+  bool c2 = a > kTan3Pi8;
+  dd ns = two_sum(a, -1.0), ds = two_sum(a, 1.0);
+  dd nn, dn;
+  nn.hi = c2 ? -1.0 : (c1 ? ns.hi : a);
+  nn.lo = c2 ? 0.0 : (c1 ? ns.lo : 0.0);
+  dn.hi = c2 ? a : (c1 ? ds.hi : 1.0);
+  dn.lo = c2 ? 0.0 : (c1 ? ds.lo : 0.0);
+  dd b = dd_div(nn, dn);
+  double z = b.hi * b.hi;
+  double P = estrin<VEM_ATAN_D_N>(cAtanD, z);
+  double corr = fma(b.hi * z, P, fma(-b.lo, z, b.lo));
+  double offh = c2 ? kPio2Qd0 : (c1 ? kPio4Hi : 0.0);
+  double offl = c2 ? kPio2Qd1 : (c1 ? kPio4Lo : 0.0);
+  dd s = two_sum(offh, b.hi);
+  double y = s.hi + (s.lo + (offl + corr));
+  y = (a == kInf) ? kPio2Qd0 : y;
+  y = copysign_b(y, x);
+  return canon_d(y);
+}
+
+template <int N, bool kU10>
+__device__ __forceinline__ double exp_core_d(double x, const double* c) {
+  bool ok = (x >= kExpUnf) && (x <= kExpOvf);
+  double xs = ok ? x : 0.0;
+  double kd = rint(xs * kInvLn2);
+  double r1 = fma(kd, -kExpL1, xs);
+  double r = fma(kd, -kExpL2, r1);
+  double P = estrin<N>(c, r);
+  double y;
+  if (kU10) {
+    double rl = fma(-kd, kExpL2, r1 - r);
+    double s = 1.0 + r;
+    double se = (1.0 - s) + r;
+    y = s + (se + fma(r * r, P, rl));
+  } else {
+    y = 1.0 + fma(r * r, P, r);
+  }
+  y = ldexp2(y, (long long)kd);
+  y = (x > kExpOvf) ? kInf : y;
+  y = (x < kExpUnf) ? 0.0 : y;
+  y = (x != x) ? x : y;
+  return canon_d(y);
+}
+__device__ __forceinline__ double exp_d_u10(double x) { return exp_core_d<VEM_EXP_D_N, true>(x, cExpD); }
+__device__ __forceinline__ double exp_d_u35(double x) { return exp_core_d<VEM_EXP_D_U35_N, false>(x, cExpDU35); }
+
+__device__ __forceinline__ void log_split(double a, double& m, double& E) {
+  bool sub = a < 0x1p-1022;
+  double as = sub ? a * 0x1p64 : a;
+  long long eb = (long long)((bits_d(as * kFourThirds) >> 52) & 0x7ff) - 1023;
+  m = from_bits_d(bits_d(as) - ((uint64_t)eb << 52));
+  E = (double)(eb - (sub ? 64 : 0));
+}
+
+template <bool kU10>
+__device__ __forceinline__ double log_core_d(double x) {
+  bool ok = (x > 0.0) && (x < kInf);
+  double a = ok ? x : 1.0;
+  double m, E;
+  log_split(a, m, E);
+  double xn = m - 1.0;
+  double dh = m + 1.0;
+  double dl = m - (dh - 1.0);
+  double t = 1.0 / dh;
+  double sh = xn * t;
+  double u = fma(t, xn, -sh);
+  double v = fma(dl, -t, fma(dh, -t, 1.0));
+  double sl = fma(sh, v, u);
+  double z = sh * sh;
+  double P = estrin<VEM_LOG_D_N>(cLogD, z);
+  double w = fma(sh * z, P, 2.0 * sl);
+  double ph_ = E * kLn2Hi;
+  double pl = fma(E, kLn2Hi, -ph_);
+  pl = fma(E, kLn2Lo, pl);
+  double vv = 2.0 * sh;
+  double y;
+  if (kU10) {
+    dd S = two_sum(ph_, vv);
+    y = S.hi + (S.lo + (pl + w));
+  } else {
+    y = ph_ + (vv + (pl + w));
+  }
+  y = (x == 0.0) ? -kInf : y;
+  y = (x < 0.0) ? from_bits_d(kCanonNanD) : y;
+  y = (x == kInf) ? x : y;
+  y = (x != x) ? x : y;
+  return canon_d(y);
+}
+
+template <int NL>
+__device__ __forceinline__ dd log_dd_full(double a, const double* c, double c0l, double c1l) {
+  double m, E;
+  log_split(a, m, E);
+  double xn = m - 1.0;
+  double dh = m + 1.0;
+  double dl = m - (dh - 1.0);
+  double t = 1.0 / dh;
+  double sh = xn * t;
+  double u = fma(t, xn, -sh);
+  double v = fma(dl, -t, fma(dh, -t, 1.0));
+  dd s = {sh, fma(sh, v, u)};
+  dd z = dd_squ(s);
+  double Phi = estrin<NL - 2>(c + 2, z.hi);
+  dd c1 = {c[1], c1l}, c0 = {c[0], c0l};
+  dd T = dd_add2_d(c1, z.hi * Phi);
+  T = dd_add2(c0, dd_mul(z, T));
+  dd w = dd_mul(dd_mul(s, z), T);
+  dd s2 = {s.hi * 2.0, s.lo * 2.0};
+  dd lm = dd_add2(s2, w);
+  dd el = two_prod(E, kLn2Hi);
+  el.lo = fma(E, kLn2Lo, el.lo);
+  return dd_add2(el, lm);
+}
+
+template <int NE>
+__device__ __forceinline__ double exp_dd(dd t, const double* c, double c0l, double c1l) {
+  bool ok = (t.hi >= -760.0) && (t.hi <= 720.0);
+  double th = ok ? t.hi : 0.0, tl = ok ? t.lo : 0.0;
+  double kd = rint(th * kInvLn2);
+  double rh0 = fma(kd, -kExpL1, th);
+  dd r = dd_normalize(dd_add2(dd{rh0, tl}, two_prod(kd, -kExpL2)));
+  double Ehi = estrin<NE - 2>(c + 2, r.hi);
+  dd c1 = {c[1], c1l}, c0 = {c[0], c0l};
+  dd U = dd_add2_d(c1, r.hi * Ehi);
+  U = dd_add2(c0, dd_mul(r, U));
+  dd V = dd_mul(dd_squ(r), U);
+  dd W = dd_add2(r, V);
+  dd Y = dd_add2_d(W, 1.0);
+  double y = ldexp2(Y.hi + Y.lo, (long long)kd);
+  y = (t.hi > kExpOvf) ? kInf : y;
+  y = (t.hi < kExpUnf) ? 0.0 : y;
+  return y;
+}
+
+__device__ __forceinline__ bool is_int_d(double y) { return (fabs(y) < kInf) && (trunc(y) == y); }
+__device__ __forceinline__ bool is_odd_d(double y) {
+  return is_int_d(y) && (fabs(y) < 0x1p53) && (trunc(y * 0.5) * 2.0 != y);
+}
+
+template <int NL, int NE>
+__device__ __forceinline__ double pow_core_d(double x, double y, const double* cl, double cl0, double cl1,
+                                             const double* ce, double ce0, double ce1) {
+  double ax = fabs(x);
+  bool fin = (ax > 0.0) && (ax < kInf) && (fabs(y) < kInf);
+  double axs = fin ? ax : 1.0;
+  double ys = fin ? y : 0.0;
+  dd L = log_dd_full<NL>(axs, cl, cl0, cl1);
+  dd T = dd_mul_d(L, ys);
+  double R = exp_dd<NE>(T, ce, ce0, ce1);
+  bool yint = is_int_d(y), yodd = is_odd_d(y);
+  double res = (x < 0.0 && yodd) ? -R : R;
+  res = (x < 0.0 && !yint && fabs(y) < kInf) ? from_bits_d(kCanonNanD) : res;
+  if (x == 0.0) {
+    if (y < 0.0) res = yodd ? copysign_b(kInf, x) : kInf;
+    else res = yodd ? x : 0.0;
+  }
+  if (ax == kInf) {
+    if (y < 0.0) res = (yodd && x < 0.0) ? -0.0 : 0.0;
+    else res = (yodd && x < 0.0) ? -kInf : kInf;
+  }
+  if (fabs(y) == kInf) {
+    if (ax == 1.0) res = 1.0;
+    else res = ((ax < 1.0) == (y < 0.0)) ? kInf : 0.0;
+  }
+  if (x != x || y != y) res = from_bits_d(kCanonNanD);
+  if (y == 0.0 || x == 1.0) res = 1.0;
+  return canon_d(res);
+}
+__device__ __forceinline__ double pow_d_u10(double x, double y) {
+  return pow_core_d<VEM_POWLOG_D_N, VEM_POWEXP_D_N>(x, y, cPowLogD, VEM_POWLOG_D_C0L, VEM_POWLOG_D_C1L,
+                                                     cPowExpD, VEM_POWEXP_D_C0L, VEM_POWEXP_D_C1L);
+}
+__device__ __forceinline__ double pow_d_u35(double x, double y) {
+  return pow_core_d<VEM_POWLOG_D_U35_N, VEM_POWEXP_D_U35_N>(
+      x, y, cPowLogDU35, VEM_POWLOG_D_U35_C0L, VEM_POWLOG_D_U35_C1L, cPowExpDU35, VEM_POWEXP_D_U35_C0L,
+      VEM_POWEXP_D_U35_C1L);
+}
+
+// fmod: staged-divisor FP long division (oracle: fmod_core).
+__device__ __forceinline__ long long ilogb_pos(double x) {
+  uint64_t b = bits_d(x);
+  long long e = (long long)(b >> 52);
+  return e != 0 ? e - 1023 : (long long)(63 - __clzll((long long)b)) - 1074;
+}
+__device__ __forceinline__ double fmod_core(double x, double y) {
+  double n = fabs(x), d = fabs(y);
+  bool ok = (n < kInf) && (d > 0.0) && (d < kInf);
+  double ns = ok ? n : 0.0, ds0 = ok ? d : 1.0;
+  long long ed = ilogb_pos(ds0);
+  double ds = ldexp2(ds0, -ed);
+  double rds = toward0_pos(1.0 / ds);
+  double r = ns;
+  while (r >= ds0) {
+    long long er = ilogb_pos(r);
+    long long k = er - ed - 50;
+    k = k > 0 ? k : 0;
+    double D = ldexp2(ds0, k);
+    double rs = ldexp2(r, -ed - k);
+    double Q = trunc(toward0_pos(rs * rds));
+    double Q2 = Q + 1.0;
+    double p1 = Q * D, e1 = fma(Q, D, -p1);
+    double V1 = (r - p1) - e1;
+    double p2 = Q2 * D, e2 = fma(Q2, D, -p2);
+    double V2 = (r - p2) - e2;
+    r = (V2 >= 0.0) ? V2 : V1;
+  }
+  double res = copysign_b(r, x);
+  res = (n < d) ? x : res;
+  res = (d == kInf && n < kInf) ? x : res;
+  res = (!(n < kInf) || d == 0.0 || x != x || y != y) ? from_bits_d(kCanonNanD) : res;
+  return canon_d(res);
+}
+__device__ __forceinline__ double fmod_d(double x, double y) { return fmod_core(x, y); }
+
+// ===================================== f32 functions (binary64 internals)
+struct redf { double r; int q; };
+
+__device__ __forceinline__ redf ph_f(float xf, const double* __restrict__ tab) {
+  bool bad = !(fabsf(xf) <= 3.4028234663852886e38f);
+  float xs = bad ? 0.0f : xf;
+  uint32_t b = bits_f(xs) & 0x7fffffffu;
+  int fe = (int)(b >> 23);
+  int E = (fe == 0 ? 1 : fe) - 150;
+  int idx = E + 23;
+  idx = idx < 0 ? 0 : idx;
+  double ax = (double)from_bits_f(b);
+  double Mp = ax * pow2_bits(23 - idx);
+  const double* T = tab + 3 * idx;
+  double T0 = T[0], T1 = T[1], T2 = T[2];
+  double p0 = Mp * T0;
+  double e0 = fma(Mp, T0, -p0);
+  double q0 = rint(p0);
+  double f0 = p0 - q0;
+  dd s = two_sum_fast(f0, e0);
+  double p1 = Mp * T1;
+  double e1 = fma(Mp, T1, -p1);
+  double tt = e1 + Mp * T2;
+  dd u = dd_add2(s, dd{p1, tt});
+  double q1 = rint(u.hi);
+  u.hi = u.hi - q1;
+  dd fr = two_sum_fast(u.hi, u.lo);
+  double r = fma(fr.hi, kPio2Qd0, fma(fr.hi, kPio2Qd1, fr.lo * kPio2Qd0));
+  int q = (int)q0 + (int)q1;
+  if (xs < 0.0f) {
+    r = -r;
+    q = -q;
+  }
+  return {r, q & 3};
+}
+
+__device__ __forceinline__ double sincos_core_f(double r, int cosform) {
+  bool cf = cosform != 0;
+  double c0 = cf ? -0.5 : cSinF[0];
+  double c1 = cf ? cCosF[0] : cSinF[1];
+  double c2 = cf ? cCosF[1] : cSinF[2];
+  double c3 = cf ? cCosF[2] : cSinF[3];
+  double c4 = cf ? cCosF[3] : 0.0;
+  double c[5] = {c0, c1, c2, c3, c4};
+  double z = r * r;
+  double P = estrin<5>(c, z);
+  double A = cf ? 1.0 : r;
+  return fma(A * z, P, A);
+}
+
+__device__ __forceinline__ float sin_f_u10(float x, const double* tab) {
+  redf r = ph_f(x, tab);
+  double y = sincos_core_f(r.r, r.q & 1);
+  y = neg_if(y, r.q & 2);
+  float o = (float)y;
+  o = (x == 0.0f) ? x : o;
+  return canon_f(isinf(x) ? from_bits_f(kCanonNanF) : (x != x ? x : o));
+}
+__device__ __forceinline__ float cos_f_u10(float x, const double* tab) {
+  redf r = ph_f(x, tab);
+  double y = sincos_core_f(r.r, (r.q & 1) ^ 1);
+  y = neg_if(y, (r.q + 1) & 2);
+  float o = (float)y;
+  return canon_f(isinf(x) ? from_bits_f(kCanonNanF) : (x != x ? x : o));
+}
+__device__ __forceinline__ float tan_f_u10(float x, const double* tab) {
+  redf r = ph_f(x, tab);
+  double z = r.r * r.r;
+  double P = estrin<VEM_TAN_F_N>(cTanF, z);
+  double t = fma(r.r * z, P, r.r);
+  double y = (r.q & 1) ? -1.0 / t : t;
+  float o = (float)y;
+  o = (x == 0.0f) ? x : o;
+  return canon_f(isinf(x) ? from_bits_f(kCanonNanF) : (x != x ? x : o));
+}
+
+template <int N>
+__device__ __forceinline__ float exp_core_f(float x, const double* c) {
+  float xc = fminf(fmaxf(x, -150.0f), 130.0f);
+  double xd = (double)xc;
+  double kd = rint(xd * kInvLn2);
+  double r = fma(kd, -kExpL1, xd);
+  r = fma(kd, -kExpL2, r);
+  double P = estrin<N>(c, r);
+  double y = fma(r, P, 1.0);
+  y = y * pow2_bits((long long)kd);
+  float o = (float)y;
+  return canon_f((x != x) ? x : o);
+}
+__device__ __forceinline__ float exp_f_u10(float x) { return exp_core_f<VEM_EXP_F_N>(x, cExpF); }
+__device__ __forceinline__ float exp_f_u35(float x) { return exp_core_f<VEM_EXP_F_U35_N>(x, cExpFU35); }
+
+template <int N>
+__device__ __forceinline__ double log_f_internal(double a, const double* c) {
+  long long eb = (long long)((bits_d(a * kFourThirds) >> 52) & 0x7ff) - 1023;
+  double m = from_bits_d(bits_d(a) - ((uint64_t)eb << 52));
+  double E = (double)eb;
+  double xn = m - 1.0;
+  double dh = m + 1.0;
+  double t0 = (double)(1.0f / (float)dh);
+  double t = fma(t0, fma(-dh, t0, 1.0), t0);
+  double s = xn * t;
+  double z = s * s;
+  double P = estrin<N>(c, z);
+  return fma(E, kLn2Hi, fma(s * z, P, fma(E, kLn2Lo, 2.0 * s)));
+}
+template <int N>
+__device__ __forceinline__ float log_core_f(float x, const double* c) {
+  bool ok = (x > 0.0f) && (x < kInfF);
+  double a = ok ? (double)x : 1.0;
+  double y = log_f_internal<N>(a, c);
+  float o = (float)y;
+  o = (x == 0.0f) ? -kInfF : o;
+  o = (x < 0.0f) ? from_bits_f(kCanonNanF) : o;
+  o = (x == kInfF) ? x : o;
+  o = (x != x) ? x : o;
+  return canon_f(o);
+}
+__device__ __forceinline__ float log_f_u10(float x) { return log_core_f<VEM_LOG_F_N>(x, cLogF); }
+__device__ __forceinline__ float log_f_u35(float x) { return log_core_f<VEM_LOG_F_U35_N>(x, cLogFU35); }
+
+__device__ __forceinline__ bool is_int_f(float y) { return (fabsf(y) < kInfF) && (truncf(y) == y); }
+__device__ __forceinline__ bool is_odd_f(float y) {
+  return is_int_f(y) && (fabsf(y) < 0x1p24f) && (truncf(y * 0.5f) * 2.0f != y);
+}
+template <int NL, int NE>
+__device__ __forceinline__ float pow_core_f(float x, float y, const double* cl, const double* ce) {
+  float ax = fabsf(x);
+  bool fin = (ax > 0.0f) && (ax < kInfF) && (fabsf(y) < kInfF);
+  double a = fin ? (double)ax : 1.0;
+  double yd = fin ? (double)y : 0.0;
+  double t = yd * log_f_internal<NL>(a, cl);
+  double tc = fmin(fmax(t, -200.0), 200.0);
+  double kd = rint(tc * kInvLn2);
+  double r = fma(kd, -kExpL1, tc);
+  r = fma(kd, -kExpL2, r);
+  double P = estrin<NE>(ce, r);
+  double R = fma(r, P, 1.0) * pow2_bits((long long)kd);
+  float Rf = (float)R;
+  bool yint = is_int_f(y), yodd = is_odd_f(y);
+  float res = (x < 0.0f && yodd) ? -Rf : Rf;
+  res = (x < 0.0f && !yint && fabsf(y) < kInfF) ? from_bits_f(kCanonNanF) : res;
+  if (x == 0.0f) {
+    if (y < 0.0f) res = yodd ? copysignf(kInfF, x) : kInfF;
+    else res = yodd ? x : 0.0f;
+  }
+  if (ax == kInfF) {
+    if (y < 0.0f) res = (yodd && x < 0.0f) ? -0.0f : 0.0f;
+    else res = (yodd && x < 0.0f) ? -kInfF : kInfF;
+  }
+  if (fabsf(y) == kInfF) {
+    if (ax == 1.0f) res = 1.0f;
+    else res = ((ax < 1.0f) == (y < 0.0f)) ? kInfF : 0.0f;
+  }
+  if (x != x || y != y) res = from_bits_f(kCanonNanF);
+  if (y == 0.0f || x == 1.0f) res = 1.0f;
+  return canon_f(res);
+}
+__device__ __forceinline__ float pow_f_u10(float x, float y) {
+  return pow_core_f<VEM_POWLOG_F_N, VEM_POWEXP_F_N>(x, y, cPowLogF, cPowExpF);
+}
+__device__ __forceinline__ float pow_f_u35(float x, float y) {
+  return pow_core_f<VEM_POWLOG_F_U35_N, VEM_POWEXP_F_U35_N>(x, y, cPowLogFU35, cPowExpFU35);
+}
+__device__ __forceinline__ float fmod_f(float x, float y) {
+  double r = fmod_core((double)x, (double)y);
+  return canon_f((float)r);
+}
+
+}  // namespace vem

@@ -1,0 +1,125 @@
+"""GPU parity: every C-ABI entry point vs the CPU oracle, BIT-EXACT.
+
+Inputs: special values (singletons / all pairs), random bit patterns
+("random bits ... reinterprets"), and the BASELINE.json
+config domains, at sizes the oracle finishes in seconds.  Comparison is on
+raw bit patterns (NaNs are canonical on both sides), reporting the first
+mismatching index.  Calls go through the C ABI (ctypes) on device buffers.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from cases import binary_cases, unary_cases
+from oracle_lib import oracle_eval, reduce_oracle
+
+pytestmark = pytest.mark.gpu
+
+from paper_2001_09258_b200 import _lib  # noqa: E402
+
+N = 1 << 16
+
+
+def _bits(a):
+    return a.view(np.uint64 if a.dtype == np.float64 else np.uint32)
+
+
+def _assert_bit_exact(name, got, exp, *inputs):
+    g, e = _bits(got), _bits(exp)
+    bad = np.nonzero(g != e)[0]
+    if bad.size:
+        i = bad[0]
+        args = ", ".join(repr(a[i]) for a in inputs)
+        raise AssertionError(f"{name}: {bad.size}/{g.size} mismatches; first at {i}: f({args}) "
+                             f"gpu={got[i]!r} ({g[i]:#x}) oracle={exp[i]!r} ({e[i]:#x})")
+
+
+def _gpu(name, *arrs):
+    import torch
+    from paper_2001_09258_b200 import api
+    ts = [torch.from_numpy(a).cuda() for a in arrs]
+    out = api.call(name, *ts)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+@pytest.mark.parametrize("name", sorted(_lib.UNARY))
+def test_unary_bit_exact(cuda, name):
+    x = unary_cases(name, N)
+    got = _gpu(name, x)
+    exp = oracle_eval(name, x)
+    _assert_bit_exact(name, got, exp, x)
+
+
+@pytest.mark.parametrize("name", sorted(_lib.BINARY))
+def test_binary_bit_exact(cuda, name):
+    x, y = binary_cases(name, N)
+    got = _gpu(name, x, y)
+    exp = oracle_eval(name, x, y)
+    _assert_bit_exact(name, got, exp, x, y)
+
+
+@pytest.mark.parametrize("name", ["sin_d_u10", "exp_f_u10", "pow_d_u10"])
+def test_unaligned_and_ragged(cuda, name):
+    """Scalar (unaligned) kernel path and ragged tails give identical bits."""
+    import torch
+    from paper_2001_09258_b200 import api
+    n = 1000 + 3
+    if name in _lib.BINARY:
+        x, y = binary_cases(name, n)
+        x, y = x[:n], y[:n]
+        tx = torch.from_numpy(np.concatenate([[0.0], x]).astype(x.dtype)).cuda()[1:]
+        ty = torch.from_numpy(np.concatenate([[0.0], y]).astype(y.dtype)).cuda()[1:]
+        got = api.call(name, tx, ty).cpu().numpy()
+        _assert_bit_exact(name, got, oracle_eval(name, x, y), x, y)
+    else:
+        x = unary_cases(name, n)[:n]
+        tx = torch.from_numpy(np.concatenate([[0.0], x]).astype(x.dtype)).cuda()[1:]
+        got = api.call(name, tx).cpu().numpy()
+        _assert_bit_exact(name, got, oracle_eval(name, x), x)
+    for m in (0, 1, 2, 3, 5, 7):
+        xs = unary_cases("sin_d_u10", 64)[:m] if name not in _lib.BINARY else None
+        if xs is not None and name == "sin_d_u10":
+            got = _gpu(name, xs) if m else np.empty(0)
+            _assert_bit_exact(name, got, oracle_eval(name, xs), xs)
+
+
+@pytest.mark.parametrize("kind,level", [("trig", 0), ("cw", 1), ("cw", 2), ("ph", 0)])
+def test_reduction_bit_exact(cuda, kind, level):
+    import torch
+    from paper_2001_09258_b200 import api, inputs as I
+    if kind == "cw" and level == 1:
+        x = I.uniform(31, N, -15, 15)
+    elif kind == "cw":
+        x = I.log_uniform(32, N, 1e-3, 1e14, signed=True)
+    else:
+        x = np.concatenate([unary_cases("sin_d_u10", N), I.log_uniform(33, N, 1e-300, 1e300, signed=True)])
+    hi, lo, q = api.trig_reduce(torch.from_numpy(x).cuda(), kind, level)
+    torch.cuda.synchronize()
+    ehi, elo, eq = reduce_oracle(kind, x, level)
+    _assert_bit_exact(f"{kind}{level}.hi", hi.cpu().numpy(), ehi, x)
+    _assert_bit_exact(f"{kind}{level}.lo", lo.cpu().numpy(), elo, x)
+    assert np.array_equal(q.cpu().numpy(), eq)
+
+
+def test_round_ta_matches_reference_rule(cuda):
+    """CUDA round() == backend.hpp:47-52 round_ta on ties and neighbours
+    (exercised through cw1 quadrants at k.5 boundaries of 2x/pi)."""
+    import torch
+    from paper_2001_09258_b200 import api
+    ks = np.arange(-9, 10, dtype=np.float64) + 0.5
+    t = np.concatenate([ks, np.nextafter(ks, np.inf), np.nextafter(ks, -np.inf)])
+    x = t / float.fromhex("0x1.45f306dc9c883p-1")
+    x = x[np.abs(x) <= 15]
+    hi, lo, q = api.trig_reduce(torch.from_numpy(x).cuda(), "cw", 1)
+    ehi, elo, eq = reduce_oracle("cw", x, 1)
+    assert np.array_equal(q.cpu().numpy(), eq)
+    _assert_bit_exact("cw1", hi.cpu().numpy(), ehi, x)
+
+
+def test_launch_counter_and_version(cuda):
+    before = _lib.launch_count()
+    _gpu("exp_d_u10", np.linspace(-1, 1, 100))
+    assert _lib.launch_count() == before + 1
+    assert b"sm_100a" in _lib.lib().vem_version()
