@@ -1,0 +1,499 @@
+#!/usr/bin/env python3
+"""vem-b200 benchmark: Gelem/s of the batched elementwise math path on B200.
+
+Contract (driver): python bench.py --gpus N --steps K --warmup W
+  N=1 directly; N>1 under torch.distributed.run (one rank per GPU, NCCL).
+Workload (default, BASELINE.json configs[1] -- the config the metric is
+quoted on): exp / log / pow x {f32, f64} x {u10, u35}, 2^28 elements each,
+inputs drawn from the config's domains.  One STEP = one pass of all 12 entry
+points over their resident 2^28-element inputs (12 x 2^28 elements).
+  value      = elements processed by all ranks / max-over-ranks step time
+  e2e        = same metric through the C ABI with HOST buffers (pinned
+               H2D + kernel + D2H inside the timed region, every step)
+  roofline   = dominant kernel (largest share of the step): algorithmic bytes
+               per launch / its CUDA-event duration vs measured HBM peak;
+               plus its FP64-pipe roofline against the measured DFMA peak
+  cpu_baseline = the CPU oracle port (oracle/, all host threads) on a bounded
+               sample; SLEEF 3.8 AVX-512 timed beside it for context
+Inputs are 2-4 GiB per array (>> 126 MB L2), so no L2 flush is needed.
+`--impl reference` times the reference CPU path (oracle port, all host
+threads) on the same workload instead (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+import zlib
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Gelements/s per function (f32/f64, u10/u35) at 1-8 B200 + roofline fraction"
+UNIT = "Gelem/s"
+
+# (entry point, config, fn, prec)
+WORKLOADS = {
+    "cfg2": [("exp_d_u10", 2), ("exp_d_u35", 2), ("log_d_u10", 2), ("log_d_u35", 2), ("pow_d_u10", 2),
+             ("pow_d_u35", 2), ("exp_f_u10", 2), ("exp_f_u35", 2), ("log_f_u10", 2), ("log_f_u35", 2),
+             ("pow_f_u10", 2), ("pow_f_u35", 2)],
+    "cfg1": [("sin_d_u10", 1), ("cos_d_u10", 1)],
+    "cfg3": [("sin_d_u10_ph", 3), ("cos_d_u10_ph", 3), ("tan_d_u10_ph", 3), ("sin_f_u10_ph", 3),
+             ("cos_f_u10_ph", 3), ("tan_f_u10_ph", 3)],
+    "cfg4": [("fmod_d", 4), ("fmod_f", 4)],
+    "cfg5": [("sin_d_u10", 5), ("cos_d_u10", 5), ("tan_d_u10", 5), ("atan_d_u10", 5), ("exp_d_u10", 5),
+             ("log_d_u10", 5), ("pow_d_u10", 5), ("fmod_d", 5)],
+}
+LOG2N = {"cfg1": 24, "cfg2": 28, "cfg3": 28, "cfg4": 26, "cfg5": 28}
+CONFIG_TEXT = {
+    "cfg1": "sin/cos f64 u10, 2^24 x U[-pi,pi] (Cody-Waite path)",
+    "cfg2": "exp/log/pow x f32/f64 x u10/u35, 2^28 elements each (BASELINE configs[1] domains)",
+    "cfg3": "sin/cos/tan u10 f64+f32, 2^28, |x| log-U[1,1e300]/[1,3e38] +-, forced Payne-Hanek",
+    "cfg4": "fmod f64+f32, 2^26 pairs, log-U[1e-300,1e300]/[1e-37,3e38] +-",
+    "cfg5": "8 fns f64 u10, log-U[1e-300,1e300] +- with 1% specials (per-rank 2^28 shard)",
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="vem", choices=["vem", "reference"])
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--only", default="", help="comma list of entry points (profiling)")
+    ap.add_argument("--log2n", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------- inputs
+def device_inputs(fn_name: str, cfg: int, n: int, dev, seed: int):
+    """Config-domain inputs generated ON the device (torch Philox): same
+    distributions as paper_2001_09258_b200.inputs (the host generator used by
+    the parity tests), without shipping 2-4 GiB from the host."""
+    import torch
+    fn, p = fn_name.split("_")[0], fn_name.split("_")[1]
+    dt = torch.float64 if p == "d" else torch.float32
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+
+    def U(a, b):
+        return (a + (b - a) * torch.rand(n, dtype=torch.float64, device=dev, generator=g))
+
+    def LU(a, b, signed=False):
+        import math
+        la, lb = math.log10(a), math.log10(b)
+        v = torch.pow(10.0, U(la, lb))
+        if signed:
+            s = torch.rand(n, device=dev, generator=g) < 0.5
+            v = torch.where(s, -v, v)
+        return v
+
+    def specials(v):
+        pick = torch.rand(n, device=dev, generator=g) < 0.01
+        which = torch.randint(0, 9, (n,), device=dev, generator=g)
+        sp = torch.tensor([0.0, -0.0, float("inf"), float("-inf"), float("nan"), 5e-324, 1e-310,
+                           1.7976931348623157e308, -1.7976931348623157e308], dtype=torch.float64, device=dev)
+        return torch.where(pick, sp[which], v)
+
+    if cfg == 1:
+        xs = [U(-3.141592653589793, 3.141592653589793)]
+    elif cfg == 2:
+        if p == "d":
+            xs = {"exp": lambda: [U(-700, 700)], "log": lambda: [LU(1e-300, 1e300)],
+                  "pow": lambda: [LU(1e-10, 1e10), U(-30, 30)]}[fn]()
+        else:
+            xs = {"exp": lambda: [U(-87, 88)], "log": lambda: [LU(1e-37, 3e38)],
+                  "pow": lambda: [LU(1e-3, 1e3), U(-10, 10)]}[fn]()
+    elif cfg == 3:
+        xs = [LU(1.0, 1e300 if p == "d" else 3e38, signed=True)]
+    elif cfg == 4:
+        lo, hi = (1e-300, 1e300) if p == "d" else (1e-37, 3e38)
+        xs = [LU(lo, hi, True), LU(lo, hi, True)]
+    else:
+        x = specials(LU(1e-300, 1e300, True))
+        if fn == "pow":
+            xs = [x, U(-30, 30)]
+        elif fn == "fmod":
+            xs = [x, specials(LU(1e-300, 1e300, True))]
+        else:
+            xs = [x]
+    if dt == torch.float32:
+        xs = [torch.clamp(v, -3.4028234663852886e38, 3.4028234663852886e38).to(dt) for v in xs]
+    return [v.to(dt).contiguous() for v in xs]
+
+
+# --------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-f", self.path], stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        if self.proc is None:
+            return out
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 8:
+                    rows.append(parts)
+            os.unlink(self.path)
+        except Exception:
+            pass
+        if not rows:
+            return out
+        sm = sorted(float(r[0]) for r in rows if r[0].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            for nm, v in zip(names, r[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        out["sm_mhz"] = sm[len(sm) // 2] if sm else None
+        try:
+            out["sm_max_mhz"] = float(rows[0][1])
+        except Exception:
+            pass
+        out["reasons"] = sorted(reasons)
+        out["samples"] = len(rows)
+        return out
+
+
+# --------------------------------------------------------------- CPU legs
+def cpu_oracle_rate(work, sample_log2: int, threads: int):
+    """Oracle port (oracle/vem_oracle.c, OpenMP on `threads` host threads) over a
+    bounded host sample of every entry point; returns (Gelem/s, seconds, n)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import oracle_eval
+    from paper_2001_09258_b200 import inputs as I
+    os.environ["OMP_NUM_THREADS"] = str(threads)
+    n = 1 << sample_log2
+    total_t = 0.0
+    total_n = 0
+    per = {}
+    for name, cfg in work:
+        fn, p = name.split("_")[0], name.split("_")[1]
+        arrs = I.config_inputs(cfg, fn, p, n)
+        oracle_eval(name, *[a[:4096] for a in arrs])  # warm (threads, pages)
+        t0 = time.perf_counter()
+        oracle_eval(name, *arrs)
+        dt = time.perf_counter() - t0
+        per[name] = round(n / dt / 1e9, 4)
+        total_t += dt
+        total_n += n
+    return total_n / total_t / 1e9, total_t, total_n, per
+
+
+def cpu_sleef_rate(work, sample_log2: int, threads: int):
+    """Upstream SLEEF 3.8 AVX-512 (torch's libtorch_cpu.so) on the same sample."""
+    import ctypes
+    import numpy as np
+    path = os.path.join(ROOT, "oracle", "_build", "libvem_sleef.so")
+    if not os.path.exists(path):
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")], check=False)
+    if not os.path.exists(path):
+        return None
+    L = ctypes.CDLL(path)
+    L.sleef_run.restype = ctypes.c_double
+    L.sleef_run.argtypes = [ctypes.c_char_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                            ctypes.c_int]
+    from paper_2001_09258_b200 import inputs as I
+    n = 1 << sample_log2
+    tt = 0.0
+    per = {}
+    for name, cfg in work:
+        fn, p = name.split("_")[0], name.split("_")[1]
+        arrs = I.config_inputs(cfg, fn, p, n)
+        out = np.empty_like(arrs[0])
+        y = arrs[1].ctypes.data if len(arrs) > 1 else None
+        best = None
+        for _ in range(3):
+            t = L.sleef_run(name.encode(), arrs[0].ctypes.data, y, out.ctypes.data, n, threads)
+            best = t if best is None or t < best else best
+        per[name] = round(n / best / 1e9, 4)
+        tt += best
+    return {"value": round(len(work) * n / tt / 1e9, 4), "unit": UNIT, "cores": threads,
+            "kind": "sleef-3.8-avx512", "per_function": per,
+            "note": "SLEEF has no u35 exp/pow: those rows time the u10 entry"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference CPU path (oracle port; the reference tree
+    has no function kernels) on all host threads."""
+    if rank != 0:
+        return
+    work = WORKLOADS[args.workload]
+    if args.only:
+        keep = set(args.only.split(","))
+        work = [w for w in work if w[0] in keep]
+    threads = os.cpu_count() or 1
+    lg = 22
+    for _ in range(args.warmup):
+        cpu_oracle_rate(work[:1], 16, threads)
+    vals = []
+    t_all = 0.0
+    per = {}
+    for _ in range(args.steps):
+        v, t, n, per = cpu_oracle_rate(work, lg, threads)
+        vals.append(v)
+        t_all += t
+    value = sum(vals) / len(vals)
+    ms = t_all / max(1, args.steps) * 1e3
+    line = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64/f32", "data": "synthetic",
+            "config": {"workload": args.workload, "text": CONFIG_TEXT[args.workload],
+                       "sample": f"2^{lg} elements per entry point per step (host arrays)"},
+            "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": f"{len(work)} entry points x 2^{lg} elements, oracle/vem_oracle.c "
+                                       f"(OpenMP, {threads} threads)", "per_function": per},
+            "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------- GPU arm
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2001_09258_b200 import _lib, api, build
+
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if rank == 0:
+        build.build()
+    if world > 1:
+        dist.barrier()
+    _lib.lib()
+
+    work = WORKLOADS[args.workload]
+    if args.only:
+        keep = set(args.only.split(","))
+        work = [w for w in work if w[0] in keep]
+    n = 1 << (args.log2n or LOG2N[args.workload])
+
+    # resident inputs (u10/u35 of one function share inputs)
+    cache = {}
+    bufs = []
+    for name, cfg in work:
+        base = name.replace("_u35", "_u10") if "_u35" in name else name
+        key = (base.split("_")[0], base.split("_")[1], cfg)
+        if key not in cache:
+            cache[key] = device_inputs(name, cfg, n, dev, seed=zlib.crc32(repr(key).encode()) + 7919 * rank)
+        bufs.append(cache[key])
+    outs = {}
+    for ins in bufs:
+        outs.setdefault(ins[0].dtype, torch.empty_like(ins[0]))
+    stream = torch.cuda.current_stream()
+
+    def step(evs=None):
+        for i, (name, _) in enumerate(work):
+            ins = bufs[i]
+            if evs is not None:
+                evs[i][0].record(stream)
+            api.call(name, *ins, out=outs[ins[0].dtype])
+            if evs is not None:
+                evs[i][1].record(stream)
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+
+    # per-kernel event pairs for every timed step
+    evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in work]
+           for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = _lib.launch_count()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for s in range(args.steps):
+        step(evs[s])
+    t1.record(stream)
+    torch.cuda.synchronize()
+    launches = _lib.launch_count() - launches0
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms_total = t0.elapsed_time(t1)
+    per_kernel_ms = [sum(evs[s][i][0].elapsed_time(evs[s][i][1]) for s in range(args.steps)) / args.steps
+                     for i in range(len(work))]
+    if world > 1:
+        t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    elems_step = len(work) * n * world
+    value = elems_step / (ms_step * 1e-3) / 1e9
+
+    # ---------------- e2e: C ABI with HOST buffers (pinned), copies timed
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_leg(work, bufs, outs, n, args, dev, stream, world)
+
+    # ---------------- roofline of the dominant kernel
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    hbm_src = "measured (MEASURED_PEAKS.json)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
+    dom = max(range(len(work)), key=lambda i: per_kernel_ms[i])
+    dname = work[dom][0]
+    esz = bufs[dom][0].element_size()
+    bytes_per_launch = n * esz * (len(bufs[dom]) + 1)
+    ach = bytes_per_launch / (per_kernel_ms[dom] * 1e-3) / 1e9
+    fp64_peak = _lib.probe_peak("fp64")
+    traffic = None
+    fp64_per_elem = None
+    prof = os.path.join(ROOT, "profiles", "kernel_metrics.json")
+    if os.path.exists(prof):
+        try:
+            km = json.load(open(prof)).get(dname, {})
+            if km.get("dram_bytes_per_elem") is not None:
+                traffic = km["dram_bytes_per_elem"] * n
+            fp64_per_elem = km.get("fp64_inst_per_elem")
+        except Exception:
+            pass
+    pipe = None
+    if fp64_per_elem:
+        ach_ops = fp64_per_elem * n / (per_kernel_ms[dom] * 1e-3) / 1e9
+        pipe = {"pipe": "fp64", "achieved": round(ach_ops, 1), "peak": round(fp64_peak, 1), "unit": "Ginst/s",
+                "frac": round(ach_ops / fp64_peak, 4), "fp64_inst_per_elem": fp64_per_elem,
+                "peak_source": "measured (vem_probe_peak DFMA microbenchmark, this run)"}
+    roofline = {"bound": "hbm", "kernel": dname, "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(ach / hbm_peak, 4), "traffic": traffic, "bytes_per_launch": bytes_per_launch,
+                "bytes_per_elem": esz * (len(bufs[dom]) + 1), "elems_per_launch": n,
+                "ms_per_launch": round(per_kernel_ms[dom], 4), "peak_source": hbm_src,
+                "fp64_pipe": pipe, "fp64_dfma_peak_ginst_s": round(fp64_peak, 1)}
+
+    per_function = {}
+    for i, (name, cfg) in enumerate(work):
+        esz_i = bufs[i][0].element_size() * (len(bufs[i]) + 1)
+        g = n / (per_kernel_ms[i] * 1e-3) / 1e9
+        per_function[name] = {"gelem_s": round(g, 2), "ms": round(per_kernel_ms[i], 4),
+                              "hbm_frac": round(g * esz_i / hbm_peak, 4)}
+
+    cpu = None
+    sleef = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        v, t, cn, per = cpu_oracle_rate(work, 23, threads)
+        cpu = {"value": round(v, 4), "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"{len(work)} entry points x 2^23 elements of the same config domains "
+                         f"({t:.1f} s of CPU work), oracle/vem_oracle.c, OpenMP {threads} threads",
+               "per_function": per}
+        try:
+            sleef = cpu_sleef_rate(work, 23, threads)
+        except Exception as ex:  # context only
+            sleef = {"error": str(ex)}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64/f32 (per entry point)",
+                "data": "synthetic (config-domain inputs generated on device, seeded)",
+                "config": {"workload": args.workload, "text": CONFIG_TEXT[args.workload],
+                           "elements_per_entry_point_per_rank": n, "entry_points": [w[0] for w in work],
+                           "l2": "inputs >= 1 GiB per array (> 126 MB L2), no flush needed",
+                           "parallelism": f"data-parallel shards x{world} (no collective on the data path)"},
+                "gpu_launches": int(launches), "clocks": clk, "roofline": roofline,
+                "per_function": per_function, "e2e": e2e, "cpu_baseline": cpu, "sleef_cpu": sleef}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def e2e_leg(work, bufs, outs, n, args, dev, stream, world):
+    """Same step through the C ABI with HOST buffers: every step copies that
+    step's inputs host->device from pinned memory, runs the kernel, and reads
+    the result back device->host; chunked over two streams so copies in each
+    direction overlap the kernels (vem's host pipeline)."""
+    import torch
+    from paper_2001_09258_b200 import api
+    chunk = 1 << 24
+    host_in = []
+    host_out = {}
+    for ins in bufs:
+        host_in.append([t.to("cpu").pin_memory() for t in ins])
+    for ins in bufs:
+        host_out.setdefault(ins[0].dtype, torch.empty(n, dtype=ins[0].dtype).pin_memory())
+    streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+    h2d = sum(t.numel() * t.element_size() for ins in bufs for t in ins)
+    d2h = sum(ins[0].numel() * ins[0].element_size() for ins in bufs)
+
+    def one_step():
+        for i, (name, _) in enumerate(work):
+            hin = host_in[i]
+            dins = bufs[i]
+            dout = outs[dins[0].dtype]
+            hout = host_out[dins[0].dtype]
+            for j, c0 in enumerate(range(0, n, chunk)):
+                c1 = min(n, c0 + chunk)
+                s = streams[j % 2]  # a given range always uses the same stream
+                with torch.cuda.stream(s):
+                    for hd, dd_ in zip(hin, dins):
+                        dd_[c0:c1].copy_(hd[c0:c1], non_blocking=True)
+                    api.call(name, *[d[c0:c1] for d in dins], out=dout[c0:c1])
+                    hout[c0:c1].copy_(dout[c0:c1], non_blocking=True)
+
+    one_step()
+    torch.cuda.synchronize()
+    steps = max(1, min(args.steps, 3))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one_step()
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / steps
+    return {"value": round(len(work) * n * world / dt / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": round(dt * 1e3, 2), "steps": steps,
+            "path": "pinned host -> H2D (chunked 2^24, 2 streams) -> vem C ABI -> D2H, host wall clock"}
+
+
+if __name__ == "__main__":
+    main()

@@ -97,6 +97,10 @@ uint64_t vem_launch_count(void);
 /* Library version string. */
 const char* vem_version(void);
 
+/* FP64 (kind 0) / FP32 (kind 1) FMA pipe throughput microbenchmark on the
+ * current device: independent FMA chains, no memory traffic; writes Gop/s. */
+int vem_probe_peak(int kind, int iters, double* gops_out);
+
 /* ---- multi-GPU host driver ------------------- */
 /* Evaluates function `name` (e.g. "sin_d_u10") over HOST arrays sharded
  * contiguously across `ngpu` devices: one host thread per device, its own

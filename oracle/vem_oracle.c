@@ -909,3 +909,8 @@ double vo_dbg_exp_dd(double th, double tl) {
   dd_t t = {th, tl};
   return exp_dd(t, C_POWEXP_D, VEM_POWEXP_D_N, VEM_POWEXP_D_C0L, VEM_POWEXP_D_C1L);
 }
+
+/* every f32 trig lane takes the f32 Payne-Hanek path: forced variants alias */
+void vo_sin_f_u10_ph_arr(const float* x, float* y, size_t n) { vo_sin_f_u10_arr(x, y, n); }
+void vo_cos_f_u10_ph_arr(const float* x, float* y, size_t n) { vo_cos_f_u10_arr(x, y, n); }
+void vo_tan_f_u10_ph_arr(const float* x, float* y, size_t n) { vo_tan_f_u10_arr(x, y, n); }

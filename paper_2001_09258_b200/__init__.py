@@ -6,11 +6,5 @@ include/vem.h; this package is the thin host mirror (ctypes) over it.
 from . import _lib  # noqa: F401
 from ._lib import ALL, BINARY, UNARY, VemError, launch_count  # noqa: F401
 
-__all__ = ["ALL", "BINARY", "UNARY", "VemError", "launch_count", "api"]
-
-
-def __getattr__(name):
-    if name == "api":
-        from . import api
-        return api
-    raise AttributeError(name)
+__all__ = ["ALL", "BINARY", "UNARY", "VemError", "launch_count"]
+# the torch-facing mirror lives in paper_2001_09258_b200.api (imports torch)

@@ -67,6 +67,8 @@ def lib() -> ctypes.CDLL:
     L.vem_run_sharded.argtypes = [ctypes.c_char_p, _P, _P, _P, _N, ctypes.c_int,
                                   ctypes.POINTER(ctypes.c_double)]
     L.vem_run_sharded.restype = ctypes.c_int
+    L.vem_probe_peak.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
+    L.vem_probe_peak.restype = ctypes.c_int
     _lib = L
     return L
 
@@ -78,6 +80,13 @@ def check(rc: int, what: str):
 
 def launch_count() -> int:
     return int(lib().vem_launch_count())
+
+
+def probe_peak(kind: str = "fp64", iters: int = 4096) -> float:
+    """Measured FMA throughput in Gop/s (one FMA = one op) on the current device."""
+    v = ctypes.c_double(0.0)
+    check(lib().vem_probe_peak(0 if kind == "fp64" else 1, iters, ctypes.byref(v)), "vem_probe_peak")
+    return v.value
 
 
 def ph_table_bytes() -> bytes:

@@ -17,7 +17,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libvem.so")
-SOURCES = ["vem_kernels.cu", "vem_host.cu"]
+SOURCES = ["vem_kernels.cu", "vem_host.cu", "vem_probe.cu"]
 HEADERS = ["vem_math.cuh", "vem_coeffs.h", "vem_ph_tables.h", "../../include/vem.h"]
 
 NVCC_FLAGS = [
