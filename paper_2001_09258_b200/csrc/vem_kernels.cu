@@ -16,6 +16,7 @@
 
 #include "../../include/vem.h"
 #include "vem_math.cuh"
+#include "vem_stream.cuh"
 
 namespace vem {
 
@@ -133,6 +134,78 @@ __global__ void __launch_bounds__(kThreads) k_binary(const T* __restrict__ x, co
   }
 }
 
+// ------------------------------------------------- TMA-staged streaming
+// NIN inputs (1 or 2); tiles of kThreads*VPT 16-byte vectors per input;
+// STAGES tiles in flight per CTA (see vem_stream.cuh).  Elements past the
+// last full tile are finished by a grid-stride scalar loop in the same launch.
+template <class Op, class T, int NIN, int TABLE, int VPT, int STAGES>
+__global__ void __launch_bounds__(kThreads) k_stream(const T* __restrict__ a, const T* __restrict__ b,
+                                                     T* __restrict__ out, size_t n) {
+  using V = typename Vec16<T>::type;
+  constexpr int W = Vec16<T>::n;
+  constexpr int TILE_V = kThreads * VPT;
+  constexpr uint32_t TILE_BYTES = TILE_V * 16;
+  constexpr int TILE_E = TILE_V * W;
+  extern __shared__ __align__(128) unsigned char dsm[];
+  __shared__ uint64_t bars[STAGES];
+  __shared__ __align__(16) double stab[TableSize<TABLE>::n];
+  V* buf = reinterpret_cast<V*>(dsm);
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; s++) tma::mbar_init(&bars[s], 1);
+    tma::fence_barrier_init();
+  }
+  const double* tab = stage_table<TABLE>(stab);  // includes __syncthreads()
+  if constexpr (TABLE == kNoTable) __syncthreads();
+  Op op;
+  const size_t ntiles = n / TILE_E;
+  const size_t G = gridDim.x;
+  const size_t my = ntiles > blockIdx.x ? (ntiles - blockIdx.x + G - 1) / G : 0;
+  uint64_t pol = 0;
+  auto issue = [&](int s, size_t tile) {
+    tma::mbar_expect_tx(&bars[s], NIN * TILE_BYTES);
+    tma::bulk_g2s(buf + (size_t)(s * NIN) * TILE_V, reinterpret_cast<const V*>(a) + tile * TILE_V, TILE_BYTES,
+                  &bars[s], pol);
+    if constexpr (NIN == 2)
+      tma::bulk_g2s(buf + (size_t)(s * NIN + 1) * TILE_V, reinterpret_cast<const V*>(b) + tile * TILE_V,
+                    TILE_BYTES, &bars[s], pol);
+  };
+  if (tid == 0) {
+    pol = tma::policy_evict_first();
+    for (int s = 0; s < STAGES && (size_t)s < my; s++) issue(s, blockIdx.x + (size_t)s * G);
+  }
+  for (size_t j = 0; j < my; j++) {
+    const int s = (int)(j % STAGES);
+    tma::mbar_wait(&bars[s], (uint32_t)((j / STAGES) & 1));
+    V va[VPT], vb[VPT];
+#pragma unroll
+    for (int v = 0; v < VPT; v++) {
+      va[v] = buf[(size_t)(s * NIN) * TILE_V + v * kThreads + tid];
+      if constexpr (NIN == 2) vb[v] = buf[(size_t)(s * NIN + 1) * TILE_V + v * kThreads + tid];
+    }
+    __syncthreads();  // stage s fully consumed -> refill it
+    if (tid == 0 && j + STAGES < my) issue(s, blockIdx.x + (j + STAGES) * G);
+    V* ov = reinterpret_cast<V*>(out) + (blockIdx.x + j * G) * TILE_V;
+#pragma unroll
+    for (int v = 0; v < VPT; v++) {
+      V o;
+#pragma unroll
+      for (int k = 0; k < W; k++) {
+        if constexpr (NIN == 2) vget(o, k) = op(vget(va[v], k), vget(vb[v], k));
+        else vget(o, k) = op(vget(va[v], k), tab);
+      }
+      __stcs(ov + v * kThreads + tid, o);
+    }
+  }
+  // remainder (< one tile)
+  const size_t done = ntiles * TILE_E;
+  for (size_t i = done + (size_t)blockIdx.x * kThreads + tid; i < n; i += G * kThreads) {
+    if constexpr (NIN == 2) out[i] = op(a[i], b[i]);
+    else out[i] = op(a[i], tab);
+  }
+}
+
 // ------------------------------------------------------------- functors
 #define VEM_UNARY_OP(NAME, T, EXPR)                                                   \
   struct NAME {                                                                       \
@@ -236,6 +309,31 @@ static int launch_binary(const T* x, const T* y2, T* out, size_t n, vem_stream_t
   return (int)cudaGetLastError();
 }
 
+template <class Op, class T, int NIN, int TABLE, int VPT, int STAGES>
+static int launch_stream(const T* a, const T* b, T* out, size_t n, vem_stream_t s) {
+  if (n == 0) return 0;
+  if (!(aligned16(a) && aligned16(out) && (NIN == 1 || aligned16(b)))) {
+    if constexpr (NIN == 2) return launch_binary<Op, T, 1>(a, b, out, n, s);
+    else return launch_unary<Op, T, TABLE, 1>(a, out, n, s);
+  }
+  auto k = k_stream<Op, T, NIN, TABLE, VPT, STAGES>;
+  constexpr int smem = STAGES * NIN * kThreads * VPT * 16;
+  static const int occ = [k] {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int bpm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpm, k, kThreads, smem) != cudaSuccess || bpm < 1) bpm = 1;
+    return bpm;
+  }();
+  constexpr size_t tile_e = (size_t)kThreads * VPT * Vec16<T>::n;
+  size_t tiles = n / tile_e;
+  size_t cap = (size_t)num_sms() * occ;
+  size_t g = tiles < cap ? tiles : cap;
+  if (g < 1) g = 1;
+  k<<<(int)g, kThreads, smem, (cudaStream_t)s>>>(a, b, out, n);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return (int)cudaGetLastError();
+}
+
 // ---------------------------------------------------- reduction kernels
 template <int MODE>  // 0 trig_reduce, 1 cw1, 2 cw2, 3 ph
 __global__ void __launch_bounds__(kThreads) k_reduce_d(const double* __restrict__ x, double* hi, double* lo,
@@ -288,35 +386,35 @@ using namespace vem;
 // vectors in flight, FP64-pipe-bound ones 2 (register pressure).
 extern "C" {
 
-int vem_sin_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return launch_unary<OpSinD, double, kTableD, 2>(x, y, n, s); }
-int vem_cos_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return launch_unary<OpCosD, double, kTableD, 2>(x, y, n, s); }
-int vem_tan_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return launch_unary<OpTanD, double, kTableD, 2>(x, y, n, s); }
-int vem_sin_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return launch_unary<OpSinDPh, double, kTableD, 1>(x, y, n, s); }
-int vem_cos_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return launch_unary<OpCosDPh, double, kTableD, 1>(x, y, n, s); }
-int vem_tan_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return launch_unary<OpTanDPh, double, kTableD, 1>(x, y, n, s); }
-int vem_atan_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return launch_unary<OpAtanD, double, kNoTable, 2>(x, y, n, s); }
-int vem_exp_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return launch_unary<OpExpD, double, kNoTable, 4>(x, y, n, s); }
-int vem_exp_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return launch_unary<OpExpDU35, double, kNoTable, 4>(x, y, n, s); }
-int vem_log_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return launch_unary<OpLogD, double, kNoTable, 2>(x, y, n, s); }
-int vem_log_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return launch_unary<OpLogDU35, double, kNoTable, 2>(x, y, n, s); }
-int vem_pow_d_u10(const double* x, const double* y2, double* o, size_t n, vem_stream_t s) { return launch_binary<OpPowD, double, 1>(x, y2, o, n, s); }
-int vem_pow_d_u35(const double* x, const double* y2, double* o, size_t n, vem_stream_t s) { return launch_binary<OpPowDU35, double, 1>(x, y2, o, n, s); }
-int vem_fmod_d(const double* x, const double* y2, double* o, size_t n, vem_stream_t s) { return launch_binary<OpFmodD, double, 1>(x, y2, o, n, s); }
+int vem_sin_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpSinD, double, 1, kTableD, 2, 4>(x, nullptr, y, n, s); }
+int vem_cos_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpCosD, double, 1, kTableD, 2, 4>(x, nullptr, y, n, s); }
+int vem_tan_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpTanD, double, 1, kTableD, 2, 4>(x, nullptr, y, n, s); }
+int vem_sin_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpSinDPh, double, 1, kTableD, 1, 4>(x, nullptr, y, n, s); }
+int vem_cos_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpCosDPh, double, 1, kTableD, 1, 4>(x, nullptr, y, n, s); }
+int vem_tan_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpTanDPh, double, 1, kTableD, 1, 4>(x, nullptr, y, n, s); }
+int vem_atan_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpAtanD, double, 1, kNoTable, 2, 4>(x, nullptr, y, n, s); }
+int vem_exp_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpExpD, double, 1, kNoTable, 2, 4>(x, nullptr, y, n, s); }
+int vem_exp_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpExpDU35, double, 1, kNoTable, 2, 4>(x, nullptr, y, n, s); }
+int vem_log_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpLogD, double, 1, kNoTable, 2, 4>(x, nullptr, y, n, s); }
+int vem_log_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpLogDU35, double, 1, kNoTable, 2, 4>(x, nullptr, y, n, s); }
+int vem_pow_d_u10(const double* x, const double* y2, double* o, size_t n, vem_stream_t s) { return launch_stream<OpPowD, double, 2, kNoTable, 1, 4>(x, y2, o, n, s); }
+int vem_pow_d_u35(const double* x, const double* y2, double* o, size_t n, vem_stream_t s) { return launch_stream<OpPowDU35, double, 2, kNoTable, 1, 4>(x, y2, o, n, s); }
+int vem_fmod_d(const double* x, const double* y2, double* o, size_t n, vem_stream_t s) { return launch_stream<OpFmodD, double, 2, kNoTable, 1, 4>(x, y2, o, n, s); }
 
-int vem_sin_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return launch_unary<OpSinF, float, kTableF, 1>(x, y, n, s); }
-int vem_cos_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return launch_unary<OpCosF, float, kTableF, 1>(x, y, n, s); }
-int vem_tan_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return launch_unary<OpTanF, float, kTableF, 1>(x, y, n, s); }
+int vem_sin_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return launch_stream<OpSinF, float, 1, kTableF, 1, 4>(x, nullptr, y, n, s); }
+int vem_cos_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return launch_stream<OpCosF, float, 1, kTableF, 1, 4>(x, nullptr, y, n, s); }
+int vem_tan_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return launch_stream<OpTanF, float, 1, kTableF, 1, 4>(x, nullptr, y, n, s); }
 // every f32 trig lane takes the f32 Payne-Hanek path: the forced variants are the same kernels
 int vem_sin_f_u10_ph(const float* x, float* y, size_t n, vem_stream_t s) { return vem_sin_f_u10(x, y, n, s); }
 int vem_cos_f_u10_ph(const float* x, float* y, size_t n, vem_stream_t s) { return vem_cos_f_u10(x, y, n, s); }
 int vem_tan_f_u10_ph(const float* x, float* y, size_t n, vem_stream_t s) { return vem_tan_f_u10(x, y, n, s); }
-int vem_exp_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return launch_unary<OpExpF, float, kNoTable, 2>(x, y, n, s); }
-int vem_exp_f_u35(const float* x, float* y, size_t n, vem_stream_t s) { return launch_unary<OpExpFU35, float, kNoTable, 2>(x, y, n, s); }
-int vem_log_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return launch_unary<OpLogF, float, kNoTable, 2>(x, y, n, s); }
-int vem_log_f_u35(const float* x, float* y, size_t n, vem_stream_t s) { return launch_unary<OpLogFU35, float, kNoTable, 2>(x, y, n, s); }
-int vem_pow_f_u10(const float* x, const float* y2, float* o, size_t n, vem_stream_t s) { return launch_binary<OpPowF, float, 1>(x, y2, o, n, s); }
-int vem_pow_f_u35(const float* x, const float* y2, float* o, size_t n, vem_stream_t s) { return launch_binary<OpPowFU35, float, 1>(x, y2, o, n, s); }
-int vem_fmod_f(const float* x, const float* y2, float* o, size_t n, vem_stream_t s) { return launch_binary<OpFmodF, float, 1>(x, y2, o, n, s); }
+int vem_exp_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return launch_stream<OpExpF, float, 1, kNoTable, 2, 4>(x, nullptr, y, n, s); }
+int vem_exp_f_u35(const float* x, float* y, size_t n, vem_stream_t s) { return launch_stream<OpExpFU35, float, 1, kNoTable, 2, 4>(x, nullptr, y, n, s); }
+int vem_log_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return launch_stream<OpLogF, float, 1, kNoTable, 1, 4>(x, nullptr, y, n, s); }
+int vem_log_f_u35(const float* x, float* y, size_t n, vem_stream_t s) { return launch_stream<OpLogFU35, float, 1, kNoTable, 1, 4>(x, nullptr, y, n, s); }
+int vem_pow_f_u10(const float* x, const float* y2, float* o, size_t n, vem_stream_t s) { return launch_stream<OpPowF, float, 2, kNoTable, 1, 4>(x, y2, o, n, s); }
+int vem_pow_f_u35(const float* x, const float* y2, float* o, size_t n, vem_stream_t s) { return launch_stream<OpPowFU35, float, 2, kNoTable, 1, 4>(x, y2, o, n, s); }
+int vem_fmod_f(const float* x, const float* y2, float* o, size_t n, vem_stream_t s) { return launch_stream<OpFmodF, float, 2, kNoTable, 1, 4>(x, y2, o, n, s); }
 
 int vem_trig_reduce_d(const double* x, double* hi, double* lo, int* q, size_t n, vem_stream_t s) {
   return launch_reduce_d<0>(x, hi, lo, q, n, s);

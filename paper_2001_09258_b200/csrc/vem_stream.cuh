@@ -1,0 +1,69 @@
+// TMA-staged streaming for the elementwise kernels (sm_100a).
+//
+// Every CTA is persistent and walks tiles t = blockIdx.x + j*gridDim.x of the
+// input arrays.  One elected thread issues bulk copies (cp.async.bulk
+// global->shared, completion counted on an mbarrier by transaction bytes)
+// for up to STAGES tiles ahead; all threads wait on the stage's mbarrier
+// phase, pull their elements out of shared memory (LDS.128, conflict-free),
+// release the stage with a CTA barrier, and then compute and store
+// (st.global.cs: outputs are written once).  Loads therefore stay in flight
+// while the FP64 pipe works, without spending registers on prefetch and
+// without per-thread 64-bit address arithmetic on the load side.
+#pragma once
+
+#include <cstdint>
+
+namespace vem {
+namespace tma {
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t a = smem_addr(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra.uni DONE;\n"
+      "bra.uni LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(a),
+      "r"(phase)
+      : "memory");
+}
+
+// bulk copy global -> shared::cta (via the cluster window of this CTA),
+// completion reported to `bar` as transaction bytes; evict-first L2 policy.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
+      "%4;" ::"r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+}  // namespace tma
+}  // namespace vem
