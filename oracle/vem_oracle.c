@@ -29,6 +29,7 @@
 
 #include "vem_coeffs.h"
 #include "vem_ph_tables.h"
+#include "vem_log_tables.h"
 
 typedef struct { double hi, lo; } dd_t;
 
@@ -70,6 +71,8 @@ static inline float canon_f(float y) { return (y != y) ? from_bits_f(CANON_NAN_F
 
 static const double PH_D[4 * VEM_PH_D_ENTRIES] = {VEM_PH_D_INIT};
 static const double PH_F[3 * VEM_PH_F_ENTRIES] = {VEM_PH_F_INIT};
+static const double LOGT[4 * 256] = {VEM_LOGT_INIT};
+static const double EXPT[2 * 128] = {VEM_EXPT_INIT};
 
 /* ------------------------------------------- primitives (backend.hpp) */
 /* backend.hpp:47-52 round_ta: nearest integer, ties away from zero */
@@ -295,11 +298,6 @@ static const double C_TAN_D[] = VEM_TAN_D_ARR;
 static const double C_ATAN_D[] = VEM_ATAN_D_ARR;
 static const double C_EXP_D[] = VEM_EXP_D_ARR;
 static const double C_EXP_D_U35[] = VEM_EXP_D_U35_ARR;
-static const double C_LOG_D[] = VEM_LOG_D_ARR;
-static const double C_POWLOG_D[] = VEM_POWLOG_D_ARR;
-static const double C_POWEXP_D[] = VEM_POWEXP_D_ARR;
-static const double C_POWLOG_D_U35[] = VEM_POWLOG_D_U35_ARR;
-static const double C_POWEXP_D_U35[] = VEM_POWEXP_D_U35_ARR;
 
 /* sin/cos core on the reduced argument r = rh + rl, |r| <= 0.80, using a
  * per-lane SELECTED polynomial (sin form for even effective quadrant, cos
@@ -417,17 +415,18 @@ double vo_atan_d_u10(double x) {
 
 /* exp: k = rint(x/ln2), r = x - k*L1 - k*L2
  * (constants.hpp:44-46), 13-term polynomial (u10) / 12-term (u35), no DD
- * (SPEC.md:406), ldexp2 reconstruction, saturation (constants.hpp:53-54). */
-static double exp_core_d(double x, const double* c, int n, int u10) {
-  int ok = (x >= K_EXP_UNF) && (x <= K_EXP_OVF);
-  double xs = ok ? x : 0.0;
+ * (SPEC.md:406).  Fast path |x| < 708: the result is normal, so 2^k is applied
+ * by adding k to the exponent field (== ldexp2, exact).  Slow path: ldexp2
+ * (backend.hpp:133-138, single rounding into subnormals) and saturation
+ * (constants.hpp:53-54); NaN in, canonical NaN out. */
+#define EXP_FAST_HI 0x40862000u /* |x| < 708 */
+static inline double exp_poly_d(double xs, const double* c, int n, int u10, double* kd_out) {
   double kd = rint(xs * K_INV_LN2);
   double r1 = fma(kd, -K_EXP_L1, xs);
   double r = fma(kd, -K_EXP_L2, r1);
   double P = estrin(c, n, r);
   double y;
   if (u10) {
-    /* r = rh + rl exactly-ish; exp(r) = (1 + rh) + (rl + rh^2 P) */
     double rl = fma(-kd, K_EXP_L2, r1 - r);
     double s = 1.0 + r;
     double se = (1.0 - s) + r;
@@ -435,153 +434,195 @@ static double exp_core_d(double x, const double* c, int n, int u10) {
   } else {
     y = 1.0 + fma(r * r, P, r);
   }
+  *kd_out = kd;
+  return y;
+}
+static double exp_core_d(double x, const double* c, int n, int u10) {
+  uint32_t hx = (uint32_t)(bits_d(x) >> 32) & 0x7fffffffu;
+  double kd;
+  if (hx < EXP_FAST_HI) {
+    double y = exp_poly_d(x, c, n, u10, &kd);
+    return from_bits_d(bits_d(y) + ((uint64_t)(int64_t)kd << 52));
+  }
+  int ok = (x >= K_EXP_UNF) && (x <= K_EXP_OVF);
+  double xs = ok ? x : 0.0;
+  double y = exp_poly_d(xs, c, n, u10, &kd);
   y = ldexp2(y, (int64_t)kd);
   y = (x > K_EXP_OVF) ? INFINITY : y;
   y = (x < K_EXP_UNF) ? 0.0 : y;
-  y = (x != x) ? x : y;
-  return canon_d(y);
+  y = (x != x) ? from_bits_d(CANON_NAN_D) : y;
+  return y;
 }
 double vo_exp_d_u10(double x) { return exp_core_d(x, C_EXP_D, VEM_EXP_D_N, 1); }
 double vo_exp_d_u35(double x) { return exp_core_d(x, C_EXP_D_U35, VEM_EXP_D_U35_N, 0); }
 
-/* log decomposition: denormals x 2^64, e = ilogb(RN(4a/3)),
- * m = a*2^-e in [0.75, 1.5). */
-static inline void log_split(double a, double* m, double* E) {
-  int sub = a < 0x1p-1022;
-  double as = sub ? a * 0x1p64 : a;
-  int64_t eb = (int64_t)((bits_d(as * K_FOUR_THIRDS) >> 52) & 0x7ff) - 1023;
-  *m = from_bits_d(bits_d(as) - ((uint64_t)eb << 52));
-  *E = (double)(eb - (sub ? 64 : 0));
+/* ---- table-driven log / exp cores (tools/genlogtables.py)
+ * a = 2^E * m, m in [0.75, 1.5) (the paper's split, so
+ * x near 1 has E = 0 and no cancellation); idx = top 8 bits of
+ * bits(m) - bits(0.75); r = m*invc - 1 formed exactly as rh + rl (two_prod,
+ * Sterbenz), |r| <= 2^-8; log(a) = E*ln2 + logc + log1p(r).  No division. */
+#define LN2_H42 VEM_LN2_H42
+#define LN2_T42 VEM_LN2_T42
+static const double C_LOG1P_D[] = VEM_LOG1P_D_ARR;
+static const double C_LOG1P_D_U35[] = VEM_LOG1P_D_U35_ARR;
+static const double C_EXPJ_D[] = VEM_EXPJ_D_ARR;
+static const double C_LOG1P_F[] = VEM_LOG1P_F_ARR;
+static const double C_LOG1P_F_U35[] = VEM_LOG1P_F_U35_ARR;
+
+typedef struct { double rh, rl, E, logc_hi, logc_lo; } logred_t;
+
+/* a: positive normal finite binary64 */
+static inline logred_t log_reduce(double a, double Eadj) {
+  uint64_t ix = bits_d(a);
+  uint64_t tmp = ix - 0x3fe8000000000000ull;
+  int64_t k = (int64_t)tmp >> 52;
+  int idx = (int)((tmp >> 44) & 255u);
+  double m = from_bits_d(ix - ((uint64_t)k << 52));
+  const double* t = LOGT + 4 * idx;
+  double p = m * t[0];
+  logred_t o;
+  o.rl = fma(m, t[0], -p);
+  o.rh = p - 1.0;
+  o.E = (double)k + Eadj;
+  o.logc_hi = t[1];
+  o.logc_lo = t[2];
+  return o;
 }
 
-static double log_core_d(double x, int u10) {
-  int ok = (x > 0.0) && (x < INFINITY);
-  double a = ok ? x : 1.0;
-  double m, E;
-  log_split(a, &m, &E);
-  double xn = m - 1.0;
-  double dh = m + 1.0;
-  double dl = m - (dh - 1.0);
-  double t = 1.0 / dh;
-  double sh = xn * t;
-  double u = fma(t, xn, -sh);
-  double v = fma(dl, -t, fma(dh, -t, 1.0));
-  double sl = fma(sh, v, u);
-  double z = sh * sh;
-  double P = estrin(C_LOG_D, VEM_LOG_D_N, z);
-  double w = fma(sh * z, P, 2.0 * sl);
-  double ph_ = E * K_LN2_HI;
-  double pl = fma(E, K_LN2_HI, -ph_);
-  pl = fma(E, K_LN2_LO, pl);
-  double vv = 2.0 * sh;
-  double y;
+/* log1p(rh + rl) as DD: rh - rh^2/2 (exact) + rh^3 Q(rh) + rl(1 - rh) */
+static inline dd_t log1p_dd(double rh, double rl, const double* c, int n) {
+  double z = rh * rh;
+  double Q = estrin(c, n, rh);
+  double t3 = (rh * z) * Q;
+  double h2 = -0.5 * rh;
+  double p2 = rh * h2;
+  double e2 = fma(rh, h2, -p2);
+  double lo = e2 + (t3 + fma(-rl, rh, rl));
+  dd_t S = two_sum_fast(rh, p2);
+  S.lo = S.lo + lo;
+  return S;
+}
+
+/* E*ln2 + logc as DD (E*LN2_H42 exact for |E| < 2^11) */
+static inline dd_t eln2_logc(const logred_t* g) {
+  double eh = g->E * LN2_H42;
+  dd_t H = two_sum_fast(eh, g->logc_hi);
+  H.lo = H.lo + fma(g->E, LN2_T42, g->logc_lo);
+  return H;
+}
+
+static double log_fast_d(double a, double Eadj, int u10) {
+  logred_t g = log_reduce(a, Eadj);
+  dd_t H = eln2_logc(&g);
+  dd_t L;
   if (u10) {
-    dd_t S = two_sum(ph_, vv);
-    y = S.hi + (S.lo + (pl + w));
+    L = log1p_dd(g.rh, g.rl, C_LOG1P_D, VEM_LOG1P_D_N);
   } else {
-    y = ph_ + (vv + (pl + w));
+    double z = g.rh * g.rh;
+    double Q = estrin(C_LOG1P_D_U35, VEM_LOG1P_D_U35_N, g.rh);
+    L.hi = g.rh;
+    L.lo = fma(z, fma(g.rh, Q, -0.5), g.rl);
   }
-  y = (x == 0.0) ? -INFINITY : y;
-  y = (x < 0.0) ? from_bits_d(CANON_NAN_D) : y;
-  y = (x == INFINITY) ? x : y;
-  y = (x != x) ? x : y;
-  return canon_d(y);
+  dd_t T = two_sum(H.hi, L.hi);
+  return T.hi + (T.lo + (H.lo + L.lo));
+}
+
+/* log: fast path for positive normal finite x; slow path: subnormals (x 2^64,
+ * PAPER.md:797-803), 0 -> -inf, <0 -> NaN, inf, NaN. */
+static double log_core_d(double x, int u10) {
+  uint64_t ix = bits_d(x);
+  if (ix - 0x0010000000000000ull < 0x7fe0000000000000ull) return log_fast_d(x, 0.0, u10);
+  if (x > 0.0 && x < 0x1p-1022) return log_fast_d(x * 0x1p64, -64.0, u10);
+  if (x == 0.0) return -INFINITY;
+  if (x == INFINITY) return x;
+  return from_bits_d(CANON_NAN_D); /* negative or NaN */
 }
 double vo_log_d_u10(double x) { return log_core_d(x, 1); }
 double vo_log_d_u35(double x) { return log_core_d(x, 0); }
 
-/* pow internals: DD log (11 terms) x y -> DD exp. */
-static dd_t log_dd_full(double a, const double* c, int n, double c0l, double c1l) {
-  double m, E;
-  log_split(a, &m, &E);
-  double xn = m - 1.0;
-  double dh = m + 1.0;
-  double dl = m - (dh - 1.0);
-  double t = 1.0 / dh;
-  double sh = xn * t;
-  double u = fma(t, xn, -sh);
-  double v = fma(dl, -t, fma(dh, -t, 1.0));
-  dd_t s = {sh, fma(sh, v, u)};
-  dd_t z = dd_squ(s);
-  double Phi = estrin(c + 2, n - 2, z.hi);
-  dd_t c1 = {c[1], c1l}, c0 = {c[0], c0l};
-  dd_t T = dd_add2_d(c1, z.hi * Phi);
-  T = dd_add2(c0, dd_mul(z, T));
-  dd_t w = dd_mul(dd_mul(s, z), T);
-  dd_t s2 = {s.hi * 2.0, s.lo * 2.0};
-  dd_t lm = dd_add2(s2, w);
-  dd_t el = two_prod(E, K_LN2_HI);
-  el.lo = fma(E, K_LN2_LO, el.lo);
-  return dd_add2(el, lm);
+/* pow internals: log as a double-double (rel. err ~2^-70) */
+static inline dd_t log_dd(double a, double Eadj, const double* c, int n) {
+  logred_t g = log_reduce(a, Eadj);
+  dd_t H = eln2_logc(&g);
+  dd_t L = log1p_dd(g.rh, g.rl, c, n);
+  return dd_add2(H, L);
 }
 
-/* DD exp of t = th + tl; returns exp(t) rounded, with ldexp2 scaling. */
-static double exp_dd(dd_t t, const double* c, int n, double c0l, double c1l) {
-  int ok = (t.hi >= -760.0) && (t.hi <= 720.0);
-  double th = ok ? t.hi : 0.0, tl = ok ? t.lo : 0.0;
-  double kd = rint(th * K_INV_LN2);
-  double rh0 = fma(kd, -K_EXP_L1, th);
-  dd_t r0 = {rh0, tl};
-  dd_t r = dd_normalize(dd_add2(r0, two_prod(kd, -K_EXP_L2)));
-  double Ehi = estrin(c + 2, n - 2, r.hi);
-  dd_t c1 = {c[1], c1l}, c0 = {c[0], c0l};
-  dd_t U = dd_add2_d(c1, r.hi * Ehi);
-  U = dd_add2(c0, dd_mul(r, U));
-  dd_t V = dd_mul(dd_squ(r), U);
-  dd_t W = dd_add2(r, V);
-  dd_t Y = dd_add2_d(W, 1.0);
-  double y = ldexp2(Y.hi + Y.lo, (int64_t)kd);
+/* exp of a double-double t with a 128-entry 2^(i/128) table (EXPT):
+ * k = rint(t*128/ln2), r = t - k*ln2/128 (3-part constant), |r| <= ln2/256,
+ * exp(t) = 2^(k>>7) * T[k&127] * (1 + em1(r)).  |th| < 708: normal result,
+ * exponent-field scaling; otherwise saturation / ldexp2. */
+static double exp_dd(dd_t t) {
+  double th = t.hi, tl = t.lo;
+  uint32_t hx = (uint32_t)(bits_d(th) >> 32) & 0x7fffffffu;
+  int fast = hx < EXP_FAST_HI;
+  if (!fast) {
+    int ok = (th >= -760.0) && (th <= 720.0);
+    th = ok ? th : 0.0;
+    tl = ok ? tl : 0.0;
+  }
+  double kd = rint(th * VEM_EXPJ_INV);
+  int64_t k = (int64_t)kd;
+  double r1 = fma(kd, -VEM_EXPJ_L1, th);
+  double r2 = fma(kd, -VEM_EXPJ_L2, tl);
+  dd_t r = two_sum(r1, r2);
+  double z = r.hi * r.hi;
+  double Q = estrin(C_EXPJ_D, VEM_EXPJ_D_N, r.hi);
+  double s2 = z * fma(r.hi, Q, 0.5);
+  double em1l = r.lo + fma(r.hi, r.lo, s2);
+  const double* T = EXPT + 2 * (k & 127);
+  double u = fma(T[0], r.hi, fma(T[0], em1l, T[1]));
+  double R = T[0] + u;
+  int64_t e = k >> 7;
+  if (fast) return from_bits_d(bits_d(R) + ((uint64_t)e << 52));
+  double y = ldexp2(R, e);
   y = (t.hi > K_EXP_OVF) ? INFINITY : y;
   y = (t.hi < K_EXP_UNF) ? 0.0 : y;
   return y;
 }
 
-/* C99 Annex F pow special cases, applied at the end. */
+/* C99 Annex F pow special cases. */
 static inline int is_int_d(double y) { return (fabs(y) < INFINITY) && (trunc(y) == y); }
 static inline int is_odd_d(double y) {
   return is_int_d(y) && (fabs(y) < 0x1p53) && (trunc(y * 0.5) * 2.0 != y);
 }
 
-static double pow_core_d(double x, double y, const double* cl, int nl, double cl0, double cl1,
-                         const double* ce, int ne, double ce0, double ce1) {
+/* pow = exp(y * log|x|).  Fast path: x positive normal
+ * finite, y finite nonzero -- no special-case logic at all.  Slow path:
+ * subnormal/negative x and every C99 special value. */
+static double pow_core_d(double x, double y, const double* cl, int nl) {
+  uint64_t ux = bits_d(x), uy = bits_d(y);
+  int fx = (ux - 0x0010000000000000ull) < 0x7fe0000000000000ull;
+  int fy = ((uy & 0x7fffffffffffffffull) - 1ull) < 0x7fefffffffffffffull;
+  if (fx && fy) return exp_dd(dd_mul_d(log_dd(x, 0.0, cl, nl), y));
   double ax = fabs(x);
   int fin = (ax > 0.0) && (ax < INFINITY) && (fabs(y) < INFINITY);
-  double axs = fin ? ax : 1.0;
-  double ys = fin ? y : 0.0;
-  dd_t L = log_dd_full(axs, cl, nl, cl0, cl1);
-  dd_t T = dd_mul_d(L, ys);
-  double R = exp_dd(T, ce, ne, ce0, ce1);
+  double R = 1.0;
+  if (fin) {
+    int sub = ax < 0x1p-1022;
+    R = exp_dd(dd_mul_d(log_dd(sub ? ax * 0x1p64 : ax, sub ? -64.0 : 0.0, cl, nl), y));
+  }
   int yint = is_int_d(y), yodd = is_odd_d(y);
   double res = (x < 0.0 && yodd) ? -R : R;
   res = (x < 0.0 && !yint && fabs(y) < INFINITY) ? from_bits_d(CANON_NAN_D) : res;
-  /* x = +-0 */
   if (x == 0.0) {
     if (y < 0.0) res = yodd ? copysign_b(INFINITY, x) : INFINITY;
     else res = yodd ? x : 0.0;
   }
-  /* x = +-inf */
   if (ax == INFINITY) {
     if (y < 0.0) res = (yodd && x < 0.0) ? -0.0 : 0.0;
     else res = (yodd && x < 0.0) ? -INFINITY : INFINITY;
   }
-  /* y = +-inf */
   if (fabs(y) == INFINITY) {
     if (ax == 1.0) res = 1.0;
     else res = ((ax < 1.0) == (y < 0.0)) ? INFINITY : 0.0;
   }
   if (x != x || y != y) res = from_bits_d(CANON_NAN_D);
   if (y == 0.0 || x == 1.0) res = 1.0;
-  return canon_d(res);
+  return res;
 }
-double vo_pow_d_u10(double x, double y) {
-  return pow_core_d(x, y, C_POWLOG_D, VEM_POWLOG_D_N, VEM_POWLOG_D_C0L, VEM_POWLOG_D_C1L,
-                    C_POWEXP_D, VEM_POWEXP_D_N, VEM_POWEXP_D_C0L, VEM_POWEXP_D_C1L);
-}
-double vo_pow_d_u35(double x, double y) {
-  return pow_core_d(x, y, C_POWLOG_D_U35, VEM_POWLOG_D_U35_N, VEM_POWLOG_D_U35_C0L,
-                    VEM_POWLOG_D_U35_C1L, C_POWEXP_D_U35, VEM_POWEXP_D_U35_N,
-                    VEM_POWEXP_D_U35_C0L, VEM_POWEXP_D_U35_C1L);
-}
+double vo_pow_d_u10(double x, double y) { return pow_core_d(x, y, C_LOG1P_D, VEM_LOG1P_D_N); }
+double vo_pow_d_u35(double x, double y) { return pow_core_d(x, y, C_LOG1P_D_U35, VEM_LOG1P_D_U35_N); }
 
 /* fmod -- exact remainder by FP long division (Alg. 1, PAPER.md:958-975,
  * 1445-1469) restated for unbounded quotient ratios: each step divides by a
@@ -633,12 +674,6 @@ static const double C_COS_F[] = VEM_COS_F_ARR;
 static const double C_TAN_F[] = VEM_TAN_F_ARR;
 static const double C_EXP_F[] = VEM_EXP_F_ARR;
 static const double C_EXP_F_U35[] = VEM_EXP_F_U35_ARR;
-static const double C_LOG_F[] = VEM_LOG_F_ARR;
-static const double C_LOG_F_U35[] = VEM_LOG_F_U35_ARR;
-static const double C_POWLOG_F[] = VEM_POWLOG_F_ARR;
-static const double C_POWEXP_F[] = VEM_POWEXP_F_ARR;
-static const double C_POWLOG_F_U35[] = VEM_POWLOG_F_U35_ARR;
-static const double C_POWEXP_F_U35[] = VEM_POWEXP_F_U35_ARR;
 
 /* f32 Payne-Hanek in binary64 (new; the reference is double-only):
  * |x| = M*2^E, M < 2^24; table T(E) = centred 2^E*2/pi mod 4, 3 limbs.
@@ -730,53 +765,62 @@ static float exp_core_f(float x, const double* c, int n) {
 float vo_exp_f_u10(float x) { return exp_core_f(x, C_EXP_F, VEM_EXP_F_N); }
 float vo_exp_f_u35(float x) { return exp_core_f(x, C_EXP_F_U35, VEM_EXP_F_U35_N); }
 
-/* f32 log in binary64: e, m from the exact double; s = (m-1)/(m+1) with a
- * float-seeded reciprocal refined once in binary64 (the seed 1/(float)(m+1) is
- * an IEEE-rounded division, identical on host and device). */
+/* f32 log in binary64 with the same 256-entry table: r = m*invc - 1 by one
+ * fma (its rounding is far below binary32 resolution), log1p(r) = r + r^2 Q(r).
+ * Every positive finite binary32 (incl. subnormals) is a normal binary64. */
 static inline double log_f_internal(double a, const double* c, int n) {
-  int64_t eb = (int64_t)((bits_d(a * K_FOUR_THIRDS) >> 52) & 0x7ff) - 1023;
-  double m = from_bits_d(bits_d(a) - ((uint64_t)eb << 52));
-  double E = (double)eb;
-  double xn = m - 1.0;
-  double dh = m + 1.0;
-  double t0 = (double)(1.0f / (float)dh);
-  double t = fma(t0, fma(-dh, t0, 1.0), t0);
-  double s = xn * t;
-  double z = s * s;
-  double P = estrin(c, n, z);
-  return fma(E, K_LN2_HI, fma(s * z, P, fma(E, K_LN2_LO, 2.0 * s)));
+  uint64_t ix = bits_d(a);
+  uint64_t tmp = ix - 0x3fe8000000000000ull;
+  int64_t k = (int64_t)tmp >> 52;
+  int idx = (int)((tmp >> 44) & 255u);
+  double m = from_bits_d(ix - ((uint64_t)k << 52));
+  const double* t = LOGT + 4 * idx;
+  double r = fma(m, t[0], -1.0);
+  double Q = estrin(c, n, r);
+  double L = fma(r * r, Q, r);
+  return fma((double)k, K_LN2_HI, t[1] + L);
 }
 static float log_core_f(float x, const double* c, int n) {
-  int ok = (x > 0.0f) && (x < INFINITY);
-  double a = ok ? (double)x : 1.0;
-  double y = log_f_internal(a, c, n);
-  float o = (float)y;
-  o = (x == 0.0f) ? -INFINITY : o;
-  o = (x < 0.0f) ? from_bits_f(CANON_NAN_F) : o;
-  o = (x == INFINITY) ? x : o;
-  o = (x != x) ? x : o;
-  return canon_f(o);
+  uint32_t ux = bits_f(x);
+  if (ux - 1u < 0x7f7fffffu) return (float)log_f_internal((double)x, c, n);
+  if (x == 0.0f) return -INFINITY;
+  if (x == INFINITY) return x;
+  return from_bits_f(CANON_NAN_F);
 }
-float vo_log_f_u10(float x) { return log_core_f(x, C_LOG_F, VEM_LOG_F_N); }
-float vo_log_f_u35(float x) { return log_core_f(x, C_LOG_F_U35, VEM_LOG_F_U35_N); }
+float vo_log_f_u10(float x) { return log_core_f(x, C_LOG1P_F, VEM_LOG1P_F_N); }
+float vo_log_f_u35(float x) { return log_core_f(x, C_LOG1P_F_U35, VEM_LOG1P_F_U35_N); }
 
 static inline int is_int_f(float y) { return (fabsf(y) < INFINITY) && (truncf(y) == y); }
 static inline int is_odd_f(float y) {
   return is_int_f(y) && (fabsf(y) < 0x1p24f) && (truncf(y * 0.5f) * 2.0f != y);
 }
-static float pow_core_f(float x, float y, const double* cl, int nl, const double* ce, int ne) {
+/* exp(t) for the f32 pow, |t| <= 200: EXPT hi limb x (1 + r + r^2/2 + r^3/6) */
+static inline double exp_f_internal(double t) {
+  double kd = rint(t * VEM_EXPJ_INV);
+  int64_t k = (int64_t)kd;
+  double r = fma(kd, -VEM_EXPJ_L1, t);
+  r = fma(kd, -VEM_EXPJ_L2, r);
+  double p = fma(r * r, fma(r, 0x1.5555555555555p-3, 0.5), r);
+  double R = fma(EXPT[2 * (k & 127)], p, EXPT[2 * (k & 127)]);
+  return from_bits_d(bits_d(R) + ((uint64_t)(k >> 7) << 52));
+}
+static float pow_core_f(float x, float y, const double* cl, int nl) {
+  uint32_t ux = bits_f(x), uy = bits_f(y);
+  int fx = (ux - 1u) < 0x7f7fffffu;             /* x in (0, inf) */
+  int fy = ((uy & 0x7fffffffu) - 1u) < 0x7f7fffffu; /* y finite, != 0 */
+  if (fx && fy) {
+    double t = (double)y * log_f_internal((double)x, cl, nl);
+    t = fmin(fmax(t, -200.0), 200.0);
+    return (float)exp_f_internal(t);
+  }
   float ax = fabsf(x);
   int fin = (ax > 0.0f) && (ax < INFINITY) && (fabsf(y) < INFINITY);
-  double a = fin ? (double)ax : 1.0;
-  double yd = fin ? (double)y : 0.0;
-  double t = yd * log_f_internal(a, cl, nl);
-  double tc = fmin(fmax(t, -200.0), 200.0);
-  double kd = rint(tc * K_INV_LN2);
-  double r = fma(kd, -K_EXP_L1, tc);
-  r = fma(kd, -K_EXP_L2, r);
-  double P = estrin(ce, ne, r);
-  double R = fma(r, P, 1.0) * pow2_bits((int64_t)kd);
-  float Rf = (float)R;
+  float Rf = 1.0f;
+  if (fin) {
+    double t = (double)y * log_f_internal((double)ax, cl, nl);
+    t = fmin(fmax(t, -200.0), 200.0);
+    Rf = (float)exp_f_internal(t);
+  }
   int yint = is_int_f(y), yodd = is_odd_f(y);
   float res = (x < 0.0f && yodd) ? -Rf : Rf;
   res = (x < 0.0f && !yint && fabsf(y) < INFINITY) ? from_bits_f(CANON_NAN_F) : res;
@@ -794,12 +838,10 @@ static float pow_core_f(float x, float y, const double* cl, int nl, const double
   }
   if (x != x || y != y) res = from_bits_f(CANON_NAN_F);
   if (y == 0.0f || x == 1.0f) res = 1.0f;
-  return canon_f(res);
+  return res;
 }
-float vo_pow_f_u10(float x, float y) { return pow_core_f(x, y, C_POWLOG_F, VEM_POWLOG_F_N, C_POWEXP_F, VEM_POWEXP_F_N); }
-float vo_pow_f_u35(float x, float y) {
-  return pow_core_f(x, y, C_POWLOG_F_U35, VEM_POWLOG_F_U35_N, C_POWEXP_F_U35, VEM_POWEXP_F_U35_N);
-}
+float vo_pow_f_u10(float x, float y) { return pow_core_f(x, y, C_LOG1P_F, VEM_LOG1P_F_N); }
+float vo_pow_f_u35(float x, float y) { return pow_core_f(x, y, C_LOG1P_F_U35, VEM_LOG1P_F_U35_N); }
 
 float vo_fmod_f(float x, float y) {
   /* fmodf(x,y) == (float)fmod((double)x,(double)y) exactly: the remainder is
@@ -902,12 +944,12 @@ int vo_fmod_d_iters(double x, double y) {
 
 /* debug hooks (tests only) */
 void vo_dbg_log_dd(double a, double* hi, double* lo) {
-  dd_t r = log_dd_full(a, C_POWLOG_D, VEM_POWLOG_D_N, VEM_POWLOG_D_C0L, VEM_POWLOG_D_C1L);
+  dd_t r = log_dd(a, 0.0, C_LOG1P_D, VEM_LOG1P_D_N);
   *hi = r.hi; *lo = r.lo;
 }
 double vo_dbg_exp_dd(double th, double tl) {
   dd_t t = {th, tl};
-  return exp_dd(t, C_POWEXP_D, VEM_POWEXP_D_N, VEM_POWEXP_D_C0L, VEM_POWEXP_D_C1L);
+  return exp_dd(t);
 }
 
 /* every f32 trig lane takes the f32 Payne-Hanek path: forced variants alias */

@@ -22,11 +22,14 @@ namespace vem {
 
 static std::atomic<uint64_t> g_launches{0};
 
-enum TableKind { kNoTable = 0, kTableD = 1, kTableF = 2 };
+enum TableKind { kNoTable = 0, kTableD = 1, kTableF = 2, kTableLog = 3 };
 
 template <int TABLE>
 struct TableSize {
-  static constexpr int n = TABLE == kTableD ? 4 * VEM_PH_D_ENTRIES : (TABLE == kTableF ? 3 * VEM_PH_F_ENTRIES : 2);
+  static constexpr int n = TABLE == kTableD   ? 4 * VEM_PH_D_ENTRIES
+                           : TABLE == kTableF ? 3 * VEM_PH_F_ENTRIES
+                           : TABLE == kTableLog ? kLogTabN
+                                                : 2;
 };
 
 template <int TABLE>
@@ -34,7 +37,7 @@ __device__ __forceinline__ const double* stage_table(double* stab) {
   if constexpr (TABLE == kNoTable) {
     return nullptr;
   } else {
-    const double* src = TABLE == kTableD ? gPhD : gPhF;
+    const double* src = TABLE == kTableD ? gPhD : (TABLE == kTableF ? gPhF : gLogExp);
     constexpr int n2 = TableSize<TABLE>::n / 2;
     const double2* s2 = reinterpret_cast<const double2*>(src);
     double2* d2 = reinterpret_cast<double2*>(stab);
@@ -93,9 +96,11 @@ __global__ void __launch_bounds__(kThreads) k_unary(const T* __restrict__ x, T* 
 }
 
 // ----------------------------------------------------------- binary kernel
-template <class Op, class T, int U, bool VEC>
+template <class Op, class T, int TABLE, int U, bool VEC>
 __global__ void __launch_bounds__(kThreads) k_binary(const T* __restrict__ x, const T* __restrict__ y2,
                                                      T* __restrict__ out, size_t n) {
+  __shared__ __align__(16) double stab[TableSize<TABLE>::n];
+  const double* tab = stage_table<TABLE>(stab);
   Op op;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -122,15 +127,15 @@ __global__ void __launch_bounds__(kThreads) k_binary(const T* __restrict__ x, co
         if (j < nv) {
           V o;
 #pragma unroll
-          for (int k = 0; k < W; k++) vget(o, k) = op(vget(a[u], k), vget(b[u], k));
+          for (int k = 0; k < W; k++) vget(o, k) = op(vget(a[u], k), vget(b[u], k), tab);
           __stcs(ov + j, o);
         }
       }
     }
     const size_t done = nv * W;
-    if (tid < n - done) out[done + tid] = op(x[done + tid], y2[done + tid]);
+    if (tid < n - done) out[done + tid] = op(x[done + tid], y2[done + tid], tab);
   } else {
-    for (size_t i = tid; i < n; i += stride) out[i] = op(x[i], y2[i]);
+    for (size_t i = tid; i < n; i += stride) out[i] = op(x[i], y2[i], tab);
   }
 }
 
@@ -192,7 +197,7 @@ __global__ void __launch_bounds__(kThreads) k_stream(const T* __restrict__ a, co
       V o;
 #pragma unroll
       for (int k = 0; k < W; k++) {
-        if constexpr (NIN == 2) vget(o, k) = op(vget(va[v], k), vget(vb[v], k));
+        if constexpr (NIN == 2) vget(o, k) = op(vget(va[v], k), vget(vb[v], k), tab);
         else vget(o, k) = op(vget(va[v], k), tab);
       }
       __stcs(ov + v * kThreads + tid, o);
@@ -201,7 +206,7 @@ __global__ void __launch_bounds__(kThreads) k_stream(const T* __restrict__ a, co
   // remainder (< one tile)
   const size_t done = ntiles * TILE_E;
   for (size_t i = done + (size_t)blockIdx.x * kThreads + tid; i < n; i += G * kThreads) {
-    if constexpr (NIN == 2) out[i] = op(a[i], b[i]);
+    if constexpr (NIN == 2) out[i] = op(a[i], b[i], tab);
     else out[i] = op(a[i], tab);
   }
 }
@@ -220,27 +225,27 @@ VEM_UNARY_OP(OpTanDPh, double, (tan_d_u10<true>(x, tab)))
 VEM_UNARY_OP(OpAtanD, double, ((void)tab, atan_d_u10(x)))
 VEM_UNARY_OP(OpExpD, double, ((void)tab, exp_d_u10(x)))
 VEM_UNARY_OP(OpExpDU35, double, ((void)tab, exp_d_u35(x)))
-VEM_UNARY_OP(OpLogD, double, ((void)tab, log_core_d<true>(x)))
-VEM_UNARY_OP(OpLogDU35, double, ((void)tab, log_core_d<false>(x)))
+VEM_UNARY_OP(OpLogD, double, (log_core_d<true>(x, tab)))
+VEM_UNARY_OP(OpLogDU35, double, (log_core_d<false>(x, tab)))
 VEM_UNARY_OP(OpSinF, float, (sin_f_u10(x, tab)))
 VEM_UNARY_OP(OpCosF, float, (cos_f_u10(x, tab)))
 VEM_UNARY_OP(OpTanF, float, (tan_f_u10(x, tab)))
 VEM_UNARY_OP(OpExpF, float, ((void)tab, exp_f_u10(x)))
 VEM_UNARY_OP(OpExpFU35, float, ((void)tab, exp_f_u35(x)))
-VEM_UNARY_OP(OpLogF, float, ((void)tab, log_f_u10(x)))
-VEM_UNARY_OP(OpLogFU35, float, ((void)tab, log_f_u35(x)))
+VEM_UNARY_OP(OpLogF, float, (log_f_u10(x, tab)))
+VEM_UNARY_OP(OpLogFU35, float, (log_f_u35(x, tab)))
 #undef VEM_UNARY_OP
 
 #define VEM_BINARY_OP(NAME, T, EXPR)                                              \
   struct NAME {                                                                   \
-    __device__ __forceinline__ T operator()(T x, T y) const { return EXPR; }      \
+    __device__ __forceinline__ T operator()(T x, T y, const double* tab) const { return EXPR; } \
   };
-VEM_BINARY_OP(OpPowD, double, pow_d_u10(x, y))
-VEM_BINARY_OP(OpPowDU35, double, pow_d_u35(x, y))
-VEM_BINARY_OP(OpFmodD, double, fmod_d(x, y))
-VEM_BINARY_OP(OpPowF, float, pow_f_u10(x, y))
-VEM_BINARY_OP(OpPowFU35, float, pow_f_u35(x, y))
-VEM_BINARY_OP(OpFmodF, float, fmod_f(x, y))
+VEM_BINARY_OP(OpPowD, double, pow_d_u10(x, y, tab))
+VEM_BINARY_OP(OpPowDU35, double, pow_d_u35(x, y, tab))
+VEM_BINARY_OP(OpFmodD, double, ((void)tab, fmod_d(x, y)))
+VEM_BINARY_OP(OpPowF, float, pow_f_u10(x, y, tab))
+VEM_BINARY_OP(OpPowFU35, float, pow_f_u35(x, y, tab))
+VEM_BINARY_OP(OpFmodF, float, ((void)tab, fmod_f(x, y)))
 #undef VEM_BINARY_OP
 
 // ------------------------------------------------------------- launching
@@ -290,17 +295,17 @@ static int launch_unary(const T* x, T* y, size_t n, vem_stream_t s) {
   return (int)cudaGetLastError();
 }
 
-template <class Op, class T, int U>
+template <class Op, class T, int TABLE, int U>
 static int launch_binary(const T* x, const T* y2, T* out, size_t n, vem_stream_t s) {
   if (n == 0) return 0;
   cudaStream_t st = (cudaStream_t)s;
   if (aligned16(x) && aligned16(y2) && aligned16(out)) {
-    auto k = k_binary<Op, T, U, true>;
+    auto k = k_binary<Op, T, TABLE, U, true>;
     static const int occ = occupancy(k);
     int g = grid_for(occ, n / Vec16<T>::n + 1, U);
     k<<<g, kThreads, 0, st>>>(x, y2, out, n);
   } else {
-    auto k = k_binary<Op, T, 1, false>;
+    auto k = k_binary<Op, T, TABLE, 1, false>;
     static const int occ = occupancy(k);
     int g = grid_for(occ, n, 1);
     k<<<g, kThreads, 0, st>>>(x, y2, out, n);
@@ -313,7 +318,7 @@ template <class Op, class T, int NIN, int TABLE, int VPT, int STAGES>
 static int launch_stream(const T* a, const T* b, T* out, size_t n, vem_stream_t s) {
   if (n == 0) return 0;
   if (!(aligned16(a) && aligned16(out) && (NIN == 1 || aligned16(b)))) {
-    if constexpr (NIN == 2) return launch_binary<Op, T, 1>(a, b, out, n, s);
+    if constexpr (NIN == 2) return launch_binary<Op, T, TABLE, 1>(a, b, out, n, s);
     else return launch_unary<Op, T, TABLE, 1>(a, out, n, s);
   }
   auto k = k_stream<Op, T, NIN, TABLE, VPT, STAGES>;
@@ -395,10 +400,10 @@ int vem_tan_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { ret
 int vem_atan_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpAtanD, double, 1, kNoTable, 2, 4>(x, nullptr, y, n, s); }
 int vem_exp_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpExpD, double, 1, kNoTable, 2, 4>(x, nullptr, y, n, s); }
 int vem_exp_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpExpDU35, double, 1, kNoTable, 2, 4>(x, nullptr, y, n, s); }
-int vem_log_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpLogD, double, 1, kNoTable, 2, 4>(x, nullptr, y, n, s); }
-int vem_log_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpLogDU35, double, 1, kNoTable, 2, 4>(x, nullptr, y, n, s); }
-int vem_pow_d_u10(const double* x, const double* y2, double* o, size_t n, vem_stream_t s) { return launch_stream<OpPowD, double, 2, kNoTable, 1, 4>(x, y2, o, n, s); }
-int vem_pow_d_u35(const double* x, const double* y2, double* o, size_t n, vem_stream_t s) { return launch_stream<OpPowDU35, double, 2, kNoTable, 1, 4>(x, y2, o, n, s); }
+int vem_log_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpLogD, double, 1, kTableLog, 2, 4>(x, nullptr, y, n, s); }
+int vem_log_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpLogDU35, double, 1, kTableLog, 2, 4>(x, nullptr, y, n, s); }
+int vem_pow_d_u10(const double* x, const double* y2, double* o, size_t n, vem_stream_t s) { return launch_stream<OpPowD, double, 2, kTableLog, 1, 4>(x, y2, o, n, s); }
+int vem_pow_d_u35(const double* x, const double* y2, double* o, size_t n, vem_stream_t s) { return launch_stream<OpPowDU35, double, 2, kTableLog, 1, 4>(x, y2, o, n, s); }
 int vem_fmod_d(const double* x, const double* y2, double* o, size_t n, vem_stream_t s) { return launch_stream<OpFmodD, double, 2, kNoTable, 1, 4>(x, y2, o, n, s); }
 
 int vem_sin_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return launch_stream<OpSinF, float, 1, kTableF, 1, 4>(x, nullptr, y, n, s); }
@@ -410,10 +415,10 @@ int vem_cos_f_u10_ph(const float* x, float* y, size_t n, vem_stream_t s) { retur
 int vem_tan_f_u10_ph(const float* x, float* y, size_t n, vem_stream_t s) { return vem_tan_f_u10(x, y, n, s); }
 int vem_exp_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return launch_stream<OpExpF, float, 1, kNoTable, 2, 4>(x, nullptr, y, n, s); }
 int vem_exp_f_u35(const float* x, float* y, size_t n, vem_stream_t s) { return launch_stream<OpExpFU35, float, 1, kNoTable, 2, 4>(x, nullptr, y, n, s); }
-int vem_log_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return launch_stream<OpLogF, float, 1, kNoTable, 1, 4>(x, nullptr, y, n, s); }
-int vem_log_f_u35(const float* x, float* y, size_t n, vem_stream_t s) { return launch_stream<OpLogFU35, float, 1, kNoTable, 1, 4>(x, nullptr, y, n, s); }
-int vem_pow_f_u10(const float* x, const float* y2, float* o, size_t n, vem_stream_t s) { return launch_stream<OpPowF, float, 2, kNoTable, 1, 4>(x, y2, o, n, s); }
-int vem_pow_f_u35(const float* x, const float* y2, float* o, size_t n, vem_stream_t s) { return launch_stream<OpPowFU35, float, 2, kNoTable, 1, 4>(x, y2, o, n, s); }
+int vem_log_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return launch_stream<OpLogF, float, 1, kTableLog, 1, 4>(x, nullptr, y, n, s); }
+int vem_log_f_u35(const float* x, float* y, size_t n, vem_stream_t s) { return launch_stream<OpLogFU35, float, 1, kTableLog, 1, 4>(x, nullptr, y, n, s); }
+int vem_pow_f_u10(const float* x, const float* y2, float* o, size_t n, vem_stream_t s) { return launch_stream<OpPowF, float, 2, kTableLog, 1, 4>(x, y2, o, n, s); }
+int vem_pow_f_u35(const float* x, const float* y2, float* o, size_t n, vem_stream_t s) { return launch_stream<OpPowFU35, float, 2, kTableLog, 1, 4>(x, y2, o, n, s); }
 int vem_fmod_f(const float* x, const float* y2, float* o, size_t n, vem_stream_t s) { return launch_stream<OpFmodF, float, 2, kNoTable, 1, 4>(x, y2, o, n, s); }
 
 int vem_trig_reduce_d(const double* x, double* hi, double* lo, int* q, size_t n, vem_stream_t s) {

@@ -16,6 +16,7 @@
 
 #include "vem_coeffs.h"
 #include "vem_ph_tables.h"
+#include "vem_log_tables.h"
 
 namespace vem {
 
@@ -71,26 +72,25 @@ __constant__ double cTanD[] = VEM_TAN_D_ARR;
 __constant__ double cAtanD[] = VEM_ATAN_D_ARR;
 __constant__ double cExpD[] = VEM_EXP_D_ARR;
 __constant__ double cExpDU35[] = VEM_EXP_D_U35_ARR;
-__constant__ double cLogD[] = VEM_LOG_D_ARR;
-__constant__ double cPowLogD[] = VEM_POWLOG_D_ARR;
-__constant__ double cPowExpD[] = VEM_POWEXP_D_ARR;
-__constant__ double cPowLogDU35[] = VEM_POWLOG_D_U35_ARR;
-__constant__ double cPowExpDU35[] = VEM_POWEXP_D_U35_ARR;
 __constant__ double cSinF[] = VEM_SIN_F_ARR;
 __constant__ double cCosF[] = VEM_COS_F_ARR;
 __constant__ double cTanF[] = VEM_TAN_F_ARR;
 __constant__ double cExpF[] = VEM_EXP_F_ARR;
 __constant__ double cExpFU35[] = VEM_EXP_F_U35_ARR;
-__constant__ double cLogF[] = VEM_LOG_F_ARR;
-__constant__ double cLogFU35[] = VEM_LOG_F_U35_ARR;
-__constant__ double cPowLogF[] = VEM_POWLOG_F_ARR;
-__constant__ double cPowExpF[] = VEM_POWEXP_F_ARR;
-__constant__ double cPowLogFU35[] = VEM_POWLOG_F_U35_ARR;
-__constant__ double cPowExpFU35[] = VEM_POWEXP_F_U35_ARR;
+
+__constant__ double cLog1pD[] = VEM_LOG1P_D_ARR;
+__constant__ double cLog1pDU35[] = VEM_LOG1P_D_U35_ARR;
+__constant__ double cExpjD[] = VEM_EXPJ_D_ARR;
+__constant__ double cLog1pF[] = VEM_LOG1P_F_ARR;
+__constant__ double cLog1pFU35[] = VEM_LOG1P_F_U35_ARR;
 
 // Payne-Hanek tables (global copy; kernels stage them into shared memory).
 __device__ const double gPhD[4 * VEM_PH_D_ENTRIES] = {VEM_PH_D_INIT};
 __device__ const double gPhF[3 * VEM_PH_F_ENTRIES] = {VEM_PH_F_INIT};
+// log / exp tables (tools/genlogtables.py), staged together: LOGT quads then
+// EXPT pairs.
+constexpr int kLogTabN = 4 * 256 + 2 * 128;
+__device__ const double gLogExp[kLogTabN] = {VEM_LOGT_INIT VEM_EXPT_INIT};
 
 // ---------------------------------------------------- primitives
 // backend.hpp:47-52 round_ta == CUDA round() (ties away from zero) for every
@@ -394,10 +394,10 @@ __device__ __forceinline__ double atan_d_u10(double x) {
   return canon_d(y);
 }
 
+constexpr uint32_t kExpFastHi = 0x40862000u;  // |x| < 708
+
 template <int N, bool kU10>
-__device__ __forceinline__ double exp_core_d(double x, const double* c) {
-  bool ok = (x >= kExpUnf) && (x <= kExpOvf);
-  double xs = ok ? x : 0.0;
+__device__ __forceinline__ double exp_poly_d(double xs, const double* c, double& kd_out) {
   double kd = rint(xs * kInvLn2);
   double r1 = fma(kd, -kExpL1, xs);
   double r = fma(kd, -kExpL2, r1);
@@ -411,98 +411,134 @@ __device__ __forceinline__ double exp_core_d(double x, const double* c) {
   } else {
     y = 1.0 + fma(r * r, P, r);
   }
+  kd_out = kd;
+  return y;
+}
+// oracle: exp_core_d.  Fast path: exponent-field scaling (result normal).
+template <int N, bool kU10>
+__device__ __forceinline__ double exp_core_d(double x, const double* c) {
+  uint32_t hx = (uint32_t)__double2hiint(x) & 0x7fffffffu;
+  double kd;
+  if (hx < kExpFastHi) {
+    double y = exp_poly_d<N, kU10>(x, c, kd);
+    return from_bits_d(bits_d(y) + ((uint64_t)(long long)kd << 52));
+  }
+  bool ok = (x >= kExpUnf) && (x <= kExpOvf);
+  double xs = ok ? x : 0.0;
+  double y = exp_poly_d<N, kU10>(xs, c, kd);
   y = ldexp2(y, (long long)kd);
   y = (x > kExpOvf) ? kInf : y;
   y = (x < kExpUnf) ? 0.0 : y;
-  y = (x != x) ? x : y;
-  return canon_d(y);
+  y = (x != x) ? from_bits_d(kCanonNanD) : y;
+  return y;
 }
 __device__ __forceinline__ double exp_d_u10(double x) { return exp_core_d<VEM_EXP_D_N, true>(x, cExpD); }
 __device__ __forceinline__ double exp_d_u35(double x) { return exp_core_d<VEM_EXP_D_U35_N, false>(x, cExpDU35); }
 
-__device__ __forceinline__ void log_split(double a, double& m, double& E) {
-  bool sub = a < 0x1p-1022;
-  double as = sub ? a * 0x1p64 : a;
-  long long eb = (long long)((bits_d(as * kFourThirds) >> 52) & 0x7ff) - 1023;
-  m = from_bits_d(bits_d(as) - ((uint64_t)eb << 52));
-  E = (double)(eb - (sub ? 64 : 0));
+// ---- table-driven log / exp (oracle: log_reduce, log1p_dd, ... ) -------
+// `lt` points at the staged LOGT (4 doubles per entry) followed by EXPT.
+struct logred { double rh, rl, E, logc_hi, logc_lo; };
+
+__device__ __forceinline__ logred log_reduce(double a, double Eadj, const double* __restrict__ lt) {
+  uint64_t ix = bits_d(a);
+  uint64_t tmp = ix - 0x3fe8000000000000ull;
+  long long k = (long long)tmp >> 52;
+  int idx = (int)((tmp >> 44) & 255u);
+  double m = from_bits_d(ix - ((uint64_t)k << 52));
+  const double2* t2 = reinterpret_cast<const double2*>(lt + 4 * idx);
+  double2 e0 = t2[0];
+  double logc_lo = lt[4 * idx + 2];
+  double p = m * e0.x;
+  logred o;
+  o.rl = fma(m, e0.x, -p);
+  o.rh = p - 1.0;
+  o.E = (double)k + Eadj;
+  o.logc_hi = e0.y;
+  o.logc_lo = logc_lo;
+  return o;
+}
+
+template <int N>
+__device__ __forceinline__ dd log1p_dd(double rh, double rl, const double* c) {
+  double z = rh * rh;
+  double Q = estrin<N>(c, rh);
+  double t3 = (rh * z) * Q;
+  double h2 = -0.5 * rh;
+  double p2 = rh * h2;
+  double e2 = fma(rh, h2, -p2);
+  double lo = e2 + (t3 + fma(-rl, rh, rl));
+  dd S = two_sum_fast(rh, p2);
+  S.lo = S.lo + lo;
+  return S;
+}
+
+__device__ __forceinline__ dd eln2_logc(const logred& g) {
+  double eh = g.E * VEM_LN2_H42;
+  dd H = two_sum_fast(eh, g.logc_hi);
+  H.lo = H.lo + fma(g.E, VEM_LN2_T42, g.logc_lo);
+  return H;
 }
 
 template <bool kU10>
-__device__ __forceinline__ double log_core_d(double x) {
-  bool ok = (x > 0.0) && (x < kInf);
-  double a = ok ? x : 1.0;
-  double m, E;
-  log_split(a, m, E);
-  double xn = m - 1.0;
-  double dh = m + 1.0;
-  double dl = m - (dh - 1.0);
-  double t = 1.0 / dh;
-  double sh = xn * t;
-  double u = fma(t, xn, -sh);
-  double v = fma(dl, -t, fma(dh, -t, 1.0));
-  double sl = fma(sh, v, u);
-  double z = sh * sh;
-  double P = estrin<VEM_LOG_D_N>(cLogD, z);
-  double w = fma(sh * z, P, 2.0 * sl);
-  double ph_ = E * kLn2Hi;
-  double pl = fma(E, kLn2Hi, -ph_);
-  pl = fma(E, kLn2Lo, pl);
-  double vv = 2.0 * sh;
-  double y;
+__device__ __forceinline__ double log_fast_d(double a, double Eadj, const double* lt) {
+  logred g = log_reduce(a, Eadj, lt);
+  dd H = eln2_logc(g);
+  dd L;
   if (kU10) {
-    dd S = two_sum(ph_, vv);
-    y = S.hi + (S.lo + (pl + w));
+    L = log1p_dd<VEM_LOG1P_D_N>(g.rh, g.rl, cLog1pD);
   } else {
-    y = ph_ + (vv + (pl + w));
+    double z = g.rh * g.rh;
+    double Q = estrin<VEM_LOG1P_D_U35_N>(cLog1pDU35, g.rh);
+    L.hi = g.rh;
+    L.lo = fma(z, fma(g.rh, Q, -0.5), g.rl);
   }
-  y = (x == 0.0) ? -kInf : y;
-  y = (x < 0.0) ? from_bits_d(kCanonNanD) : y;
-  y = (x == kInf) ? x : y;
-  y = (x != x) ? x : y;
-  return canon_d(y);
+  dd T = two_sum(H.hi, L.hi);
+  return T.hi + (T.lo + (H.lo + L.lo));
 }
 
-template <int NL>
-__device__ __forceinline__ dd log_dd_full(double a, const double* c, double c0l, double c1l) {
-  double m, E;
-  log_split(a, m, E);
-  double xn = m - 1.0;
-  double dh = m + 1.0;
-  double dl = m - (dh - 1.0);
-  double t = 1.0 / dh;
-  double sh = xn * t;
-  double u = fma(t, xn, -sh);
-  double v = fma(dl, -t, fma(dh, -t, 1.0));
-  dd s = {sh, fma(sh, v, u)};
-  dd z = dd_squ(s);
-  double Phi = estrin<NL - 2>(c + 2, z.hi);
-  dd c1 = {c[1], c1l}, c0 = {c[0], c0l};
-  dd T = dd_add2_d(c1, z.hi * Phi);
-  T = dd_add2(c0, dd_mul(z, T));
-  dd w = dd_mul(dd_mul(s, z), T);
-  dd s2 = {s.hi * 2.0, s.lo * 2.0};
-  dd lm = dd_add2(s2, w);
-  dd el = two_prod(E, kLn2Hi);
-  el.lo = fma(E, kLn2Lo, el.lo);
-  return dd_add2(el, lm);
+template <bool kU10>
+__device__ __forceinline__ double log_core_d(double x, const double* lt) {
+  uint64_t ix = bits_d(x);
+  if (ix - 0x0010000000000000ull < 0x7fe0000000000000ull) return log_fast_d<kU10>(x, 0.0, lt);
+  if (x > 0.0 && x < 0x1p-1022) return log_fast_d<kU10>(x * 0x1p64, -64.0, lt);
+  if (x == 0.0) return -kInf;
+  if (x == kInf) return x;
+  return from_bits_d(kCanonNanD);
 }
 
-template <int NE>
-__device__ __forceinline__ double exp_dd(dd t, const double* c, double c0l, double c1l) {
-  bool ok = (t.hi >= -760.0) && (t.hi <= 720.0);
-  double th = ok ? t.hi : 0.0, tl = ok ? t.lo : 0.0;
-  double kd = rint(th * kInvLn2);
-  double rh0 = fma(kd, -kExpL1, th);
-  dd r = dd_normalize(dd_add2(dd{rh0, tl}, two_prod(kd, -kExpL2)));
-  double Ehi = estrin<NE - 2>(c + 2, r.hi);
-  dd c1 = {c[1], c1l}, c0 = {c[0], c0l};
-  dd U = dd_add2_d(c1, r.hi * Ehi);
-  U = dd_add2(c0, dd_mul(r, U));
-  dd V = dd_mul(dd_squ(r), U);
-  dd W = dd_add2(r, V);
-  dd Y = dd_add2_d(W, 1.0);
-  double y = ldexp2(Y.hi + Y.lo, (long long)kd);
+template <int N>
+__device__ __forceinline__ dd log_dd(double a, double Eadj, const double* c, const double* lt) {
+  logred g = log_reduce(a, Eadj, lt);
+  dd H = eln2_logc(g);
+  dd L = log1p_dd<N>(g.rh, g.rl, c);
+  return dd_add2(H, L);
+}
+
+__device__ __forceinline__ double exp_dd(dd t, const double* __restrict__ lt) {
+  const double* expt = lt + 4 * 256;
+  double th = t.hi, tl = t.lo;
+  uint32_t hx = (uint32_t)__double2hiint(th) & 0x7fffffffu;
+  bool fast = hx < kExpFastHi;
+  if (!fast) {
+    bool ok = (th >= -760.0) && (th <= 720.0);
+    th = ok ? th : 0.0;
+    tl = ok ? tl : 0.0;
+  }
+  double kd = rint(th * VEM_EXPJ_INV);
+  long long k = (long long)kd;
+  double r1 = fma(kd, -VEM_EXPJ_L1, th);
+  double r2 = fma(kd, -VEM_EXPJ_L2, tl);
+  dd r = two_sum(r1, r2);
+  double z = r.hi * r.hi;
+  double Q = estrin<VEM_EXPJ_D_N>(cExpjD, r.hi);
+  double s2 = z * fma(r.hi, Q, 0.5);
+  double em1l = r.lo + fma(r.hi, r.lo, s2);
+  double2 T = reinterpret_cast<const double2*>(expt)[k & 127];
+  double u = fma(T.x, r.hi, fma(T.x, em1l, T.y));
+  double R = T.x + u;
+  long long e = k >> 7;
+  if (fast) return from_bits_d(bits_d(R) + ((uint64_t)e << 52));
+  double y = ldexp2(R, e);
   y = (t.hi > kExpOvf) ? kInf : y;
   y = (t.hi < kExpUnf) ? 0.0 : y;
   return y;
@@ -513,16 +549,15 @@ __device__ __forceinline__ bool is_odd_d(double y) {
   return is_int_d(y) && (fabs(y) < 0x1p53) && (trunc(y * 0.5) * 2.0 != y);
 }
 
-template <int NL, int NE>
-__device__ __forceinline__ double pow_core_d(double x, double y, const double* cl, double cl0, double cl1,
-                                             const double* ce, double ce0, double ce1) {
+template <int NL>
+__device__ __noinline__ double pow_slow_d(double x, double y, const double* cl, const double* lt) {
   double ax = fabs(x);
   bool fin = (ax > 0.0) && (ax < kInf) && (fabs(y) < kInf);
-  double axs = fin ? ax : 1.0;
-  double ys = fin ? y : 0.0;
-  dd L = log_dd_full<NL>(axs, cl, cl0, cl1);
-  dd T = dd_mul_d(L, ys);
-  double R = exp_dd<NE>(T, ce, ce0, ce1);
+  double R = 1.0;
+  if (fin) {
+    bool sub = ax < 0x1p-1022;
+    R = exp_dd(dd_mul_d(log_dd<NL>(sub ? ax * 0x1p64 : ax, sub ? -64.0 : 0.0, cl, lt), y), lt);
+  }
   bool yint = is_int_d(y), yodd = is_odd_d(y);
   double res = (x < 0.0 && yodd) ? -R : R;
   res = (x < 0.0 && !yint && fabs(y) < kInf) ? from_bits_d(kCanonNanD) : res;
@@ -540,16 +575,23 @@ __device__ __forceinline__ double pow_core_d(double x, double y, const double* c
   }
   if (x != x || y != y) res = from_bits_d(kCanonNanD);
   if (y == 0.0 || x == 1.0) res = 1.0;
-  return canon_d(res);
+  return res;
 }
-__device__ __forceinline__ double pow_d_u10(double x, double y) {
-  return pow_core_d<VEM_POWLOG_D_N, VEM_POWEXP_D_N>(x, y, cPowLogD, VEM_POWLOG_D_C0L, VEM_POWLOG_D_C1L,
-                                                     cPowExpD, VEM_POWEXP_D_C0L, VEM_POWEXP_D_C1L);
+
+// oracle: pow_core_d (fast path without any special-value logic)
+template <int NL>
+__device__ __forceinline__ double pow_core_d(double x, double y, const double* cl, const double* lt) {
+  uint64_t ux = bits_d(x), uy = bits_d(y);
+  bool fx = (ux - 0x0010000000000000ull) < 0x7fe0000000000000ull;
+  bool fy = ((uy & 0x7fffffffffffffffull) - 1ull) < 0x7fefffffffffffffull;
+  if (fx && fy) return exp_dd(dd_mul_d(log_dd<NL>(x, 0.0, cl, lt), y), lt);
+  return pow_slow_d<NL>(x, y, cl, lt);
 }
-__device__ __forceinline__ double pow_d_u35(double x, double y) {
-  return pow_core_d<VEM_POWLOG_D_U35_N, VEM_POWEXP_D_U35_N>(
-      x, y, cPowLogDU35, VEM_POWLOG_D_U35_C0L, VEM_POWLOG_D_U35_C1L, cPowExpDU35, VEM_POWEXP_D_U35_C0L,
-      VEM_POWEXP_D_U35_C1L);
+__device__ __forceinline__ double pow_d_u10(double x, double y, const double* lt) {
+  return pow_core_d<VEM_LOG1P_D_N>(x, y, cLog1pD, lt);
+}
+__device__ __forceinline__ double pow_d_u35(double x, double y, const double* lt) {
+  return pow_core_d<VEM_LOG1P_D_U35_N>(x, y, cLog1pDU35, lt);
 }
 
 // fmod: staged-divisor FP long division (oracle: fmod_core).
@@ -681,52 +723,54 @@ __device__ __forceinline__ float exp_f_u10(float x) { return exp_core_f<VEM_EXP_
 __device__ __forceinline__ float exp_f_u35(float x) { return exp_core_f<VEM_EXP_F_U35_N>(x, cExpFU35); }
 
 template <int N>
-__device__ __forceinline__ double log_f_internal(double a, const double* c) {
-  long long eb = (long long)((bits_d(a * kFourThirds) >> 52) & 0x7ff) - 1023;
-  double m = from_bits_d(bits_d(a) - ((uint64_t)eb << 52));
-  double E = (double)eb;
-  double xn = m - 1.0;
-  double dh = m + 1.0;
-  double t0 = (double)(1.0f / (float)dh);
-  double t = fma(t0, fma(-dh, t0, 1.0), t0);
-  double s = xn * t;
-  double z = s * s;
-  double P = estrin<N>(c, z);
-  return fma(E, kLn2Hi, fma(s * z, P, fma(E, kLn2Lo, 2.0 * s)));
+__device__ __forceinline__ double log_f_internal(double a, const double* c, const double* __restrict__ lt) {
+  uint64_t ix = bits_d(a);
+  uint64_t tmp = ix - 0x3fe8000000000000ull;
+  long long k = (long long)tmp >> 52;
+  int idx = (int)((tmp >> 44) & 255u);
+  double m = from_bits_d(ix - ((uint64_t)k << 52));
+  double2 t = reinterpret_cast<const double2*>(lt + 4 * idx)[0];
+  double r = fma(m, t.x, -1.0);
+  double Q = estrin<N>(c, r);
+  double L = fma(r * r, Q, r);
+  return fma((double)k, kLn2Hi, t.y + L);
 }
 template <int N>
-__device__ __forceinline__ float log_core_f(float x, const double* c) {
-  bool ok = (x > 0.0f) && (x < kInfF);
-  double a = ok ? (double)x : 1.0;
-  double y = log_f_internal<N>(a, c);
-  float o = (float)y;
-  o = (x == 0.0f) ? -kInfF : o;
-  o = (x < 0.0f) ? from_bits_f(kCanonNanF) : o;
-  o = (x == kInfF) ? x : o;
-  o = (x != x) ? x : o;
-  return canon_f(o);
+__device__ __forceinline__ float log_core_f(float x, const double* c, const double* lt) {
+  uint32_t ux = bits_f(x);
+  if (ux - 1u < 0x7f7fffffu) return (float)log_f_internal<N>((double)x, c, lt);
+  if (x == 0.0f) return -kInfF;
+  if (x == kInfF) return x;
+  return from_bits_f(kCanonNanF);
 }
-__device__ __forceinline__ float log_f_u10(float x) { return log_core_f<VEM_LOG_F_N>(x, cLogF); }
-__device__ __forceinline__ float log_f_u35(float x) { return log_core_f<VEM_LOG_F_U35_N>(x, cLogFU35); }
+__device__ __forceinline__ float log_f_u10(float x, const double* lt) { return log_core_f<VEM_LOG1P_F_N>(x, cLog1pF, lt); }
+__device__ __forceinline__ float log_f_u35(float x, const double* lt) { return log_core_f<VEM_LOG1P_F_U35_N>(x, cLog1pFU35, lt); }
 
 __device__ __forceinline__ bool is_int_f(float y) { return (fabsf(y) < kInfF) && (truncf(y) == y); }
 __device__ __forceinline__ bool is_odd_f(float y) {
   return is_int_f(y) && (fabsf(y) < 0x1p24f) && (truncf(y * 0.5f) * 2.0f != y);
 }
-template <int NL, int NE>
-__device__ __forceinline__ float pow_core_f(float x, float y, const double* cl, const double* ce) {
+__device__ __forceinline__ double exp_f_internal(double t, const double* __restrict__ lt) {
+  const double* expt = lt + 4 * 256;
+  double kd = rint(t * VEM_EXPJ_INV);
+  long long k = (long long)kd;
+  double r = fma(kd, -VEM_EXPJ_L1, t);
+  r = fma(kd, -VEM_EXPJ_L2, r);
+  double p = fma(r * r, fma(r, 0x1.5555555555555p-3, 0.5), r);
+  double T = expt[2 * (k & 127)];
+  double R = fma(T, p, T);
+  return from_bits_d(bits_d(R) + ((uint64_t)(k >> 7) << 52));
+}
+template <int NL>
+__device__ __noinline__ float pow_slow_f(float x, float y, const double* cl, const double* lt) {
   float ax = fabsf(x);
   bool fin = (ax > 0.0f) && (ax < kInfF) && (fabsf(y) < kInfF);
-  double a = fin ? (double)ax : 1.0;
-  double yd = fin ? (double)y : 0.0;
-  double t = yd * log_f_internal<NL>(a, cl);
-  double tc = fmin(fmax(t, -200.0), 200.0);
-  double kd = rint(tc * kInvLn2);
-  double r = fma(kd, -kExpL1, tc);
-  r = fma(kd, -kExpL2, r);
-  double P = estrin<NE>(ce, r);
-  double R = fma(r, P, 1.0) * pow2_bits((long long)kd);
-  float Rf = (float)R;
+  float Rf = 1.0f;
+  if (fin) {
+    double t = (double)y * log_f_internal<NL>((double)ax, cl, lt);
+    t = fmin(fmax(t, -200.0), 200.0);
+    Rf = (float)exp_f_internal(t, lt);
+  }
   bool yint = is_int_f(y), yodd = is_odd_f(y);
   float res = (x < 0.0f && yodd) ? -Rf : Rf;
   res = (x < 0.0f && !yint && fabsf(y) < kInfF) ? from_bits_f(kCanonNanF) : res;
@@ -744,13 +788,25 @@ __device__ __forceinline__ float pow_core_f(float x, float y, const double* cl, 
   }
   if (x != x || y != y) res = from_bits_f(kCanonNanF);
   if (y == 0.0f || x == 1.0f) res = 1.0f;
-  return canon_f(res);
+  return res;
 }
-__device__ __forceinline__ float pow_f_u10(float x, float y) {
-  return pow_core_f<VEM_POWLOG_F_N, VEM_POWEXP_F_N>(x, y, cPowLogF, cPowExpF);
+template <int NL>
+__device__ __forceinline__ float pow_core_f(float x, float y, const double* cl, const double* lt) {
+  uint32_t ux = bits_f(x), uy = bits_f(y);
+  bool fx = (ux - 1u) < 0x7f7fffffu;
+  bool fy = ((uy & 0x7fffffffu) - 1u) < 0x7f7fffffu;
+  if (fx && fy) {
+    double t = (double)y * log_f_internal<NL>((double)x, cl, lt);
+    t = fmin(fmax(t, -200.0), 200.0);
+    return (float)exp_f_internal(t, lt);
+  }
+  return pow_slow_f<NL>(x, y, cl, lt);
 }
-__device__ __forceinline__ float pow_f_u35(float x, float y) {
-  return pow_core_f<VEM_POWLOG_F_U35_N, VEM_POWEXP_F_U35_N>(x, y, cPowLogFU35, cPowExpFU35);
+__device__ __forceinline__ float pow_f_u10(float x, float y, const double* lt) {
+  return pow_core_f<VEM_LOG1P_F_N>(x, y, cLog1pF, lt);
+}
+__device__ __forceinline__ float pow_f_u35(float x, float y, const double* lt) {
+  return pow_core_f<VEM_LOG1P_F_U35_N>(x, y, cLog1pFU35, lt);
 }
 __device__ __forceinline__ float fmod_f(float x, float y) {
   double r = fmod_core((double)x, (double)y);

@@ -100,6 +100,33 @@ def log_weight():
     return w
 
 
+# log1p(r) = r - r^2/2 + r^3*Q(r)   (table-driven log core)
+def log1p3_target():
+    return _safe(lambda r: (mp.log1p(r) - r + r * r / 2) / (r ** 3), lambda r: mp.mpf(1) / 3 - r / 4)
+
+
+def log1p3_weight():
+    return lambda r: abs(r ** 3 / mp.log1p(r))
+
+
+# log1p(r) = r + r^2*Q(r)   (f32 table-driven log)
+def log1p2_target():
+    return _safe(lambda r: (mp.log1p(r) - r) / (r * r), lambda r: -mp.mpf(1) / 2 + r / 3)
+
+
+def log1p2_weight():
+    return lambda r: abs(r * r / mp.log1p(r))
+
+
+# exp(r) = 1 + r + r^2/2 + r^3*Q(r)   (table-driven exp core)
+def exp3_target():
+    return _safe(lambda r: (mp.exp(r) - 1 - r - r * r / 2) / (r ** 3), lambda r: mp.mpf(1) / 6 + r / 24)
+
+
+def exp3_weight():
+    return lambda r: abs(r ** 3) / mp.exp(r)
+
+
 # ---------------------------------------------------------------- registry
 # name: (target, weight, domain lo, domain hi, powers, dd_terms, description)
 R_TRIG = mp.mpf("0.80")          # |r| bound after CW1/CW2/PH (CW2 slack)
@@ -109,7 +136,21 @@ S_LOG = mp.mpf("0.2")             # |s| for m in [0.75, 1.5)
 R_EXP = LN2 / 2 * mp.mpf("1.0001")
 T_PI8 = mp.tan(mp.pi / 8) * mp.mpf("1.0001")
 
+R_L1P = mp.mpf(2) ** -8 * mp.mpf("1.01")
+R_EXPJ = LN2 / 256 * mp.mpf("1.01")
+
 SPECS = {
+    # ---- table-driven cores
+    "log1p_d": (log1p3_target(), log1p3_weight(), -R_L1P, R_L1P, list(range(6)), 0,
+                "log1p(r) = r - r^2/2 + r^3*P(r), |r|<=2^-8 (table-driven log)"),
+    "log1p_d_u35": (log1p3_target(), log1p3_weight(), -R_L1P, R_L1P, list(range(5)), 0,
+                    "log1p(r) = r - r^2/2 + r^3*P(r), |r|<=2^-8 (u35)"),
+    "expj_d": (exp3_target(), exp3_weight(), -R_EXPJ, R_EXPJ, list(range(4)), 0,
+               "exp(r) = 1 + r + r^2/2 + r^3*P(r), |r|<=ln2/256 (table-driven exp)"),
+    "log1p_f": (log1p2_target(), log1p2_weight(), -R_L1P, R_L1P, list(range(3)), 0,
+                "f32 log1p(r) = r + r^2*P(r), |r|<=2^-8"),
+    "log1p_f_u35": (log1p2_target(), log1p2_weight(), -R_L1P, R_L1P, list(range(2)), 0,
+                    "f32 log1p(r) = r + r^2*P(r), |r|<=2^-8 (u35)"),
     # ---- float64 (u10 unless suffixed)
     "sin_d": (odd_target(mp.sin, -1 / mp.mpf(6)), odd_weight(mp.sin), 0, R_TRIG ** 2, list(range(6)), 0,
               "sin(r) = r + r*z*P(z), z=r^2, |r|<=0.80"),
@@ -123,16 +164,6 @@ SPECS = {
               "exp(r) = 1 + r + r^2*P(r), |r|<=ln2/2 (13 terms)"),
     "exp_d_u35": (exp_target(), exp_weight(), -R_EXP, R_EXP, list(range(10)), 0,
                   "exp(r) = 1 + r + r^2*P(r), |r|<=ln2/2 (12 terms)"),
-    "log_d": (log_target(), log_weight(), 0, S_LOG ** 2, list(range(7)), 0,
-              "log(m) = 2s + s*z*P(z), z=s^2, |s|<=0.2 (8 terms)"),
-    "powlog_d": (log_target(), log_weight(), 0, S_LOG ** 2, list(range(10)), 2,
-                 "pow-internal DD log(m) = 2s + s*z*P(z), |s|<=0.2 (11 terms)"),
-    "powexp_d": (exp_target(), exp_weight(), -R_EXP, R_EXP, list(range(11)), 2,
-                 "pow-internal DD exp(r) = 1 + r + r^2*P(r) (13 terms)"),
-    "powlog_d_u35": (log_target(), log_weight(), 0, S_LOG ** 2, list(range(9)), 2,
-                     "pow u35 DD log(m) (10 terms)"),
-    "powexp_d_u35": (exp_target(), exp_weight(), -R_EXP, R_EXP, list(range(10)), 2,
-                     "pow u35 DD exp(r) (12 terms)"),
     # ---- float32 (binary64 internals)
     "sin_f": (odd_target(mp.sin, -1 / mp.mpf(6)), odd_weight(mp.sin), 0, R_TRIG_F ** 2, list(range(4)), 0,
               "f32 sin(r) = r + r*z*P(z), |r|<=pi/4"),
@@ -144,18 +175,6 @@ SPECS = {
               "f32 exp(r) = 1 + r*P(r), |r|<=ln2/2"),
     "exp_f_u35": (exp1_target(), exp1_weight(), -R_EXP, R_EXP, list(range(6)), 0,
                   "f32 exp u35 (r) = 1 + r*P(r)"),
-    "log_f": (log_target(), log_weight(), 0, S_LOG ** 2, list(range(4)), 0,
-              "f32 log(m) = 2s + s*z*P(z)"),
-    "log_f_u35": (log_target(), log_weight(), 0, S_LOG ** 2, list(range(3)), 0,
-                  "f32 log u35"),
-    "powlog_f": (log_target(), log_weight(), 0, S_LOG ** 2, list(range(5)), 0,
-                 "f32 pow-internal log(m)"),
-    "powexp_f": (exp1_target(), exp1_weight(), -R_EXP, R_EXP, list(range(8)), 0,
-                 "f32 pow-internal exp(r) = 1 + r*P(r)"),
-    "powlog_f_u35": (log_target(), log_weight(), 0, S_LOG ** 2, list(range(4)), 0,
-                     "f32 pow u35 log(m)"),
-    "powexp_f_u35": (exp1_target(), exp1_weight(), -R_EXP, R_EXP, list(range(6)), 0,
-                     "f32 pow u35 exp(r)"),
 }
 
 

@@ -167,15 +167,38 @@ def fit_rounded(g, w, a, b, powers, dd_terms=0, ngrid=3000, prec=192, lead_fixed
             # shrink reference to n+1 points for the smaller system
             ref = None
             idx += 1
-        # evaluate final error
-        maxe = mp.mpf(0)
-        for k, x in enumerate(grid):
-            s = mp.mpf(0)
-            for p, cv in fixed:
-                s += cv * x ** p
-            e = abs(wv[k] * (s - gv[k]))
-            if e > maxe:
-                maxe = e
+        def grid_err(fx):
+            m = mp.mpf(0)
+            for k, x in enumerate(grid):
+                s = mp.mpf(0)
+                for p, cv in fx:
+                    s += cv * x ** p
+                e = abs(wv[k] * (s - gv[k]))
+                if e > m:
+                    m = e
+            return m
+
+        maxe = grid_err(fixed)
+        # alternative: round the unconstrained minimax fit directly; keep
+        # whichever rounded coefficient set has the smaller grid error
+        base = [(p, mp.mpf(v)) for p, v in (lead_fixed or {}).items()]
+        free0 = [p for p in powers if p not in dict(base)]
+        c_all, _, _ = remez(gv, wv, grid, free0, fixed=base)
+        alt_fixed = list(base)
+        alt_out = []
+        for i, p in enumerate(free0):
+            if i < dd_terms:
+                hi, lo = to_dd(c_all[i])
+                alt_fixed.append((p, mp.mpf(hi) + mp.mpf(lo)))
+                alt_out.append((p, hi, lo))
+            else:
+                hi = to_double(c_all[i])
+                alt_fixed.append((p, mp.mpf(hi)))
+                alt_out.append((p, hi, None))
+        alt_e = grid_err(alt_fixed)
+        if alt_e < maxe:
+            maxe = alt_e
+            out = alt_out
         if lead_fixed:
             for p, v in lead_fixed.items():
                 out.append((p, float(v), None))
