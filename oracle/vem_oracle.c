@@ -71,8 +71,13 @@ static inline float canon_f(float y) { return (y != y) ? from_bits_f(CANON_NAN_F
 
 static const double PH_D[4 * VEM_PH_D_ENTRIES] = {VEM_PH_D_INIT};
 static const double PH_F[3 * VEM_PH_F_ENTRIES] = {VEM_PH_F_INIT};
-static const double LOGT[4 * 256] = {VEM_LOGT_INIT};
-static const double EXPT[2 * 128] = {VEM_EXPT_INIT};
+static const double LOGT_INVC[256] = {VEM_LOGT_INVC_INIT};
+static const double LOGT_HI[256] = {VEM_LOGT_HI_INIT};
+static const double LOGT_LO[256] = {VEM_LOGT_LO_INIT};
+static const double EXPT_HI[128] = {VEM_EXPT_HI_INIT};
+static const double EXPT_LO[128] = {VEM_EXPT_LO_INIT};
+static const double LOGTF_HI[256] = {VEM_LOGTF_HI_INIT};
+static const float LOGTF_INVC[256] = {VEM_LOGTF_INVC_INIT};
 
 /* ------------------------------------------- primitives (backend.hpp) */
 /* backend.hpp:47-52 round_ta: nearest integer, ties away from zero */
@@ -162,20 +167,16 @@ static inline dd_t dd_div(dd_t x, dd_t y) { /* ddarith.hpp:220-228 (FMA) */
 }
 static inline dd_t dd_normalize(dd_t x) { return two_sum_fast(x.hi, x.lo); } /* ddarith.hpp:103 */
 
-/* Estrin evaluation with fixed bracketing; the CUDA
- * kernels (vem_math.cuh: vem_estrin) apply the identical pairing. */
-static inline double estrin(const double* c, int n, double x) {
-  double t[24];
-  for (int i = 0; i < n; i++) t[i] = c[i];
-  double p = x;
-  while (n > 1) {
-    int m = 0;
-    for (int i = 0; i + 1 < n; i += 2) t[m++] = fma(t[i + 1], p, t[i]);
-    if (n & 1) t[m++] = t[n - 1];
-    n = m;
-    if (n > 1) p = p * p;
-  }
-  return t[0];
+/* Polynomial evaluation: Horner, c[0] + x*(c[1] + x*(...)).  The paper uses
+ * Estrin's scheme to cut FMA latency on out-of-order CPUs;
+ * on the GPU the kernels are throughput-bound with thousands of independent
+ * lanes in flight, and Horner issues the fewest instructions (n-1 FMAs, one
+ * constant-bank operand each, no power precomputation).  The CUDA kernels
+ * (vem_math.cuh: poly) use the identical order. */
+static inline double poly(const double* c, int n, double x) {
+  double acc = c[n - 1];
+  for (int i = n - 2; i >= 0; i--) acc = fma(acc, x, c[i]);
+  return acc;
 }
 
 /* ============================================ trig reduction (f64) */
@@ -307,7 +308,7 @@ static double sincos_core_d(double rh, double rl, int cosform) {
   double c[VEM_SIN_D_N];
   for (int i = 0; i < VEM_SIN_D_N; i++) c[i] = cosform ? C_COS_D[i] : C_SIN_D[i];
   double z = rh * rh;
-  double P = estrin(c, VEM_SIN_D_N, z);
+  double P = poly(c, VEM_SIN_D_N, z);
   /* sin form: rh + (rl - rl*z/2 + rh*z*P) */
   double As = rh, Bs = 0.0, Ms = rh * z, Ts = fma(-0.5 * z, rl, rl);
   /* cos form: w + (((1-w) - z/2) + (z^2*P - (zl/2 + rh*rl))), w = 1 - z/2 */
@@ -351,7 +352,7 @@ double vo_cos_d_u10_ph(double x) {
 static double tan_core_d(double rh, double rl, int odd) {
   double hh = rh * 0.5, hl = rl * 0.5;
   double z = hh * hh;
-  double P = estrin(C_TAN_D, VEM_TAN_D_N, z);
+  double P = poly(C_TAN_D, VEM_TAN_D_N, z);
   double corr = fma(hh * z, P, fma(hl, z, hl));
   dd_t t = two_sum_fast(hh, corr);
   dd_t t2 = dd_squ(t);
@@ -402,7 +403,7 @@ double vo_atan_d_u10(double x) {
   dn.lo = c2 ? 0.0 : (c1 ? ds.lo : 0.0);
   dd_t b = dd_div(nn, dn);
   double z = b.hi * b.hi;
-  double P = estrin(C_ATAN_D, VEM_ATAN_D_N, z);
+  double P = poly(C_ATAN_D, VEM_ATAN_D_N, z);
   double corr = fma(b.hi * z, P, fma(-b.lo, z, b.lo));
   double offh = c2 ? K_PIO2_QD0 : (c1 ? K_PIO4_HI : 0.0);
   double offl = c2 ? K_PIO2_QD1 : (c1 ? K_PIO4_LO : 0.0);
@@ -424,7 +425,7 @@ static inline double exp_poly_d(double xs, const double* c, int n, int u10, doub
   double kd = rint(xs * K_INV_LN2);
   double r1 = fma(kd, -K_EXP_L1, xs);
   double r = fma(kd, -K_EXP_L2, r1);
-  double P = estrin(c, n, r);
+  double P = poly(c, n, r);
   double y;
   if (u10) {
     double rl = fma(-kd, K_EXP_L2, r1 - r);
@@ -478,21 +479,21 @@ static inline logred_t log_reduce(double a, double Eadj) {
   int64_t k = (int64_t)tmp >> 52;
   int idx = (int)((tmp >> 44) & 255u);
   double m = from_bits_d(ix - ((uint64_t)k << 52));
-  const double* t = LOGT + 4 * idx;
-  double p = m * t[0];
+  double invc = LOGT_INVC[idx];
+  double p = m * invc;
   logred_t o;
-  o.rl = fma(m, t[0], -p);
+  o.rl = fma(m, invc, -p);
   o.rh = p - 1.0;
   o.E = (double)k + Eadj;
-  o.logc_hi = t[1];
-  o.logc_lo = t[2];
+  o.logc_hi = LOGT_HI[idx];
+  o.logc_lo = LOGT_LO[idx];
   return o;
 }
 
 /* log1p(rh + rl) as DD: rh - rh^2/2 (exact) + rh^3 Q(rh) + rl(1 - rh) */
 static inline dd_t log1p_dd(double rh, double rl, const double* c, int n) {
   double z = rh * rh;
-  double Q = estrin(c, n, rh);
+  double Q = poly(c, n, rh);
   double t3 = (rh * z) * Q;
   double h2 = -0.5 * rh;
   double p2 = rh * h2;
@@ -519,7 +520,7 @@ static double log_fast_d(double a, double Eadj, int u10) {
     L = log1p_dd(g.rh, g.rl, C_LOG1P_D, VEM_LOG1P_D_N);
   } else {
     double z = g.rh * g.rh;
-    double Q = estrin(C_LOG1P_D_U35, VEM_LOG1P_D_U35_N, g.rh);
+    double Q = poly(C_LOG1P_D_U35, VEM_LOG1P_D_U35_N, g.rh);
     L.hi = g.rh;
     L.lo = fma(z, fma(g.rh, Q, -0.5), g.rl);
   }
@@ -567,12 +568,12 @@ static double exp_dd(dd_t t) {
   double r2 = fma(kd, -VEM_EXPJ_L2, tl);
   dd_t r = two_sum(r1, r2);
   double z = r.hi * r.hi;
-  double Q = estrin(C_EXPJ_D, VEM_EXPJ_D_N, r.hi);
+  double Q = poly(C_EXPJ_D, VEM_EXPJ_D_N, r.hi);
   double s2 = z * fma(r.hi, Q, 0.5);
   double em1l = r.lo + fma(r.hi, r.lo, s2);
-  const double* T = EXPT + 2 * (k & 127);
-  double u = fma(T[0], r.hi, fma(T[0], em1l, T[1]));
-  double R = T[0] + u;
+  double Th = EXPT_HI[k & 127], Tl = EXPT_LO[k & 127];
+  double u = fma(Th, r.hi, fma(Th, em1l, Tl));
+  double R = Th + u;
   int64_t e = k >> 7;
   if (fast) return from_bits_d(bits_d(R) + ((uint64_t)e << 52));
   double y = ldexp2(R, e);
@@ -719,7 +720,7 @@ static double sincos_core_f(double r, int cosform) {
   for (int i = 0; i < 4; i++) c[i] = cosform ? (i == 0 ? -0.5 : C_COS_F[i - 1]) : C_SIN_F[i];
   c[4] = cosform ? C_COS_F[3] : 0.0;
   double z = r * r;
-  double P = estrin(c, 5, z);
+  double P = poly(c, 5, z);
   double A = cosform ? 1.0 : r;
   return fma(A * z, P, A);
 }
@@ -742,7 +743,7 @@ float vo_cos_f_u10(float x) {
 float vo_tan_f_u10(float x) {
   redf_t r = ph_f(x);
   double z = r.r * r.r;
-  double P = estrin(C_TAN_F, VEM_TAN_F_N, z);
+  double P = poly(C_TAN_F, VEM_TAN_F_N, z);
   double t = fma(r.r * z, P, r.r);
   double y = (r.q & 1) ? -1.0 / t : t;
   float o = (float)y;
@@ -756,7 +757,7 @@ static float exp_core_f(float x, const double* c, int n) {
   double kd = rint(xd * K_INV_LN2);
   double r = fma(kd, -K_EXP_L1, xd);
   r = fma(kd, -K_EXP_L2, r);
-  double P = estrin(c, n, r);
+  double P = poly(c, n, r);
   double y = fma(r, P, 1.0);
   y = y * pow2_bits((int64_t)kd);
   float o = (float)y;
@@ -774,11 +775,10 @@ static inline double log_f_internal(double a, const double* c, int n) {
   int64_t k = (int64_t)tmp >> 52;
   int idx = (int)((tmp >> 44) & 255u);
   double m = from_bits_d(ix - ((uint64_t)k << 52));
-  const double* t = LOGT + 4 * idx;
-  double r = fma(m, t[0], -1.0);
-  double Q = estrin(c, n, r);
+  double r = fma(m, (double)LOGTF_INVC[idx], -1.0); /* exact: 24 x 24 bits */
+  double Q = poly(c, n, r);
   double L = fma(r * r, Q, r);
-  return fma((double)k, K_LN2_HI, t[1] + L);
+  return fma((double)k, K_LN2_HI, LOGTF_HI[idx] + L);
 }
 static float log_core_f(float x, const double* c, int n) {
   uint32_t ux = bits_f(x);
@@ -801,7 +801,8 @@ static inline double exp_f_internal(double t) {
   double r = fma(kd, -VEM_EXPJ_L1, t);
   r = fma(kd, -VEM_EXPJ_L2, r);
   double p = fma(r * r, fma(r, 0x1.5555555555555p-3, 0.5), r);
-  double R = fma(EXPT[2 * (k & 127)], p, EXPT[2 * (k & 127)]);
+  double T = EXPT_HI[k & 127];
+  double R = fma(T, p, T);
   return from_bits_d(bits_d(R) + ((uint64_t)(k >> 7) << 52));
 }
 static float pow_core_f(float x, float y, const double* cl, int nl) {

@@ -38,10 +38,14 @@ __device__ __forceinline__ const double* stage_table(double* stab) {
     return nullptr;
   } else {
     const double* src = TABLE == kTableD ? gPhD : (TABLE == kTableF ? gPhF : gLogExp);
-    constexpr int n2 = TableSize<TABLE>::n / 2;
+    constexpr int n2 = (TABLE == kTableLog ? kLogTabD : TableSize<TABLE>::n) / 2;
     const double2* s2 = reinterpret_cast<const double2*>(src);
     double2* d2 = reinterpret_cast<double2*>(stab);
     for (int i = threadIdx.x; i < n2; i += blockDim.x) d2[i] = __ldg(s2 + i);
+    if constexpr (TABLE == kTableLog) {
+      const double2* f2 = reinterpret_cast<const double2*>(gLogTfInvc);
+      for (int i = threadIdx.x; i < 64; i += blockDim.x) d2[kLtfInvc / 2 + i] = __ldg(f2 + i);
+    }
     __syncthreads();
     return stab;
   }

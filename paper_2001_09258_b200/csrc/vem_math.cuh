@@ -87,10 +87,15 @@ __constant__ double cLog1pFU35[] = VEM_LOG1P_F_U35_ARR;
 // Payne-Hanek tables (global copy; kernels stage them into shared memory).
 __device__ const double gPhD[4 * VEM_PH_D_ENTRIES] = {VEM_PH_D_INIT};
 __device__ const double gPhF[3 * VEM_PH_F_ENTRIES] = {VEM_PH_F_INIT};
-// log / exp tables (tools/genlogtables.py), staged together: LOGT quads then
-// EXPT pairs.
-constexpr int kLogTabN = 4 * 256 + 2 * 128;
-__device__ const double gLogExp[kLogTabN] = {VEM_LOGT_INIT VEM_EXPT_INIT};
+// log / exp tables (tools/genlogtables.py), structure of arrays, staged into
+// one shared-memory block (offsets in doubles):
+constexpr int kLtInvc = 0, kLtHi = 256, kLtLo = 512, kLtExpHi = 768, kLtExpLo = 896, kLtfHi = 1024,
+              kLtfInvc = 1280;  // 256 floats = 128 doubles
+constexpr int kLogTabD = 1280;
+constexpr int kLogTabN = kLogTabD + 128;
+__device__ const double gLogExp[kLogTabD] = {VEM_LOGT_INVC_INIT VEM_LOGT_HI_INIT VEM_LOGT_LO_INIT
+                                                 VEM_EXPT_HI_INIT VEM_EXPT_LO_INIT VEM_LOGTF_HI_INIT};
+__device__ const float gLogTfInvc[256] = {VEM_LOGTF_INVC_INIT};
 
 // ---------------------------------------------------- primitives
 // backend.hpp:47-52 round_ta == CUDA round() (ties away from zero) for every
@@ -165,49 +170,22 @@ __device__ __forceinline__ dd dd_div(dd x, dd y) {
 }
 __device__ __forceinline__ dd dd_normalize(dd x) { return two_sum_fast(x.hi, x.lo); }
 
-// Estrin with the oracle's fixed bracketing (oracle/vem_oracle.c: estrin).
+// Horner, the oracle's order (oracle/vem_oracle.c: poly): n-1 DFMAs, each
+// with its coefficient as a constant-bank operand.
 template <int N>
-__device__ __forceinline__ double estrin(const double* c, double x) {
-  double t[N];
+__device__ __forceinline__ double poly(const double* c, double x) {
+  double acc = c[N - 1];
 #pragma unroll
-  for (int i = 0; i < N; i++) t[i] = c[i];
-  double p = x;
-  int n = N;
-#pragma unroll
-  for (int lvl = 0; lvl < 6; lvl++) {
-    if (n > 1) {
-      int m = 0;
-#pragma unroll
-      for (int i = 0; i + 1 < N; i += 2)
-        if (i + 1 < n) t[m++] = fma(t[i + 1], p, t[i]);
-      if (n & 1) t[m++] = t[n - 1];
-      n = m;
-      if (n > 1) p = p * p;
-    }
-  }
-  return t[0];
+  for (int i = N - 2; i >= 0; i--) acc = fma(acc, x, c[i]);
+  return acc;
 }
 // Same with per-lane selected coefficients (a ? ca[i] : cb[i]).
 template <int N>
-__device__ __forceinline__ double estrin_sel(const double* ca, const double* cb, bool a, double x) {
-  double t[N];
+__device__ __forceinline__ double poly_sel(const double* ca, const double* cb, bool a, double x) {
+  double acc = a ? ca[N - 1] : cb[N - 1];
 #pragma unroll
-  for (int i = 0; i < N; i++) t[i] = a ? ca[i] : cb[i];
-  double p = x;
-  int n = N;
-#pragma unroll
-  for (int lvl = 0; lvl < 6; lvl++) {
-    if (n > 1) {
-      int m = 0;
-#pragma unroll
-      for (int i = 0; i + 1 < N; i += 2)
-        if (i + 1 < n) t[m++] = fma(t[i + 1], p, t[i]);
-      if (n & 1) t[m++] = t[n - 1];
-      n = m;
-      if (n > 1) p = p * p;
-    }
-  }
-  return t[0];
+  for (int i = N - 2; i >= 0; i--) acc = fma(acc, x, a ? ca[i] : cb[i]);
+  return acc;
 }
 
 // ===================================================== reduction (f64)
@@ -321,7 +299,7 @@ __device__ __forceinline__ red trig_reduce(double x, const double* __restrict__ 
 __device__ __forceinline__ double sincos_core_d(double rh, double rl, int cosform) {
   bool cf = cosform != 0;
   double z = rh * rh;
-  double P = estrin_sel<VEM_SIN_D_N>(cCosD, cSinD, cf, z);
+  double P = poly_sel<VEM_SIN_D_N>(cCosD, cSinD, cf, z);
   double As = rh, Bs = 0.0, Ms = rh * z, Ts = fma(-0.5 * z, rl, rl);
   double zl = fma(rh, rh, -z);
   double hz = 0.5 * z;
@@ -350,7 +328,7 @@ __device__ __forceinline__ double cos_d_u10(double x, const double* tab) {
 __device__ __forceinline__ double tan_core_d(double rh, double rl, int odd) {
   double hh = rh * 0.5, hl = rl * 0.5;
   double z = hh * hh;
-  double P = estrin<VEM_TAN_D_N>(cTanD, z);
+  double P = poly<VEM_TAN_D_N>(cTanD, z);
   double corr = fma(hh * z, P, fma(hl, z, hl));
   dd t = two_sum_fast(hh, corr);
   dd t2 = dd_squ(t);
@@ -383,7 +361,7 @@ __device__ __forceinline__ double atan_d_u10(double x) {
   dn.lo = c2 ? 0.0 : (c1 ? ds.lo : 0.0);
   dd b = dd_div(nn, dn);
   double z = b.hi * b.hi;
-  double P = estrin<VEM_ATAN_D_N>(cAtanD, z);
+  double P = poly<VEM_ATAN_D_N>(cAtanD, z);
   double corr = fma(b.hi * z, P, fma(-b.lo, z, b.lo));
   double offh = c2 ? kPio2Qd0 : (c1 ? kPio4Hi : 0.0);
   double offl = c2 ? kPio2Qd1 : (c1 ? kPio4Lo : 0.0);
@@ -401,7 +379,7 @@ __device__ __forceinline__ double exp_poly_d(double xs, const double* c, double&
   double kd = rint(xs * kInvLn2);
   double r1 = fma(kd, -kExpL1, xs);
   double r = fma(kd, -kExpL2, r1);
-  double P = estrin<N>(c, r);
+  double P = poly<N>(c, r);
   double y;
   if (kU10) {
     double rl = fma(-kd, kExpL2, r1 - r);
@@ -445,23 +423,21 @@ __device__ __forceinline__ logred log_reduce(double a, double Eadj, const double
   long long k = (long long)tmp >> 52;
   int idx = (int)((tmp >> 44) & 255u);
   double m = from_bits_d(ix - ((uint64_t)k << 52));
-  const double2* t2 = reinterpret_cast<const double2*>(lt + 4 * idx);
-  double2 e0 = t2[0];
-  double logc_lo = lt[4 * idx + 2];
-  double p = m * e0.x;
+  double invc = lt[kLtInvc + idx];
+  double p = m * invc;
   logred o;
-  o.rl = fma(m, e0.x, -p);
+  o.rl = fma(m, invc, -p);
   o.rh = p - 1.0;
   o.E = (double)k + Eadj;
-  o.logc_hi = e0.y;
-  o.logc_lo = logc_lo;
+  o.logc_hi = lt[kLtHi + idx];
+  o.logc_lo = lt[kLtLo + idx];
   return o;
 }
 
 template <int N>
 __device__ __forceinline__ dd log1p_dd(double rh, double rl, const double* c) {
   double z = rh * rh;
-  double Q = estrin<N>(c, rh);
+  double Q = poly<N>(c, rh);
   double t3 = (rh * z) * Q;
   double h2 = -0.5 * rh;
   double p2 = rh * h2;
@@ -488,7 +464,7 @@ __device__ __forceinline__ double log_fast_d(double a, double Eadj, const double
     L = log1p_dd<VEM_LOG1P_D_N>(g.rh, g.rl, cLog1pD);
   } else {
     double z = g.rh * g.rh;
-    double Q = estrin<VEM_LOG1P_D_U35_N>(cLog1pDU35, g.rh);
+    double Q = poly<VEM_LOG1P_D_U35_N>(cLog1pDU35, g.rh);
     L.hi = g.rh;
     L.lo = fma(z, fma(g.rh, Q, -0.5), g.rl);
   }
@@ -515,7 +491,6 @@ __device__ __forceinline__ dd log_dd(double a, double Eadj, const double* c, con
 }
 
 __device__ __forceinline__ double exp_dd(dd t, const double* __restrict__ lt) {
-  const double* expt = lt + 4 * 256;
   double th = t.hi, tl = t.lo;
   uint32_t hx = (uint32_t)__double2hiint(th) & 0x7fffffffu;
   bool fast = hx < kExpFastHi;
@@ -530,12 +505,12 @@ __device__ __forceinline__ double exp_dd(dd t, const double* __restrict__ lt) {
   double r2 = fma(kd, -VEM_EXPJ_L2, tl);
   dd r = two_sum(r1, r2);
   double z = r.hi * r.hi;
-  double Q = estrin<VEM_EXPJ_D_N>(cExpjD, r.hi);
+  double Q = poly<VEM_EXPJ_D_N>(cExpjD, r.hi);
   double s2 = z * fma(r.hi, Q, 0.5);
   double em1l = r.lo + fma(r.hi, r.lo, s2);
-  double2 T = reinterpret_cast<const double2*>(expt)[k & 127];
-  double u = fma(T.x, r.hi, fma(T.x, em1l, T.y));
-  double R = T.x + u;
+  double Th = lt[kLtExpHi + (k & 127)], Tl = lt[kLtExpLo + (k & 127)];
+  double u = fma(Th, r.hi, fma(Th, em1l, Tl));
+  double R = Th + u;
   long long e = k >> 7;
   if (fast) return from_bits_d(bits_d(R) + ((uint64_t)e << 52));
   double y = ldexp2(R, e);
@@ -675,7 +650,7 @@ __device__ __forceinline__ double sincos_core_f(double r, int cosform) {
   double c4 = cf ? cCosF[3] : 0.0;
   double c[5] = {c0, c1, c2, c3, c4};
   double z = r * r;
-  double P = estrin<5>(c, z);
+  double P = poly<5>(c, z);
   double A = cf ? 1.0 : r;
   return fma(A * z, P, A);
 }
@@ -698,7 +673,7 @@ __device__ __forceinline__ float cos_f_u10(float x, const double* tab) {
 __device__ __forceinline__ float tan_f_u10(float x, const double* tab) {
   redf r = ph_f(x, tab);
   double z = r.r * r.r;
-  double P = estrin<VEM_TAN_F_N>(cTanF, z);
+  double P = poly<VEM_TAN_F_N>(cTanF, z);
   double t = fma(r.r * z, P, r.r);
   double y = (r.q & 1) ? -1.0 / t : t;
   float o = (float)y;
@@ -713,7 +688,7 @@ __device__ __forceinline__ float exp_core_f(float x, const double* c) {
   double kd = rint(xd * kInvLn2);
   double r = fma(kd, -kExpL1, xd);
   r = fma(kd, -kExpL2, r);
-  double P = estrin<N>(c, r);
+  double P = poly<N>(c, r);
   double y = fma(r, P, 1.0);
   y = y * pow2_bits((long long)kd);
   float o = (float)y;
@@ -729,11 +704,10 @@ __device__ __forceinline__ double log_f_internal(double a, const double* c, cons
   long long k = (long long)tmp >> 52;
   int idx = (int)((tmp >> 44) & 255u);
   double m = from_bits_d(ix - ((uint64_t)k << 52));
-  double2 t = reinterpret_cast<const double2*>(lt + 4 * idx)[0];
-  double r = fma(m, t.x, -1.0);
-  double Q = estrin<N>(c, r);
+  double r = fma(m, (double)reinterpret_cast<const float*>(lt + kLtfInvc)[idx], -1.0);
+  double Q = poly<N>(c, r);
   double L = fma(r * r, Q, r);
-  return fma((double)k, kLn2Hi, t.y + L);
+  return fma((double)k, kLn2Hi, lt[kLtfHi + idx] + L);
 }
 template <int N>
 __device__ __forceinline__ float log_core_f(float x, const double* c, const double* lt) {
@@ -751,13 +725,12 @@ __device__ __forceinline__ bool is_odd_f(float y) {
   return is_int_f(y) && (fabsf(y) < 0x1p24f) && (truncf(y * 0.5f) * 2.0f != y);
 }
 __device__ __forceinline__ double exp_f_internal(double t, const double* __restrict__ lt) {
-  const double* expt = lt + 4 * 256;
   double kd = rint(t * VEM_EXPJ_INV);
   long long k = (long long)kd;
   double r = fma(kd, -VEM_EXPJ_L1, t);
   r = fma(kd, -VEM_EXPJ_L2, r);
   double p = fma(r * r, fma(r, 0x1.5555555555555p-3, 0.5), r);
-  double T = expt[2 * (k & 127)];
+  double T = lt[kLtExpHi + (k & 127)];
   double R = fma(T, p, T);
   return from_bits_d(bits_d(R) + ((uint64_t)(k >> 7) << 52));
 }
