@@ -104,6 +104,14 @@ static inline double copysign_b(double m, double s) {
 static inline double neg_if(double y, int c) {
   return from_bits_d(bits_d(y) ^ ((uint64_t)(c != 0) << 63));
 }
+/* nearest integer of a*b by one fma against 1.5*2^52 (ties-to-even of the
+ * exactly rounded product+shift); |a*b| < 2^31.  k = the low word. */
+#define K_SHIFT 0x1.8p52
+static inline double rint_fma(double a, double b, int32_t* k) {
+  double u = fma(a, b, K_SHIFT);
+  *k = (int32_t)(uint32_t)bits_d(u);
+  return u - K_SHIFT;
+}
 /* backend.hpp:418-423 toward_zero for positive finite x */
 static inline double toward0_pos(double x) { return from_bits_d(bits_d(x) - 1); }
 
@@ -421,8 +429,8 @@ double vo_atan_d_u10(double x) {
  * (backend.hpp:133-138, single rounding into subnormals) and saturation
  * (constants.hpp:53-54); NaN in, canonical NaN out. */
 #define EXP_FAST_HI 0x40862000u /* |x| < 708 */
-static inline double exp_poly_d(double xs, const double* c, int n, int u10, double* kd_out) {
-  double kd = rint(xs * K_INV_LN2);
+static inline double exp_poly_d(double xs, const double* c, int n, int u10, int32_t* k_out) {
+  double kd = rint_fma(xs, K_INV_LN2, k_out);
   double r1 = fma(kd, -K_EXP_L1, xs);
   double r = fma(kd, -K_EXP_L2, r1);
   double P = poly(c, n, r);
@@ -435,20 +443,19 @@ static inline double exp_poly_d(double xs, const double* c, int n, int u10, doub
   } else {
     y = 1.0 + fma(r * r, P, r);
   }
-  *kd_out = kd;
   return y;
 }
 static double exp_core_d(double x, const double* c, int n, int u10) {
   uint32_t hx = (uint32_t)(bits_d(x) >> 32) & 0x7fffffffu;
-  double kd;
+  int32_t k;
   if (hx < EXP_FAST_HI) {
-    double y = exp_poly_d(x, c, n, u10, &kd);
-    return from_bits_d(bits_d(y) + ((uint64_t)(int64_t)kd << 52));
+    double y = exp_poly_d(x, c, n, u10, &k);
+    return from_bits_d(bits_d(y) + ((uint64_t)(int64_t)k << 52));
   }
   int ok = (x >= K_EXP_UNF) && (x <= K_EXP_OVF);
   double xs = ok ? x : 0.0;
-  double y = exp_poly_d(xs, c, n, u10, &kd);
-  y = ldexp2(y, (int64_t)kd);
+  double y = exp_poly_d(xs, c, n, u10, &k);
+  y = ldexp2(y, (int64_t)k);
   y = (x > K_EXP_OVF) ? INFINITY : y;
   y = (x < K_EXP_UNF) ? 0.0 : y;
   y = (x != x) ? from_bits_d(CANON_NAN_D) : y;
@@ -484,7 +491,7 @@ static inline logred_t log_reduce(double a, double Eadj) {
   logred_t o;
   o.rl = fma(m, invc, -p);
   o.rh = p - 1.0;
-  o.E = (double)k + Eadj;
+  o.E = (double)(int32_t)k + Eadj;
   o.logc_hi = LOGT_HI[idx];
   o.logc_lo = LOGT_LO[idx];
   return o;
@@ -546,7 +553,11 @@ static inline dd_t log_dd(double a, double Eadj, const double* c, int n) {
   logred_t g = log_reduce(a, Eadj);
   dd_t H = eln2_logc(&g);
   dd_t L = log1p_dd(g.rh, g.rl, c, n);
-  return dd_add2(H, L);
+  /* |H.hi| >= |L.hi| or H.hi == 0 (E != 0: |H| > ln2 - 0.41; E = 0: |logc|
+   * exceeds the interval half-width except c = 1 where logc = 0) */
+  dd_t S = two_sum_fast(H.hi, L.hi);
+  S.lo = S.lo + (H.lo + L.lo);
+  return S;
 }
 
 /* exp of a double-double t with a 128-entry 2^(i/128) table (EXPT):
@@ -562,11 +573,11 @@ static double exp_dd(dd_t t) {
     th = ok ? th : 0.0;
     tl = ok ? tl : 0.0;
   }
-  double kd = rint(th * VEM_EXPJ_INV);
-  int64_t k = (int64_t)kd;
+  int32_t k;
+  double kd = rint_fma(th, VEM_EXPJ_INV, &k);
   double r1 = fma(kd, -VEM_EXPJ_L1, th);
   double r2 = fma(kd, -VEM_EXPJ_L2, tl);
-  dd_t r = two_sum(r1, r2);
+  dd_t r = two_sum_fast(r1, r2); /* |r2| <~ 2^-26; if |r1| < |r2| the error is < 2^-79 */
   double z = r.hi * r.hi;
   double Q = poly(C_EXPJ_D, VEM_EXPJ_D_N, r.hi);
   double s2 = z * fma(r.hi, Q, 0.5);
@@ -574,9 +585,9 @@ static double exp_dd(dd_t t) {
   double Th = EXPT_HI[k & 127], Tl = EXPT_LO[k & 127];
   double u = fma(Th, r.hi, fma(Th, em1l, Tl));
   double R = Th + u;
-  int64_t e = k >> 7;
-  if (fast) return from_bits_d(bits_d(R) + ((uint64_t)e << 52));
-  double y = ldexp2(R, e);
+  int32_t e = k >> 7;
+  if (fast) return from_bits_d(bits_d(R) + ((uint64_t)(int64_t)e << 52));
+  double y = ldexp2(R, (int64_t)e);
   y = (t.hi > K_EXP_OVF) ? INFINITY : y;
   y = (t.hi < K_EXP_UNF) ? 0.0 : y;
   return y;
@@ -592,9 +603,10 @@ static inline int is_odd_d(double y) {
  * finite, y finite nonzero -- no special-case logic at all.  Slow path:
  * subnormal/negative x and every C99 special value. */
 static double pow_core_d(double x, double y, const double* cl, int nl) {
-  uint64_t ux = bits_d(x), uy = bits_d(y);
-  int fx = (ux - 0x0010000000000000ull) < 0x7fe0000000000000ull;
-  int fy = ((uy & 0x7fffffffffffffffull) - 1ull) < 0x7fefffffffffffffull;
+  uint32_t hx = (uint32_t)(bits_d(x) >> 32);
+  uint32_t hy = (uint32_t)(bits_d(y) >> 32) & 0x7fffffffu, ly = (uint32_t)bits_d(y);
+  int fx = (hx - 0x00100000u) < 0x7fe00000u;           /* x positive normal finite */
+  int fy = (hy < 0x7ff00000u) && ((hy | ly) != 0u);     /* y finite, nonzero */
   if (fx && fy) return exp_dd(dd_mul_d(log_dd(x, 0.0, cl, nl), y));
   double ax = fabs(x);
   int fin = (ax > 0.0) && (ax < INFINITY) && (fabs(y) < INFINITY);
@@ -754,12 +766,13 @@ float vo_tan_f_u10(float x) {
 static float exp_core_f(float x, const double* c, int n) {
   float xc = fminf(fmaxf(x, -150.0f), 130.0f);
   double xd = (double)xc;
-  double kd = rint(xd * K_INV_LN2);
+  int32_t k;
+  double kd = rint_fma(xd, K_INV_LN2, &k);
   double r = fma(kd, -K_EXP_L1, xd);
   r = fma(kd, -K_EXP_L2, r);
   double P = poly(c, n, r);
   double y = fma(r, P, 1.0);
-  y = y * pow2_bits((int64_t)kd);
+  y = from_bits_d(bits_d(y) + ((uint64_t)(int64_t)k << 52)); /* |k| <= 217: normal */
   float o = (float)y;
   return canon_f((x != x) ? x : o);
 }
@@ -778,7 +791,7 @@ static inline double log_f_internal(double a, const double* c, int n) {
   double r = fma(m, (double)LOGTF_INVC[idx], -1.0); /* exact: 24 x 24 bits */
   double Q = poly(c, n, r);
   double L = fma(r * r, Q, r);
-  return fma((double)k, K_LN2_HI, LOGTF_HI[idx] + L);
+  return fma((double)(int32_t)k, K_LN2_HI, LOGTF_HI[idx] + L);
 }
 static float log_core_f(float x, const double* c, int n) {
   uint32_t ux = bits_f(x);
@@ -796,14 +809,14 @@ static inline int is_odd_f(float y) {
 }
 /* exp(t) for the f32 pow, |t| <= 200: EXPT hi limb x (1 + r + r^2/2 + r^3/6) */
 static inline double exp_f_internal(double t) {
-  double kd = rint(t * VEM_EXPJ_INV);
-  int64_t k = (int64_t)kd;
+  int32_t k;
+  double kd = rint_fma(t, VEM_EXPJ_INV, &k);
   double r = fma(kd, -VEM_EXPJ_L1, t);
   r = fma(kd, -VEM_EXPJ_L2, r);
   double p = fma(r * r, fma(r, 0x1.5555555555555p-3, 0.5), r);
   double T = EXPT_HI[k & 127];
   double R = fma(T, p, T);
-  return from_bits_d(bits_d(R) + ((uint64_t)(k >> 7) << 52));
+  return from_bits_d(bits_d(R) + ((uint64_t)(int64_t)(k >> 7) << 52));
 }
 static float pow_core_f(float x, float y, const double* cl, int nl) {
   uint32_t ux = bits_f(x), uy = bits_f(y);

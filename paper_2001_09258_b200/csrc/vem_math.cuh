@@ -118,6 +118,13 @@ __device__ __forceinline__ double neg_if(double y, int c) {
   return from_bits_d(bits_d(y) ^ ((uint64_t)(c != 0) << 63));
 }
 __device__ __forceinline__ double toward0_pos(double x) { return from_bits_d(bits_d(x) - 1); }
+// nearest integer of a*b via one fma against 1.5*2^52 (oracle: rint_fma)
+constexpr double kShift = 0x1.8p52;
+__device__ __forceinline__ double rint_fma(double a, double b, int& k) {
+  double u = fma(a, b, kShift);
+  k = __double2loint(u);
+  return u - kShift;
+}
 
 // ------------------------------------------------------ DD (ddarith.hpp)
 __device__ __forceinline__ dd two_sum(double a, double b) {
@@ -375,8 +382,8 @@ __device__ __forceinline__ double atan_d_u10(double x) {
 constexpr uint32_t kExpFastHi = 0x40862000u;  // |x| < 708
 
 template <int N, bool kU10>
-__device__ __forceinline__ double exp_poly_d(double xs, const double* c, double& kd_out) {
-  double kd = rint(xs * kInvLn2);
+__device__ __forceinline__ double exp_poly_d(double xs, const double* c, int& k_out) {
+  double kd = rint_fma(xs, kInvLn2, k_out);
   double r1 = fma(kd, -kExpL1, xs);
   double r = fma(kd, -kExpL2, r1);
   double P = poly<N>(c, r);
@@ -389,22 +396,21 @@ __device__ __forceinline__ double exp_poly_d(double xs, const double* c, double&
   } else {
     y = 1.0 + fma(r * r, P, r);
   }
-  kd_out = kd;
   return y;
 }
 // oracle: exp_core_d.  Fast path: exponent-field scaling (result normal).
 template <int N, bool kU10>
 __device__ __forceinline__ double exp_core_d(double x, const double* c) {
   uint32_t hx = (uint32_t)__double2hiint(x) & 0x7fffffffu;
-  double kd;
+  int k;
   if (hx < kExpFastHi) {
-    double y = exp_poly_d<N, kU10>(x, c, kd);
-    return from_bits_d(bits_d(y) + ((uint64_t)(long long)kd << 52));
+    double y = exp_poly_d<N, kU10>(x, c, k);
+    return __hiloint2double(__double2hiint(y) + (k << 20), __double2loint(y));
   }
   bool ok = (x >= kExpUnf) && (x <= kExpOvf);
   double xs = ok ? x : 0.0;
-  double y = exp_poly_d<N, kU10>(xs, c, kd);
-  y = ldexp2(y, (long long)kd);
+  double y = exp_poly_d<N, kU10>(xs, c, k);
+  y = ldexp2(y, (long long)k);
   y = (x > kExpOvf) ? kInf : y;
   y = (x < kExpUnf) ? 0.0 : y;
   y = (x != x) ? from_bits_d(kCanonNanD) : y;
@@ -428,7 +434,7 @@ __device__ __forceinline__ logred log_reduce(double a, double Eadj, const double
   logred o;
   o.rl = fma(m, invc, -p);
   o.rh = p - 1.0;
-  o.E = (double)k + Eadj;
+  o.E = (double)(int)k + Eadj;
   o.logc_hi = lt[kLtHi + idx];
   o.logc_lo = lt[kLtLo + idx];
   return o;
@@ -487,7 +493,9 @@ __device__ __forceinline__ dd log_dd(double a, double Eadj, const double* c, con
   logred g = log_reduce(a, Eadj, lt);
   dd H = eln2_logc(g);
   dd L = log1p_dd<N>(g.rh, g.rl, c);
-  return dd_add2(H, L);
+  dd S = two_sum_fast(H.hi, L.hi);
+  S.lo = S.lo + (H.lo + L.lo);
+  return S;
 }
 
 __device__ __forceinline__ double exp_dd(dd t, const double* __restrict__ lt) {
@@ -499,11 +507,11 @@ __device__ __forceinline__ double exp_dd(dd t, const double* __restrict__ lt) {
     th = ok ? th : 0.0;
     tl = ok ? tl : 0.0;
   }
-  double kd = rint(th * VEM_EXPJ_INV);
-  long long k = (long long)kd;
+  int k;
+  double kd = rint_fma(th, VEM_EXPJ_INV, k);
   double r1 = fma(kd, -VEM_EXPJ_L1, th);
   double r2 = fma(kd, -VEM_EXPJ_L2, tl);
-  dd r = two_sum(r1, r2);
+  dd r = two_sum_fast(r1, r2);
   double z = r.hi * r.hi;
   double Q = poly<VEM_EXPJ_D_N>(cExpjD, r.hi);
   double s2 = z * fma(r.hi, Q, 0.5);
@@ -511,9 +519,9 @@ __device__ __forceinline__ double exp_dd(dd t, const double* __restrict__ lt) {
   double Th = lt[kLtExpHi + (k & 127)], Tl = lt[kLtExpLo + (k & 127)];
   double u = fma(Th, r.hi, fma(Th, em1l, Tl));
   double R = Th + u;
-  long long e = k >> 7;
-  if (fast) return from_bits_d(bits_d(R) + ((uint64_t)e << 52));
-  double y = ldexp2(R, e);
+  int e = k >> 7;
+  if (fast) return __hiloint2double(__double2hiint(R) + (e << 20), __double2loint(R));
+  double y = ldexp2(R, (long long)e);
   y = (t.hi > kExpOvf) ? kInf : y;
   y = (t.hi < kExpUnf) ? 0.0 : y;
   return y;
@@ -556,9 +564,10 @@ __device__ __noinline__ double pow_slow_d(double x, double y, const double* cl, 
 // oracle: pow_core_d (fast path without any special-value logic)
 template <int NL>
 __device__ __forceinline__ double pow_core_d(double x, double y, const double* cl, const double* lt) {
-  uint64_t ux = bits_d(x), uy = bits_d(y);
-  bool fx = (ux - 0x0010000000000000ull) < 0x7fe0000000000000ull;
-  bool fy = ((uy & 0x7fffffffffffffffull) - 1ull) < 0x7fefffffffffffffull;
+  uint32_t hx = (uint32_t)__double2hiint(x);
+  uint32_t hy = (uint32_t)__double2hiint(y) & 0x7fffffffu, ly = (uint32_t)__double2loint(y);
+  bool fx = (hx - 0x00100000u) < 0x7fe00000u;
+  bool fy = (hy < 0x7ff00000u) && ((hy | ly) != 0u);
   if (fx && fy) return exp_dd(dd_mul_d(log_dd<NL>(x, 0.0, cl, lt), y), lt);
   return pow_slow_d<NL>(x, y, cl, lt);
 }
@@ -685,12 +694,13 @@ template <int N>
 __device__ __forceinline__ float exp_core_f(float x, const double* c) {
   float xc = fminf(fmaxf(x, -150.0f), 130.0f);
   double xd = (double)xc;
-  double kd = rint(xd * kInvLn2);
+  int k;
+  double kd = rint_fma(xd, kInvLn2, k);
   double r = fma(kd, -kExpL1, xd);
   r = fma(kd, -kExpL2, r);
   double P = poly<N>(c, r);
   double y = fma(r, P, 1.0);
-  y = y * pow2_bits((long long)kd);
+  y = __hiloint2double(__double2hiint(y) + (k << 20), __double2loint(y));
   float o = (float)y;
   return canon_f((x != x) ? x : o);
 }
@@ -707,7 +717,7 @@ __device__ __forceinline__ double log_f_internal(double a, const double* c, cons
   double r = fma(m, (double)reinterpret_cast<const float*>(lt + kLtfInvc)[idx], -1.0);
   double Q = poly<N>(c, r);
   double L = fma(r * r, Q, r);
-  return fma((double)k, kLn2Hi, lt[kLtfHi + idx] + L);
+  return fma((double)(int)k, kLn2Hi, lt[kLtfHi + idx] + L);
 }
 template <int N>
 __device__ __forceinline__ float log_core_f(float x, const double* c, const double* lt) {
@@ -725,14 +735,14 @@ __device__ __forceinline__ bool is_odd_f(float y) {
   return is_int_f(y) && (fabsf(y) < 0x1p24f) && (truncf(y * 0.5f) * 2.0f != y);
 }
 __device__ __forceinline__ double exp_f_internal(double t, const double* __restrict__ lt) {
-  double kd = rint(t * VEM_EXPJ_INV);
-  long long k = (long long)kd;
+  int k;
+  double kd = rint_fma(t, VEM_EXPJ_INV, k);
   double r = fma(kd, -VEM_EXPJ_L1, t);
   r = fma(kd, -VEM_EXPJ_L2, r);
   double p = fma(r * r, fma(r, 0x1.5555555555555p-3, 0.5), r);
   double T = lt[kLtExpHi + (k & 127)];
   double R = fma(T, p, T);
-  return from_bits_d(bits_d(R) + ((uint64_t)(k >> 7) << 52));
+  return __hiloint2double(__double2hiint(R) + ((k >> 7) << 20), __double2loint(R));
 }
 template <int NL>
 __device__ __noinline__ float pow_slow_f(float x, float y, const double* cl, const double* lt) {
