@@ -638,46 +638,55 @@ double vo_pow_d_u10(double x, double y) { return pow_core_d(x, y, C_LOG1P_D, VEM
 double vo_pow_d_u35(double x, double y) { return pow_core_d(x, y, C_LOG1P_D_U35, VEM_LOG1P_D_U35_N); }
 
 /* fmod -- exact remainder by FP long division (Alg. 1, PAPER.md:958-975,
- * 1445-1469) restated for unbounded quotient ratios: each step divides by a
- * staged divisor D = d*2^k with r/D < 2^51, so the ratio never overflows
- * (SLEEF/the paper return NaN when |x/y| > DBL_MAX).
- * One division per call (1/ds, ds = d scaled into [1,2)); the quotient
- * estimate is forced low with nextafter-toward-zero steps and
- * the off-by-one resolved exactly with two candidate remainders. */
+ * 1445-1469), restated on normalised mantissas so the quotient ratio never
+ * overflows (SLEEF/the paper return NaN when |x/y| > DBL_MAX, SURVEY.md §0
+ * item 6):  n = mn*2^en, d = md*2^ed with mn, md in [1,2) (exact, subnormals
+ * via clz), E = en - ed, and n mod d = 2^ed * ((mn * 2^E) mod md).  Each step
+ * shifts the running remainder r in [0, md) left by s = min(E, 50) bits and
+ * removes Q*md, Q = trunc(toward0(r*2^s * toward0(1/md))), which
+ * is floor or floor-1 of the true quotient (< 2^51); the off-by-one is resolved
+ * exactly with two candidate remainders.  One division per call; the loop runs
+ * ceil(E/50) times.  Exact, hence bit-identical to glibc fmod. */
 static inline int64_t ilogb_pos(double x) { /* x > 0 finite, subnormals exact */
   uint64_t b = bits_d(x);
   int64_t e = (int64_t)(b >> 52);
   if (e != 0) return e - 1023;
   return (int64_t)(63 - __builtin_clzll(b)) - 1074;
 }
-
+/* x > 0 finite with ilogb e: x * 2^-e in [1, 2), exactly (bit manipulation) */
+static inline double mant_1_2(double x, int64_t e) {
+  uint64_t b = bits_d(x);
+  uint64_t m = (e >= -1022) ? (b & 0x000fffffffffffffull) : ((b << (-1022 - e)) & 0x000fffffffffffffull);
+  return from_bits_d(m | 0x3ff0000000000000ull);
+}
+/* one long-division step of width s (1 <= s <= 50); r > 0 */
+static inline double fmod_step(double r, int s, double md, double rmd) {
+  double rs = r * pow2_bits(s);
+  double Q = trunc(toward0_pos(rs * rmd));
+  double Q2 = Q + 1.0;
+  double p1 = Q * md, e1 = fma(Q, md, -p1);
+  double V1 = (rs - p1) - e1;
+  double p2 = Q2 * md, e2 = fma(Q2, md, -p2);
+  double V2 = (rs - p2) - e2;
+  return (V2 >= 0.0) ? V2 : V1;
+}
+static _Thread_local int g_fmod_steps; /* iteration counter for vo_fmod_d_iters */
 static double fmod_core(double x, double y) {
   double n = fabs(x), d = fabs(y);
-  int ok = (n < INFINITY) && (d > 0.0) && (d < INFINITY);
-  double ns = ok ? n : 0.0, ds0 = ok ? d : 1.0;
-  int64_t ed = ilogb_pos(ds0);
-  double ds = ldexp2(ds0, -ed);
-  double rds = toward0_pos(1.0 / ds);
-  double r = ns;
-  while (r >= ds0) {
-    int64_t er = ilogb_pos(r);
-    int64_t k = er - ed - 50;
-    k = k > 0 ? k : 0;
-    double D = ldexp2(ds0, k);
-    double rs = ldexp2(r, -ed - k);
-    double Q = trunc(toward0_pos(rs * rds));
-    double Q2 = Q + 1.0;
-    double p1 = Q * D, e1 = fma(Q, D, -p1);
-    double V1 = (r - p1) - e1;
-    double p2 = Q2 * D, e2 = fma(Q2, D, -p2);
-    double V2 = (r - p2) - e2;
-    r = (V2 >= 0.0) ? V2 : V1;
+  if (x != x || y != y || !(n < INFINITY) || d == 0.0) return from_bits_d(CANON_NAN_D);
+  if (d == INFINITY || n < d) return x;
+  int64_t en = ilogb_pos(n), ed = ilogb_pos(d);
+  double mn = mant_1_2(n, en), md = mant_1_2(d, ed);
+  int64_t E = en - ed;
+  double rmd = toward0_pos(1.0 / md);
+  double r = (E == 0) ? mn - md : mn;
+  while (E > 0 && r != 0.0) {
+    int s = E > 50 ? 50 : (int)E;
+    E -= s;
+    r = fmod_step(r, s, md, rmd);
+    g_fmod_steps++;
   }
-  double res = copysign_b(r, x);
-  res = (n < d) ? x : res;
-  res = (d == INFINITY && n < INFINITY) ? x : res;
-  res = (!(n < INFINITY) || d == 0.0 || x != x || y != y) ? from_bits_d(CANON_NAN_D) : res;
-  return canon_d(res);
+  return copysign_b(ldexp2(r, ed), x);
 }
 double vo_fmod_d(double x, double y) { return fmod_core(x, y); }
 
@@ -931,29 +940,9 @@ BINARY_ARR(vo_fmod_f, float)
 
 /* fmod iteration count (for the step-curve property) */
 int vo_fmod_d_iters(double x, double y) {
-  double n = fabs(x), d = fabs(y);
-  if (!(n < INFINITY) || !(d > 0.0) || !(d < INFINITY)) return 0;
-  int64_t ed = ilogb_pos(d);
-  double ds = ldexp2(d, -ed);
-  double rds = toward0_pos(1.0 / ds);
-  double r = n;
-  int it = 0;
-  while (r >= d) {
-    int64_t er = ilogb_pos(r);
-    int64_t k = er - ed - 50;
-    k = k > 0 ? k : 0;
-    double D = ldexp2(d, k);
-    double rs = ldexp2(r, -ed - k);
-    double Q = trunc(toward0_pos(rs * rds));
-    double Q2 = Q + 1.0;
-    double p1 = Q * D, e1 = fma(Q, D, -p1);
-    double V1 = (r - p1) - e1;
-    double p2 = Q2 * D, e2 = fma(Q2, D, -p2);
-    double V2 = (r - p2) - e2;
-    r = (V2 >= 0.0) ? V2 : V1;
-    it++;
-  }
-  return it;
+  g_fmod_steps = 0;
+  (void)fmod_core(x, y);
+  return g_fmod_steps;
 }
 
 /* debug hooks (tests only) */

@@ -215,6 +215,67 @@ __global__ void __launch_bounds__(kThreads) k_stream(const T* __restrict__ a, co
   }
 }
 
+// ------------------------------------------------------------ fmod
+// The remainder loop runs ceil(E/50) steps, E = exponent gap of |x| and |y|;
+// a plain SIMT loop makes every lane wait for its warp's slowest element
+// (config 4: mean ~7 vs warp-max ~30 steps).  Here lanes are REFILLED: each
+// warp walks a private sequence of 512-element chunks (chunk c, c + W, ...
+// for W warps in the grid), and whenever lanes finish an element they take
+// the next ones from that sequence (ballot + prefix popcount), so a warp
+// stays full until its whole sequence is exhausted.  Per-element math is the
+// oracle's (setup / step / finish), hence bit-identical results.
+constexpr int kFmodChunk = 512;
+
+template <class T>
+__global__ void __launch_bounds__(kThreads) k_fmod(const T* __restrict__ a, const T* __restrict__ b,
+                                                   T* __restrict__ out, size_t n) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const size_t warps = (size_t)gridDim.x * (kThreads / 32);
+  const size_t w = (size_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  const size_t nchunks = (n + kFmodChunk - 1) / kFmodChunk;
+  const size_t mych = nchunks > w ? (nchunks - w + warps - 1) / warps : 0;
+  const size_t total = mych * kFmodChunk;  // virtual index space of this warp
+  size_t head = 0;
+  fmod_state st;
+  size_t gi = 0;
+  bool active = false;
+  auto vmap = [&](size_t v) -> size_t { return (w + (v / kFmodChunk) * warps) * kFmodChunk + (v % kFmodChunk); };
+  auto fetch = [&]() {
+    while (true) {
+      unsigned need = __ballot_sync(0xffffffffu, !active);
+      if (need == 0u || head >= total) break;
+      size_t v = head + __popc(need & lt_mask);
+      head += __popc(need);
+      if (!active && v < total) {
+        size_t g = vmap(v);
+        if (g < n) {
+          double res;
+          if (fmod_setup((double)__ldcs(a + g), (double)__ldcs(b + g), st, res)) {
+            __stcs(out + g, (T)res);
+          } else {
+            gi = g;
+            active = true;
+          }
+        }
+      }
+    }
+  };
+  fetch();
+  while (__any_sync(0xffffffffu, active)) {
+    if (active) {
+      int s = st.E > 50 ? 50 : st.E;
+      st.E -= s;
+      st.r = fmod_step(st.r, s, st.md, st.rmd);
+      if (st.E == 0 || st.r == 0.0) {
+        __stcs(out + gi, (T)fmod_finish(st));
+        active = false;
+      }
+    }
+    fetch();
+  }
+}
+
 // ------------------------------------------------------------- functors
 #define VEM_UNARY_OP(NAME, T, EXPR)                                                   \
   struct NAME {                                                                       \
@@ -343,6 +404,20 @@ static int launch_stream(const T* a, const T* b, T* out, size_t n, vem_stream_t 
   return (int)cudaGetLastError();
 }
 
+template <class T>
+static int launch_fmod(const T* a, const T* b, T* out, size_t n, vem_stream_t s) {
+  if (n == 0) return 0;
+  auto k = k_fmod<T>;
+  static const int occ = occupancy(k);
+  size_t chunks = (n + kFmodChunk - 1) / kFmodChunk;
+  size_t warps_cap = (size_t)num_sms() * occ * (kThreads / 32);
+  size_t warps = chunks < warps_cap ? chunks : warps_cap;
+  size_t g = (warps + (kThreads / 32) - 1) / (kThreads / 32);
+  k<<<(int)(g < 1 ? 1 : g), kThreads, 0, (cudaStream_t)s>>>(a, b, out, n);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return (int)cudaGetLastError();
+}
+
 // ---------------------------------------------------- reduction kernels
 template <int MODE>  // 0 trig_reduce, 1 cw1, 2 cw2, 3 ph
 __global__ void __launch_bounds__(kThreads) k_reduce_d(const double* __restrict__ x, double* hi, double* lo,
@@ -408,7 +483,7 @@ int vem_log_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return
 int vem_log_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpLogDU35, double, 1, kTableLog, 2, 4>(x, nullptr, y, n, s); }
 int vem_pow_d_u10(const double* x, const double* y2, double* o, size_t n, vem_stream_t s) { return launch_stream<OpPowD, double, 2, kTableLog, 1, 4>(x, y2, o, n, s); }
 int vem_pow_d_u35(const double* x, const double* y2, double* o, size_t n, vem_stream_t s) { return launch_stream<OpPowDU35, double, 2, kTableLog, 1, 4>(x, y2, o, n, s); }
-int vem_fmod_d(const double* x, const double* y2, double* o, size_t n, vem_stream_t s) { return launch_stream<OpFmodD, double, 2, kNoTable, 1, 4>(x, y2, o, n, s); }
+int vem_fmod_d(const double* x, const double* y2, double* o, size_t n, vem_stream_t s) { return launch_fmod<double>(x, y2, o, n, s); }
 
 int vem_sin_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return launch_stream<OpSinF, float, 1, kTableF, 1, 4>(x, nullptr, y, n, s); }
 int vem_cos_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return launch_stream<OpCosF, float, 1, kTableF, 1, 4>(x, nullptr, y, n, s); }
@@ -423,7 +498,7 @@ int vem_log_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return l
 int vem_log_f_u35(const float* x, float* y, size_t n, vem_stream_t s) { return launch_stream<OpLogFU35, float, 1, kTableLog, 1, 4>(x, nullptr, y, n, s); }
 int vem_pow_f_u10(const float* x, const float* y2, float* o, size_t n, vem_stream_t s) { return launch_stream<OpPowF, float, 2, kTableLog, 1, 4>(x, y2, o, n, s); }
 int vem_pow_f_u35(const float* x, const float* y2, float* o, size_t n, vem_stream_t s) { return launch_stream<OpPowFU35, float, 2, kTableLog, 1, 4>(x, y2, o, n, s); }
-int vem_fmod_f(const float* x, const float* y2, float* o, size_t n, vem_stream_t s) { return launch_stream<OpFmodF, float, 2, kNoTable, 1, 4>(x, y2, o, n, s); }
+int vem_fmod_f(const float* x, const float* y2, float* o, size_t n, vem_stream_t s) { return launch_fmod<float>(x, y2, o, n, s); }
 
 int vem_trig_reduce_d(const double* x, double* hi, double* lo, int* q, size_t n, vem_stream_t s) {
   return launch_reduce_d<0>(x, hi, lo, q, n, s);

@@ -578,39 +578,68 @@ __device__ __forceinline__ double pow_d_u35(double x, double y, const double* lt
   return pow_core_d<VEM_LOG1P_D_U35_N>(x, y, cLog1pDU35, lt);
 }
 
-// fmod: staged-divisor FP long division (oracle: fmod_core).
-__device__ __forceinline__ long long ilogb_pos(double x) {
+// fmod: normalised-mantissa FP long division (oracle: fmod_core).  The
+// per-element state is split into setup / step / finish so the kernel can
+// refill lanes (vem_kernels.cu: k_fmod).
+__device__ __forceinline__ int ilogb_pos(double x) {
   uint64_t b = bits_d(x);
-  long long e = (long long)(b >> 52);
-  return e != 0 ? e - 1023 : (long long)(63 - __clzll((long long)b)) - 1074;
+  int e = (int)(b >> 52);
+  return e != 0 ? e - 1023 : (63 - __clzll((long long)b)) - 1074;
+}
+__device__ __forceinline__ double mant_1_2(double x, int e) {
+  uint64_t b = bits_d(x);
+  uint64_t m = (e >= -1022) ? (b & 0x000fffffffffffffull) : ((b << (-1022 - e)) & 0x000fffffffffffffull);
+  return from_bits_d(m | 0x3ff0000000000000ull);
+}
+__device__ __forceinline__ double fmod_step(double r, int s, double md, double rmd) {
+  double rs = r * __hiloint2double((1023 + s) << 20, 0);
+  double Q = trunc(toward0_pos(rs * rmd));
+  double Q2 = Q + 1.0;
+  double p1 = Q * md, e1 = fma(Q, md, -p1);
+  double V1 = (rs - p1) - e1;
+  double p2 = Q2 * md, e2 = fma(Q2, md, -p2);
+  double V2 = (rs - p2) - e2;
+  return (V2 >= 0.0) ? V2 : V1;
+}
+struct fmod_state {
+  double r, md, rmd, x;
+  int E, ed;
+};
+// returns true when the element is finished already (result in `res`)
+__device__ __forceinline__ bool fmod_setup(double x, double y, fmod_state& st, double& res) {
+  double n = fabs(x), d = fabs(y);
+  if (x != x || y != y || !(n < kInf) || d == 0.0) {
+    res = from_bits_d(kCanonNanD);
+    return true;
+  }
+  if (d == kInf || n < d) {
+    res = x;
+    return true;
+  }
+  int en = ilogb_pos(n), ed = ilogb_pos(d);
+  double mn = mant_1_2(n, en), md = mant_1_2(d, ed);
+  int E = en - ed;
+  st.md = md;
+  st.rmd = toward0_pos(1.0 / md);
+  st.r = (E == 0) ? mn - md : mn;
+  st.E = E;
+  st.ed = ed;
+  st.x = x;
+  return false;
+}
+__device__ __forceinline__ double fmod_finish(const fmod_state& st) {
+  return copysign_b(ldexp2(st.r, st.ed), st.x);
 }
 __device__ __forceinline__ double fmod_core(double x, double y) {
-  double n = fabs(x), d = fabs(y);
-  bool ok = (n < kInf) && (d > 0.0) && (d < kInf);
-  double ns = ok ? n : 0.0, ds0 = ok ? d : 1.0;
-  long long ed = ilogb_pos(ds0);
-  double ds = ldexp2(ds0, -ed);
-  double rds = toward0_pos(1.0 / ds);
-  double r = ns;
-  while (r >= ds0) {
-    long long er = ilogb_pos(r);
-    long long k = er - ed - 50;
-    k = k > 0 ? k : 0;
-    double D = ldexp2(ds0, k);
-    double rs = ldexp2(r, -ed - k);
-    double Q = trunc(toward0_pos(rs * rds));
-    double Q2 = Q + 1.0;
-    double p1 = Q * D, e1 = fma(Q, D, -p1);
-    double V1 = (r - p1) - e1;
-    double p2 = Q2 * D, e2 = fma(Q2, D, -p2);
-    double V2 = (r - p2) - e2;
-    r = (V2 >= 0.0) ? V2 : V1;
+  fmod_state st;
+  double res;
+  if (fmod_setup(x, y, st, res)) return res;
+  while (st.E > 0 && st.r != 0.0) {
+    int s = st.E > 50 ? 50 : st.E;
+    st.E -= s;
+    st.r = fmod_step(st.r, s, st.md, st.rmd);
   }
-  double res = copysign_b(r, x);
-  res = (n < d) ? x : res;
-  res = (d == kInf && n < kInf) ? x : res;
-  res = (!(n < kInf) || d == 0.0 || x != x || y != y) ? from_bits_d(kCanonNanD) : res;
-  return canon_d(res);
+  return fmod_finish(st);
 }
 __device__ __forceinline__ double fmod_d(double x, double y) { return fmod_core(x, y); }
 
