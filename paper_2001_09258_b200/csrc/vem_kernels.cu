@@ -219,44 +219,89 @@ __global__ void __launch_bounds__(kThreads) k_stream(const T* __restrict__ a, co
 // The remainder loop runs ceil(E/50) steps, E = exponent gap of |x| and |y|;
 // a plain SIMT loop makes every lane wait for its warp's slowest element
 // (config 4: mean ~7 vs warp-max ~30 steps).  Here lanes are REFILLED: each
-// warp walks a private sequence of 512-element chunks (chunk c, c + W, ...
-// for W warps in the grid), and whenever lanes finish an element they take
-// the next ones from that sequence (ballot + prefix popcount), so a warp
-// stays full until its whole sequence is exhausted.  Per-element math is the
-// oracle's (setup / step / finish), hence bit-identical results.
-constexpr int kFmodChunk = 512;
+// warp walks a private sequence of chunks (c = w, w + W, ... for W warps in
+// the grid) staged into its own shared-memory double buffer by TMA bulk
+// copies (lane 0 issues, per-warp mbarriers), and whenever lanes finish an
+// element they take the next ones from that sequence (ballot + prefix
+// popcount), so a warp stays full until its whole sequence is exhausted.
+// Per-element math is the oracle's (setup / step / finish): bit-identical.
+template <class T>
+struct FmodChunk { static constexpr int n = 1024 / sizeof(T); };  // 1 KB per input per stage
+constexpr int kWarps = kThreads / 32;
 
 template <class T>
 __global__ void __launch_bounds__(kThreads) k_fmod(const T* __restrict__ a, const T* __restrict__ b,
                                                    T* __restrict__ out, size_t n) {
-  const int lane = threadIdx.x & 31;
+  constexpr int kFmodChunk = FmodChunk<T>::n;
+  __shared__ __align__(128) T sx[kWarps][2][kFmodChunk];
+  __shared__ __align__(128) T sy[kWarps][2][kFmodChunk];
+  __shared__ uint64_t bars[kWarps][2];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
-  const size_t warps = (size_t)gridDim.x * (kThreads / 32);
-  const size_t w = (size_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
-  const size_t nchunks = (n + kFmodChunk - 1) / kFmodChunk;
-  const size_t mych = nchunks > w ? (nchunks - w + warps - 1) / warps : 0;
-  const size_t total = mych * kFmodChunk;  // virtual index space of this warp
-  size_t head = 0;
+  const size_t W = (size_t)gridDim.x * kWarps;
+  const size_t w = (size_t)blockIdx.x * kWarps + wl;
+  const size_t nfull = n / kFmodChunk;                       // chunks staged by TMA
+  const size_t nch = (n + kFmodChunk - 1) / kFmodChunk;
+  const size_t mych = nch > w ? (nch - w + W - 1) / W : 0;   // chunks of this warp
+  constexpr uint32_t CB = kFmodChunk * sizeof(T);
+  uint64_t pol = 0;
+  if (lane == 0) {
+    tma::mbar_init(&bars[wl][0], 1);
+    tma::mbar_init(&bars[wl][1], 1);
+    tma::fence_barrier_init();
+    pol = tma::policy_evict_first();
+  }
+  __syncwarp();
+  auto issue = [&](size_t j) {  // chunk j of this warp -> stage j & 1 (full chunks only)
+    size_t c = w + j * W;
+    if (c >= nfull) return;
+    int st_ = (int)(j & 1);
+    tma::mbar_expect_tx(&bars[wl][st_], 2 * CB);
+    tma::bulk_g2s(&sx[wl][st_][0], a + c * kFmodChunk, CB, &bars[wl][st_], pol);
+    tma::bulk_g2s(&sy[wl][st_][0], b + c * kFmodChunk, CB, &bars[wl][st_], pol);
+  };
+  if (lane == 0) {
+    if (mych > 0) issue(0);
+    if (mych > 1) issue(1);
+  }
+  size_t j = 0;          // current chunk (of this warp)
+  size_t head = 0;       // next unassigned element within chunk j
+  bool ready = false;    // chunk j waited for
   fmod_state st;
   size_t gi = 0;
   bool active = false;
-  auto vmap = [&](size_t v) -> size_t { return (w + (v / kFmodChunk) * warps) * kFmodChunk + (v % kFmodChunk); };
   auto fetch = [&]() {
-    while (true) {
+    while (j < mych) {
+      const size_t c = w + j * W;
+      const bool full = c < nfull;
+      const size_t valid = full ? kFmodChunk : n - c * kFmodChunk;
+      if (!ready) {
+        if (full) tma::mbar_wait(&bars[wl][j & 1], (uint32_t)((j >> 1) & 1));
+        ready = true;
+      }
       unsigned need = __ballot_sync(0xffffffffu, !active);
-      if (need == 0u || head >= total) break;
+      if (need == 0u) return;
+      if (head >= valid) {  // chunk consumed: recycle its stage, move on
+        __syncwarp();
+        if (lane == 0 && j + 2 < mych) issue(j + 2);
+        j++;
+        head = 0;
+        ready = false;
+        continue;
+      }
       size_t v = head + __popc(need & lt_mask);
       head += __popc(need);
-      if (!active && v < total) {
-        size_t g = vmap(v);
-        if (g < n) {
-          double res;
-          if (fmod_setup((double)__ldcs(a + g), (double)__ldcs(b + g), st, res)) {
-            __stcs(out + g, (T)res);
-          } else {
-            gi = g;
-            active = true;
-          }
+      if (!active && v < valid) {
+        const int st_ = (int)(j & 1);
+        T xv = full ? sx[wl][st_][v] : a[c * kFmodChunk + v];
+        T yv = full ? sy[wl][st_][v] : b[c * kFmodChunk + v];
+        size_t g = c * kFmodChunk + v;
+        double res;
+        if (fmod_setup((double)xv, (double)yv, st, res)) {
+          __stcs(out + g, (T)res);
+        } else {
+          gi = g;
+          active = true;
         }
       }
     }
@@ -407,8 +452,13 @@ static int launch_stream(const T* a, const T* b, T* out, size_t n, vem_stream_t 
 template <class T>
 static int launch_fmod(const T* a, const T* b, T* out, size_t n, vem_stream_t s) {
   if (n == 0) return 0;
+  if (!(aligned16(a) && aligned16(b))) {
+    if constexpr (sizeof(T) == 8) return launch_binary<OpFmodD, T, kNoTable, 1>(a, b, out, n, s);
+    else return launch_binary<OpFmodF, T, kNoTable, 1>(a, b, out, n, s);
+  }
   auto k = k_fmod<T>;
   static const int occ = occupancy(k);
+  constexpr int kFmodChunk = FmodChunk<T>::n;
   size_t chunks = (n + kFmodChunk - 1) / kFmodChunk;
   size_t warps_cap = (size_t)num_sms() * occ * (kThreads / 32);
   size_t warps = chunks < warps_cap ? chunks : warps_cap;

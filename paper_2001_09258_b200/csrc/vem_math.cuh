@@ -625,7 +625,11 @@ __device__ __forceinline__ bool fmod_setup(double x, double y, fmod_state& st, d
   st.E = E;
   st.ed = ed;
   st.x = x;
-  return false;
+  if (E == 0) {  // mn >= md: one exact subtraction finishes it
+    res = copysign_b(ldexp2(st.r, ed), x);
+    return true;
+  }
+  return false;  // st.E > 0 and st.r = mn >= 1
 }
 __device__ __forceinline__ double fmod_finish(const fmod_state& st) {
   return copysign_b(ldexp2(st.r, st.ed), st.x);
