@@ -218,106 +218,116 @@ __global__ void __launch_bounds__(kThreads) k_stream(const T* __restrict__ a, co
 // ------------------------------------------------------------ fmod
 // The remainder loop runs ceil(E/50) steps, E = exponent gap of |x| and |y|;
 // a plain SIMT loop makes every lane wait for its warp's slowest element
-// (config 4: mean ~7 vs warp-max ~30 steps).  Here lanes are REFILLED: each
-// warp walks a private sequence of chunks (c = w, w + W, ... for W warps in
-// the grid) staged into its own shared-memory double buffer by TMA bulk
-// copies (lane 0 issues, per-warp mbarriers), and whenever lanes finish an
-// element they take the next ones from that sequence (ballot + prefix
-// popcount), so a warp stays full until its whole sequence is exhausted.
-// Per-element math is the oracle's (setup / step / finish): bit-identical.
-template <class T>
-struct FmodChunk { static constexpr int n = 1024 / sizeof(T); };  // 1 KB per input per stage
-constexpr int kWarps = kThreads / 32;
+// (config 4: mean ~7 vs warp-max ~30 steps).  Two phases per warp instead:
+//   1. setup, uniform over a chunk of 64 elements (coalesced loads, one
+//      division each): trivial elements (|x| < |y|, specials, equal
+//      exponents) are finished and stored at once; the others are appended,
+//      compacted by ballot + prefix popcount, to a per-warp work ring in
+//      shared memory (r, md, 1/md, E, ed|sign: 32 B);
+//   2. long division: every active lane takes one 50-bit step; whenever at
+//      least kRefill lanes are idle they pull the next ring entries.
+// So lanes only idle while the ring is empty; per-element math is the
+// oracle's (setup / step / finish), hence bit-identical results.
+constexpr int kFmodWarps = 4;        // 128-thread CTAs
+constexpr int kFmodChunk = 64;       // elements per warp per phase 1
+constexpr int kFmodRing = 64;        // ring entries per warp (>= chunk)
+constexpr int kRefill = 8;
 
 template <class T>
-__global__ void __launch_bounds__(kThreads) k_fmod(const T* __restrict__ a, const T* __restrict__ b,
-                                                   T* __restrict__ out, size_t n) {
-  constexpr int kFmodChunk = FmodChunk<T>::n;
-  __shared__ __align__(128) T sx[kWarps][2][kFmodChunk];
-  __shared__ __align__(128) T sy[kWarps][2][kFmodChunk];
-  __shared__ uint64_t bars[kWarps][2];
+__global__ void __launch_bounds__(kFmodWarps * 32) k_fmod(const T* __restrict__ a, const T* __restrict__ b,
+                                                          T* __restrict__ out, size_t n) {
+  __shared__ double s_r[kFmodWarps][kFmodRing], s_md[kFmodWarps][kFmodRing], s_rmd[kFmodWarps][kFmodRing];
+  __shared__ int2 s_e[kFmodWarps][kFmodRing];
+  __shared__ unsigned long long s_g[kFmodWarps][kFmodRing];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
-  const size_t W = (size_t)gridDim.x * kWarps;
-  const size_t w = (size_t)blockIdx.x * kWarps + wl;
-  const size_t nfull = n / kFmodChunk;                       // chunks staged by TMA
+  const size_t W = (size_t)gridDim.x * kFmodWarps;
+  const size_t w = (size_t)blockIdx.x * kFmodWarps + wl;
   const size_t nch = (n + kFmodChunk - 1) / kFmodChunk;
-  const size_t mych = nch > w ? (nch - w + W - 1) / W : 0;   // chunks of this warp
-  constexpr uint32_t CB = kFmodChunk * sizeof(T);
-  uint64_t pol = 0;
-  if (lane == 0) {
-    tma::mbar_init(&bars[wl][0], 1);
-    tma::mbar_init(&bars[wl][1], 1);
-    tma::fence_barrier_init();
-    pol = tma::policy_evict_first();
-  }
-  __syncwarp();
-  auto issue = [&](size_t j) {  // chunk j of this warp -> stage j & 1 (full chunks only)
-    size_t c = w + j * W;
-    if (c >= nfull) return;
-    int st_ = (int)(j & 1);
-    tma::mbar_expect_tx(&bars[wl][st_], 2 * CB);
-    tma::bulk_g2s(&sx[wl][st_][0], a + c * kFmodChunk, CB, &bars[wl][st_], pol);
-    tma::bulk_g2s(&sy[wl][st_][0], b + c * kFmodChunk, CB, &bars[wl][st_], pol);
-  };
-  if (lane == 0) {
-    if (mych > 0) issue(0);
-    if (mych > 1) issue(1);
-  }
-  size_t j = 0;          // current chunk (of this warp)
-  size_t head = 0;       // next unassigned element within chunk j
-  bool ready = false;    // chunk j waited for
-  fmod_state st;
+  const size_t mych = nch > w ? (nch - w + W - 1) / W : 0;
+  unsigned head = 0, tail = 0;  // ring consumer / producer counters (warp-uniform)
+  fmod_state st = {0.0, 1.0, 1.0, 1.0, 0, 0};
   size_t gi = 0;
   bool active = false;
-  auto fetch = [&]() {
-    while (j < mych) {
-      const size_t c = w + j * W;
-      const bool full = c < nfull;
-      const size_t valid = full ? kFmodChunk : n - c * kFmodChunk;
-      if (!ready) {
-        if (full) tma::mbar_wait(&bars[wl][j & 1], (uint32_t)((j >> 1) & 1));
-        ready = true;
-      }
-      unsigned need = __ballot_sync(0xffffffffu, !active);
-      if (need == 0u) return;
-      if (head >= valid) {  // chunk consumed: recycle its stage, move on
-        __syncwarp();
-        if (lane == 0 && j + 2 < mych) issue(j + 2);
-        j++;
-        head = 0;
-        ready = false;
-        continue;
-      }
-      size_t v = head + __popc(need & lt_mask);
-      head += __popc(need);
-      if (!active && v < valid) {
-        const int st_ = (int)(j & 1);
-        T xv = full ? sx[wl][st_][v] : a[c * kFmodChunk + v];
-        T yv = full ? sy[wl][st_][v] : b[c * kFmodChunk + v];
-        size_t g = c * kFmodChunk + v;
-        double res;
-        if (fmod_setup((double)xv, (double)yv, st, res)) {
-          __stcs(out + g, (T)res);
-        } else {
-          gi = g;
-          active = true;
-        }
-      }
-    }
-  };
-  fetch();
-  while (__any_sync(0xffffffffu, active)) {
+
+  auto step_all = [&]() {
     if (active) {
-      int s = st.E > 50 ? 50 : st.E;
-      st.E -= s;
-      st.r = fmod_step(st.r, s, st.md, st.rmd);
+      int sh = st.E > 50 ? 50 : st.E;
+      st.E -= sh;
+      st.r = fmod_step(st.r, sh, st.md, st.rmd);
       if (st.E == 0 || st.r == 0.0) {
         __stcs(out + gi, (T)fmod_finish(st));
         active = false;
       }
     }
-    fetch();
+  };
+  auto refill = [&](bool force) {
+    unsigned idle = __ballot_sync(0xffffffffu, !active);
+    int nidle = __popc(idle);
+    unsigned avail = tail - head;
+    if (avail == 0u || nidle == 0 || (!force && nidle < kRefill && avail >= (unsigned)kRefill)) return;
+    unsigned k = head + __popc(idle & lt_mask);
+    if (!active && k < tail) {
+      int sl = (int)(k % kFmodRing);
+      st.r = s_r[wl][sl];
+      st.md = s_md[wl][sl];
+      st.rmd = s_rmd[wl][sl];
+      int2 e = s_e[wl][sl];
+      st.E = e.x;
+      st.ed = e.y >> 1;
+      st.x = (e.y & 1) ? -1.0 : 1.0;
+      gi = (size_t)s_g[wl][sl];
+      active = true;
+    }
+    head += min((unsigned)nidle, avail);
+    __syncwarp();
+  };
+
+  for (size_t j = 0; j < mych; j++) {
+    // ---- phase 1: setup a chunk, compact the non-trivial elements into the ring
+    const size_t base = (w + j * W) * kFmodChunk;
+    const size_t valid = min((size_t)kFmodChunk, n - base);
+    T xv[kFmodChunk / 32], yv[kFmodChunk / 32];
+#pragma unroll
+    for (int k = 0; k < kFmodChunk / 32; k++) {
+      size_t e = (size_t)(k * 32 + lane);
+      xv[k] = e < valid ? __ldcs(a + base + e) : (T)0;
+      yv[k] = e < valid ? __ldcs(b + base + e) : (T)1;
+    }
+#pragma unroll
+    for (int k = 0; k < kFmodChunk / 32; k++) {
+      size_t e = (size_t)(k * 32 + lane);
+      fmod_state s0;
+      double res;
+      bool in = e < valid;
+      bool todo = false;
+      if (in) {
+        if (fmod_setup((double)xv[k], (double)yv[k], s0, res)) __stcs(out + base + e, (T)res);
+        else todo = true;
+      }
+      unsigned m = __ballot_sync(0xffffffffu, todo);
+      if (todo) {
+        int sl = (int)((tail + __popc(m & lt_mask)) % kFmodRing);
+        s_r[wl][sl] = s0.r;
+        s_md[wl][sl] = s0.md;
+        s_rmd[wl][sl] = s0.rmd;
+        s_e[wl][sl] = make_int2(s0.E, (s0.ed << 1) | (s0.x < 0.0 ? 1 : 0));
+        s_g[wl][sl] = (unsigned long long)(base + e);
+      }
+      tail += __popc(m);
+    }
+    __syncwarp();
+    // ---- phase 2: step until the ring is empty
+    while (true) {
+      refill(false);
+      if (tail == head) break;
+      step_all();
+    }
+  }
+  // ---- drain
+  while (__any_sync(0xffffffffu, active)) {
+    step_all();
+    refill(true);
   }
 }
 
@@ -457,13 +467,17 @@ static int launch_fmod(const T* a, const T* b, T* out, size_t n, vem_stream_t s)
     else return launch_binary<OpFmodF, T, kNoTable, 1>(a, b, out, n, s);
   }
   auto k = k_fmod<T>;
-  static const int occ = occupancy(k);
-  constexpr int kFmodChunk = FmodChunk<T>::n;
+  static const int occ = [k] {
+    int bpm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpm, k, kFmodWarps * 32, 0) != cudaSuccess || bpm < 1)
+      bpm = 1;
+    return bpm;
+  }();
   size_t chunks = (n + kFmodChunk - 1) / kFmodChunk;
-  size_t warps_cap = (size_t)num_sms() * occ * (kThreads / 32);
+  size_t warps_cap = (size_t)num_sms() * occ * kFmodWarps;
   size_t warps = chunks < warps_cap ? chunks : warps_cap;
-  size_t g = (warps + (kThreads / 32) - 1) / (kThreads / 32);
-  k<<<(int)(g < 1 ? 1 : g), kThreads, 0, (cudaStream_t)s>>>(a, b, out, n);
+  size_t g = (warps + kFmodWarps - 1) / kFmodWarps;
+  k<<<(int)(g < 1 ? 1 : g), kFmodWarps * 32, 0, (cudaStream_t)s>>>(a, b, out, n);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return (int)cudaGetLastError();
 }
