@@ -713,20 +713,21 @@ static redf_t ph_f(float xf) {
   double Mp = ax * pow2_bits(23 - idx);
   const double* T = PH_F + 3 * idx;
   double p0 = Mp * T[0];
-  double e0 = fma(Mp, T[0], -p0);
-  double q0 = rint(p0);
-  double f0 = p0 - q0;
-  dd_t s = two_sum_fast(f0, e0);
+  double e0 = fma(Mp, T[0], -p0);          /* exact */
+  int32_t k0, k1;
+  double q0 = rint_fma(p0, 1.0, &k0);      /* |p0| < 2^25 */
+  double f0 = p0 - q0;                     /* exact, |f0| <= 1/2 */
   double p1 = Mp * T[1];
   double e1 = fma(Mp, T[1], -p1);
-  double tt = e1 + Mp * T[2];
-  dd_t p1d = {p1, tt};
-  dd_t u = dd_add2(s, p1d);
-  double q1 = rint(u.hi);
-  u.hi = u.hi - q1;
-  dd_t fr = two_sum_fast(u.hi, u.lo);
-  double r = fma(fr.hi, K_PIO2_QD0, fma(fr.hi, K_PIO2_QD1, fr.lo * K_PIO2_QD0));
-  int q = (int)q0 + (int)q1;
+  double m2 = Mp * T[2];
+  double t = e0 + p1;                      /* |.| <~ 2^-27, error <~ 2^-81 */
+  double sm = f0 + t;
+  double c = (f0 - sm) + t;                /* rounding error of sm (<~ 2^-79 off if |f0| < |t|) */
+  double q1 = rint_fma(sm, 1.0, &k1);
+  double fh = sm - q1;                     /* exact */
+  double fl = c + (e1 + m2);
+  double r = fma(fh, K_PIO2_QD0, fma(fh, K_PIO2_QD1, fl * K_PIO2_QD0));
+  int q = k0 + k1;
   if (xs < 0.0f) {
     r = -r;
     q = -q;

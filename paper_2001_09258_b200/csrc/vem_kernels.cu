@@ -22,7 +22,10 @@ namespace vem {
 
 static std::atomic<uint64_t> g_launches{0};
 
-enum TableKind { kNoTable = 0, kTableD = 1, kTableF = 2, kTableLog = 3 };
+// kTableDG: the f64 Payne-Hanek table is read from global memory (L1-resident,
+// __ldg) rather than staged: the 32 KB stage would cost occupancy on inputs
+// that never leave the Cody-Waite range.
+enum TableKind { kNoTable = 0, kTableD = 1, kTableF = 2, kTableLog = 3, kTableDG = 4 };
 
 template <int TABLE>
 struct TableSize {
@@ -36,6 +39,9 @@ template <int TABLE>
 __device__ __forceinline__ const double* stage_table(double* stab) {
   if constexpr (TABLE == kNoTable) {
     return nullptr;
+  } else if constexpr (TABLE == kTableDG) {
+    __syncthreads();
+    return gPhD;
   } else {
     const double* src = TABLE == kTableD ? gPhD : (TABLE == kTableF ? gPhF : gLogExp);
     constexpr int n2 = (TABLE == kTableLog ? kLogTabD : TableSize<TABLE>::n) / 2;
@@ -534,12 +540,12 @@ using namespace vem;
 // vectors in flight, FP64-pipe-bound ones 2 (register pressure).
 extern "C" {
 
-int vem_sin_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpSinD, double, 1, kTableD, 2, 4>(x, nullptr, y, n, s); }
-int vem_cos_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpCosD, double, 1, kTableD, 2, 4>(x, nullptr, y, n, s); }
-int vem_tan_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpTanD, double, 1, kTableD, 2, 4>(x, nullptr, y, n, s); }
-int vem_sin_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpSinDPh, double, 1, kTableD, 1, 4>(x, nullptr, y, n, s); }
-int vem_cos_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpCosDPh, double, 1, kTableD, 1, 4>(x, nullptr, y, n, s); }
-int vem_tan_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpTanDPh, double, 1, kTableD, 1, 4>(x, nullptr, y, n, s); }
+int vem_sin_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpSinD, double, 1, kTableDG, 2, 4>(x, nullptr, y, n, s); }
+int vem_cos_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpCosD, double, 1, kTableDG, 2, 4>(x, nullptr, y, n, s); }
+int vem_tan_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpTanD, double, 1, kTableDG, 2, 4>(x, nullptr, y, n, s); }
+int vem_sin_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpSinDPh, double, 1, kTableDG, 1, 4>(x, nullptr, y, n, s); }
+int vem_cos_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpCosDPh, double, 1, kTableDG, 1, 4>(x, nullptr, y, n, s); }
+int vem_tan_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpTanDPh, double, 1, kTableDG, 1, 4>(x, nullptr, y, n, s); }
 int vem_atan_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpAtanD, double, 1, kNoTable, 2, 4>(x, nullptr, y, n, s); }
 int vem_exp_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpExpD, double, 1, kNoTable, 2, 4>(x, nullptr, y, n, s); }
 int vem_exp_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpExpDU35, double, 1, kNoTable, 2, 4>(x, nullptr, y, n, s); }

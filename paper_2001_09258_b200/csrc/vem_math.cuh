@@ -251,7 +251,7 @@ __device__ __forceinline__ red ph(double x_in, const double* __restrict__ tab) {
   idx = (idx > 1023) ? 1023 : idx;
   double m = ldexp2(a, 52 - idx);
   const double2* f2 = reinterpret_cast<const double2*>(tab + (idx << 2));
-  double2 fa = f2[0], fb = f2[1];
+  double2 fa = __ldg(f2), fb = __ldg(f2 + 1);
   long long q = 0;
   dd u = two_prod(m, fa.x);
   u = rfrac_q(u, q);
@@ -290,11 +290,11 @@ __device__ __forceinline__ red ph(double x_in, const double* __restrict__ tab) {
 // reduction.hpp:189-206 (deterministic, per lane).  Lanes of one warp that
 // agree skip the heavier paths; disagreeing warps run both (SIMT divergence).
 __device__ __forceinline__ red trig_reduce(double x, const double* __restrict__ tab) {
-  double ax = fabs(x);
+  const uint64_t ab = bits_d(x) & 0x7fffffffffffffffull;  // |x| <= c  <=>  bits(|x|) <= bits(c)
   red r;
-  if (ax <= kCw1Max) {
+  if (ab <= 0x402e000000000000ull) {         // 15
     r = cw1(x);
-  } else if (ax <= kCw2Max) {
+  } else if (ab <= 0x42d6bcc41e900000ull) {  // 1e14
     r = cw2(x);
   } else {
     r = ph(x, tab);
@@ -303,33 +303,43 @@ __device__ __forceinline__ red trig_reduce(double x, const double* __restrict__ 
 }
 
 // ===================================================== f64 functions
+// oracle: sincos_core_d (same values; selects hoisted to the inputs of the
+// shared operations so the two forms cost one multiply, one final sum)
 __device__ __forceinline__ double sincos_core_d(double rh, double rl, int cosform) {
   bool cf = cosform != 0;
   double z = rh * rh;
   double P = poly_sel<VEM_SIN_D_N>(cCosD, cSinD, cf, z);
-  double As = rh, Bs = 0.0, Ms = rh * z, Ts = fma(-0.5 * z, rl, rl);
-  double zl = fma(rh, rh, -z);
   double hz = 0.5 * z;
+  double M = z * (cf ? z : rh);              // cos: z*z, sin: rh*z
+  double Ts = fma(-hz, rl, rl);              // sin: rl - rl*z/2
+  double zl = fma(rh, rh, -z);
+  double Tc = -fma(0.5, zl, rh * rl);        // cos: -(zl/2 + rh*rl)
   double w = 1.0 - hz;
-  double Ac = w, Bc = (1.0 - w) - hz, Mc = z * z, Tc = -fma(0.5, zl, rh * rl);
-  double A = cf ? Ac : As, B = cf ? Bc : Bs, M = cf ? Mc : Ms, T = cf ? Tc : Ts;
+  double Bc = (1.0 - w) - hz;
+  double A = cf ? w : rh, B = cf ? Bc : 0.0, T = cf ? Tc : Ts;
   return A + (B + fma(M, P, T));
 }
 
+__device__ __forceinline__ bool is_zero_bits(double x) { return (bits_d(x) << 1) == 0ull; }
+__device__ __forceinline__ bool not_finite_bits(double x) {
+  return ((uint32_t)__double2hiint(x) & 0x7fffffffu) >= 0x7ff00000u;
+}
+
+// NaN can only come from a non-finite input: canonicalised by an integer test
 template <bool kForcePh>
 __device__ __forceinline__ double sin_d_u10(double x, const double* tab) {
   red r = kForcePh ? ph(x, tab) : trig_reduce(x, tab);
   double y = sincos_core_d(r.hi, r.lo, r.q & 1);
   y = neg_if(y, r.q & 2);
-  y = (x == 0.0) ? x : y;
-  return canon_d(y);
+  y = is_zero_bits(x) ? x : y;
+  return not_finite_bits(x) ? from_bits_d(kCanonNanD) : y;
 }
 template <bool kForcePh>
 __device__ __forceinline__ double cos_d_u10(double x, const double* tab) {
   red r = kForcePh ? ph(x, tab) : trig_reduce(x, tab);
   double y = sincos_core_d(r.hi, r.lo, (r.q & 1) ^ 1);
   y = neg_if(y, (r.q + 1) & 2);
-  return canon_d(y);
+  return not_finite_bits(x) ? from_bits_d(kCanonNanD) : y;
 }
 
 __device__ __forceinline__ double tan_core_d(double rh, double rl, int odd) {
@@ -664,18 +674,20 @@ __device__ __forceinline__ redf ph_f(float xf, const double* __restrict__ tab) {
   double T0 = T[0], T1 = T[1], T2 = T[2];
   double p0 = Mp * T0;
   double e0 = fma(Mp, T0, -p0);
-  double q0 = rint(p0);
+  int k0, k1;
+  double q0 = rint_fma(p0, 1.0, k0);
   double f0 = p0 - q0;
-  dd s = two_sum_fast(f0, e0);
   double p1 = Mp * T1;
   double e1 = fma(Mp, T1, -p1);
-  double tt = e1 + Mp * T2;
-  dd u = dd_add2(s, dd{p1, tt});
-  double q1 = rint(u.hi);
-  u.hi = u.hi - q1;
-  dd fr = two_sum_fast(u.hi, u.lo);
-  double r = fma(fr.hi, kPio2Qd0, fma(fr.hi, kPio2Qd1, fr.lo * kPio2Qd0));
-  int q = (int)q0 + (int)q1;
+  double m2 = Mp * T2;
+  double t = e0 + p1;
+  double sm = f0 + t;
+  double c = (f0 - sm) + t;
+  double q1 = rint_fma(sm, 1.0, k1);
+  double fh = sm - q1;
+  double fl = c + (e1 + m2);
+  double r = fma(fh, kPio2Qd0, fma(fh, kPio2Qd1, fl * kPio2Qd0));
+  int q = k0 + k1;
   if (xs < 0.0f) {
     r = -r;
     q = -q;
