@@ -540,12 +540,12 @@ using namespace vem;
 // vectors in flight, FP64-pipe-bound ones 2 (register pressure).
 extern "C" {
 
-int vem_sin_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpSinD, double, 1, kTableDG, 2, 4>(x, nullptr, y, n, s); }
-int vem_cos_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpCosD, double, 1, kTableDG, 2, 4>(x, nullptr, y, n, s); }
-int vem_tan_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpTanD, double, 1, kTableDG, 2, 4>(x, nullptr, y, n, s); }
-int vem_sin_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpSinDPh, double, 1, kTableDG, 1, 4>(x, nullptr, y, n, s); }
-int vem_cos_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpCosDPh, double, 1, kTableDG, 1, 4>(x, nullptr, y, n, s); }
-int vem_tan_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpTanDPh, double, 1, kTableDG, 1, 4>(x, nullptr, y, n, s); }
+int vem_sin_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpSinD, double, 1, kTableD, 2, 2>(x, nullptr, y, n, s); }
+int vem_cos_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpCosD, double, 1, kTableD, 2, 2>(x, nullptr, y, n, s); }
+int vem_tan_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpTanD, double, 1, kTableD, 2, 2>(x, nullptr, y, n, s); }
+int vem_sin_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpSinDPh, double, 1, kTableD, 1, 4>(x, nullptr, y, n, s); }
+int vem_cos_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpCosDPh, double, 1, kTableD, 1, 4>(x, nullptr, y, n, s); }
+int vem_tan_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpTanDPh, double, 1, kTableD, 1, 4>(x, nullptr, y, n, s); }
 int vem_atan_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpAtanD, double, 1, kNoTable, 2, 4>(x, nullptr, y, n, s); }
 int vem_exp_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpExpD, double, 1, kNoTable, 2, 4>(x, nullptr, y, n, s); }
 int vem_exp_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return launch_stream<OpExpDU35, double, 1, kNoTable, 2, 4>(x, nullptr, y, n, s); }

@@ -205,7 +205,7 @@ __device__ __forceinline__ red cw1(double x) {
   dd tail = two_prod(qd, -kCw1T1);
   tail.lo = fma(qd, -kCw1T2, tail.lo);
   dd r = dd_normalize(dd_add2(dd{r0, 0.0}, tail));
-  return {r.hi, r.lo, (int)((long long)qd & 3)};
+  return {r.hi, r.lo, (int)qd & 3};  // |qd| <= 10
 }
 
 // reduction.hpp:163-178
@@ -226,7 +226,7 @@ __device__ __forceinline__ red cw2(double x) {
   dtail.lo = fma(qs, -kCw2D2, dtail.lo);
   acc = dd_add2(acc, dtail);
   acc = dd_normalize(acc);
-  return {acc.hi, acc.lo, (int)((long long)ql & 3)};
+  return {acc.hi, acc.lo, (int)ql & 3};  // |ql| < 2^24
 }
 
 // reduction.hpp:35-43
@@ -251,7 +251,7 @@ __device__ __forceinline__ red ph(double x_in, const double* __restrict__ tab) {
   idx = (idx > 1023) ? 1023 : idx;
   double m = ldexp2(a, 52 - idx);
   const double2* f2 = reinterpret_cast<const double2*>(tab + (idx << 2));
-  double2 fa = __ldg(f2), fb = __ldg(f2 + 1);
+  double2 fa = f2[0], fb = f2[1];
   long long q = 0;
   dd u = two_prod(m, fa.x);
   u = rfrac_q(u, q);
