@@ -452,14 +452,11 @@ static double exp_core_d(double x, const double* c, int n, int u10) {
     double y = exp_poly_d(x, c, n, u10, &k);
     return from_bits_d(bits_d(y) + ((uint64_t)(int64_t)k << 52));
   }
-  int ok = (x >= K_EXP_UNF) && (x <= K_EXP_OVF);
-  double xs = ok ? x : 0.0;
-  double y = exp_poly_d(xs, c, n, u10, &k);
-  y = ldexp2(y, (int64_t)k);
-  y = (x > K_EXP_OVF) ? INFINITY : y;
-  y = (x < K_EXP_UNF) ? 0.0 : y;
-  y = (x != x) ? from_bits_d(CANON_NAN_D) : y;
-  return y;
+  if (x > K_EXP_OVF) return INFINITY;       /* saturation, constants.hpp:53-54 */
+  if (x < K_EXP_UNF) return 0.0;
+  if (x != x) return from_bits_d(CANON_NAN_D);
+  double y = exp_poly_d(x, c, n, u10, &k);  /* 708 <= |x|: ldexp2 rounds once */
+  return ldexp2(y, (int64_t)k);
 }
 double vo_exp_d_u10(double x) { return exp_core_d(x, C_EXP_D, VEM_EXP_D_N, 1); }
 double vo_exp_d_u35(double x) { return exp_core_d(x, C_EXP_D_U35, VEM_EXP_D_U35_N, 0); }
@@ -605,9 +602,13 @@ static inline int is_odd_d(double y) {
 static double pow_core_d(double x, double y, const double* cl, int nl) {
   uint32_t hx = (uint32_t)(bits_d(x) >> 32);
   uint32_t hy = (uint32_t)(bits_d(y) >> 32) & 0x7fffffffu, ly = (uint32_t)bits_d(y);
-  int fx = (hx - 0x00100000u) < 0x7fe00000u;           /* x positive normal finite */
-  int fy = (hy < 0x7ff00000u) && ((hy | ly) != 0u);     /* y finite, nonzero */
-  if (fx && fy) return exp_dd(dd_mul_d(log_dd(x, 0.0, cl, nl), y));
+  int fx = ((hx & 0x7fffffffu) - 0x00100000u) < 0x7fe00000u; /* x normal finite */
+  int fy = (hy < 0x7ff00000u) && ((hy | ly) != 0u);           /* y finite, nonzero */
+  if (fx && fy) {
+    double R = exp_dd(dd_mul_d(log_dd(fabs(x), 0.0, cl, nl), y));
+    if (x < 0.0) R = is_int_d(y) ? (is_odd_d(y) ? -R : R) : from_bits_d(CANON_NAN_D);
+    return R;
+  }
   double ax = fabs(x);
   int fin = (ax > 0.0) && (ax < INFINITY) && (fabs(y) < INFINITY);
   double R = 1.0;

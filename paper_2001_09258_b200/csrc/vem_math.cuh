@@ -417,14 +417,11 @@ __device__ __forceinline__ double exp_core_d(double x, const double* c) {
     double y = exp_poly_d<N, kU10>(x, c, k);
     return __hiloint2double(__double2hiint(y) + (k << 20), __double2loint(y));
   }
-  bool ok = (x >= kExpUnf) && (x <= kExpOvf);
-  double xs = ok ? x : 0.0;
-  double y = exp_poly_d<N, kU10>(xs, c, k);
-  y = ldexp2(y, (long long)k);
-  y = (x > kExpOvf) ? kInf : y;
-  y = (x < kExpUnf) ? 0.0 : y;
-  y = (x != x) ? from_bits_d(kCanonNanD) : y;
-  return y;
+  if (x > kExpOvf) return kInf;
+  if (x < kExpUnf) return 0.0;
+  if (x != x) return from_bits_d(kCanonNanD);
+  double y = exp_poly_d<N, kU10>(x, c, k);
+  return ldexp2(y, (long long)k);
 }
 __device__ __forceinline__ double exp_d_u10(double x) { return exp_core_d<VEM_EXP_D_N, true>(x, cExpD); }
 __device__ __forceinline__ double exp_d_u35(double x) { return exp_core_d<VEM_EXP_D_U35_N, false>(x, cExpDU35); }
@@ -576,9 +573,14 @@ template <int NL>
 __device__ __forceinline__ double pow_core_d(double x, double y, const double* cl, const double* lt) {
   uint32_t hx = (uint32_t)__double2hiint(x);
   uint32_t hy = (uint32_t)__double2hiint(y) & 0x7fffffffu, ly = (uint32_t)__double2loint(y);
-  bool fx = (hx - 0x00100000u) < 0x7fe00000u;
+  bool fx = ((hx & 0x7fffffffu) - 0x00100000u) < 0x7fe00000u;
   bool fy = (hy < 0x7ff00000u) && ((hy | ly) != 0u);
-  if (fx && fy) return exp_dd(dd_mul_d(log_dd<NL>(x, 0.0, cl, lt), y), lt);
+  if (fx && fy) {
+    double ax = __hiloint2double((int)(hx & 0x7fffffffu), __double2loint(x));
+    double R = exp_dd(dd_mul_d(log_dd<NL>(ax, 0.0, cl, lt), y), lt);
+    if ((int)hx < 0) R = is_int_d(y) ? (is_odd_d(y) ? -R : R) : from_bits_d(kCanonNanD);
+    return R;
+  }
   return pow_slow_d<NL>(x, y, cl, lt);
 }
 __device__ __forceinline__ double pow_d_u10(double x, double y, const double* lt) {
