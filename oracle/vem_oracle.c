@@ -835,7 +835,7 @@ static float pow_core_f(float x, float y, const double* cl, int nl) {
   int fy = ((uy & 0x7fffffffu) - 1u) < 0x7f7fffffu; /* y finite, != 0 */
   if (fx && fy) {
     double t = (double)y * log_f_internal((double)x, cl, nl);
-    t = fmin(fmax(t, -200.0), 200.0);
+    if (((uint32_t)(bits_d(t) >> 32) & 0x7fffffffu) >= 0x40690000u) t = (t > 0.0) ? 200.0 : -200.0;
     return (float)exp_f_internal(t);
   }
   float ax = fabsf(x);

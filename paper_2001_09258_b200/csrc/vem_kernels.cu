@@ -49,8 +49,7 @@ __device__ __forceinline__ const double* stage_table(double* stab) {
     double2* d2 = reinterpret_cast<double2*>(stab);
     for (int i = threadIdx.x; i < n2; i += blockDim.x) d2[i] = __ldg(s2 + i);
     if constexpr (TABLE == kTableLog) {
-      const double2* f2 = reinterpret_cast<const double2*>(gLogTfInvc);
-      for (int i = threadIdx.x; i < 64; i += blockDim.x) d2[kLtfInvc / 2 + i] = __ldg(f2 + i);
+      for (int i = threadIdx.x; i < 256; i += blockDim.x) stab[kLtfInvc + i] = (double)__ldg(gLogTfInvc + i);
     }
     __syncthreads();
     return stab;

@@ -65,6 +65,23 @@ constexpr double kDblMax = 1.7976931348623157e308;
 constexpr double kInf = __builtin_huge_val();
 constexpr float kInfF = __builtin_huge_valf();
 
+
+// Constant-bank copies of scalar constants used as DFMA/DMUL operands: a
+// c[bank][offset] operand is free, a 64-bit immediate costs two UMOVs per use.
+__constant__ double ccShift = 0x1.8p52;
+__constant__ double ccInvLn2 = 0x1.71547652b82fep+0;
+__constant__ double ccExpL1 = 0x1.62e42fefa3800p-1;
+__constant__ double ccExpL2 = 0x1.ef35793c76730p-45;
+__constant__ double ccLn2Hi = 0x1.62e42fefa39efp-1;
+__constant__ double ccLn2H42 = VEM_LN2_H42;
+__constant__ double ccLn2T42 = VEM_LN2_T42;
+__constant__ double ccExpjInv = VEM_EXPJ_INV;
+__constant__ double ccExpjL1 = VEM_EXPJ_L1;
+__constant__ double ccExpjL2 = VEM_EXPJ_L2;
+__constant__ double ccPio2Qd0 = 0x1.921fb54442d18p+0;
+__constant__ double ccPio2Qd1 = 0x1.1a62633145c07p-54;
+__constant__ double ccSixth = 0x1.5555555555555p-3;
+
 // Coefficients live in the constant bank: uniform operands of DFMA.
 __constant__ double cSinD[] = VEM_SIN_D_ARR;
 __constant__ double cCosD[] = VEM_COS_D_ARR;
@@ -90,9 +107,9 @@ __device__ const double gPhF[3 * VEM_PH_F_ENTRIES] = {VEM_PH_F_INIT};
 // log / exp tables (tools/genlogtables.py), structure of arrays, staged into
 // one shared-memory block (offsets in doubles):
 constexpr int kLtInvc = 0, kLtHi = 256, kLtLo = 512, kLtExpHi = 768, kLtExpLo = 896, kLtfHi = 1024,
-              kLtfInvc = 1280;  // 256 floats = 128 doubles
+              kLtfInvc = 1280;  // 256 binary32 invc, widened to binary64 when staged
 constexpr int kLogTabD = 1280;
-constexpr int kLogTabN = kLogTabD + 128;
+constexpr int kLogTabN = kLogTabD + 256;
 __device__ const double gLogExp[kLogTabD] = {VEM_LOGT_INVC_INIT VEM_LOGT_HI_INIT VEM_LOGT_LO_INIT
                                                  VEM_EXPT_HI_INIT VEM_EXPT_LO_INIT VEM_LOGTF_HI_INIT};
 __device__ const float gLogTfInvc[256] = {VEM_LOGTF_INVC_INIT};
@@ -121,9 +138,9 @@ __device__ __forceinline__ double toward0_pos(double x) { return from_bits_d(bit
 // nearest integer of a*b via one fma against 1.5*2^52 (oracle: rint_fma)
 constexpr double kShift = 0x1.8p52;
 __device__ __forceinline__ double rint_fma(double a, double b, int& k) {
-  double u = fma(a, b, kShift);
+  double u = fma(a, b, ccShift);
   k = __double2loint(u);
-  return u - kShift;
+  return u - ccShift;
 }
 
 // ------------------------------------------------------ DD (ddarith.hpp)
@@ -393,13 +410,13 @@ constexpr uint32_t kExpFastHi = 0x40862000u;  // |x| < 708
 
 template <int N, bool kU10>
 __device__ __forceinline__ double exp_poly_d(double xs, const double* c, int& k_out) {
-  double kd = rint_fma(xs, kInvLn2, k_out);
-  double r1 = fma(kd, -kExpL1, xs);
-  double r = fma(kd, -kExpL2, r1);
+  double kd = rint_fma(xs, ccInvLn2, k_out);
+  double r1 = fma(kd, -ccExpL1, xs);
+  double r = fma(kd, -ccExpL2, r1);
   double P = poly<N>(c, r);
   double y;
   if (kU10) {
-    double rl = fma(-kd, kExpL2, r1 - r);
+    double rl = fma(-kd, ccExpL2, r1 - r);
     double s = 1.0 + r;
     double se = (1.0 - s) + r;
     y = s + (se + fma(r * r, P, rl));
@@ -462,9 +479,9 @@ __device__ __forceinline__ dd log1p_dd(double rh, double rl, const double* c) {
 }
 
 __device__ __forceinline__ dd eln2_logc(const logred& g) {
-  double eh = g.E * VEM_LN2_H42;
+  double eh = g.E * ccLn2H42;
   dd H = two_sum_fast(eh, g.logc_hi);
-  H.lo = H.lo + fma(g.E, VEM_LN2_T42, g.logc_lo);
+  H.lo = H.lo + fma(g.E, ccLn2T42, g.logc_lo);
   return H;
 }
 
@@ -515,9 +532,9 @@ __device__ __forceinline__ double exp_dd(dd t, const double* __restrict__ lt) {
     tl = ok ? tl : 0.0;
   }
   int k;
-  double kd = rint_fma(th, VEM_EXPJ_INV, k);
-  double r1 = fma(kd, -VEM_EXPJ_L1, th);
-  double r2 = fma(kd, -VEM_EXPJ_L2, tl);
+  double kd = rint_fma(th, ccExpjInv, k);
+  double r1 = fma(kd, -ccExpjL1, th);
+  double r2 = fma(kd, -ccExpjL2, tl);
   dd r = two_sum_fast(r1, r2);
   double z = r.hi * r.hi;
   double Q = poly<VEM_EXPJ_D_N>(cExpjD, r.hi);
@@ -688,7 +705,7 @@ __device__ __forceinline__ redf ph_f(float xf, const double* __restrict__ tab) {
   double q1 = rint_fma(sm, 1.0, k1);
   double fh = sm - q1;
   double fl = c + (e1 + m2);
-  double r = fma(fh, kPio2Qd0, fma(fh, kPio2Qd1, fl * kPio2Qd0));
+  double r = fma(fh, ccPio2Qd0, fma(fh, ccPio2Qd1, fl * ccPio2Qd0));
   int q = k0 + k1;
   if (xs < 0.0f) {
     r = -r;
@@ -742,9 +759,9 @@ __device__ __forceinline__ float exp_core_f(float x, const double* c) {
   float xc = fminf(fmaxf(x, -150.0f), 130.0f);
   double xd = (double)xc;
   int k;
-  double kd = rint_fma(xd, kInvLn2, k);
-  double r = fma(kd, -kExpL1, xd);
-  r = fma(kd, -kExpL2, r);
+  double kd = rint_fma(xd, ccInvLn2, k);
+  double r = fma(kd, -ccExpL1, xd);
+  r = fma(kd, -ccExpL2, r);
   double P = poly<N>(c, r);
   double y = fma(r, P, 1.0);
   y = __hiloint2double(__double2hiint(y) + (k << 20), __double2loint(y));
@@ -761,10 +778,10 @@ __device__ __forceinline__ double log_f_internal(double a, const double* c, cons
   long long k = (long long)tmp >> 52;
   int idx = (int)((tmp >> 44) & 255u);
   double m = from_bits_d(ix - ((uint64_t)k << 52));
-  double r = fma(m, (double)reinterpret_cast<const float*>(lt + kLtfInvc)[idx], -1.0);
+  double r = fma(m, lt[kLtfInvc + idx], -1.0);  // == (double)invc_f32: exact product
   double Q = poly<N>(c, r);
   double L = fma(r * r, Q, r);
-  return fma((double)(int)k, kLn2Hi, lt[kLtfHi + idx] + L);
+  return fma((double)(int)k, ccLn2Hi, lt[kLtfHi + idx] + L);
 }
 template <int N>
 __device__ __forceinline__ float log_core_f(float x, const double* c, const double* lt) {
@@ -783,10 +800,10 @@ __device__ __forceinline__ bool is_odd_f(float y) {
 }
 __device__ __forceinline__ double exp_f_internal(double t, const double* __restrict__ lt) {
   int k;
-  double kd = rint_fma(t, VEM_EXPJ_INV, k);
-  double r = fma(kd, -VEM_EXPJ_L1, t);
-  r = fma(kd, -VEM_EXPJ_L2, r);
-  double p = fma(r * r, fma(r, 0x1.5555555555555p-3, 0.5), r);
+  double kd = rint_fma(t, ccExpjInv, k);
+  double r = fma(kd, -ccExpjL1, t);
+  r = fma(kd, -ccExpjL2, r);
+  double p = fma(r * r, fma(r, ccSixth, 0.5), r);
   double T = lt[kLtExpHi + (k & 127)];
   double R = fma(T, p, T);
   return __hiloint2double(__double2hiint(R) + ((k >> 7) << 20), __double2loint(R));
@@ -827,7 +844,7 @@ __device__ __forceinline__ float pow_core_f(float x, float y, const double* cl, 
   bool fy = ((uy & 0x7fffffffu) - 1u) < 0x7f7fffffu;
   if (fx && fy) {
     double t = (double)y * log_f_internal<NL>((double)x, cl, lt);
-    t = fmin(fmax(t, -200.0), 200.0);
+    if (((uint32_t)__double2hiint(t) & 0x7fffffffu) >= 0x40690000u) t = (t > 0.0) ? 200.0 : -200.0;
     return (float)exp_f_internal(t, lt);
   }
   return pow_slow_f<NL>(x, y, cl, lt);
