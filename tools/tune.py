@@ -1,0 +1,85 @@
+#!/usr/bin/env python3
+"""Launch-shape sweep for the streaming kernels (dev tool, runs on a GPU).
+
+Builds a tuning variant of the library (-DVEM_TUNE) into
+paper_2001_09258_b200/_tune/libvem_tune.so, then times every entry point
+(filtered by argv[2]) at 2^argv[1] elements for each (VPT, STAGES) variant:
+ 0:(1,2) 1:(1,4) 2:(2,2) 3:(2,3) 4:(2,4) 5:(4,2) and -1 = the shipped choice.
+Prints one JSON line per entry point with Gelem/s per variant.
+"""
+import ctypes
+import json
+import os
+import subprocess
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2001_09258_b200 import _lib, build  # noqa: E402
+from paper_2001_09258_b200 import inputs as I  # noqa: E402
+
+CFG = {"sin": 1, "cos": 1, "tan": 3, "atan": 5, "exp": 2, "log": 2, "pow": 2, "fmod": 4}
+
+
+def build_tune():
+    out = os.path.join(ROOT, "paper_2001_09258_b200", "_tune")
+    os.makedirs(out, exist_ok=True)
+    objs = []
+    for src in build.SOURCES:
+        o = os.path.join(out, src.replace(".cu", ".o"))
+        subprocess.run([build.nvcc(), *build.NVCC_FLAGS, "-DVEM_TUNE", "-c", os.path.join(build.CSRC, src), "-o", o],
+                       check=True)
+        objs.append(o)
+    lib = os.path.join(out, "libvem_tune.so")
+    subprocess.run([build.nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static", *objs,
+                    "-o", lib], check=True)
+    return lib
+
+
+def main():
+    lg = int(sys.argv[1]) if len(sys.argv) > 1 else 26
+    flt = sys.argv[2].split(",") if len(sys.argv) > 2 else []
+    L = ctypes.CDLL(build_tune())
+    L.vem_tune_set.argtypes = [ctypes.c_int]
+    n = 1 << lg
+    stream = torch.cuda.current_stream().cuda_stream
+    for name in sorted(_lib.ALL):
+        if flt and not any(f in name for f in flt):
+            continue
+        if name.startswith("fmod"):
+            continue
+        fn, p = name.split("_")[0], name.split("_")[1]
+        cfg = 3 if name.endswith("_ph") else CFG[fn]
+        arrs = I.config_inputs(cfg, fn, p, n)
+        ts = [torch.from_numpy(a).cuda() for a in arrs]
+        out = torch.empty_like(ts[0])
+        f = getattr(L, "vem_" + name)
+        if len(ts) == 2:
+            f.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_size_t, ctypes.c_void_p]
+            call = lambda: f(ts[0].data_ptr(), ts[1].data_ptr(), out.data_ptr(), n, stream)  # noqa: E731
+        else:
+            f.argtypes = [ctypes.c_void_p] * 2 + [ctypes.c_size_t, ctypes.c_void_p]
+            call = lambda: f(ts[0].data_ptr(), out.data_ptr(), n, stream)  # noqa: E731
+        res = {}
+        for v in (-1, 0, 1, 2, 3, 4, 5):
+            L.vem_tune_set(v)
+            for _ in range(3):
+                call()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(10):
+                call()
+            e1.record()
+            torch.cuda.synchronize()
+            res[v] = round(n / (e0.elapsed_time(e1) / 10) / 1e6, 1)
+        best = max(res, key=res.get)
+        print(json.dumps({"fn": name, "gelem_s": res, "best": best}), flush=True)
+        del ts, out
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
