@@ -148,6 +148,15 @@ __global__ void __launch_bounds__(kThreads) k_binary(const T* __restrict__ x, co
   }
 }
 
+// Ops whose per-lane work depends on a data class (the trig reduction
+// selector, reduction.hpp:189-206: CW1 / CW2 / Payne-Hanek).  For these the
+// streaming kernel regroups each warp's elements by class (warp-level
+// ballot/popcount compaction through shared memory) so that lanes of one
+// warp take the same reduction path; results are scattered back to their
+// original slots before the coalesced store.  Warps whose elements all share
+// one class skip the regrouping.
+template <class Op> struct SortsByClass { static constexpr bool value = false; };
+
 // ------------------------------------------------- TMA-staged streaming
 // NIN inputs (1 or 2); tiles of kThreads*VPT 16-byte vectors per input;
 // STAGES tiles in flight per CTA (see vem_stream.cuh).  Elements past the
@@ -160,9 +169,13 @@ __global__ void __launch_bounds__(kThreads) k_stream(const T* __restrict__ a, co
   constexpr int TILE_V = kThreads * VPT;
   constexpr uint32_t TILE_BYTES = TILE_V * 16;
   constexpr int TILE_E = TILE_V * W;
+  constexpr bool kSort = SortsByClass<Op>::value && NIN == 1;
+  constexpr int NE = VPT * W;  // elements per lane per tile
   extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ uint64_t bars[STAGES];
   __shared__ __align__(16) double stab[TableSize<TABLE>::n];
+  __shared__ __align__(16) T wscr[kSort ? kThreads * NE : 1];
+  __shared__ unsigned short widx[kSort ? kThreads * NE : 1];
   V* buf = reinterpret_cast<V*>(dsm);
   const int tid = threadIdx.x;
   if (tid == 0) {
@@ -201,15 +214,82 @@ __global__ void __launch_bounds__(kThreads) k_stream(const T* __restrict__ a, co
     __syncthreads();  // stage s fully consumed -> refill it
     if (tid == 0 && j + STAGES < my) issue(s, blockIdx.x + (j + STAGES) * G);
     V* ov = reinterpret_cast<V*>(out) + (blockIdx.x + j * G) * TILE_V;
+    bool done = false;
+    if constexpr (kSort) {
+      const int lane = tid & 31;
+      const unsigned lt_mask = (1u << lane) - 1u;
+      T xe[NE];
+      int cl[NE];
 #pragma unroll
-    for (int v = 0; v < VPT; v++) {
-      V o;
+      for (int v = 0; v < VPT; v++)
 #pragma unroll
-      for (int k = 0; k < W; k++) {
-        if constexpr (NIN == 2) vget(o, k) = op(vget(va[v], k), vget(vb[v], k), tab);
-        else vget(o, k) = op(vget(va[v], k), tab);
+        for (int k = 0; k < W; k++) xe[v * W + k] = vget(va[v], k);
+      bool same = true;
+#pragma unroll
+      for (int e = 0; e < NE; e++) {
+        cl[e] = Op::cls(xe[e]);
+        same = same && (cl[e] == cl[0]);
       }
-      __stcs(ov + v * kThreads + tid, o);
+      const int c_l0 = __shfl_sync(0xffffffffu, cl[0], 0);
+      if (!__all_sync(0xffffffffu, same && cl[0] == c_l0)) {
+        T* sx = wscr + (tid >> 5) * (32 * NE);
+        unsigned short* si = widx + (tid >> 5) * (32 * NE);
+        unsigned m2[NE], m1[NE];
+        int n2 = 0, n1 = 0;
+#pragma unroll
+        for (int e = 0; e < NE; e++) {
+          m2[e] = __ballot_sync(0xffffffffu, cl[e] == 2);
+          m1[e] = __ballot_sync(0xffffffffu, cl[e] == 1);
+          n2 += __popc(m2[e]);
+          n1 += __popc(m1[e]);
+        }
+        int a2 = 0, a1 = n2, a0 = n2 + n1;  // heaviest class first
+#pragma unroll
+        for (int e = 0; e < NE; e++) {
+          const unsigned m0 = ~(m2[e] | m1[e]);
+          const int pos = cl[e] == 2 ? a2 + __popc(m2[e] & lt_mask)
+                        : cl[e] == 1 ? a1 + __popc(m1[e] & lt_mask)
+                                     : a0 + __popc(m0 & lt_mask);
+          a2 += __popc(m2[e]);
+          a1 += __popc(m1[e]);
+          a0 += __popc(m0);
+          sx[pos] = xe[e];
+          si[pos] = (unsigned short)(e * 32 + lane);
+        }
+        __syncwarp();
+        T xs[NE];
+        int ids[NE];
+#pragma unroll
+        for (int r = 0; r < NE; r++) {
+          xs[r] = sx[r * 32 + lane];
+          ids[r] = si[r * 32 + lane];
+        }
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < NE; r++) sx[ids[r]] = op(xs[r], tab);
+        __syncwarp();
+#pragma unroll
+        for (int v = 0; v < VPT; v++) {
+          V o;
+#pragma unroll
+          for (int k = 0; k < W; k++) vget(o, k) = sx[(v * W + k) * 32 + lane];
+          __stcs(ov + v * kThreads + tid, o);
+        }
+        __syncwarp();
+        done = true;
+      }
+    }
+    if (!done) {
+#pragma unroll
+      for (int v = 0; v < VPT; v++) {
+        V o;
+#pragma unroll
+        for (int k = 0; k < W; k++) {
+          if constexpr (NIN == 2) vget(o, k) = op(vget(va[v], k), vget(vb[v], k), tab);
+          else vget(o, k) = op(vget(va[v], k), tab);
+        }
+        __stcs(ov + v * kThreads + tid, o);
+      }
     }
   }
   // remainder (< one tile)
@@ -341,9 +421,16 @@ __global__ void __launch_bounds__(kFmodWarps * 32) k_fmod(const T* __restrict__ 
   struct NAME {                                                                       \
     __device__ __forceinline__ T operator()(T x, const double* tab) const { return EXPR; } \
   };
-VEM_UNARY_OP(OpSinD, double, (sin_d_u10<false>(x, tab)))
-VEM_UNARY_OP(OpCosD, double, (cos_d_u10<false>(x, tab)))
-VEM_UNARY_OP(OpTanD, double, (tan_d_u10<false>(x, tab)))
+#define VEM_TRIG_OP(NAME, EXPR)                                                          \
+  struct NAME {                                                                          \
+    __device__ __forceinline__ double operator()(double x, const double* tab) const { return EXPR; } \
+    __device__ __forceinline__ static int cls(double x) { return trig_class(x); }      \
+  };                                                                                     \
+  template <> struct SortsByClass<NAME> { static constexpr bool value = true; };
+VEM_TRIG_OP(OpSinD, (sin_d_u10<false>(x, tab)))
+VEM_TRIG_OP(OpCosD, (cos_d_u10<false>(x, tab)))
+VEM_TRIG_OP(OpTanD, (tan_d_u10<false>(x, tab)))
+#undef VEM_TRIG_OP
 VEM_UNARY_OP(OpSinDPh, double, (sin_d_u10<true>(x, tab)))
 VEM_UNARY_OP(OpCosDPh, double, (cos_d_u10<true>(x, tab)))
 VEM_UNARY_OP(OpTanDPh, double, (tan_d_u10<true>(x, tab)))

@@ -304,6 +304,12 @@ __device__ __forceinline__ red ph(double x_in, const double* __restrict__ tab) {
   return o;
 }
 
+// reduction path class of x: 0 = CW1 (|x| <= 15), 1 = CW2 (<= 1e14), 2 = PH
+__device__ __forceinline__ int trig_class(double x) {
+  const uint64_t ab = bits_d(x) & 0x7fffffffffffffffull;
+  return ab <= 0x402e000000000000ull ? 0 : (ab <= 0x42d6bcc41e900000ull ? 1 : 2);
+}
+
 // reduction.hpp:189-206 (deterministic, per lane).  Lanes of one warp that
 // agree skip the heavier paths; disagreeing warps run both (SIMT divergence).
 __device__ __forceinline__ red trig_reduce(double x, const double* __restrict__ tab) {
