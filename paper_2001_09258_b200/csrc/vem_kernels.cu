@@ -29,8 +29,8 @@ enum TableKind { kNoTable = 0, kTableD = 1, kTableF = 2, kTableLog = 3, kTableDG
 
 template <int TABLE>
 struct TableSize {
-  static constexpr int n = TABLE == kTableD   ? 4 * VEM_PH_D_ENTRIES
-                           : TABLE == kTableF ? 3 * VEM_PH_F_ENTRIES
+  static constexpr int n = TABLE == kTableD   ? 4 * VEM_PH_D_ENTRIES + kSinCosCoefN
+                           : TABLE == kTableF ? 3 * VEM_PH_F_ENTRIES + kSinCosCoefN
                            : TABLE == kTableLog ? kLogTabN
                                                 : 2;
 };
@@ -44,12 +44,16 @@ __device__ __forceinline__ const double* stage_table(double* stab) {
     return gPhD;
   } else {
     const double* src = TABLE == kTableD ? gPhD : (TABLE == kTableF ? gPhF : gLogExp);
-    constexpr int n2 = (TABLE == kTableLog ? kLogTabD : TableSize<TABLE>::n) / 2;
+    constexpr int n2 = (TABLE == kTableLog ? kLogTabD : TableSize<TABLE>::n - kSinCosCoefN) / 2;
     const double2* s2 = reinterpret_cast<const double2*>(src);
     double2* d2 = reinterpret_cast<double2*>(stab);
     for (int i = threadIdx.x; i < n2; i += blockDim.x) d2[i] = __ldg(s2 + i);
     if constexpr (TABLE == kTableLog) {
       for (int i = threadIdx.x; i < 256; i += blockDim.x) stab[kLtfInvc + i] = (double)__ldg(gLogTfInvc + i);
+    }
+    if constexpr (TABLE == kTableD || TABLE == kTableF) {  // per-lane coefficient sets (sin | cos)
+      const double* cs = TABLE == kTableD ? gSinCosD : gSinCosF;
+      if (threadIdx.x < kSinCosCoefN) stab[TableSize<TABLE>::n - kSinCosCoefN + threadIdx.x] = cs[threadIdx.x];
     }
     __syncthreads();
     return stab;

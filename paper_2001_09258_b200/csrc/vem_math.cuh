@@ -101,6 +101,17 @@ __constant__ double cExpjD[] = VEM_EXPJ_D_ARR;
 __constant__ double cLog1pF[] = VEM_LOG1P_F_ARR;
 __constant__ double cLog1pFU35[] = VEM_LOG1P_F_U35_ARR;
 
+// sin | cos coefficient sets, 8-double aligned, staged behind the PH tables so
+// a lane fetches its quadrant's set with LDS.128 instead of per-coefficient
+// selects (2 distinct addresses per warp, conflict-free).
+constexpr int kSinCosCoefN = 16;
+__device__ const double gSinCosD[kSinCosCoefN] = {
+    VEM_SIN_D_C0, VEM_SIN_D_C1, VEM_SIN_D_C2, VEM_SIN_D_C3, VEM_SIN_D_C4, VEM_SIN_D_C5, 0.0, 0.0,
+    VEM_COS_D_C0, VEM_COS_D_C1, VEM_COS_D_C2, VEM_COS_D_C3, VEM_COS_D_C4, VEM_COS_D_C5, 0.0, 0.0};
+__device__ const double gSinCosF[kSinCosCoefN] = {
+    VEM_SIN_F_C0, VEM_SIN_F_C1, VEM_SIN_F_C2, VEM_SIN_F_C3, 0.0,          0.0, 0.0, 0.0,
+    -0.5,         VEM_COS_F_C0, VEM_COS_F_C1, VEM_COS_F_C2, VEM_COS_F_C3, 0.0, 0.0, 0.0};
+
 // Payne-Hanek tables (global copy; kernels stage them into shared memory).
 __device__ const double gPhD[4 * VEM_PH_D_ENTRIES] = {VEM_PH_D_INIT};
 __device__ const double gPhF[3 * VEM_PH_F_ENTRIES] = {VEM_PH_F_INIT};
@@ -310,17 +321,22 @@ __device__ __forceinline__ int trig_class(double x) {
   return ab <= 0x402e000000000000ull ? 0 : (ab <= 0x42d6bcc41e900000ull ? 1 : 2);
 }
 
-// reduction.hpp:189-206 (deterministic, per lane).  Lanes of one warp that
-// agree skip the heavier paths; disagreeing warps run both (SIMT divergence).
+// reduction.hpp:189-206 (deterministic, per lane).  Like the reference's
+// `if (!all(small))` skips, each heavier method runs only if some lane of the
+// warp needs it (warp vote -> uniform branch, never if-converted), and is
+// selected per lane, so every lane's result is the per-lane Det result.
 __device__ __forceinline__ red trig_reduce(double x, const double* __restrict__ tab) {
-  const uint64_t ab = bits_d(x) & 0x7fffffffffffffffull;  // |x| <= c  <=>  bits(|x|) <= bits(c)
-  red r;
-  if (ab <= 0x402e000000000000ull) {         // 15
-    r = cw1(x);
-  } else if (ab <= 0x42d6bcc41e900000ull) {  // 1e14
-    r = cw2(x);
-  } else {
-    r = ph(x, tab);
+  const int c = trig_class(x);
+  const unsigned mask = __activemask();
+  red r = {0.0, 0.0, 0};
+  if (__any_sync(mask, c == 0)) r = cw1(x);
+  if (__any_sync(mask, c == 1)) {
+    red r2 = cw2(x);
+    if (c == 1) r = r2;
+  }
+  if (__any_sync(mask, c == 2)) {
+    red r3 = ph(x, tab);
+    if (c == 2) r = r3;
   }
   return r;
 }
@@ -328,10 +344,12 @@ __device__ __forceinline__ red trig_reduce(double x, const double* __restrict__ 
 // ===================================================== f64 functions
 // oracle: sincos_core_d (same values; selects hoisted to the inputs of the
 // shared operations so the two forms cost one multiply, one final sum)
-__device__ __forceinline__ double sincos_core_d(double rh, double rl, int cosform) {
+__device__ __forceinline__ double sincos_core_d(double rh, double rl, int cosform, const double* tab) {
   bool cf = cosform != 0;
   double z = rh * rh;
-  double P = poly_sel<VEM_SIN_D_N>(cCosD, cSinD, cf, z);
+  const double2* cs = reinterpret_cast<const double2*>(tab + 4 * VEM_PH_D_ENTRIES + (cf ? 8 : 0));
+  const double2 c01 = cs[0], c23 = cs[1], c45 = cs[2];
+  double P = fma(fma(fma(fma(fma(c45.y, z, c45.x), z, c23.y), z, c23.x), z, c01.y), z, c01.x);
   double hz = 0.5 * z;
   double M = z * (cf ? z : rh);              // cos: z*z, sin: rh*z
   double Ts = fma(-hz, rl, rl);              // sin: rl - rl*z/2
@@ -352,7 +370,7 @@ __device__ __forceinline__ bool not_finite_bits(double x) {
 template <bool kForcePh>
 __device__ __forceinline__ double sin_d_u10(double x, const double* tab) {
   red r = kForcePh ? ph(x, tab) : trig_reduce(x, tab);
-  double y = sincos_core_d(r.hi, r.lo, r.q & 1);
+  double y = sincos_core_d(r.hi, r.lo, r.q & 1, tab);
   y = neg_if(y, r.q & 2);
   y = is_zero_bits(x) ? x : y;
   return not_finite_bits(x) ? from_bits_d(kCanonNanD) : y;
@@ -360,7 +378,7 @@ __device__ __forceinline__ double sin_d_u10(double x, const double* tab) {
 template <bool kForcePh>
 __device__ __forceinline__ double cos_d_u10(double x, const double* tab) {
   red r = kForcePh ? ph(x, tab) : trig_reduce(x, tab);
-  double y = sincos_core_d(r.hi, r.lo, (r.q & 1) ^ 1);
+  double y = sincos_core_d(r.hi, r.lo, (r.q & 1) ^ 1, tab);
   y = neg_if(y, (r.q + 1) & 2);
   return not_finite_bits(x) ? from_bits_d(kCanonNanD) : y;
 }
@@ -720,23 +738,20 @@ __device__ __forceinline__ redf ph_f(float xf, const double* __restrict__ tab) {
   return {r, q & 3};
 }
 
-__device__ __forceinline__ double sincos_core_f(double r, int cosform) {
+__device__ __forceinline__ double sincos_core_f(double r, int cosform, const double* tab) {
   bool cf = cosform != 0;
-  double c0 = cf ? -0.5 : cSinF[0];
-  double c1 = cf ? cCosF[0] : cSinF[1];
-  double c2 = cf ? cCosF[1] : cSinF[2];
-  double c3 = cf ? cCosF[2] : cSinF[3];
-  double c4 = cf ? cCosF[3] : 0.0;
-  double c[5] = {c0, c1, c2, c3, c4};
+  const double2* cs = reinterpret_cast<const double2*>(tab + 3 * VEM_PH_F_ENTRIES + (cf ? 8 : 0));
+  const double2 c01 = cs[0], c23 = cs[1];
+  const double c4 = tab[3 * VEM_PH_F_ENTRIES + (cf ? 12 : 4)];
   double z = r * r;
-  double P = poly<5>(c, z);
+  double P = fma(fma(fma(fma(c4, z, c23.y), z, c23.x), z, c01.y), z, c01.x);
   double A = cf ? 1.0 : r;
   return fma(A * z, P, A);
 }
 
 __device__ __forceinline__ float sin_f_u10(float x, const double* tab) {
   redf r = ph_f(x, tab);
-  double y = sincos_core_f(r.r, r.q & 1);
+  double y = sincos_core_f(r.r, r.q & 1, tab);
   y = neg_if(y, r.q & 2);
   float o = (float)y;
   o = (x == 0.0f) ? x : o;
@@ -744,7 +759,7 @@ __device__ __forceinline__ float sin_f_u10(float x, const double* tab) {
 }
 __device__ __forceinline__ float cos_f_u10(float x, const double* tab) {
   redf r = ph_f(x, tab);
-  double y = sincos_core_f(r.r, (r.q & 1) ^ 1);
+  double y = sincos_core_f(r.r, (r.q & 1) ^ 1, tab);
   y = neg_if(y, (r.q + 1) & 2);
   float o = (float)y;
   return canon_f(isinf(x) ? from_bits_f(kCanonNanF) : (x != x ? x : o));
