@@ -32,6 +32,7 @@ struct TableSize {
   static constexpr int n = TABLE == kTableD   ? 4 * VEM_PH_D_ENTRIES + kSinCosCoefN
                            : TABLE == kTableF ? 3 * VEM_PH_F_ENTRIES + kSinCosCoefN
                            : TABLE == kTableLog ? kLogTabN
+                           : TABLE == kTableDG ? kSinCosCoefN
                                                 : 2;
 };
 
@@ -40,8 +41,9 @@ __device__ __forceinline__ const double* stage_table(double* stab) {
   if constexpr (TABLE == kNoTable) {
     return nullptr;
   } else if constexpr (TABLE == kTableDG) {
+    if (threadIdx.x < kSinCosCoefN) stab[threadIdx.x] = gSinCosD[threadIdx.x];
     __syncthreads();
-    return gPhD;
+    return stab;
   } else {
     const double* src = TABLE == kTableD ? gPhD : (TABLE == kTableF ? gPhF : gLogExp);
     constexpr int n2 = (TABLE == kTableLog ? kLogTabD : TableSize<TABLE>::n - kSinCosCoefN) / 2;
@@ -431,12 +433,13 @@ __global__ void __launch_bounds__(kFmodWarps * 32) k_fmod(const T* __restrict__ 
     __device__ __forceinline__ static int cls(double x) { return trig_class(x); }      \
   };                                                                                     \
   template <> struct SortsByClass<NAME> { static constexpr bool value = true; };
-VEM_TRIG_OP(OpSinD, (sin_d_u10<false>(x, tab)))
-VEM_TRIG_OP(OpCosD, (cos_d_u10<false>(x, tab)))
-VEM_TRIG_OP(OpTanD, (tan_d_u10<false>(x, tab)))
+// selector variants: PH table from global memory (L1), coefficients staged
+VEM_TRIG_OP(OpSinD, (sin_d_u10<false>(x, gPhD, tab)))
+VEM_TRIG_OP(OpCosD, (cos_d_u10<false>(x, gPhD, tab)))
+VEM_TRIG_OP(OpTanD, (tan_d_u10<false>(x, gPhD)))
 #undef VEM_TRIG_OP
-VEM_UNARY_OP(OpSinDPh, double, (sin_d_u10<true>(x, tab)))
-VEM_UNARY_OP(OpCosDPh, double, (cos_d_u10<true>(x, tab)))
+VEM_UNARY_OP(OpSinDPh, double, (sin_d_u10<true>(x, tab, tab + 4 * VEM_PH_D_ENTRIES)))
+VEM_UNARY_OP(OpCosDPh, double, (cos_d_u10<true>(x, tab, tab + 4 * VEM_PH_D_ENTRIES)))
 VEM_UNARY_OP(OpTanDPh, double, (tan_d_u10<true>(x, tab)))
 VEM_UNARY_OP(OpAtanD, double, ((void)tab, atan_d_u10(x)))
 VEM_UNARY_OP(OpExpD, double, ((void)tab, exp_d_u10(x)))
@@ -652,9 +655,9 @@ static int launch_tuned(const T* a, const T* b, T* o, size_t n, vem_stream_t s) 
 // vectors in flight, FP64-pipe-bound ones 2 (register pressure).
 extern "C" {
 
-int vem_sin_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpSinD, double, 1, kTableD, 2, 2>(x, nullptr, y, n, s); }
-int vem_cos_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpCosD, double, 1, kTableD, 2, 2>(x, nullptr, y, n, s); }
-int vem_tan_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpTanD, double, 1, kTableD, 2, 2>(x, nullptr, y, n, s); }
+int vem_sin_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpSinD, double, 1, kTableDG, 2, 2>(x, nullptr, y, n, s); }
+int vem_cos_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpCosD, double, 1, kTableDG, 2, 2>(x, nullptr, y, n, s); }
+int vem_tan_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpTanD, double, 1, kTableDG, 2, 2>(x, nullptr, y, n, s); }
 int vem_sin_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpSinDPh, double, 1, kTableD, 2, 2>(x, nullptr, y, n, s); }
 int vem_cos_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpCosDPh, double, 1, kTableD, 2, 2>(x, nullptr, y, n, s); }
 int vem_tan_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpTanDPh, double, 1, kTableD, 2, 2>(x, nullptr, y, n, s); }

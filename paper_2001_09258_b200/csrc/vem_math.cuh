@@ -321,22 +321,18 @@ __device__ __forceinline__ int trig_class(double x) {
   return ab <= 0x402e000000000000ull ? 0 : (ab <= 0x42d6bcc41e900000ull ? 1 : 2);
 }
 
-// reduction.hpp:189-206 (deterministic, per lane).  Like the reference's
-// `if (!all(small))` skips, each heavier method runs only if some lane of the
-// warp needs it (warp vote -> uniform branch, never if-converted), and is
-// selected per lane, so every lane's result is the per-lane Det result.
+// reduction.hpp:189-206 (deterministic, per lane).  A lane takes only its own
+// method; warps whose lanes agree (all warps after the class regrouping in
+// the streaming kernel) therefore skip the heavier methods entirely.
 __device__ __forceinline__ red trig_reduce(double x, const double* __restrict__ tab) {
   const int c = trig_class(x);
-  const unsigned mask = __activemask();
-  red r = {0.0, 0.0, 0};
-  if (__any_sync(mask, c == 0)) r = cw1(x);
-  if (__any_sync(mask, c == 1)) {
-    red r2 = cw2(x);
-    if (c == 1) r = r2;
-  }
-  if (__any_sync(mask, c == 2)) {
-    red r3 = ph(x, tab);
-    if (c == 2) r = r3;
+  red r;
+  if (c == 0) {
+    r = cw1(x);
+  } else if (c == 1) {
+    r = cw2(x);
+  } else {
+    r = ph(x, tab);
   }
   return r;
 }
@@ -344,10 +340,10 @@ __device__ __forceinline__ red trig_reduce(double x, const double* __restrict__ 
 // ===================================================== f64 functions
 // oracle: sincos_core_d (same values; selects hoisted to the inputs of the
 // shared operations so the two forms cost one multiply, one final sum)
-__device__ __forceinline__ double sincos_core_d(double rh, double rl, int cosform, const double* tab) {
+__device__ __forceinline__ double sincos_core_d(double rh, double rl, int cosform, const double* coef) {
   bool cf = cosform != 0;
   double z = rh * rh;
-  const double2* cs = reinterpret_cast<const double2*>(tab + 4 * VEM_PH_D_ENTRIES + (cf ? 8 : 0));
+  const double2* cs = reinterpret_cast<const double2*>(coef + (cf ? 8 : 0));
   const double2 c01 = cs[0], c23 = cs[1], c45 = cs[2];
   double P = fma(fma(fma(fma(fma(c45.y, z, c45.x), z, c23.y), z, c23.x), z, c01.y), z, c01.x);
   double hz = 0.5 * z;
@@ -367,18 +363,19 @@ __device__ __forceinline__ bool not_finite_bits(double x) {
 }
 
 // NaN can only come from a non-finite input: canonicalised by an integer test
+// `tab`: Payne-Hanek table (shared or global); `coef`: the sin|cos block
 template <bool kForcePh>
-__device__ __forceinline__ double sin_d_u10(double x, const double* tab) {
+__device__ __forceinline__ double sin_d_u10(double x, const double* tab, const double* coef) {
   red r = kForcePh ? ph(x, tab) : trig_reduce(x, tab);
-  double y = sincos_core_d(r.hi, r.lo, r.q & 1, tab);
+  double y = sincos_core_d(r.hi, r.lo, r.q & 1, coef);
   y = neg_if(y, r.q & 2);
   y = is_zero_bits(x) ? x : y;
   return not_finite_bits(x) ? from_bits_d(kCanonNanD) : y;
 }
 template <bool kForcePh>
-__device__ __forceinline__ double cos_d_u10(double x, const double* tab) {
+__device__ __forceinline__ double cos_d_u10(double x, const double* tab, const double* coef) {
   red r = kForcePh ? ph(x, tab) : trig_reduce(x, tab);
-  double y = sincos_core_d(r.hi, r.lo, (r.q & 1) ^ 1, tab);
+  double y = sincos_core_d(r.hi, r.lo, (r.q & 1) ^ 1, coef);
   y = neg_if(y, (r.q + 1) & 2);
   return not_finite_bits(x) ? from_bits_d(kCanonNanD) : y;
 }
