@@ -339,7 +339,8 @@ __global__ void __launch_bounds__(kFmodWarps * 32) k_fmod(const T* __restrict__ 
   unsigned head = 0, tail = 0;  // ring consumer / producer counters (warp-uniform)
   fmod_state st = {0.0, 1.0, 1.0, 1.0, 0, 0};
   size_t gi = 0;
-  bool active = false;
+  bool active = false;  // stepping
+  bool pend = false;    // finished, result not stored yet (stored at the next refill)
 
   auto step_all = [&]() {
     if (active) {
@@ -347,28 +348,36 @@ __global__ void __launch_bounds__(kFmodWarps * 32) k_fmod(const T* __restrict__ 
       st.E -= sh;
       st.r = fmod_step(st.r, sh, st.md, st.rmd);
       if (st.E == 0 || st.r == 0.0) {
-        __stcs(out + gi, (T)fmod_finish(st));
         active = false;
+        pend = true;
       }
     }
   };
+  // finishing is deferred into the (divergent) refill block, so the step
+  // loop itself carries no per-iteration finish code
   auto refill = [&](bool force) {
     unsigned idle = __ballot_sync(0xffffffffu, !active);
     int nidle = __popc(idle);
     unsigned avail = tail - head;
-    if (avail == 0u || nidle == 0 || (!force && nidle < kRefill && avail >= (unsigned)kRefill)) return;
+    if (nidle == 0 || (!force && (nidle < kRefill || avail == 0u))) return;
     unsigned k = head + __popc(idle & lt_mask);
-    if (!active && k < tail) {
-      int sl = (int)(k % kFmodRing);
-      st.r = s_r[wl][sl];
-      st.md = s_md[wl][sl];
-      st.rmd = s_rmd[wl][sl];
-      int2 e = s_e[wl][sl];
-      st.E = e.x;
-      st.ed = e.y >> 1;
-      st.x = (e.y & 1) ? -1.0 : 1.0;
-      gi = (size_t)s_g[wl][sl];
-      active = true;
+    if (!active) {
+      if (pend) {
+        __stcs(out + gi, (T)fmod_finish(st));
+        pend = false;
+      }
+      if (k < tail) {
+        int sl = (int)(k % kFmodRing);
+        st.r = s_r[wl][sl];
+        st.md = s_md[wl][sl];
+        st.rmd = s_rmd[wl][sl];
+        int2 e = s_e[wl][sl];
+        st.E = e.x;
+        st.ed = e.y >> 1;
+        st.x = (e.y & 1) ? -1.0 : 1.0;
+        gi = (size_t)s_g[wl][sl];
+        active = true;
+      }
     }
     head += min((unsigned)nidle, avail);
     __syncwarp();
@@ -408,18 +417,21 @@ __global__ void __launch_bounds__(kFmodWarps * 32) k_fmod(const T* __restrict__ 
       tail += __popc(m);
     }
     __syncwarp();
-    // ---- phase 2: step until the ring is empty
+    // ---- phase 2: step (two per refill check) until the ring is empty
     while (true) {
       refill(false);
       if (tail == head) break;
+      step_all();
       step_all();
     }
   }
   // ---- drain
   while (__any_sync(0xffffffffu, active)) {
     step_all();
+    step_all();
     refill(true);
   }
+  if (pend) __stcs(out + gi, (T)fmod_finish(st));
 }
 
 // ------------------------------------------------------------- functors
