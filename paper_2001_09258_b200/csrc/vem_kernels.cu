@@ -167,9 +167,9 @@ template <class Op> struct SortsByClass { static constexpr bool value = false; }
 // NIN inputs (1 or 2); tiles of kThreads*VPT 16-byte vectors per input;
 // STAGES tiles in flight per CTA (see vem_stream.cuh).  Elements past the
 // last full tile are finished by a grid-stride scalar loop in the same launch.
-template <class Op, class T, int NIN, int TABLE, int VPT, int STAGES>
-__global__ void __launch_bounds__(kThreads) k_stream(const T* __restrict__ a, const T* __restrict__ b,
-                                                     T* __restrict__ out, size_t n) {
+template <class Op, class T, int NIN, int TABLE, int VPT, int STAGES, int MINB = 1>
+__global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__ a, const T* __restrict__ b,
+                                                           T* __restrict__ out, size_t n) {
   using V = typename Vec16<T>::type;
   constexpr int W = Vec16<T>::n;
   constexpr int TILE_V = kThreads * VPT;
@@ -545,14 +545,14 @@ static int launch_binary(const T* x, const T* y2, T* out, size_t n, vem_stream_t
   return (int)cudaGetLastError();
 }
 
-template <class Op, class T, int NIN, int TABLE, int VPT, int STAGES>
+template <class Op, class T, int NIN, int TABLE, int VPT, int STAGES, int MINB = 1>
 static int launch_stream(const T* a, const T* b, T* out, size_t n, vem_stream_t s) {
   if (n == 0) return 0;
   if (!(aligned16(a) && aligned16(out) && (NIN == 1 || aligned16(b)))) {
     if constexpr (NIN == 2) return launch_binary<Op, T, TABLE, 1>(a, b, out, n, s);
     else return launch_unary<Op, T, TABLE, 1>(a, out, n, s);
   }
-  auto k = k_stream<Op, T, NIN, TABLE, VPT, STAGES>;
+  auto k = k_stream<Op, T, NIN, TABLE, VPT, STAGES, MINB>;
   constexpr int smem = STAGES * NIN * kThreads * VPT * 16;
   static const int occ = [k] {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -655,6 +655,9 @@ static int launch_tuned(const T* a, const T* b, T* o, size_t n, vem_stream_t s) 
     case 3: return launch_stream<Op, T, NIN, TAB, 2, 3>(a, b, o, n, s);
     case 4: return launch_stream<Op, T, NIN, TAB, 2, 4>(a, b, o, n, s);
     case 5: return launch_stream<Op, T, NIN, TAB, 4, 2>(a, b, o, n, s);
+    case 6: return launch_stream<Op, T, NIN, TAB, VPT, ST, 2>(a, b, o, n, s);
+    case 7: return launch_stream<Op, T, NIN, TAB, VPT, ST, 3>(a, b, o, n, s);
+    case 8: return launch_stream<Op, T, NIN, TAB, VPT, ST, 4>(a, b, o, n, s);
     default: return launch_stream<Op, T, NIN, TAB, VPT, ST>(a, b, o, n, s);
   }
 }

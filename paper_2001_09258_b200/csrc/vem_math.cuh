@@ -801,9 +801,27 @@ __device__ __forceinline__ double log_f_internal(double a, const double* c, cons
   double L = fma(r * r, Q, r);
   return fma((double)(int)k, ccLn2Hi, lt[kLtfHi + idx] + L);
 }
+// Same values from the binary32 bits (positive NORMAL x only): bits(0.75f) =
+// 0x3f400000 and the 23-bit mantissa offset give the identical k, idx and m
+// as the binary64 decomposition above (which shifts them left by 29 bits).
+template <int N>
+__device__ __forceinline__ double log_f_internal_f(float x, const double* c, const double* __restrict__ lt) {
+  uint32_t ux = bits_f(x);
+  uint32_t t = ux - 0x3f400000u;
+  int k = (int)t >> 23;
+  int idx = (int)((t >> 15) & 255u);
+  double m = (double)from_bits_f(ux - ((uint32_t)k << 23));
+  double r = fma(m, lt[kLtfInvc + idx], -1.0);
+  double Q = poly<N>(c, r);
+  double L = fma(r * r, Q, r);
+  return fma((double)k, ccLn2Hi, lt[kLtfHi + idx] + L);
+}
+__device__ __forceinline__ bool is_pos_normal_f(float x) { return bits_f(x) - 0x00800000u < 0x7f000000u; }
+
 template <int N>
 __device__ __forceinline__ float log_core_f(float x, const double* c, const double* lt) {
   uint32_t ux = bits_f(x);
+  if (is_pos_normal_f(x)) return (float)log_f_internal_f<N>(x, c, lt);
   if (ux - 1u < 0x7f7fffffu) return (float)log_f_internal<N>((double)x, c, lt);
   if (x == 0.0f) return -kInfF;
   if (x == kInfF) return x;
@@ -861,7 +879,7 @@ __device__ __forceinline__ float pow_core_f(float x, float y, const double* cl, 
   bool fx = (ux - 1u) < 0x7f7fffffu;
   bool fy = ((uy & 0x7fffffffu) - 1u) < 0x7f7fffffu;
   if (fx && fy) {
-    double t = (double)y * log_f_internal<NL>((double)x, cl, lt);
+    double t = (double)y * (is_pos_normal_f(x) ? log_f_internal_f<NL>(x, cl, lt) : log_f_internal<NL>((double)x, cl, lt));
     if (((uint32_t)__double2hiint(t) & 0x7fffffffu) >= 0x40690000u) t = (t > 0.0) ? 200.0 : -200.0;
     return (float)exp_f_internal(t, lt);
   }

@@ -4,7 +4,8 @@
 Builds a tuning variant of the library (-DVEM_TUNE) into
 paper_2001_09258_b200/_tune/libvem_tune.so, then times every entry point
 (filtered by argv[2]) at 2^argv[1] elements for each (VPT, STAGES) variant:
- 0:(1,2) 1:(1,4) 2:(2,2) 3:(2,3) 4:(2,4) 5:(4,2) and -1 = the shipped choice.
+ 0:(1,2) 1:(1,4) 2:(2,2) 3:(2,3) 4:(2,4) 5:(4,2), -1 = the shipped choice, and
+ 6/7/8 = the shipped shape with __launch_bounds__ min-blocks 2/3/4.
 Prints one JSON line per entry point with Gelem/s per variant.
 """
 import ctypes
@@ -63,7 +64,7 @@ def main():
             f.argtypes = [ctypes.c_void_p] * 2 + [ctypes.c_size_t, ctypes.c_void_p]
             call = lambda: f(ts[0].data_ptr(), out.data_ptr(), n, stream)  # noqa: E731
         res = {}
-        for v in (-1, 0, 1, 2, 3, 4, 5):
+        for v in (-1, 0, 1, 2, 3, 4, 5, 6, 7, 8):
             L.vem_tune_set(v)
             for _ in range(3):
                 call()
