@@ -123,3 +123,21 @@ def test_launch_counter_and_version(cuda):
     _gpu("exp_d_u10", np.linspace(-1, 1, 100))
     assert _lib.launch_count() == before + 1
     assert b"sm_100a" in _lib.lib().vem_version()
+
+
+@pytest.mark.parametrize("name", ["exp_f_u35", "sin_d_u10", "pow_d_u10", "fmod_d"])
+def test_repeat_launches_are_deterministic(cuda, name):
+    """Ten back-to-back launches over 2^22 elements give identical bits."""
+    import torch
+    from paper_2001_09258_b200 import api
+    n = 1 << 22
+    if name in _lib.BINARY:
+        x, y = binary_cases(name, n)
+        ts = [torch.from_numpy(x[:n]).cuda(), torch.from_numpy(y[:n]).cuda()]
+    else:
+        ts = [torch.from_numpy(unary_cases(name, n)[:n]).cuda()]
+    ref = api.call(name, *ts).clone()
+    for _ in range(10):
+        out = api.call(name, *ts)
+        assert torch.equal(out.view(torch.int64 if out.dtype == torch.float64 else torch.int32),
+                           ref.view(torch.int64 if ref.dtype == torch.float64 else torch.int32))
