@@ -459,38 +459,43 @@ def main():
 
 
 def e2e_leg(work, bufs, outs, n, args, dev, stream, world):
-    """Same step through the C ABI with HOST buffers: every step copies that
-    step's inputs host->device from pinned memory, runs the kernel, and reads
-    the result back device->host; chunked over two streams so copies in each
-    direction overlap the kernels (vem's host pipeline)."""
+    """Same step through the C ABI with HOST buffers: every step uploads that
+    step's distinct inputs host->device from pinned memory (the u10 and u35
+    entry points of one function read the same arrays, so each input array is
+    uploaded once), runs every entry point, and reads every result back
+    device->host into its own pinned buffer; chunked over three streams so
+    copies in both directions overlap the kernels."""
     import torch
     from paper_2001_09258_b200 import api
     chunk = 1 << 24
     n = min(n, 1 << 26)  # 2^26 elements per entry point per rank (bounded pinned memory)
-    host_in = []
-    host_out = {}
-    for ins in bufs:
-        host_in.append([t[:n].to("cpu").pin_memory() for t in ins])
-    for ins in bufs:
-        host_out.setdefault(ins[0].dtype, torch.empty(n, dtype=ins[0].dtype).pin_memory())
-    streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
-    h2d = sum(t.numel() * t.element_size() for ins in host_in for t in ins)
-    d2h = sum(ins[0].numel() * ins[0].element_size() for ins in host_in)
+    groups = []  # (device input list, [(entry name, work index)])
+    for i, (name, _) in enumerate(work):
+        for g in groups:
+            if g[0] is bufs[i]:
+                g[1].append((name, i))
+                break
+        else:
+            groups.append((bufs[i], [(name, i)]))
+    host_in = {id(g[0]): [t[:n].to("cpu").pin_memory() for t in g[0]] for g in groups}
+    host_out = [torch.empty(n, dtype=bufs[i][0].dtype).pin_memory() for i in range(len(work))]
+    dev_out = [torch.empty(n, dtype=bufs[i][0].dtype, device=dev) for i in range(len(work))]
+    streams = [torch.cuda.Stream(dev) for _ in range(3)]
+    h2d = sum(t.numel() * t.element_size() for v in host_in.values() for t in v)
+    d2h = sum(h.numel() * h.element_size() for h in host_out)
 
     def one_step():
-        for i, (name, _) in enumerate(work):
-            hin = host_in[i]
-            dins = bufs[i]
-            dout = outs[dins[0].dtype]
-            hout = host_out[dins[0].dtype]
+        for dins, members in groups:
+            hin = host_in[id(dins)]
             for j, c0 in enumerate(range(0, n, chunk)):
                 c1 = min(n, c0 + chunk)
-                s = streams[j % 2]  # a given range always uses the same stream
+                s = streams[j % 3]  # a given range always uses the same stream
                 with torch.cuda.stream(s):
                     for hd, dd_ in zip(hin, dins):
                         dd_[c0:c1].copy_(hd[c0:c1], non_blocking=True)
-                    api.call(name, *[d[c0:c1] for d in dins], out=dout[c0:c1])
-                    hout[c0:c1].copy_(dout[c0:c1], non_blocking=True)
+                    for name, i in members:
+                        api.call(name, *[d[c0:c1] for d in dins], out=dev_out[i][c0:c1])
+                        host_out[i][c0:c1].copy_(dev_out[i][c0:c1], non_blocking=True)
 
     one_step()
     torch.cuda.synchronize()
@@ -503,7 +508,8 @@ def e2e_leg(work, bufs, outs, n, args, dev, stream, world):
     return {"value": round(len(work) * n * world / dt / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": round(dt * 1e3, 2), "steps": steps,
             "elements_per_entry_point_per_rank": n,
-            "path": "pinned host -> H2D (chunked 2^24, 2 streams) -> vem C ABI -> D2H, host wall clock"}
+            "path": "pinned host -> H2D (each distinct input once, chunked 2^24, 3 streams) -> vem C ABI "
+                    "(every entry point) -> D2H of every result, host wall clock"}
 
 
 if __name__ == "__main__":
