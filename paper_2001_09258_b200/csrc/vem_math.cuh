@@ -543,15 +543,8 @@ __device__ __forceinline__ dd log_dd(double a, double Eadj, const double* c, con
   return S;
 }
 
-__device__ __forceinline__ double exp_dd(dd t, const double* __restrict__ lt) {
-  double th = t.hi, tl = t.lo;
-  uint32_t hx = (uint32_t)__double2hiint(th) & 0x7fffffffu;
-  bool fast = hx < kExpFastHi;
-  if (!fast) {
-    bool ok = (th >= -760.0) && (th <= 720.0);
-    th = ok ? th : 0.0;
-    tl = ok ? tl : 0.0;
-  }
+// shared body of exp_dd (oracle: exp_dd): r = t - k ln2/128, 2^(i/128) table
+__device__ __forceinline__ double exp_dd_core(double th, double tl, const double* __restrict__ lt, int& e) {
   int k;
   double kd = rint_fma(th, ccExpjInv, k);
   double r1 = fma(kd, -ccExpjL1, th);
@@ -563,13 +556,26 @@ __device__ __forceinline__ double exp_dd(dd t, const double* __restrict__ lt) {
   double em1l = r.lo + fma(r.hi, r.lo, s2);
   double Th = lt[kLtExpHi + (k & 127)], Tl = lt[kLtExpLo + (k & 127)];
   double u = fma(Th, r.hi, fma(Th, em1l, Tl));
-  double R = Th + u;
-  int e = k >> 7;
-  if (fast) return __hiloint2double(__double2hiint(R) + (e << 20), __double2loint(R));
+  e = k >> 7;
+  return Th + u;
+}
+// |th| >= 708: saturation / gradual underflow (rare; kept out of line)
+__device__ __noinline__ double exp_dd_slow(dd t, const double* lt) {
+  bool ok = (t.hi >= -760.0) && (t.hi <= 720.0);
+  double th = ok ? t.hi : 0.0, tl = ok ? t.lo : 0.0;
+  int e;
+  double R = exp_dd_core(th, tl, lt, e);
   double y = ldexp2(R, (long long)e);
   y = (t.hi > kExpOvf) ? kInf : y;
   y = (t.hi < kExpUnf) ? 0.0 : y;
   return y;
+}
+__device__ __forceinline__ double exp_dd(dd t, const double* __restrict__ lt) {
+  uint32_t hx = (uint32_t)__double2hiint(t.hi) & 0x7fffffffu;
+  if (hx >= kExpFastHi) return exp_dd_slow(t, lt);
+  int e;
+  double R = exp_dd_core(t.hi, t.lo, lt, e);
+  return __hiloint2double(__double2hiint(R) + (e << 20), __double2loint(R));
 }
 
 __device__ __forceinline__ bool is_int_d(double y) { return (fabs(y) < kInf) && (trunc(y) == y); }
