@@ -70,7 +70,7 @@ static inline float canon_f(float y) { return (y != y) ? from_bits_f(CANON_NAN_F
 #define K_FOUR_THIRDS 0x1.5555555555555p+0
 
 static const double PH_D[4 * VEM_PH_D_ENTRIES] = {VEM_PH_D_INIT};
-static const double PH_F[3 * VEM_PH_F_ENTRIES] = {VEM_PH_F_INIT};
+static const uint32_t PH_F[4 * VEM_PH_F_ENTRIES] = {VEM_PH_F_INIT};
 static const double LOGT_INVC[256] = {VEM_LOGT_INVC_INIT};
 static const double LOGT_HI[256] = {VEM_LOGT_HI_INIT};
 static const double LOGT_LO[256] = {VEM_LOGT_LO_INIT};
@@ -698,42 +698,47 @@ static const double C_TAN_F[] = VEM_TAN_F_ARR;
 static const double C_EXP_F[] = VEM_EXP_F_ARR;
 static const double C_EXP_F_U35[] = VEM_EXP_F_U35_ARR;
 
-/* f32 Payne-Hanek in binary64 (new; the reference is double-only):
- * |x| = M*2^E, M < 2^24; table T(E) = centred 2^E*2/pi mod 4, 3 limbs.
+/* f32 Payne-Hanek, integer form (new; the reference is double-only):
+ * |x| = M*2^E, M in [2^23, 2^24); W(E) = floor((2^E*2/pi mod 4)*2^126)
+ * (tools/genphtable.py).  p = M*W(E) mod 2^128 carries the quadrant in its
+ * top two bits; rounding to the nearest quadrant is the +2^125 carry, and the
+ * signed fraction s = p<<2 is taken in one's complement (|error| 2^-128).
+ * tools/phf_margin.c proves |s| >= 2^(128-30) for every binary32 >= 1/2, so
+ * the top 64 bits of |s| << clz are exact to 2^-63 relative; one RN
+ * conversion and one multiply by pi/2 * 2^-(64+lz) give r.  |x| < 1/2 takes
+ * r = x, q = 0 (selected, not branched: the integer work runs on a dummy M).
  * Every f32 trig lane takes this path (no selector, no divergence). */
 typedef struct { double r; int q; } redf_t;
 static redf_t ph_f(float xf) {
-  int bad = !(fabsf(xf) <= 3.4028234663852886e38f);
-  float xs = bad ? 0.0f : xf;
-  uint32_t b = bits_f(xs) & 0x7fffffffu;
-  int32_t fe = (int32_t)(b >> 23);
-  int32_t E = (fe == 0 ? 1 : fe) - 150;
-  int32_t idx = E + 23;
-  idx = idx < 0 ? 0 : idx;
-  double ax = (double)from_bits_f(b);
-  double Mp = ax * pow2_bits(23 - idx);
-  const double* T = PH_F + 3 * idx;
-  double p0 = Mp * T[0];
-  double e0 = fma(Mp, T[0], -p0);          /* exact */
-  int32_t k0, k1;
-  double q0 = rint_fma(p0, 1.0, &k0);      /* |p0| < 2^25 */
-  double f0 = p0 - q0;                     /* exact, |f0| <= 1/2 */
-  double p1 = Mp * T[1];
-  double e1 = fma(Mp, T[1], -p1);
-  double m2 = Mp * T[2];
-  double t = e0 + p1;                      /* |.| <~ 2^-27, error <~ 2^-81 */
-  double sm = f0 + t;
-  double c = (f0 - sm) + t;                /* rounding error of sm (<~ 2^-79 off if |f0| < |t|) */
-  double q1 = rint_fma(sm, 1.0, &k1);
-  double fh = sm - q1;                     /* exact */
-  double fl = c + (e1 + m2);
-  double r = fma(fh, K_PIO2_QD0, fma(fh, K_PIO2_QD1, fl * K_PIO2_QD0));
-  int q = k0 + k1;
-  if (xs < 0.0f) {
-    r = -r;
-    q = -q;
-  }
-  redf_t o = {r, q & 3};
+  uint32_t b = bits_f(xf) & 0x7fffffffu;
+  uint32_t fe = b >> 23;
+  int small = fe < 126;
+  uint32_t idx = small ? 0 : fe - 126;
+  idx = idx > VEM_PH_F_ENTRIES - 1 ? VEM_PH_F_ENTRIES - 1 : idx;  /* inf/NaN: any entry */
+  uint32_t M = small ? 0x800000u : ((b & 0x7fffffu) | 0x800000u);
+  const uint32_t* w = PH_F + 4 * idx;
+  uint64_t t = (uint64_t)M * w[0];
+  t = (uint64_t)M * w[1] + (t >> 32);
+  uint32_t p1 = (uint32_t)t;
+  t = (uint64_t)M * w[2] + (t >> 32);
+  uint32_t p2 = (uint32_t)t;
+  uint32_t p3 = M * w[3] + (uint32_t)(t >> 32);
+  int q = (int)(((p3 + 0x20000000u) >> 30) & 3u);
+  uint32_t mask = (uint32_t)((int32_t)(p3 << 2) >> 31);
+  uint32_t u3 = p3 ^ mask, u2 = p2 ^ mask, u1 = p1 ^ mask;
+  uint32_t s3 = (u3 << 2) | (u2 >> 30);
+  int lz = s3 ? __builtin_clz(s3) : 32; /* <= 29 (phf_margin.c) */
+  int sh = lz + 2;
+  uint32_t nh = (u3 << sh) | (u2 >> (32 - sh));
+  uint32_t nl = (u2 << sh) | (u1 >> (32 - sh));
+  double d = (double)(((uint64_t)nh << 32) | nl);
+  uint32_t sgn = (mask ^ bits_f(xf)) & 0x80000000u;
+  double c = from_bits_d(((uint64_t)((0x3FF921FBu - ((uint32_t)(64 + lz) << 20)) | sgn) << 32) | 0x54442D18u);
+  double r = d * c;
+  if (bits_f(xf) >> 31) q = -q;
+  redf_t o;
+  o.r = small ? (double)xf : r;
+  o.q = small ? 0 : (q & 3);
   return o;
 }
 
@@ -901,7 +906,7 @@ void vo_ph_reduce_f(const float* x, double* r, int* q, size_t n) {
   }
 }
 const double* vo_ph_table_d(void) { return PH_D; }
-const double* vo_ph_table_f(void) { return PH_F; }
+const uint32_t* vo_ph_table_f(void) { return PH_F; }
 double vo_round_ta(double x) { return round_ta(x); }
 
 #define UNARY_ARR(name, T)                                             \

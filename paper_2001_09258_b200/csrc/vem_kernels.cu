@@ -30,7 +30,7 @@ enum TableKind { kNoTable = 0, kTableD = 1, kTableF = 2, kTableLog = 3, kTableDG
 template <int TABLE>
 struct TableSize {
   static constexpr int n = TABLE == kTableD   ? 4 * VEM_PH_D_ENTRIES + kSinCosCoefN
-                           : TABLE == kTableF ? 3 * VEM_PH_F_ENTRIES + kSinCosCoefN
+                           : TABLE == kTableF ? kPhFDoubles + kSinCosCoefN
                            : TABLE == kTableLog ? kLogTabN
                            : TABLE == kTableDG ? kSinCosCoefN
                                                 : 2;
@@ -45,7 +45,7 @@ __device__ __forceinline__ const double* stage_table(double* stab) {
     __syncthreads();
     return stab;
   } else {
-    const double* src = TABLE == kTableD ? gPhD : (TABLE == kTableF ? gPhF : gLogExp);
+    const double* src = TABLE == kTableD ? gPhD : (TABLE == kTableF ? reinterpret_cast<const double*>(gPhF) : gLogExp);
     constexpr int n2 = (TABLE == kTableLog ? kLogTabD : TableSize<TABLE>::n - kSinCosCoefN) / 2;
     const double2* s2 = reinterpret_cast<const double2*>(src);
     double2* d2 = reinterpret_cast<double2*>(stab);
@@ -163,6 +163,16 @@ __global__ void __launch_bounds__(kThreads) k_binary(const T* __restrict__ x, co
 // one class skip the regrouping.
 template <class Op> struct SortsByClass { static constexpr bool value = false; };
 
+// Ops with a split fast path (vem_math.cuh "split fast paths"): the kernel
+// evaluates a tile's elements with Op::fast (branch-free, interleavable) and
+// re-evaluates only the elements it flags as rare with the full Op.
+template <class Op> struct HasFast { static constexpr bool value = false; };
+// the full function for rare elements: one out-of-line copy per Op
+template <class Op, class T>
+__device__ __noinline__ T full_op(T x, const double* tab) { return Op()(x, tab); }
+template <class Op, class T>
+__device__ __noinline__ T full_op(T x, T y, const double* tab) { return Op()(x, y, tab); }
+
 // ------------------------------------------------- TMA-staged streaming
 // NIN inputs (1 or 2); tiles of kThreads*VPT 16-byte vectors per input;
 // STAGES tiles in flight per CTA (see vem_stream.cuh).  Elements past the
@@ -237,7 +247,19 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
         same = same && (cl[e] == cl[0]);
       }
       const int c_l0 = __shfl_sync(0xffffffffu, cl[0], 0);
-      if (!__all_sync(0xffffffffu, same && cl[0] == c_l0)) {
+      const bool uniform = __all_sync(0xffffffffu, same && cl[0] == c_l0);
+      if (uniform && c_l0 == 0) {
+        // every element of the warp takes Cody-Waite level 1: branch-free
+        // bodies, interleaved across the thread's elements
+#pragma unroll
+        for (int v = 0; v < VPT; v++) {
+          V o;
+#pragma unroll
+          for (int k = 0; k < W; k++) vget(o, k) = op.cw1(xe[v * W + k], tab);
+          __stcs(ov + v * kThreads + tid, o);
+        }
+        done = true;
+      } else if (!uniform) {
         T* sx = wscr + (tid >> 5) * (32 * NE);
         unsigned short* si = widx + (tid >> 5) * (32 * NE);
         unsigned m2[NE], m1[NE];
@@ -284,6 +306,38 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
         __syncwarp();
         done = true;
       }
+    }
+    if constexpr (HasFast<Op>::value) {
+      T res[NE];
+      bool rare[NE];
+      bool any = false;
+#pragma unroll
+      for (int v = 0; v < VPT; v++)
+#pragma unroll
+        for (int k = 0; k < W; k++) {
+          const int e = v * W + k;
+          if constexpr (NIN == 2) res[e] = op.fast(vget(va[v], k), vget(vb[v], k), tab, rare[e]);
+          else res[e] = op.fast(vget(va[v], k), tab, rare[e]);
+          any |= rare[e];
+        }
+      if (any) {
+#pragma unroll
+        for (int e = 0; e < NE; e++) {
+          if (rare[e]) {
+            const int v = e / W, k = e % W;
+            if constexpr (NIN == 2) res[e] = full_op<Op>(vget(va[v], k), vget(vb[v], k), tab);
+            else res[e] = full_op<Op>(vget(va[v], k), tab);
+          }
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < VPT; v++) {
+        V o;
+#pragma unroll
+        for (int k = 0; k < W; k++) vget(o, k) = res[v * W + k];
+        __stcs(ov + v * kThreads + tid, o);
+      }
+      done = true;
     }
     if (!done) {
 #pragma unroll
@@ -439,45 +493,67 @@ __global__ void __launch_bounds__(kFmodWarps * 32) k_fmod(const T* __restrict__ 
   struct NAME {                                                                       \
     __device__ __forceinline__ T operator()(T x, const double* tab) const { return EXPR; } \
   };
-#define VEM_TRIG_OP(NAME, EXPR)                                                          \
+#define VEM_TRIG_OP(NAME, FN, ...)                                                       \
   struct NAME {                                                                          \
-    __device__ __forceinline__ double operator()(double x, const double* tab) const { return EXPR; } \
+    __device__ __forceinline__ double operator()(double x, const double* tab) const {   \
+      return FN<kSel>(x, gPhD __VA_ARGS__);                                              \
+    }                                                                                    \
+    __device__ __forceinline__ double cw1(double x, const double* tab) const {          \
+      return FN<kCw1>(x, gPhD __VA_ARGS__);                                              \
+    }                                                                                    \
     __device__ __forceinline__ static int cls(double x) { return trig_class(x); }      \
   };                                                                                     \
   template <> struct SortsByClass<NAME> { static constexpr bool value = true; };
 // selector variants: PH table from global memory (L1), coefficients staged
-VEM_TRIG_OP(OpSinD, (sin_d_u10<false>(x, gPhD, tab)))
-VEM_TRIG_OP(OpCosD, (cos_d_u10<false>(x, gPhD, tab)))
-VEM_TRIG_OP(OpTanD, (tan_d_u10<false>(x, gPhD)))
+VEM_TRIG_OP(OpSinD, sin_d_u10, , tab)
+VEM_TRIG_OP(OpCosD, cos_d_u10, , tab)
+VEM_TRIG_OP(OpTanD, tan_d_u10)
 #undef VEM_TRIG_OP
-VEM_UNARY_OP(OpSinDPh, double, (sin_d_u10<true>(x, tab, tab + 4 * VEM_PH_D_ENTRIES)))
-VEM_UNARY_OP(OpCosDPh, double, (cos_d_u10<true>(x, tab, tab + 4 * VEM_PH_D_ENTRIES)))
-VEM_UNARY_OP(OpTanDPh, double, (tan_d_u10<true>(x, tab)))
+VEM_UNARY_OP(OpSinDPh, double, (sin_d_u10<kPh>(x, tab, tab + 4 * VEM_PH_D_ENTRIES)))
+VEM_UNARY_OP(OpCosDPh, double, (cos_d_u10<kPh>(x, tab, tab + 4 * VEM_PH_D_ENTRIES)))
+VEM_UNARY_OP(OpTanDPh, double, (tan_d_u10<kPh>(x, tab)))
 VEM_UNARY_OP(OpAtanD, double, ((void)tab, atan_d_u10(x)))
-VEM_UNARY_OP(OpExpD, double, ((void)tab, exp_d_u10(x)))
-VEM_UNARY_OP(OpExpDU35, double, ((void)tab, exp_d_u35(x)))
-VEM_UNARY_OP(OpLogD, double, (log_core_d<true>(x, tab)))
-VEM_UNARY_OP(OpLogDU35, double, (log_core_d<false>(x, tab)))
+#define VEM_SPLIT_UNARY_OP(NAME, T, EXPR, FAST)                                          \
+  struct NAME {                                                                          \
+    __device__ __forceinline__ T operator()(T x, const double* tab) const { return EXPR; } \
+    __device__ __forceinline__ T fast(T x, const double* tab, bool& rare) const { return FAST; } \
+  };                                                                                     \
+  template <> struct HasFast<NAME> { static constexpr bool value = true; };
+VEM_SPLIT_UNARY_OP(OpExpD, double, ((void)tab, exp_d_u10(x)), ((void)tab, (exp_fast_d<VEM_EXP_D_N, true>(x, cExpD, rare))))
+VEM_SPLIT_UNARY_OP(OpExpDU35, double, ((void)tab, exp_d_u35(x)),
+                   ((void)tab, (exp_fast_d<VEM_EXP_D_U35_N, false>(x, cExpDU35, rare))))
+VEM_SPLIT_UNARY_OP(OpLogD, double, (log_core_d<true>(x, tab)), (log_fast_split_d<true>(x, tab, rare)))
+VEM_SPLIT_UNARY_OP(OpLogDU35, double, (log_core_d<false>(x, tab)), (log_fast_split_d<false>(x, tab, rare)))
 VEM_UNARY_OP(OpSinF, float, (sin_f_u10(x, tab)))
 VEM_UNARY_OP(OpCosF, float, (cos_f_u10(x, tab)))
 VEM_UNARY_OP(OpTanF, float, (tan_f_u10(x, tab)))
 VEM_UNARY_OP(OpExpF, float, ((void)tab, exp_f_u10(x)))
 VEM_UNARY_OP(OpExpFU35, float, ((void)tab, exp_f_u35(x)))
-VEM_UNARY_OP(OpLogF, float, (log_f_u10(x, tab)))
-VEM_UNARY_OP(OpLogFU35, float, (log_f_u35(x, tab)))
+VEM_SPLIT_UNARY_OP(OpLogF, float, (log_f_u10(x, tab)), (log_fast_f<VEM_LOG1P_F_N>(x, cLog1pF, tab, rare)))
+VEM_SPLIT_UNARY_OP(OpLogFU35, float, (log_f_u35(x, tab)), (log_fast_f<VEM_LOG1P_F_U35_N>(x, cLog1pFU35, tab, rare)))
 #undef VEM_UNARY_OP
+#undef VEM_SPLIT_UNARY_OP
 
 #define VEM_BINARY_OP(NAME, T, EXPR)                                              \
   struct NAME {                                                                   \
     __device__ __forceinline__ T operator()(T x, T y, const double* tab) const { return EXPR; } \
   };
-VEM_BINARY_OP(OpPowD, double, pow_d_u10(x, y, tab))
-VEM_BINARY_OP(OpPowDU35, double, pow_d_u35(x, y, tab))
+#define VEM_SPLIT_BINARY_OP(NAME, T, EXPR, FAST)                                  \
+  struct NAME {                                                                   \
+    __device__ __forceinline__ T operator()(T x, T y, const double* tab) const { return EXPR; } \
+    __device__ __forceinline__ T fast(T x, T y, const double* tab, bool& rare) const { return FAST; } \
+  };                                                                              \
+  template <> struct HasFast<NAME> { static constexpr bool value = true; };
+VEM_SPLIT_BINARY_OP(OpPowD, double, pow_d_u10(x, y, tab), (pow_fast_d<VEM_LOG1P_D_N>(x, y, cLog1pD, tab, rare)))
+VEM_SPLIT_BINARY_OP(OpPowDU35, double, pow_d_u35(x, y, tab),
+                    (pow_fast_d<VEM_LOG1P_D_U35_N>(x, y, cLog1pDU35, tab, rare)))
 VEM_BINARY_OP(OpFmodD, double, ((void)tab, fmod_d(x, y)))
-VEM_BINARY_OP(OpPowF, float, pow_f_u10(x, y, tab))
-VEM_BINARY_OP(OpPowFU35, float, pow_f_u35(x, y, tab))
+VEM_SPLIT_BINARY_OP(OpPowF, float, pow_f_u10(x, y, tab), (pow_fast_f<VEM_LOG1P_F_N>(x, y, cLog1pF, tab, rare)))
+VEM_SPLIT_BINARY_OP(OpPowFU35, float, pow_f_u35(x, y, tab),
+                    (pow_fast_f<VEM_LOG1P_F_U35_N>(x, y, cLog1pFU35, tab, rare)))
 VEM_BINARY_OP(OpFmodF, float, ((void)tab, fmod_f(x, y)))
 #undef VEM_BINARY_OP
+#undef VEM_SPLIT_BINARY_OP
 
 // ------------------------------------------------------------- launching
 static int num_sms() {
@@ -646,7 +722,7 @@ using namespace vem;
 #ifdef VEM_TUNE
 static int g_tune = -1;
 extern "C" void vem_tune_set(int v) { g_tune = v; }
-template <class Op, class T, int NIN, int TAB, int VPT, int ST>
+template <class Op, class T, int NIN, int TAB, int VPT, int ST, int MINB = 1>
 static int launch_tuned(const T* a, const T* b, T* o, size_t n, vem_stream_t s) {
   switch (g_tune) {
     case 0: return launch_stream<Op, T, NIN, TAB, 1, 2>(a, b, o, n, s);
@@ -658,7 +734,7 @@ static int launch_tuned(const T* a, const T* b, T* o, size_t n, vem_stream_t s) 
     case 6: return launch_stream<Op, T, NIN, TAB, VPT, ST, 2>(a, b, o, n, s);
     case 7: return launch_stream<Op, T, NIN, TAB, VPT, ST, 3>(a, b, o, n, s);
     case 8: return launch_stream<Op, T, NIN, TAB, VPT, ST, 4>(a, b, o, n, s);
-    default: return launch_stream<Op, T, NIN, TAB, VPT, ST>(a, b, o, n, s);
+    default: return launch_stream<Op, T, NIN, TAB, VPT, ST, MINB>(a, b, o, n, s);
   }
 }
 #define VEM_STREAM launch_tuned
@@ -670,34 +746,34 @@ static int launch_tuned(const T* a, const T* b, T* o, size_t n, vem_stream_t s) 
 // vectors in flight, FP64-pipe-bound ones 2 (register pressure).
 extern "C" {
 
-int vem_sin_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpSinD, double, 1, kTableDG, 2, 2>(x, nullptr, y, n, s); }
-int vem_cos_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpCosD, double, 1, kTableDG, 2, 2>(x, nullptr, y, n, s); }
-int vem_tan_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpTanD, double, 1, kTableDG, 2, 2>(x, nullptr, y, n, s); }
+int vem_sin_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpSinD, double, 1, kTableDG, 2, 2, 4>(x, nullptr, y, n, s); }
+int vem_cos_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpCosD, double, 1, kTableDG, 2, 2, 4>(x, nullptr, y, n, s); }
+int vem_tan_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpTanD, double, 1, kTableDG, 2, 2, 4>(x, nullptr, y, n, s); }
 int vem_sin_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpSinDPh, double, 1, kTableD, 2, 2>(x, nullptr, y, n, s); }
 int vem_cos_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpCosDPh, double, 1, kTableD, 2, 2>(x, nullptr, y, n, s); }
 int vem_tan_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpTanDPh, double, 1, kTableD, 2, 2>(x, nullptr, y, n, s); }
 int vem_atan_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpAtanD, double, 1, kNoTable, 2, 2>(x, nullptr, y, n, s); }
-int vem_exp_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpExpD, double, 1, kNoTable, 1, 2>(x, nullptr, y, n, s); }
-int vem_exp_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpExpDU35, double, 1, kNoTable, 2, 2>(x, nullptr, y, n, s); }
-int vem_log_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpLogD, double, 1, kTableLog, 4, 2>(x, nullptr, y, n, s); }
-int vem_log_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpLogDU35, double, 1, kTableLog, 2, 2>(x, nullptr, y, n, s); }
-int vem_pow_d_u10(const double* x, const double* y2, double* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpPowD, double, 2, kTableLog, 2, 2>(x, y2, o, n, s); }
-int vem_pow_d_u35(const double* x, const double* y2, double* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpPowDU35, double, 2, kTableLog, 2, 2>(x, y2, o, n, s); }
+int vem_exp_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpExpD, double, 1, kNoTable, 1, 2, 3>(x, nullptr, y, n, s); }
+int vem_exp_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpExpDU35, double, 1, kNoTable, 2, 2, 4>(x, nullptr, y, n, s); }
+int vem_log_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpLogD, double, 1, kTableLog, 4, 2, 4>(x, nullptr, y, n, s); }
+int vem_log_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpLogDU35, double, 1, kTableLog, 2, 2, 4>(x, nullptr, y, n, s); }
+int vem_pow_d_u10(const double* x, const double* y2, double* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpPowD, double, 2, kTableLog, 2, 2, 3>(x, y2, o, n, s); }
+int vem_pow_d_u35(const double* x, const double* y2, double* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpPowDU35, double, 2, kTableLog, 2, 2, 3>(x, y2, o, n, s); }
 int vem_fmod_d(const double* x, const double* y2, double* o, size_t n, vem_stream_t s) { return launch_fmod<double>(x, y2, o, n, s); }
 
-int vem_sin_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpSinF, float, 1, kTableF, 2, 2>(x, nullptr, y, n, s); }
-int vem_cos_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpCosF, float, 1, kTableF, 2, 2>(x, nullptr, y, n, s); }
-int vem_tan_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpTanF, float, 1, kTableF, 2, 2>(x, nullptr, y, n, s); }
+int vem_sin_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpSinF, float, 1, kTableF, 4, 2>(x, nullptr, y, n, s); }
+int vem_cos_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpCosF, float, 1, kTableF, 4, 2>(x, nullptr, y, n, s); }
+int vem_tan_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpTanF, float, 1, kTableF, 2, 2, 4>(x, nullptr, y, n, s); }
 // every f32 trig lane takes the f32 Payne-Hanek path: the forced variants are the same kernels
 int vem_sin_f_u10_ph(const float* x, float* y, size_t n, vem_stream_t s) { return vem_sin_f_u10(x, y, n, s); }
 int vem_cos_f_u10_ph(const float* x, float* y, size_t n, vem_stream_t s) { return vem_cos_f_u10(x, y, n, s); }
 int vem_tan_f_u10_ph(const float* x, float* y, size_t n, vem_stream_t s) { return vem_tan_f_u10(x, y, n, s); }
 int vem_exp_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpExpF, float, 1, kNoTable, 1, 2>(x, nullptr, y, n, s); }
 int vem_exp_f_u35(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpExpFU35, float, 1, kNoTable, 1, 2>(x, nullptr, y, n, s); }
-int vem_log_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpLogF, float, 1, kTableLog, 2, 4>(x, nullptr, y, n, s); }
-int vem_log_f_u35(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpLogFU35, float, 1, kTableLog, 2, 4>(x, nullptr, y, n, s); }
-int vem_pow_f_u10(const float* x, const float* y2, float* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpPowF, float, 2, kTableLog, 2, 2>(x, y2, o, n, s); }
-int vem_pow_f_u35(const float* x, const float* y2, float* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpPowFU35, float, 2, kTableLog, 2, 2>(x, y2, o, n, s); }
+int vem_log_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpLogF, float, 1, kTableLog, 4, 2>(x, nullptr, y, n, s); }
+int vem_log_f_u35(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpLogFU35, float, 1, kTableLog, 4, 2>(x, nullptr, y, n, s); }
+int vem_pow_f_u10(const float* x, const float* y2, float* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpPowF, float, 2, kTableLog, 2, 2, 3>(x, y2, o, n, s); }
+int vem_pow_f_u35(const float* x, const float* y2, float* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpPowFU35, float, 2, kTableLog, 2, 2, 3>(x, y2, o, n, s); }
 int vem_fmod_f(const float* x, const float* y2, float* o, size_t n, vem_stream_t s) { return launch_fmod<float>(x, y2, o, n, s); }
 
 int vem_trig_reduce_d(const double* x, double* hi, double* lo, int* q, size_t n, vem_stream_t s) {

@@ -114,7 +114,8 @@ __device__ const double gSinCosF[kSinCosCoefN] = {
 
 // Payne-Hanek tables (global copy; kernels stage them into shared memory).
 __device__ const double gPhD[4 * VEM_PH_D_ENTRIES] = {VEM_PH_D_INIT};
-__device__ const double gPhF[3 * VEM_PH_F_ENTRIES] = {VEM_PH_F_INIT};
+__device__ __align__(16) const uint32_t gPhF[4 * VEM_PH_F_ENTRIES] = {VEM_PH_F_INIT};
+constexpr int kPhFDoubles = 2 * VEM_PH_F_ENTRIES;  // staged size of gPhF in doubles
 // log / exp tables (tools/genlogtables.py), structure of arrays, staged into
 // one shared-memory block (offsets in doubles):
 constexpr int kLtInvc = 0, kLtHi = 256, kLtLo = 512, kLtExpHi = 768, kLtExpLo = 896, kLtfHi = 1024,
@@ -362,19 +363,31 @@ __device__ __forceinline__ bool not_finite_bits(double x) {
   return ((uint32_t)__double2hiint(x) & 0x7fffffffu) >= 0x7ff00000u;
 }
 
+// Reduction mode: kSel = per-lane selector (reduction.hpp:189-206), kPh =
+// Payne-Hanek for every lane (config 3), kCw1 = Cody-Waite level 1 only (the
+// kernels use it for warps whose elements are all |x| <= 15, where the
+// selector takes that path anyway: same values, no branches).
+enum RedMode { kSel = 0, kPh = 1, kCw1 = 2 };
+template <int kMode>
+__device__ __forceinline__ red reduce_mode(double x, const double* tab) {
+  if constexpr (kMode == kPh) return ph(x, tab);
+  else if constexpr (kMode == kCw1) return cw1(x);
+  else return trig_reduce(x, tab);
+}
+
 // NaN can only come from a non-finite input: canonicalised by an integer test
 // `tab`: Payne-Hanek table (shared or global); `coef`: the sin|cos block
-template <bool kForcePh>
+template <int kMode>
 __device__ __forceinline__ double sin_d_u10(double x, const double* tab, const double* coef) {
-  red r = kForcePh ? ph(x, tab) : trig_reduce(x, tab);
+  red r = reduce_mode<kMode>(x, tab);
   double y = sincos_core_d(r.hi, r.lo, r.q & 1, coef);
   y = neg_if(y, r.q & 2);
   y = is_zero_bits(x) ? x : y;
   return not_finite_bits(x) ? from_bits_d(kCanonNanD) : y;
 }
-template <bool kForcePh>
+template <int kMode>
 __device__ __forceinline__ double cos_d_u10(double x, const double* tab, const double* coef) {
-  red r = kForcePh ? ph(x, tab) : trig_reduce(x, tab);
+  red r = reduce_mode<kMode>(x, tab);
   double y = sincos_core_d(r.hi, r.lo, (r.q & 1) ^ 1, coef);
   y = neg_if(y, (r.q + 1) & 2);
   return not_finite_bits(x) ? from_bits_d(kCanonNanD) : y;
@@ -396,9 +409,9 @@ __device__ __forceinline__ double tan_core_d(double rh, double rl, int odd) {
   dd q = dd_div(X, Y);
   return q.hi + q.lo;
 }
-template <bool kForcePh>
+template <int kMode>
 __device__ __forceinline__ double tan_d_u10(double x, const double* tab) {
-  red r = kForcePh ? ph(x, tab) : trig_reduce(x, tab);
+  red r = reduce_mode<kMode>(x, tab);
   double y = tan_core_d(r.hi, r.lo, r.q & 1);
   y = (fabs(x) < 0x1p-27) ? x : y;
   return canon_d(y);
@@ -468,6 +481,9 @@ __device__ __forceinline__ double exp_d_u35(double x) { return exp_core_d<VEM_EX
 // `lt` points at the staged LOGT (4 doubles per entry) followed by EXPT.
 struct logred { double rh, rl, E, logc_hi, logc_lo; };
 
+// kAdj = false: Eadj is known to be 0 -> E = (double)k (same value; (double)k
+// is never -0, so the dropped "+ 0.0" cannot change a bit).
+template <bool kAdj = true>
 __device__ __forceinline__ logred log_reduce(double a, double Eadj, const double* __restrict__ lt) {
   uint64_t ix = bits_d(a);
   uint64_t tmp = ix - 0x3fe8000000000000ull;
@@ -479,7 +495,7 @@ __device__ __forceinline__ logred log_reduce(double a, double Eadj, const double
   logred o;
   o.rl = fma(m, invc, -p);
   o.rh = p - 1.0;
-  o.E = (double)(int)k + Eadj;
+  o.E = kAdj ? (double)(int)k + Eadj : (double)(int)k;
   o.logc_hi = lt[kLtHi + idx];
   o.logc_lo = lt[kLtLo + idx];
   return o;
@@ -506,9 +522,9 @@ __device__ __forceinline__ dd eln2_logc(const logred& g) {
   return H;
 }
 
-template <bool kU10>
+template <bool kU10, bool kAdj = true>
 __device__ __forceinline__ double log_fast_d(double a, double Eadj, const double* lt) {
-  logred g = log_reduce(a, Eadj, lt);
+  logred g = log_reduce<kAdj>(a, Eadj, lt);
   dd H = eln2_logc(g);
   dd L;
   if (kU10) {
@@ -533,9 +549,9 @@ __device__ __forceinline__ double log_core_d(double x, const double* lt) {
   return from_bits_d(kCanonNanD);
 }
 
-template <int N>
+template <int N, bool kAdj = true>
 __device__ __forceinline__ dd log_dd(double a, double Eadj, const double* c, const double* lt) {
-  logred g = log_reduce(a, Eadj, lt);
+  logred g = log_reduce<kAdj>(a, Eadj, lt);
   dd H = eln2_logc(g);
   dd L = log1p_dd<N>(g.rh, g.rl, c);
   dd S = two_sum_fast(H.hi, L.hi);
@@ -706,46 +722,60 @@ __device__ __forceinline__ double fmod_d(double x, double y) { return fmod_core(
 // ===================================== f32 functions (binary64 internals)
 struct redf { double r; int q; };
 
+// Final selects of the odd f32 trig functions, on the input's bits (same
+// outputs as the oracle's x == 0 / isinf / isnan chain): +-0 -> x,
+// inf/NaN -> canonical NaN, otherwise the finite result o.
+__device__ __forceinline__ float fin_f_odd(float x, float o) {
+  const uint32_t b = bits_f(x) & 0x7fffffffu;
+  o = b == 0u ? x : o;
+  return b >= 0x7f800000u ? from_bits_f(kCanonNanF) : o;
+}
+
+// oracle/vem_oracle.c ph_f: integer Payne-Hanek for binary32.  p = M*W(E)
+// mod 2^128 by three IMAD.WIDE.U32 (64-bit addend = carry chain) and one
+// IMAD; quadrant = top two bits after the +2^125 rounding carry; fraction
+// = one's-complement |p<<2|, normalised by clz (<= 29, tools/phf_margin.c),
+// top 64 bits -> one RN conversion -> one multiply by +-pi/2*2^-(64+lz).
+// FP64 work: I2F + DMUL (the binary64 formulation needed ~22 FP64 ops).
 __device__ __forceinline__ redf ph_f(float xf, const double* __restrict__ tab) {
-  bool bad = !(fabsf(xf) <= 3.4028234663852886e38f);
-  float xs = bad ? 0.0f : xf;
-  uint32_t b = bits_f(xs) & 0x7fffffffu;
-  int fe = (int)(b >> 23);
-  int E = (fe == 0 ? 1 : fe) - 150;
-  int idx = E + 23;
-  idx = idx < 0 ? 0 : idx;
-  double ax = (double)from_bits_f(b);
-  double Mp = ax * pow2_bits(23 - idx);
-  const double* T = tab + 3 * idx;
-  double T0 = T[0], T1 = T[1], T2 = T[2];
-  double p0 = Mp * T0;
-  double e0 = fma(Mp, T0, -p0);
-  int k0, k1;
-  double q0 = rint_fma(p0, 1.0, k0);
-  double f0 = p0 - q0;
-  double p1 = Mp * T1;
-  double e1 = fma(Mp, T1, -p1);
-  double m2 = Mp * T2;
-  double t = e0 + p1;
-  double sm = f0 + t;
-  double c = (f0 - sm) + t;
-  double q1 = rint_fma(sm, 1.0, k1);
-  double fh = sm - q1;
-  double fl = c + (e1 + m2);
-  double r = fma(fh, ccPio2Qd0, fma(fh, ccPio2Qd1, fl * ccPio2Qd0));
-  int q = k0 + k1;
-  if (xs < 0.0f) {
-    r = -r;
-    q = -q;
-  }
-  return {r, q & 3};
+  const uint32_t xb = bits_f(xf);
+  const uint32_t b = xb & 0x7fffffffu;
+  const uint32_t fe = b >> 23;
+  const bool small = fe < 126;
+  uint32_t idx = small ? 0u : fe - 126u;
+  idx = idx > VEM_PH_F_ENTRIES - 1 ? VEM_PH_F_ENTRIES - 1 : idx;
+  const uint32_t M = small ? 0x800000u : ((b & 0x7fffffu) | 0x800000u);
+  const uint4 w = reinterpret_cast<const uint4*>(tab)[idx];
+  uint64_t t = (uint64_t)M * w.x;
+  t = (uint64_t)M * w.y + (t >> 32);
+  const uint32_t p1 = (uint32_t)t;
+  t = (uint64_t)M * w.z + (t >> 32);
+  const uint32_t p2 = (uint32_t)t;
+  const uint32_t p3 = M * w.w + (uint32_t)(t >> 32);
+  int q = (int)(((p3 + 0x20000000u) >> 30) & 3u);
+  const uint32_t mask = (uint32_t)((int32_t)(p3 << 2) >> 31);
+  const uint32_t u3 = p3 ^ mask, u2 = p2 ^ mask, u1 = p1 ^ mask;
+  const uint32_t s3 = __funnelshift_l(u2, u3, 2);
+  const int lz = __clz(s3);
+  const int sh = lz + 2;
+  const uint32_t nh = __funnelshift_l(u2, u3, sh);
+  const uint32_t nl = __funnelshift_l(u1, u2, sh);
+  const double d = __ull2double_rn(((uint64_t)nh << 32) | nl);
+  const uint32_t sgn = (mask ^ xb) & 0x80000000u;
+  const double c = __hiloint2double((int)((0x3FF921FBu - ((uint32_t)(64 + lz) << 20)) | sgn), 0x54442D18);
+  const double r = d * c;
+  if (xb >> 31) q = -q;
+  redf o;
+  o.r = small ? (double)xf : r;
+  o.q = small ? 0 : (q & 3);
+  return o;
 }
 
 __device__ __forceinline__ double sincos_core_f(double r, int cosform, const double* tab) {
   bool cf = cosform != 0;
-  const double2* cs = reinterpret_cast<const double2*>(tab + 3 * VEM_PH_F_ENTRIES + (cf ? 8 : 0));
+  const double2* cs = reinterpret_cast<const double2*>(tab + kPhFDoubles + (cf ? 8 : 0));
   const double2 c01 = cs[0], c23 = cs[1];
-  const double c4 = tab[3 * VEM_PH_F_ENTRIES + (cf ? 12 : 4)];
+  const double c4 = tab[kPhFDoubles + (cf ? 12 : 4)];
   double z = r * r;
   double P = fma(fma(fma(fma(c4, z, c23.y), z, c23.x), z, c01.y), z, c01.x);
   double A = cf ? 1.0 : r;
@@ -756,16 +786,13 @@ __device__ __forceinline__ float sin_f_u10(float x, const double* tab) {
   redf r = ph_f(x, tab);
   double y = sincos_core_f(r.r, r.q & 1, tab);
   y = neg_if(y, r.q & 2);
-  float o = (float)y;
-  o = (x == 0.0f) ? x : o;
-  return canon_f(isinf(x) ? from_bits_f(kCanonNanF) : (x != x ? x : o));
+  return fin_f_odd(x, (float)y);
 }
 __device__ __forceinline__ float cos_f_u10(float x, const double* tab) {
   redf r = ph_f(x, tab);
   double y = sincos_core_f(r.r, (r.q & 1) ^ 1, tab);
   y = neg_if(y, (r.q + 1) & 2);
-  float o = (float)y;
-  return canon_f(isinf(x) ? from_bits_f(kCanonNanF) : (x != x ? x : o));
+  return (bits_f(x) & 0x7fffffffu) >= 0x7f800000u ? from_bits_f(kCanonNanF) : (float)y;
 }
 __device__ __forceinline__ float tan_f_u10(float x, const double* tab) {
   redf r = ph_f(x, tab);
@@ -773,9 +800,7 @@ __device__ __forceinline__ float tan_f_u10(float x, const double* tab) {
   double P = poly<VEM_TAN_F_N>(cTanF, z);
   double t = fma(r.r * z, P, r.r);
   double y = (r.q & 1) ? -1.0 / t : t;
-  float o = (float)y;
-  o = (x == 0.0f) ? x : o;
-  return canon_f(isinf(x) ? from_bits_f(kCanonNanF) : (x != x ? x : o));
+  return fin_f_odd(x, (float)y);
 }
 
 template <int N>
@@ -900,6 +925,51 @@ __device__ __forceinline__ float pow_f_u35(float x, float y, const double* lt) {
 __device__ __forceinline__ float fmod_f(float x, float y) {
   double r = fmod_core((double)x, (double)y);
   return canon_f((float)r);
+}
+
+// ============================================ split fast paths (kernels)
+// Branch-free bodies for the common inputs.  `rare` marks elements outside
+// them; the streaming kernel evaluates every element of a tile with these
+// (so the compiler interleaves the independent chains of one thread's
+// elements) and then recomputes only the rare ones with the full function.
+// For non-rare inputs each returns exactly the full function's value.
+template <int N, bool kU10>
+__device__ __forceinline__ double exp_fast_d(double x, const double* c, bool& rare) {
+  rare = ((uint32_t)__double2hiint(x) & 0x7fffffffu) >= kExpFastHi;
+  int k;
+  double y = exp_poly_d<N, kU10>(x, c, k);
+  return __hiloint2double(__double2hiint(y) + (k << 20), __double2loint(y));
+}
+template <bool kU10>
+__device__ __forceinline__ double log_fast_split_d(double x, const double* lt, bool& rare) {
+  rare = !(bits_d(x) - 0x0010000000000000ull < 0x7fe0000000000000ull);
+  return log_fast_d<kU10, false>(x, 0.0, lt);
+}
+template <int NL>
+__device__ __forceinline__ double pow_fast_d(double x, double y, const double* cl, const double* lt, bool& rare) {
+  const uint32_t hx = (uint32_t)__double2hiint(x);
+  const uint32_t hy = (uint32_t)__double2hiint(y) & 0x7fffffffu, ly = (uint32_t)__double2loint(y);
+  const bool fx = (hx - 0x00100000u) < 0x7fe00000u;  // positive normal
+  const bool fy = (hy < 0x7ff00000u) && ((hy | ly) != 0u);
+  const dd t = dd_mul_d(log_dd<NL, false>(x, 0.0, cl, lt), y);
+  rare = !(fx && fy) || (((uint32_t)__double2hiint(t.hi) & 0x7fffffffu) >= kExpFastHi);
+  int e;
+  const double R = exp_dd_core(t.hi, t.lo, lt, e);
+  return __hiloint2double(__double2hiint(R) + (e << 20), __double2loint(R));
+}
+template <int N>
+__device__ __forceinline__ float log_fast_f(float x, const double* c, const double* lt, bool& rare) {
+  rare = !is_pos_normal_f(x);
+  return (float)log_f_internal_f<N>(x, c, lt);
+}
+template <int NL>
+__device__ __forceinline__ float pow_fast_f(float x, float y, const double* cl, const double* lt, bool& rare) {
+  const uint32_t uy = bits_f(y);
+  const bool fy = ((uy & 0x7fffffffu) - 1u) < 0x7f7fffffu;
+  rare = !(is_pos_normal_f(x) && fy);
+  double t = (double)y * log_f_internal_f<NL>(x, cl, lt);
+  t = (((uint32_t)__double2hiint(t) & 0x7fffffffu) >= 0x40690000u) ? ((t > 0.0) ? 200.0 : -200.0) : t;
+  return (float)exp_f_internal(t, lt);
 }
 
 }  // namespace vem

@@ -5,6 +5,7 @@ runs 10x larger sweeps."""
 from __future__ import annotations
 
 import math
+import os
 
 import numpy as np
 import pytest
@@ -177,3 +178,42 @@ def test_special_grid_runs_everywhere():
         sp = SPECIAL_D if "_d_" in name else SPECIAL_F
         out = oracle_eval(name, sp)
         assert out.shape == sp.shape
+
+
+def test_f32_integer_payne_hanek_margin(tmp_path):
+    """The binary32 integer Payne-Hanek (oracle ph_f, kernels ph_f) needs the
+    rounded fraction of M*W(E) to keep its leading one in the top 32-bit word
+    for EVERY binary32 >= 1/2; tools/phf_margin.c checks all 2^23 x 129
+    (mantissa, exponent) pairs exhaustively (~3 s)."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = str(tmp_path / "phf_margin")
+    subprocess.run(["/usr/bin/gcc", "-O2", "-I", os.path.join(root, "paper_2001_09258_b200", "csrc"),
+                    os.path.join(root, "tools", "phf_margin.c"), "-o", exe], check=True)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout
+    assert "worst 29" in out.stdout
+
+
+def test_f32_reduction_accuracy_vs_f64_payne_hanek():
+    """r and q from the integer binary32 reduction against the double-double
+    result of the repaired reference Payne-Hanek (reduction.hpp:89-137, far
+    more accurate than binary64) on the same inputs: same quadrant, r within
+    2^-51 relative."""
+    from oracle_lib import oracle
+    import ctypes
+    L = oracle()
+    x = np.concatenate([I.log_uniform(11, 20000, 0.5, 3e38, np.float32, signed=True),
+                        I.uniform(12, 20000, -10, 10, np.float32)]).astype(np.float32)
+    r = np.zeros(x.size); q = np.zeros(x.size, np.int32)
+    P = ctypes.c_void_p
+    L.vo_ph_reduce_f.argtypes = [P, P, P, ctypes.c_size_t]
+    L.vo_ph_reduce_f(x.ctypes.data, r.ctypes.data, q.ctypes.data, x.size)
+    xd = x.astype(np.float64)
+    hi = np.zeros(x.size); lo = np.zeros(x.size); qd = np.zeros(x.size, np.int32)
+    L.vo_ph_reduce_d.argtypes = [P, P, P, P, ctypes.c_size_t]
+    L.vo_ph_reduce_d(xd.ctypes.data, hi.ctypes.data, lo.ctypes.data, qd.ctypes.data, x.size)
+    big = np.abs(x) >= 0.5
+    assert np.array_equal(q[big], qd[big] & 3)
+    rel = np.abs((r[big] - hi[big]) - lo[big]) / np.abs(hi[big])
+    assert rel.max() < 2.0 ** -51
