@@ -228,7 +228,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
       if constexpr (NIN == 2) vb[v] = buf[(size_t)(s * NIN + 1) * TILE_V + v * kThreads + tid];
     }
     __syncthreads();  // stage s fully consumed -> refill it
-    if (tid == 0 && j + STAGES < my) issue(s, blockIdx.x + (j + STAGES) * G);
+    if (tid == 0 && j + STAGES < my) {
+      tma::fence_proxy_async_smem();
+      issue(s, blockIdx.x + (j + STAGES) * G);
+    }
     V* ov = reinterpret_cast<V*>(out) + (blockIdx.x + j * G) * TILE_V;
     bool done = false;
     if constexpr (kSort) {

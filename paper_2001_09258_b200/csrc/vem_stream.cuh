@@ -48,6 +48,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       : "memory");
 }
 
+// Cross-proxy WAR: the generic-proxy LDS reads of a stage (by all threads,
+// ordered before this thread by the CTA barrier) must be ordered before the
+// async-proxy bulk copy that refills it.  Without this fence a refill can
+// land while earlier reads of the stage are still pending (observed: rare
+// elements computed from the NEXT tile's inputs).
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 // bulk copy global -> shared::cta (via the cluster window of this CTA),
 // completion reported to `bar` as transaction bytes; evict-first L2 policy.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,

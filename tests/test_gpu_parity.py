@@ -141,3 +141,38 @@ def test_repeat_launches_are_deterministic(cuda, name):
         out = api.call(name, *ts)
         assert torch.equal(out.view(torch.int64 if out.dtype == torch.float64 else torch.int32),
                            ref.view(torch.int64 if ref.dtype == torch.float64 else torch.int32))
+
+
+@pytest.mark.parametrize("name", ["log_f_u35", "exp_f_u35", "exp_d_u10", "pow_f_u10", "sin_f_u10", "cos_d_u10"])
+def test_tma_pipeline_vs_plain_kernel(cuda, name):
+    """Regression for the cross-proxy WAR race (fence.proxy.async before a
+    stage refill, vem_stream.cuh): the TMA-pipelined kernel over 2^28
+    monotone inputs (a stale or early-refilled stage shows up as a result
+    computed from another tile's input) must equal, bit for bit, the plain
+    grid-stride kernel the library uses for misaligned pointers (same math,
+    no shared-memory staging).  Several launches, since the race was rare."""
+    import torch
+    from paper_2001_09258_b200 import api
+    n = 1 << 28 if name.endswith("_f_u35") or name.endswith("_f_u10") else 1 << 27
+    dt = torch.float32 if "_f_" in name else torch.float64
+    it = torch.int32 if dt == torch.float32 else torch.int64
+    lo, hi = {"log": (1e-30, 1e30), "exp": (-80.0, 80.0), "pow": (0.01, 100.0), "sin": (-1e4, 1e4),
+              "cos": (-14.0, 14.0)}[name.split("_")[0]]
+    base = torch.empty(n + 1, dtype=dt, device="cuda")
+    if name.startswith("log") or name.startswith("pow"):
+        base.copy_(torch.logspace(np.log10(lo), np.log10(hi), n + 1, dtype=torch.float64, device="cuda").to(dt))
+    else:
+        base.copy_(torch.linspace(lo, hi, n + 1, dtype=torch.float64, device="cuda").to(dt))
+    args_al = [base[:n]]
+    args_un = [base[1:]]  # 4/8-byte offset -> unaligned -> plain kernel
+    if name.startswith("pow"):
+        y = torch.linspace(-3.0, 3.0, n + 1, dtype=torch.float64, device="cuda").to(dt)
+        args_al.append(y[:n])
+        args_un.append(y[1:])
+    ref = api.call(name, *args_un)  # elements 1..n
+    for _ in range(3):
+        got = api.call(name, *[a for a in args_al])  # elements 0..n-1
+        assert torch.equal(got[1:].view(it), ref[:-1].view(it)), name
+        del got
+    del ref, base
+    torch.cuda.empty_cache()
