@@ -13,6 +13,7 @@
 #include <atomic>
 #include <cstdint>
 #include <cstring>
+#include <type_traits>
 
 #include "../../include/vem.h"
 #include "vem_math.cuh"
@@ -161,11 +162,16 @@ __global__ void __launch_bounds__(kThreads) k_binary(const T* __restrict__ x, co
 // warp take the same reduction path; results are scattered back to their
 // original slots before the coalesced store.  Warps whose elements all share
 // one class skip the regrouping.
-template <class Op> struct SortsByClass { static constexpr bool value = false; };
+template <class Op> struct SortsByClass {
+  static constexpr bool value = false;
+  static constexpr int classes = 1;
+};
+// ops with a branch-free Cody-Waite-level-1 body for all-small warps
+template <class Op> struct HasCw1 { static constexpr bool value = false; };
 
 // Ops with a split fast path (vem_math.cuh "split fast paths"): the kernel
-// evaluates a tile's elements with Op::fast (branch-free, interleavable) and
-// re-evaluates only the elements it flags as rare with the full Op.
+// evaluates a tile's elements with Op::fast (branch-free, interleavable)
+// and passes the elements it flags to Op::slow.
 template <class Op> struct HasFast { static constexpr bool value = false; };
 // the full function for rare elements: one out-of-line copy per Op
 template <class Op, class T>
@@ -185,13 +191,15 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
   constexpr int TILE_V = kThreads * VPT;
   constexpr uint32_t TILE_BYTES = TILE_V * 16;
   constexpr int TILE_E = TILE_V * W;
-  constexpr bool kSort = SortsByClass<Op>::value && NIN == 1;
+  constexpr bool kSort = SortsByClass<Op>::value;
   constexpr int NE = VPT * W;  // elements per lane per tile
   extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ uint64_t bars[STAGES];
   __shared__ __align__(16) double stab[TableSize<TABLE>::n];
   __shared__ __align__(16) T wscr[kSort ? kThreads * NE : 1];
+  __shared__ __align__(16) T wscr2[kSort && NIN == 2 ? kThreads * NE : 1];
   __shared__ unsigned short widx[kSort ? kThreads * NE : 1];
+  __shared__ int wcur[kSort ? kThreads / 32 * 8 : 1];
   V* buf = reinterpret_cast<V*>(dsm);
   const int tid = threadIdx.x;
   if (tid == 0) {
@@ -235,69 +243,107 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
     V* ov = reinterpret_cast<V*>(out) + (blockIdx.x + j * G) * TILE_V;
     bool done = false;
     if constexpr (kSort) {
+      constexpr int K = SortsByClass<Op>::classes;
       const int lane = tid & 31;
       const unsigned lt_mask = (1u << lane) - 1u;
-      T xe[NE];
+      T xe[NE], ye[NE];
       int cl[NE];
 #pragma unroll
       for (int v = 0; v < VPT; v++)
 #pragma unroll
-        for (int k = 0; k < W; k++) xe[v * W + k] = vget(va[v], k);
+        for (int k = 0; k < W; k++) {
+          xe[v * W + k] = vget(va[v], k);
+          if constexpr (NIN == 2) ye[v * W + k] = vget(vb[v], k);
+        }
       bool same = true;
 #pragma unroll
       for (int e = 0; e < NE; e++) {
-        cl[e] = Op::cls(xe[e]);
+        if constexpr (NIN == 2) cl[e] = Op::cls(xe[e], ye[e]);
+        else cl[e] = Op::cls(xe[e]);
         same = same && (cl[e] == cl[0]);
       }
       const int c_l0 = __shfl_sync(0xffffffffu, cl[0], 0);
       const bool uniform = __all_sync(0xffffffffu, same && cl[0] == c_l0);
-      if (uniform && c_l0 == 0) {
-        // every element of the warp takes Cody-Waite level 1: branch-free
-        // bodies, interleaved across the thread's elements
-#pragma unroll
-        for (int v = 0; v < VPT; v++) {
-          V o;
-#pragma unroll
-          for (int k = 0; k < W; k++) vget(o, k) = op.cw1(xe[v * W + k], tab);
-          __stcs(ov + v * kThreads + tid, o);
-        }
-        done = true;
-      } else if (!uniform) {
+      auto regroup = [&]() {
+        // counting sort of the warp's 32*NE elements by class, heaviest
+        // class first: ballots per (row, class), prefix popcounts
         T* sx = wscr + (tid >> 5) * (32 * NE);
+        T* sy = wscr2 + (tid >> 5) * (32 * NE);
         unsigned short* si = widx + (tid >> 5) * (32 * NE);
-        unsigned m2[NE], m1[NE];
-        int n2 = 0, n1 = 0;
+        if constexpr (K == 3) {
+          // trig: two ballots per row, explicit three-way positions
+          unsigned m2[NE], m1[NE];
+          int n2 = 0, n1 = 0;
 #pragma unroll
-        for (int e = 0; e < NE; e++) {
-          m2[e] = __ballot_sync(0xffffffffu, cl[e] == 2);
-          m1[e] = __ballot_sync(0xffffffffu, cl[e] == 1);
-          n2 += __popc(m2[e]);
-          n1 += __popc(m1[e]);
-        }
-        int a2 = 0, a1 = n2, a0 = n2 + n1;  // heaviest class first
+          for (int e = 0; e < NE; e++) {
+            m2[e] = __ballot_sync(0xffffffffu, cl[e] == 2);
+            m1[e] = __ballot_sync(0xffffffffu, cl[e] == 1);
+            n2 += __popc(m2[e]);
+            n1 += __popc(m1[e]);
+          }
+          int a2 = 0, a1 = n2, a0 = n2 + n1;  // heaviest class first
 #pragma unroll
-        for (int e = 0; e < NE; e++) {
-          const unsigned m0 = ~(m2[e] | m1[e]);
-          const int pos = cl[e] == 2 ? a2 + __popc(m2[e] & lt_mask)
-                        : cl[e] == 1 ? a1 + __popc(m1[e] & lt_mask)
-                                     : a0 + __popc(m0 & lt_mask);
-          a2 += __popc(m2[e]);
-          a1 += __popc(m1[e]);
-          a0 += __popc(m0);
-          sx[pos] = xe[e];
-          si[pos] = (unsigned short)(e * 32 + lane);
+          for (int e = 0; e < NE; e++) {
+            const unsigned m0 = ~(m2[e] | m1[e]);
+            const int pos = cl[e] == 2 ? a2 + __popc(m2[e] & lt_mask)
+                          : cl[e] == 1 ? a1 + __popc(m1[e] & lt_mask)
+                                       : a0 + __popc(m0 & lt_mask);
+            a2 += __popc(m2[e]);
+            a1 += __popc(m1[e]);
+            a0 += __popc(m0);
+            sx[pos] = xe[e];
+            if constexpr (NIN == 2) sy[pos] = ye[e];
+            si[pos] = (unsigned short)(e * 32 + lane);
+          }
+        } else {
+          // K classes: per-warp class cursors in shared memory; lanes of one
+          // class in a row are ranked by match_any, the group's lowest lane
+          // advances the cursor
+          int* cur = wcur + (tid >> 5) * 8;
+          if (lane < K) cur[lane] = 0;
+          __syncwarp();
+          unsigned mm[NE];
+#pragma unroll
+          for (int e = 0; e < NE; e++) {
+            mm[e] = __match_any_sync(0xffffffffu, cl[e]);
+            if ((mm[e] & lt_mask) == 0u) atomicAdd(&cur[cl[e]], __popc(mm[e]));
+          }
+          __syncwarp();
+          if (lane == 0) {  // exclusive prefix, heaviest class first
+            int acc = 0;
+            for (int c = K - 1; c >= 0; c--) {
+              const int n = cur[c];
+              cur[c] = acc;
+              acc += n;
+            }
+          }
+          __syncwarp();
+#pragma unroll
+          for (int e = 0; e < NE; e++) {
+            const int pos = cur[cl[e]] + __popc(mm[e] & lt_mask);
+            __syncwarp();
+            if ((mm[e] & lt_mask) == 0u) cur[cl[e]] += __popc(mm[e]);
+            __syncwarp();
+            sx[pos] = xe[e];
+            if constexpr (NIN == 2) sy[pos] = ye[e];
+            si[pos] = (unsigned short)(e * 32 + lane);
+          }
         }
         __syncwarp();
-        T xs[NE];
+        T xs[NE], ys[NE];
         int ids[NE];
 #pragma unroll
         for (int r = 0; r < NE; r++) {
           xs[r] = sx[r * 32 + lane];
+          if constexpr (NIN == 2) ys[r] = sy[r * 32 + lane];
           ids[r] = si[r * 32 + lane];
         }
         __syncwarp();
 #pragma unroll
-        for (int r = 0; r < NE; r++) sx[ids[r]] = op(xs[r], tab);
+        for (int r = 0; r < NE; r++) {
+          if constexpr (NIN == 2) sx[ids[r]] = op(xs[r], ys[r], tab);
+          else sx[ids[r]] = op(xs[r], tab);
+        }
         __syncwarp();
 #pragma unroll
         for (int v = 0; v < VPT; v++) {
@@ -307,29 +353,48 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
           __stcs(ov + v * kThreads + tid, o);
         }
         __syncwarp();
+      };
+      if constexpr (HasCw1<Op>::value) {
+        if (uniform && c_l0 == 0) {
+          // every element of the warp takes Cody-Waite level 1: branch-free
+          // bodies, interleaved across the thread's elements
+#pragma unroll
+          for (int v = 0; v < VPT; v++) {
+            V o;
+#pragma unroll
+            for (int k = 0; k < W; k++) vget(o, k) = op.cw1(xe[v * W + k], tab);
+            __stcs(ov + v * kThreads + tid, o);
+          }
+          done = true;
+        } else if (!uniform) {
+          regroup();
+          done = true;
+        }
+      } else if (!uniform) {
+        regroup();
         done = true;
       }
     }
     if constexpr (HasFast<Op>::value) {
       T res[NE];
-      bool rare[NE];
-      bool any = false;
+      int code[NE];
+      int any = 0;
 #pragma unroll
       for (int v = 0; v < VPT; v++)
 #pragma unroll
         for (int k = 0; k < W; k++) {
           const int e = v * W + k;
-          if constexpr (NIN == 2) res[e] = op.fast(vget(va[v], k), vget(vb[v], k), tab, rare[e]);
-          else res[e] = op.fast(vget(va[v], k), tab, rare[e]);
-          any |= rare[e];
+          if constexpr (NIN == 2) res[e] = op.fast(vget(va[v], k), vget(vb[v], k), tab, code[e]);
+          else res[e] = op.fast(vget(va[v], k), tab, code[e]);
+          any |= code[e];
         }
       if (any) {
 #pragma unroll
         for (int e = 0; e < NE; e++) {
-          if (rare[e]) {
-            const int v = e / W, k = e % W;
-            if constexpr (NIN == 2) res[e] = full_op<Op>(vget(va[v], k), vget(vb[v], k), tab);
-            else res[e] = full_op<Op>(vget(va[v], k), tab);
+          const int v = e / W, k = e % W;
+          if (code[e]) {
+            if constexpr (NIN == 2) res[e] = Op::slow(vget(va[v], k), vget(vb[v], k), res[e], code[e], tab);
+            else res[e] = Op::slow(vget(va[v], k), res[e], code[e], tab);
           }
         }
       }
@@ -381,8 +446,8 @@ constexpr int kFmodChunk = 64;       // elements per warp per phase 1
 constexpr int kFmodRing = 64;        // ring entries per warp (>= chunk)
 constexpr int kRefill = 8;
 
-template <class T>
-__global__ void __launch_bounds__(kFmodWarps * 32) k_fmod(const T* __restrict__ a, const T* __restrict__ b,
+template <class T, int MINB = 1>
+__global__ void __launch_bounds__(kFmodWarps * 32, MINB) k_fmod(const T* __restrict__ a, const T* __restrict__ b,
                                                           T* __restrict__ out, size_t n) {
   __shared__ double s_r[kFmodWarps][kFmodRing], s_md[kFmodWarps][kFmodRing], s_rmd[kFmodWarps][kFmodRing];
   __shared__ int2 s_e[kFmodWarps][kFmodRing];
@@ -401,10 +466,8 @@ __global__ void __launch_bounds__(kFmodWarps * 32) k_fmod(const T* __restrict__ 
 
   auto step_all = [&]() {
     if (active) {
-      int sh = st.E > 50 ? 50 : st.E;
-      st.E -= sh;
-      st.r = fmod_step(st.r, sh, st.md, st.rmd);
-      if (st.E == 0 || st.r == 0.0) {
+      st.r = fmod_step50(st.r, st.md, st.rmd);
+      if (--st.E == 0) {
         active = false;
         pend = true;
       }
@@ -474,12 +537,15 @@ __global__ void __launch_bounds__(kFmodWarps * 32) k_fmod(const T* __restrict__ 
       tail += __popc(m);
     }
     __syncwarp();
-    // ---- phase 2: step (two per refill check) until the ring is empty
+    // ---- phase 2: refill, then step (two per check) until at least kRefill
+    // lanes are idle; leave when the ring is empty (next chunk's setup)
     while (true) {
       refill(false);
       if (tail == head) break;
-      step_all();
-      step_all();
+      do {
+        step_all();
+        step_all();
+      } while (__popc(__ballot_sync(0xffffffffu, !active)) < kRefill);
     }
   }
   // ---- drain
@@ -506,7 +572,11 @@ __global__ void __launch_bounds__(kFmodWarps * 32) k_fmod(const T* __restrict__ 
     }                                                                                    \
     __device__ __forceinline__ static int cls(double x) { return trig_class(x); }      \
   };                                                                                     \
-  template <> struct SortsByClass<NAME> { static constexpr bool value = true; };
+  template <> struct SortsByClass<NAME> {                                                \
+    static constexpr bool value = true;                                                  \
+    static constexpr int classes = 3;                                                    \
+  };                                                                                     \
+  template <> struct HasCw1<NAME> { static constexpr bool value = true; };
 // selector variants: PH table from global memory (L1), coefficients staged
 VEM_TRIG_OP(OpSinD, sin_d_u10, , tab)
 VEM_TRIG_OP(OpCosD, cos_d_u10, , tab)
@@ -516,24 +586,36 @@ VEM_UNARY_OP(OpSinDPh, double, (sin_d_u10<kPh>(x, tab, tab + 4 * VEM_PH_D_ENTRIE
 VEM_UNARY_OP(OpCosDPh, double, (cos_d_u10<kPh>(x, tab, tab + 4 * VEM_PH_D_ENTRIES)))
 VEM_UNARY_OP(OpTanDPh, double, (tan_d_u10<kPh>(x, tab)))
 VEM_UNARY_OP(OpAtanD, double, ((void)tab, atan_d_u10(x)))
-#define VEM_SPLIT_UNARY_OP(NAME, T, EXPR, FAST)                                          \
+// SLOW: value for a flagged element (x, r = fast result, code); `full()`
+// is the out-of-line full function
+#define VEM_SPLIT_UNARY_OP(NAME, T, EXPR, FAST, SLOW)                                    \
   struct NAME {                                                                          \
     __device__ __forceinline__ T operator()(T x, const double* tab) const { return EXPR; } \
-    __device__ __forceinline__ T fast(T x, const double* tab, bool& rare) const { return FAST; } \
+    __device__ __forceinline__ T fast(T x, const double* tab, int& code) const { return FAST; } \
+    __device__ __forceinline__ static T slow(T x, T r, int code, const double* tab) {    \
+      (void)r;                                                                           \
+      (void)code;                                                                        \
+      auto full = [&]() { return full_op<NAME>(x, tab); };                               \
+      return SLOW;                                                                       \
+    }                                                                                    \
   };                                                                                     \
   template <> struct HasFast<NAME> { static constexpr bool value = true; };
-VEM_SPLIT_UNARY_OP(OpExpD, double, ((void)tab, exp_d_u10(x)), ((void)tab, (exp_fast_d<VEM_EXP_D_N, true>(x, cExpD, rare))))
+VEM_SPLIT_UNARY_OP(OpExpD, double, ((void)tab, exp_d_u10(x)), ((void)tab, (exp_fast_d<VEM_EXP_D_N, true>(x, cExpD, code))),
+                   exp_slow_d(x, full))
 VEM_SPLIT_UNARY_OP(OpExpDU35, double, ((void)tab, exp_d_u35(x)),
-                   ((void)tab, (exp_fast_d<VEM_EXP_D_U35_N, false>(x, cExpDU35, rare))))
-VEM_SPLIT_UNARY_OP(OpLogD, double, (log_core_d<true>(x, tab)), (log_fast_split_d<true>(x, tab, rare)))
-VEM_SPLIT_UNARY_OP(OpLogDU35, double, (log_core_d<false>(x, tab)), (log_fast_split_d<false>(x, tab, rare)))
+                   ((void)tab, (exp_fast_d<VEM_EXP_D_U35_N, false>(x, cExpDU35, code))), exp_slow_d(x, full))
+VEM_SPLIT_UNARY_OP(OpLogD, double, (log_core_d<true>(x, tab)), (log_fast_split_d<true>(x, tab, code)),
+                   log_slow_d(x, full))
+VEM_SPLIT_UNARY_OP(OpLogDU35, double, (log_core_d<false>(x, tab)), (log_fast_split_d<false>(x, tab, code)),
+                   log_slow_d(x, full))
 VEM_UNARY_OP(OpSinF, float, (sin_f_u10(x, tab)))
 VEM_UNARY_OP(OpCosF, float, (cos_f_u10(x, tab)))
 VEM_UNARY_OP(OpTanF, float, (tan_f_u10(x, tab)))
 VEM_UNARY_OP(OpExpF, float, ((void)tab, exp_f_u10(x)))
 VEM_UNARY_OP(OpExpFU35, float, ((void)tab, exp_f_u35(x)))
-VEM_SPLIT_UNARY_OP(OpLogF, float, (log_f_u10(x, tab)), (log_fast_f<VEM_LOG1P_F_N>(x, cLog1pF, tab, rare)))
-VEM_SPLIT_UNARY_OP(OpLogFU35, float, (log_f_u35(x, tab)), (log_fast_f<VEM_LOG1P_F_U35_N>(x, cLog1pFU35, tab, rare)))
+VEM_SPLIT_UNARY_OP(OpLogF, float, (log_f_u10(x, tab)), (log_fast_f<VEM_LOG1P_F_N>(x, cLog1pF, tab, code)), full())
+VEM_SPLIT_UNARY_OP(OpLogFU35, float, (log_f_u35(x, tab)), (log_fast_f<VEM_LOG1P_F_U35_N>(x, cLog1pFU35, tab, code)),
+                   full())
 #undef VEM_UNARY_OP
 #undef VEM_SPLIT_UNARY_OP
 
@@ -541,20 +623,50 @@ VEM_SPLIT_UNARY_OP(OpLogFU35, float, (log_f_u35(x, tab)), (log_fast_f<VEM_LOG1P_
   struct NAME {                                                                   \
     __device__ __forceinline__ T operator()(T x, T y, const double* tab) const { return EXPR; } \
   };
-#define VEM_SPLIT_BINARY_OP(NAME, T, EXPR, FAST)                                  \
+#define VEM_SPLIT_BINARY_OP(NAME, T, EXPR, FAST, SLOW)                                 \
   struct NAME {                                                                   \
     __device__ __forceinline__ T operator()(T x, T y, const double* tab) const { return EXPR; } \
-    __device__ __forceinline__ T fast(T x, T y, const double* tab, bool& rare) const { return FAST; } \
+    __device__ __forceinline__ T fast(T x, T y, const double* tab, int& code) const { return FAST; } \
+    __device__ __forceinline__ static T slow(T x, T y, T r, int code, const double* tab) { \
+      (void)r;                                                                    \
+      (void)code;                                                                 \
+      auto full = [&]() { return full_op<NAME>(x, y, tab); };                     \
+      return SLOW;                                                                \
+    }                                                                             \
   };                                                                              \
   template <> struct HasFast<NAME> { static constexpr bool value = true; };
-VEM_SPLIT_BINARY_OP(OpPowD, double, pow_d_u10(x, y, tab), (pow_fast_d<VEM_LOG1P_D_N>(x, y, cLog1pD, tab, rare)))
+VEM_SPLIT_BINARY_OP(OpPowD, double, pow_d_u10(x, y, tab), (pow_fast_d<VEM_LOG1P_D_N>(x, y, cLog1pD, tab, code)),
+                    pow_slow_split_d(y, r, code, full))
 VEM_SPLIT_BINARY_OP(OpPowDU35, double, pow_d_u35(x, y, tab),
-                    (pow_fast_d<VEM_LOG1P_D_U35_N>(x, y, cLog1pDU35, tab, rare)))
-VEM_BINARY_OP(OpFmodD, double, ((void)tab, fmod_d(x, y)))
-VEM_SPLIT_BINARY_OP(OpPowF, float, pow_f_u10(x, y, tab), (pow_fast_f<VEM_LOG1P_F_N>(x, y, cLog1pF, tab, rare)))
+                    (pow_fast_d<VEM_LOG1P_D_U35_N>(x, y, cLog1pDU35, tab, code)), pow_slow_split_d(y, r, code, full))
+// fmod: regrouped by step class (exponent gap / 50 in 6 ranges) so the
+// lanes of a row run similar long-division trip counts
+struct OpFmodD {
+  __device__ __forceinline__ double operator()(double x, double y, const double* tab) const {
+    (void)tab;
+    return fmod_d(x, y);
+  }
+  __device__ __forceinline__ static int cls(double x, double y) { return fmod_class(x, y); }
+};
+template <> struct SortsByClass<OpFmodD> {
+  static constexpr bool value = true;
+  static constexpr int classes = kFmodClasses;
+};
+VEM_SPLIT_BINARY_OP(OpPowF, float, pow_f_u10(x, y, tab), (pow_fast_f<VEM_LOG1P_F_N>(x, y, cLog1pF, tab, code)),
+                    full())
 VEM_SPLIT_BINARY_OP(OpPowFU35, float, pow_f_u35(x, y, tab),
-                    (pow_fast_f<VEM_LOG1P_F_U35_N>(x, y, cLog1pFU35, tab, rare)))
-VEM_BINARY_OP(OpFmodF, float, ((void)tab, fmod_f(x, y)))
+                    (pow_fast_f<VEM_LOG1P_F_U35_N>(x, y, cLog1pFU35, tab, code)), full())
+struct OpFmodF {
+  __device__ __forceinline__ float operator()(float x, float y, const double* tab) const {
+    (void)tab;
+    return fmod_f(x, y);
+  }
+  __device__ __forceinline__ static int cls(float x, float y) { return fmod_class_f(x, y); }
+};
+template <> struct SortsByClass<OpFmodF> {
+  static constexpr bool value = true;
+  static constexpr int classes = kFmodClasses;
+};
 #undef VEM_BINARY_OP
 #undef VEM_SPLIT_BINARY_OP
 
@@ -649,14 +761,14 @@ static int launch_stream(const T* a, const T* b, T* out, size_t n, vem_stream_t 
   return (int)cudaGetLastError();
 }
 
-template <class T>
+template <class T, int MINB = 1>
 static int launch_fmod(const T* a, const T* b, T* out, size_t n, vem_stream_t s) {
   if (n == 0) return 0;
   if (!(aligned16(a) && aligned16(b))) {
     if constexpr (sizeof(T) == 8) return launch_binary<OpFmodD, T, kNoTable, 1>(a, b, out, n, s);
     else return launch_binary<OpFmodF, T, kNoTable, 1>(a, b, out, n, s);
   }
-  auto k = k_fmod<T>;
+  auto k = k_fmod<T, MINB>;
   static const int occ = [k] {
     int bpm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpm, k, kFmodWarps * 32, 0) != cudaSuccess || bpm < 1)
@@ -741,15 +853,31 @@ static int launch_tuned(const T* a, const T* b, T* o, size_t n, vem_stream_t s) 
   }
 }
 #define VEM_STREAM launch_tuned
+template <class T>
+static int launch_fmod_tuned(const T* a, const T* b, T* o, size_t n, vem_stream_t s) {
+  using OpF = typename std::conditional<sizeof(T) == 8, OpFmodD, OpFmodF>::type;
+  switch (g_tune) {
+    case 1: return launch_fmod<T, 8>(a, b, o, n, s);
+    case 2: return launch_fmod<T, 12>(a, b, o, n, s);
+    case 3: return launch_fmod<T, 16>(a, b, o, n, s);
+    case 4: return launch_stream<OpF, T, 2, kNoTable, 1, 2>(a, b, o, n, s);
+    case 5: return launch_stream<OpF, T, 2, kNoTable, 2, 2, 4>(a, b, o, n, s);
+    case 6: return launch_stream<OpF, T, 2, kNoTable, 4, 2>(a, b, o, n, s);
+    case 7: return launch_stream<OpF, T, 2, kNoTable, 2, 2>(a, b, o, n, s);
+    default: return launch_fmod<T>(a, b, o, n, s);
+  }
+}
+#define VEM_FMOD launch_fmod_tuned
 #else
 #define VEM_STREAM launch_stream
+#define VEM_FMOD launch_fmod
 #endif
 
 // Elements per thread in flight (16-byte vectors): HBM-bound kernels keep 4
 // vectors in flight, FP64-pipe-bound ones 2 (register pressure).
 extern "C" {
 
-int vem_sin_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpSinD, double, 1, kTableDG, 2, 2, 4>(x, nullptr, y, n, s); }
+int vem_sin_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpSinD, double, 1, kTableDG, 2, 2, 3>(x, nullptr, y, n, s); }
 int vem_cos_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpCosD, double, 1, kTableDG, 2, 2, 4>(x, nullptr, y, n, s); }
 int vem_tan_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpTanD, double, 1, kTableDG, 2, 2, 4>(x, nullptr, y, n, s); }
 int vem_sin_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpSinDPh, double, 1, kTableD, 2, 2>(x, nullptr, y, n, s); }
@@ -762,7 +890,13 @@ int vem_log_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return
 int vem_log_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpLogDU35, double, 1, kTableLog, 2, 2, 4>(x, nullptr, y, n, s); }
 int vem_pow_d_u10(const double* x, const double* y2, double* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpPowD, double, 2, kTableLog, 2, 2, 3>(x, y2, o, n, s); }
 int vem_pow_d_u35(const double* x, const double* y2, double* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpPowDU35, double, 2, kTableLog, 2, 2, 3>(x, y2, o, n, s); }
-int vem_fmod_d(const double* x, const double* y2, double* o, size_t n, vem_stream_t s) { return launch_fmod<double>(x, y2, o, n, s); }
+int vem_fmod_d(const double* x, const double* y2, double* o, size_t n, vem_stream_t s) {
+#ifdef VEM_TUNE
+  return VEM_FMOD<double>(x, y2, o, n, s);
+#else
+  return VEM_STREAM<OpFmodD, double, 2, kNoTable, 2, 2>(x, y2, o, n, s);
+#endif
+}
 
 int vem_sin_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpSinF, float, 1, kTableF, 4, 2>(x, nullptr, y, n, s); }
 int vem_cos_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpCosF, float, 1, kTableF, 4, 2>(x, nullptr, y, n, s); }
@@ -777,7 +911,13 @@ int vem_log_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return V
 int vem_log_f_u35(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpLogFU35, float, 1, kTableLog, 4, 2>(x, nullptr, y, n, s); }
 int vem_pow_f_u10(const float* x, const float* y2, float* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpPowF, float, 2, kTableLog, 2, 2, 3>(x, y2, o, n, s); }
 int vem_pow_f_u35(const float* x, const float* y2, float* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpPowFU35, float, 2, kTableLog, 2, 2, 3>(x, y2, o, n, s); }
-int vem_fmod_f(const float* x, const float* y2, float* o, size_t n, vem_stream_t s) { return launch_fmod<float>(x, y2, o, n, s); }
+int vem_fmod_f(const float* x, const float* y2, float* o, size_t n, vem_stream_t s) {
+#ifdef VEM_TUNE
+  return VEM_FMOD<float>(x, y2, o, n, s);
+#else
+  return VEM_STREAM<OpFmodF, float, 2, kNoTable, 2, 2, 4>(x, y2, o, n, s);
+#endif
+}
 
 int vem_trig_reduce_d(const double* x, double* hi, double* lo, int* q, size_t n, vem_stream_t s) {
   return launch_reduce_d<0>(x, hi, lo, q, n, s);

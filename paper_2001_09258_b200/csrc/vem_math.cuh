@@ -663,16 +663,32 @@ __device__ __forceinline__ double mant_1_2(double x, int e) {
   uint64_t m = (e >= -1022) ? (b & 0x000fffffffffffffull) : ((b << (-1022 - e)) & 0x000fffffffffffffull);
   return from_bits_d(m | 0x3ff0000000000000ull);
 }
-__device__ __forceinline__ double fmod_step(double r, int s, double md, double rmd) {
-  double rs = r * __hiloint2double((1023 + s) << 20, 0);
-  double Q = trunc(toward0_pos(rs * rmd));
-  double Q2 = Q + 1.0;
-  double p1 = Q * md, e1 = fma(Q, md, -p1);
-  double V1 = (rs - p1) - e1;
-  double p2 = Q2 * md, e2 = fma(Q2, md, -p2);
-  double V2 = (rs - p2) - e2;
+// One step of up to 50 bits: (r * 2^s) mod md, exactly (r < md, md in
+// [1,2), rmd <= 1/md within 2 ulps).  The quotient estimate
+// Q = trunc(RZ(rs * rmd)) is floor(rs/md) or one less (relative error
+// < 2^-51 on a quotient < 2^50), so the true remainders V1 = rs - Q*md in
+// [0, 2 md) and V2 = V1 - md satisfy: V2 >= 0 exactly when Q is one short.
+// Each FMA is exact whenever its value is selected: rs and Q*md are
+// multiples of 2^-52, so V1 (< md < 2 when kept) and V2 (in [0, md)) are
+// representable; a rounded V1 >= 2 or a negative V2 only feeds the
+// comparison, whose sign RN preserves.  Every step is exact, so the result
+// equals the oracle's (vem_oracle.c fmod_step: two_prod, 50-bit steps from
+// the top) bit for bit although the step split differs.
+__device__ __forceinline__ double fmod_step_rs(double rs, double md, double rmd) {
+  const double Q = trunc(__dmul_rz(rs, rmd));
+  const double V1 = fma(-Q, md, rs);
+  const double V2 = fma(-(Q + 1.0), md, rs);
   return (V2 >= 0.0) ? V2 : V1;
 }
+__device__ __forceinline__ double fmod_step(double r, int s, double md, double rmd) {
+  return fmod_step_rs(r * __hiloint2double((1023 + s) << 20, 0), md, rmd);
+}
+__device__ __forceinline__ double fmod_step50(double r, double md, double rmd) {
+  return fmod_step_rs(r * 0x1p50, md, rmd);
+}
+// After setup: r = (mn * 2^s0) mod md with s0 = E - 50*E50 in [1, 50], and
+// E = E50 full 50-bit steps still to go (the kernels' ring holds only
+// elements with E > 0).
 struct fmod_state {
   double r, md, rmd, x;
   int E, ed;
@@ -692,16 +708,23 @@ __device__ __forceinline__ bool fmod_setup(double x, double y, fmod_state& st, d
   double mn = mant_1_2(n, en), md = mant_1_2(d, ed);
   int E = en - ed;
   st.md = md;
-  st.rmd = toward0_pos(1.0 / md);
-  st.r = (E == 0) ? mn - md : mn;
-  st.E = E;
+  st.rmd = toward0_pos(1.0 / md);  // <= 1/md (1.0/md is correctly rounded)
   st.ed = ed;
   st.x = x;
   if (E == 0) {  // mn >= md: one exact subtraction finishes it
+    st.r = mn - md;
+    st.E = 0;
     res = copysign_b(ldexp2(st.r, ed), x);
     return true;
   }
-  return false;  // st.E > 0 and st.r = mn >= 1
+  const int E50 = (E - 1) / 50;
+  st.r = fmod_step(mn, E - 50 * E50, md, st.rmd);
+  st.E = E50;
+  if (E50 == 0) {
+    res = copysign_b(ldexp2(st.r, ed), x);
+    return true;
+  }
+  return false;
 }
 __device__ __forceinline__ double fmod_finish(const fmod_state& st) {
   return copysign_b(ldexp2(st.r, st.ed), st.x);
@@ -710,14 +733,26 @@ __device__ __forceinline__ double fmod_core(double x, double y) {
   fmod_state st;
   double res;
   if (fmod_setup(x, y, st, res)) return res;
-  while (st.E > 0 && st.r != 0.0) {
-    int s = st.E > 50 ? 50 : st.E;
-    st.E -= s;
-    st.r = fmod_step(st.r, s, st.md, st.rmd);
-  }
+  for (int i = 0; i < st.E; i++) st.r = fmod_step50(st.r, st.md, st.rmd);
   return fmod_finish(st);
 }
 __device__ __forceinline__ double fmod_d(double x, double y) { return fmod_core(x, y); }
+// Work class of a pair for the kernels' regrouping: the number of 50-bit
+// steps from the biased exponents (subnormals counted as exponent 0; only a
+// scheduling hint, results do not depend on it), bucketed into 6 ranges.
+constexpr int kFmodClasses = 6;
+__device__ __forceinline__ int fmod_class(double x, double y) {
+  const int ex = (int)(((uint32_t)__double2hiint(x) >> 20) & 0x7ffu);
+  const int ey = (int)(((uint32_t)__double2hiint(y) >> 20) & 0x7ffu);
+  const int n = (ex - ey - 1) / 50;  // full steps after the first (<= 0: none)
+  return n <= 0 ? 0 : (n <= 3 ? 1 : (n <= 8 ? 2 : (n <= 15 ? 3 : (n <= 24 ? 4 : 5))));
+}
+__device__ __forceinline__ int fmod_class_f(float x, float y) {
+  const int ex = (int)((bits_f(x) >> 23) & 0xffu);
+  const int ey = (int)((bits_f(y) >> 23) & 0xffu);
+  const int n = (ex - ey - 1) / 50;
+  return n <= 0 ? 0 : (n >= kFmodClasses - 1 ? kFmodClasses - 1 : n);
+}
 
 // ===================================== f32 functions (binary64 internals)
 struct redf { double r; int q; };
@@ -928,45 +963,83 @@ __device__ __forceinline__ float fmod_f(float x, float y) {
 }
 
 // ============================================ split fast paths (kernels)
-// Branch-free bodies for the common inputs.  `rare` marks elements outside
-// them; the streaming kernel evaluates every element of a tile with these
-// (so the compiler interleaves the independent chains of one thread's
-// elements) and then recomputes only the rare ones with the full function.
-// For non-rare inputs each returns exactly the full function's value.
+// Branch-free bodies for the common inputs, returning a nonzero `code` for
+// elements they do not finish.  The streaming kernel evaluates a tile's
+// elements with these (so the compiler interleaves the independent chains
+// of one thread's elements), then passes the flagged ones to the op's
+// `slow` hook (vem_kernels.cu), which selects saturated / special results
+// inline and calls the full, out-of-line function only for genuinely rare
+// inputs (subnormal operands or results, NaN operands of pow, ...).  For
+// code 0 each returns exactly the full function's value.
 template <int N, bool kU10>
-__device__ __forceinline__ double exp_fast_d(double x, const double* c, bool& rare) {
-  rare = ((uint32_t)__double2hiint(x) & 0x7fffffffu) >= kExpFastHi;
+__device__ __forceinline__ double exp_fast_d(double x, const double* c, int& code) {
+  code = ((uint32_t)__double2hiint(x) & 0x7fffffffu) >= kExpFastHi ? 1 : 0;
   int k;
   double y = exp_poly_d<N, kU10>(x, c, k);
   return __hiloint2double(__double2hiint(y) + (k << 20), __double2loint(y));
 }
+// |x| >= 708: overflow / underflow / NaN selected, the gradual-underflow and
+// near-overflow bands need the full function (`full` is called only then)
+template <class F>
+__device__ __forceinline__ double exp_slow_d(double x, F full) {
+  if ((x >= kExpUnf) && (x <= kExpOvf)) return full();
+  return (x != x) ? from_bits_d(kCanonNanD) : (x > 0.0 ? kInf : 0.0);
+}
 template <bool kU10>
-__device__ __forceinline__ double log_fast_split_d(double x, const double* lt, bool& rare) {
-  rare = !(bits_d(x) - 0x0010000000000000ull < 0x7fe0000000000000ull);
+__device__ __forceinline__ double log_fast_split_d(double x, const double* lt, int& code) {
+  code = (bits_d(x) - 0x0010000000000000ull < 0x7fe0000000000000ull) ? 0 : 1;  // positive normal
   return log_fast_d<kU10, false>(x, 0.0, lt);
 }
+template <class F>
+__device__ __forceinline__ double log_slow_d(double x, F full) {
+  const uint64_t ix = bits_d(x);
+  if (ix - 1ull < 0x000fffffffffffffull) return full();  // positive subnormal
+  return (ix << 1) == 0ull ? -kInf : (ix == 0x7ff0000000000000ull ? kInf : from_bits_d(kCanonNanD));
+}
+// pow codes: bit 0 = full function, bit 1 = negative base (sign / NaN rule),
+// bit 2 = exp overflow (t > ln(DBL_MAX)), bit 3 = exp underflow to 0.  The
+// saturation tests use the high word of t with a one-ulp-of-the-word margin:
+// t in the margin gets bit 0 instead, never a wrong saturation.
 template <int NL>
-__device__ __forceinline__ double pow_fast_d(double x, double y, const double* cl, const double* lt, bool& rare) {
+__device__ __forceinline__ double pow_fast_d(double x, double y, const double* cl, const double* lt, int& code) {
   const uint32_t hx = (uint32_t)__double2hiint(x);
   const uint32_t hy = (uint32_t)__double2hiint(y) & 0x7fffffffu, ly = (uint32_t)__double2loint(y);
-  const bool fx = (hx - 0x00100000u) < 0x7fe00000u;  // positive normal
+  const bool fx = ((hx & 0x7fffffffu) - 0x00100000u) < 0x7fe00000u;  // normal, either sign
   const bool fy = (hy < 0x7ff00000u) && ((hy | ly) != 0u);
-  const dd t = dd_mul_d(log_dd<NL, false>(x, 0.0, cl, lt), y);
-  rare = !(fx && fy) || (((uint32_t)__double2hiint(t.hi) & 0x7fffffffu) >= kExpFastHi);
+  const double ax = __hiloint2double((int)(hx & 0x7fffffffu), __double2loint(x));
+  const dd t = dd_mul_d(log_dd<NL, false>(ax, 0.0, cl, lt), y);
   int e;
   const double R = exp_dd_core(t.hi, t.lo, lt, e);
+  const uint32_t th = (uint32_t)__double2hiint(t.hi);
+  const uint32_t ht = th & 0x7fffffffu;
+  int c = ((int)hx < 0) ? 2 : 0;
+  if (ht >= kExpFastHi) {
+    const bool neg = (int)th < 0;
+    c |= (!neg && ht >= 0x40862E43u) ? 4 : ((neg && ht >= 0x40874911u) ? 8 : 1);
+  }
+  code = (fx && fy) ? c : 1;
   return __hiloint2double(__double2hiint(R) + (e << 20), __double2loint(R));
 }
+// pow of a negative finite base (pow_core_d's rule on R = pow(|x|, y))
+__device__ __forceinline__ double pow_neg_fix_d(double R, double y) {
+  return is_int_d(y) ? (is_odd_d(y) ? -R : R) : from_bits_d(kCanonNanD);
+}
+template <class F>
+__device__ __forceinline__ double pow_slow_split_d(double y, double r, int code, F full) {
+  if (code & 1) return full();
+  r = (code & 4) ? kInf : ((code & 8) ? 0.0 : r);
+  return (code & 2) ? pow_neg_fix_d(r, y) : r;
+}
 template <int N>
-__device__ __forceinline__ float log_fast_f(float x, const double* c, const double* lt, bool& rare) {
-  rare = !is_pos_normal_f(x);
+__device__ __forceinline__ float log_fast_f(float x, const double* c, const double* lt, int& code) {
+  code = is_pos_normal_f(x) ? 0 : 1;
   return (float)log_f_internal_f<N>(x, c, lt);
 }
 template <int NL>
-__device__ __forceinline__ float pow_fast_f(float x, float y, const double* cl, const double* lt, bool& rare) {
+__device__ __forceinline__ float pow_fast_f(float x, float y, const double* cl, const double* lt, int& code) {
   const uint32_t uy = bits_f(y);
   const bool fy = ((uy & 0x7fffffffu) - 1u) < 0x7f7fffffu;
-  rare = !(is_pos_normal_f(x) && fy);
+  code = (is_pos_normal_f(x) && fy) ? 0 : 1;
   double t = (double)y * log_f_internal_f<NL>(x, cl, lt);
   t = (((uint32_t)__double2hiint(t) & 0x7fffffffu) >= 0x40690000u) ? ((t > 0.0) ? 200.0 : -200.0) : t;
   return (float)exp_f_internal(t, lt);
