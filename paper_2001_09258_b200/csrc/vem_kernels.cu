@@ -428,6 +428,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
   }
 }
 
+#ifdef VEM_TUNE
+// Work-ring fmod kernel (superseded by the regrouped streaming kernel,
+// OpFmodD/OpFmodF below; kept in the tuning build for comparison).
 // ------------------------------------------------------------ fmod
 // The remainder loop runs ceil(E/50) steps, E = exponent gap of |x| and |y|;
 // a plain SIMT loop makes every lane wait for its warp's slowest element
@@ -556,6 +559,8 @@ __global__ void __launch_bounds__(kFmodWarps * 32, MINB) k_fmod(const T* __restr
   }
   if (pend) __stcs(out + gi, (T)fmod_finish(st));
 }
+
+#endif  // VEM_TUNE
 
 // ------------------------------------------------------------- functors
 #define VEM_UNARY_OP(NAME, T, EXPR)                                                   \
@@ -761,6 +766,7 @@ static int launch_stream(const T* a, const T* b, T* out, size_t n, vem_stream_t 
   return (int)cudaGetLastError();
 }
 
+#ifdef VEM_TUNE
 template <class T, int MINB = 1>
 static int launch_fmod(const T* a, const T* b, T* out, size_t n, vem_stream_t s) {
   if (n == 0) return 0;
@@ -783,6 +789,8 @@ static int launch_fmod(const T* a, const T* b, T* out, size_t n, vem_stream_t s)
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return (int)cudaGetLastError();
 }
+
+#endif  // VEM_TUNE
 
 // ---------------------------------------------------- reduction kernels
 template <int MODE>  // 0 trig_reduce, 1 cw1, 2 cw2, 3 ph
