@@ -189,9 +189,11 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------- CPU legs
-def cpu_oracle_rate(work, sample_log2: int, threads: int):
+def cpu_oracle_rate(work, sample_log2: int, threads: int, budget_s: float = 0.0):
     """Oracle port (oracle/vem_oracle.c, OpenMP on `threads` host threads) over a
-    bounded host sample of every entry point; returns (Gelem/s, seconds, n)."""
+    bounded host sample of every entry point: 2^sample_log2 elements, passes
+    repeated until each entry point has run budget_s/len(work) seconds (at
+    least one pass); returns (Gelem/s, seconds, elements, per-function)."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from oracle_lib import oracle_eval
     from paper_2001_09258_b200 import inputs as I
@@ -204,12 +206,17 @@ def cpu_oracle_rate(work, sample_log2: int, threads: int):
         fn, p = name.split("_")[0], name.split("_")[1]
         arrs = I.config_inputs(cfg, fn, p, n)
         oracle_eval(name, *[a[:4096] for a in arrs])  # warm (threads, pages)
+        reps = 0
         t0 = time.perf_counter()
-        oracle_eval(name, *arrs)
-        dt = time.perf_counter() - t0
-        per[name] = round(n / dt / 1e9, 4)
+        while True:
+            oracle_eval(name, *arrs)
+            reps += 1
+            dt = time.perf_counter() - t0
+            if dt >= budget_s / max(1, len(work)):
+                break
+        per[name] = round(reps * n / dt / 1e9, 4)
         total_t += dt
-        total_n += n
+        total_n += reps * n
     return total_n / total_t / 1e9, total_t, total_n, per
 
 
@@ -263,7 +270,7 @@ def run_reference(args, rank, world):
     t_all = 0.0
     per = {}
     for _ in range(args.steps):
-        v, t, n, per = cpu_oracle_rate(work, lg, threads)
+        v, t, n, per = cpu_oracle_rate(work, lg, threads, budget_s=3.0)
         vals.append(v)
         t_all += t
     value = sum(vals) / len(vals)
@@ -272,10 +279,12 @@ def run_reference(args, rank, world):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64/f32", "data": "synthetic",
             "config": {"workload": args.workload, "text": CONFIG_TEXT[args.workload],
-                       "sample": f"2^{lg} elements per entry point per step (host arrays)"},
+                       "sample": f"2^{lg}-element host arrays per entry point, passes repeated for ~3 s "
+                                 f"of CPU work per step"},
             "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": threads, "kind": "port",
-                             "sample": f"{len(work)} entry points x 2^{lg} elements, oracle/vem_oracle.c "
-                                       f"(OpenMP, {threads} threads)", "per_function": per},
+                             "sample": f"{len(work)} entry points x 2^{lg}-element arrays, ~3 s of CPU work "
+                                       f"per step, oracle/vem_oracle.c (OpenMP, {threads} threads)",
+                             "per_function": per},
             "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -358,6 +367,10 @@ def main():
     launches0 = _lib.launch_count()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
+    # a short device-side spin ahead of the timed region keeps the GPU busy
+    # while the host enqueues the first launches, so host launch latency
+    # (Python + ctypes) does not appear as device idle time inside it
+    torch.cuda._sleep(int(2e6))
     t0.record(stream)
     for s in range(args.steps):
         step(evs[s])
@@ -431,16 +444,21 @@ def main():
     sleef = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
-        v, t, cn, per = cpu_oracle_rate(work, 23, threads)
+        v, t, cn, per = cpu_oracle_rate(work, 23, threads, budget_s=12.0)
         cpu = {"value": round(v, 4), "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"{len(work)} entry points x 2^23 elements of the same config domains "
-                         f"({t:.1f} s of CPU work), oracle/vem_oracle.c, OpenMP {threads} threads",
+               "sample": f"{len(work)} entry points x 2^23-element arrays of the same config domains, repeated "
+                         f"passes: {cn / 1e9:.2f} G elements in {t:.1f} s of CPU work, oracle/vem_oracle.c, "
+                         f"OpenMP {threads} threads",
                "per_function": per}
         try:
             sleef = cpu_sleef_rate(work, 23, threads)
         except Exception as ex:  # context only
             sleef = {"error": str(ex)}
 
+    ws = sum(t.numel() * t.element_size() for ins in cache.values() for t in ins) + \
+        sum(t.numel() * t.element_size() for t in outs.values())
+    l2_note = (f"no flush: per-step working set {ws / 2**20:.0f} MiB (distinct inputs {n}-element arrays + "
+               f"outputs) > 126 MB L2, each input re-read only after the other kernels' traffic")
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
@@ -448,7 +466,7 @@ def main():
                 "data": "synthetic (config-domain inputs generated on device, seeded)",
                 "config": {"workload": args.workload, "text": CONFIG_TEXT[args.workload],
                            "elements_per_entry_point_per_rank": n, "entry_points": [w[0] for w in work],
-                           "l2": "inputs >= 1 GiB per array (> 126 MB L2), no flush needed",
+                           "l2": l2_note,
                            "parallelism": f"data-parallel shards x{world} (no collective on the data path)"},
                 "gpu_launches": int(launches), "clocks": clk, "roofline": roofline,
                 "per_function": per_function, "e2e": e2e, "cpu_baseline": cpu, "sleef_cpu": sleef}
