@@ -46,13 +46,23 @@ __device__ __forceinline__ const double* stage_table(double* stab) {
     __syncthreads();
     return stab;
   } else {
-    const double* src = TABLE == kTableD ? gPhD : (TABLE == kTableF ? reinterpret_cast<const double*>(gPhF) : gLogExp);
-    constexpr int n2 = (TABLE == kTableLog ? kLogTabD : TableSize<TABLE>::n - kSinCosCoefN) / 2;
-    const double2* s2 = reinterpret_cast<const double2*>(src);
-    double2* d2 = reinterpret_cast<double2*>(stab);
-    for (int i = threadIdx.x; i < n2; i += blockDim.x) d2[i] = __ldg(s2 + i);
-    if constexpr (TABLE == kTableLog) {
-      for (int i = threadIdx.x; i < 256; i += blockDim.x) stab[kLtfInvc + i] = (double)__ldg(gLogTfInvc + i);
+    if constexpr (TABLE == kTableLog) {  // SoA global -> record layout (vem_math.cuh)
+      for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+        reinterpret_cast<double2*>(stab + kSlLogIH)[i] = make_double2(gLogExp[kLtInvc + i], gLogExp[kLtHi + i]);
+        stab[kSlLogLo + i] = gLogExp[kLtLo + i];
+        reinterpret_cast<double2*>(stab + kSlLogF)[i] =
+            make_double2((double)__ldg(gLogTfInvc + i), gLogExp[kLtfHi + i]);
+        if (i < 128) {
+          reinterpret_cast<double2*>(stab + kSlExp)[i] = make_double2(gLogExp[kLtExpHi + i], gLogExp[kLtExpLo + i]);
+          stab[kSlExpHi + i] = gLogExp[kLtExpHi + i];
+        }
+      }
+    } else {
+      const double* src = TABLE == kTableD ? gPhD : reinterpret_cast<const double*>(gPhF);
+      constexpr int n2 = (TableSize<TABLE>::n - kSinCosCoefN) / 2;
+      const double2* s2 = reinterpret_cast<const double2*>(src);
+      double2* d2 = reinterpret_cast<double2*>(stab);
+      for (int i = threadIdx.x; i < n2; i += blockDim.x) d2[i] = __ldg(s2 + i);
     }
     if constexpr (TABLE == kTableD || TABLE == kTableF) {  // per-lane coefficient sets (sin | cos)
       const double* cs = TABLE == kTableD ? gSinCosD : gSinCosF;

@@ -116,12 +116,19 @@ __device__ const double gSinCosF[kSinCosCoefN] = {
 __device__ const double gPhD[4 * VEM_PH_D_ENTRIES] = {VEM_PH_D_INIT};
 __device__ __align__(16) const uint32_t gPhF[4 * VEM_PH_F_ENTRIES] = {VEM_PH_F_INIT};
 constexpr int kPhFDoubles = 2 * VEM_PH_F_ENTRIES;  // staged size of gPhF in doubles
-// log / exp tables (tools/genlogtables.py), structure of arrays, staged into
-// one shared-memory block (offsets in doubles):
-constexpr int kLtInvc = 0, kLtHi = 256, kLtLo = 512, kLtExpHi = 768, kLtExpLo = 896, kLtfHi = 1024,
-              kLtfInvc = 1280;  // 256 binary32 invc, widened to binary64 when staged
-constexpr int kLogTabD = 1280;
-constexpr int kLogTabN = kLogTabD + 256;
+// log / exp tables (tools/genlogtables.py).  Global copy: structure of
+// arrays (offsets in doubles below).  Staged shared-memory block: dense
+// 16-byte pairs where a lookup needs two values (one LDS.128, no stride
+// gaps that would idle half of the banks), dense doubles otherwise:
+//   [kSlLogIH + 2 i] {invc, logc_hi}                 i < 256  (f64 log)
+//   [kSlLogLo + i]   logc_lo                         i < 256
+//   [kSlExp + 2 j]   {2^(j/128) hi, lo}              j < 128  (exp of pow_d)
+//   [kSlExpHi + j]   2^(j/128) hi                    j < 128  (f32 exp of pow_f)
+//   [kSlLogF + 2 i]  {(double)invc_f32, logc hi}     i < 256  (f32 log/pow)
+constexpr int kLtInvc = 0, kLtHi = 256, kLtLo = 512, kLtExpHi = 768, kLtExpLo = 896, kLtfHi = 1024;
+constexpr int kLogTabD = 1280;  // global SoA doubles (+ 256 binary32 invc)
+constexpr int kSlLogIH = 0, kSlLogLo = 512, kSlExp = 768, kSlExpHi = 1024, kSlLogF = 1152;
+constexpr int kLogTabN = 1664;  // staged doubles
 __device__ const double gLogExp[kLogTabD] = {VEM_LOGT_INVC_INIT VEM_LOGT_HI_INIT VEM_LOGT_LO_INIT
                                                  VEM_EXPT_HI_INIT VEM_EXPT_LO_INIT VEM_LOGTF_HI_INIT};
 __device__ const float gLogTfInvc[256] = {VEM_LOGTF_INVC_INIT};
@@ -490,14 +497,15 @@ __device__ __forceinline__ logred log_reduce(double a, double Eadj, const double
   long long k = (long long)tmp >> 52;
   int idx = (int)((tmp >> 44) & 255u);
   double m = from_bits_d(ix - ((uint64_t)k << 52));
-  double invc = lt[kLtInvc + idx];
+  const double2 ih = reinterpret_cast<const double2*>(lt + kSlLogIH)[idx];  // {invc, hi}
+  double invc = ih.x;
   double p = m * invc;
   logred o;
   o.rl = fma(m, invc, -p);
   o.rh = p - 1.0;
   o.E = kAdj ? (double)(int)k + Eadj : (double)(int)k;
-  o.logc_hi = lt[kLtHi + idx];
-  o.logc_lo = lt[kLtLo + idx];
+  o.logc_hi = ih.y;
+  o.logc_lo = lt[kSlLogLo + idx];
   return o;
 }
 
@@ -570,7 +578,8 @@ __device__ __forceinline__ double exp_dd_core(double th, double tl, const double
   double Q = poly<VEM_EXPJ_D_N>(cExpjD, r.hi);
   double s2 = z * fma(r.hi, Q, 0.5);
   double em1l = r.lo + fma(r.hi, r.lo, s2);
-  double Th = lt[kLtExpHi + (k & 127)], Tl = lt[kLtExpLo + (k & 127)];
+  const double2 T2 = reinterpret_cast<const double2*>(lt + kSlExp)[k & 127];
+  double Th = T2.x, Tl = T2.y;
   double u = fma(Th, r.hi, fma(Th, em1l, Tl));
   e = k >> 7;
   return Th + u;
@@ -862,10 +871,11 @@ __device__ __forceinline__ double log_f_internal(double a, const double* c, cons
   long long k = (long long)tmp >> 52;
   int idx = (int)((tmp >> 44) & 255u);
   double m = from_bits_d(ix - ((uint64_t)k << 52));
-  double r = fma(m, lt[kLtfInvc + idx], -1.0);  // == (double)invc_f32: exact product
+  const double2 ih = reinterpret_cast<const double2*>(lt + kSlLogF)[idx];  // {invc, hi}
+  double r = fma(m, ih.x, -1.0);  // == (double)invc_f32: exact product
   double Q = poly<N>(c, r);
   double L = fma(r * r, Q, r);
-  return fma((double)(int)k, ccLn2Hi, lt[kLtfHi + idx] + L);
+  return fma((double)(int)k, ccLn2Hi, ih.y + L);
 }
 // Same values from the binary32 bits (positive NORMAL x only): bits(0.75f) =
 // 0x3f400000 and the 23-bit mantissa offset give the identical k, idx and m
@@ -877,10 +887,11 @@ __device__ __forceinline__ double log_f_internal_f(float x, const double* c, con
   int k = (int)t >> 23;
   int idx = (int)((t >> 15) & 255u);
   double m = (double)from_bits_f(ux - ((uint32_t)k << 23));
-  double r = fma(m, lt[kLtfInvc + idx], -1.0);
+  const double2 ih = reinterpret_cast<const double2*>(lt + kSlLogF)[idx];
+  double r = fma(m, ih.x, -1.0);
   double Q = poly<N>(c, r);
   double L = fma(r * r, Q, r);
-  return fma((double)k, ccLn2Hi, lt[kLtfHi + idx] + L);
+  return fma((double)k, ccLn2Hi, ih.y + L);
 }
 __device__ __forceinline__ bool is_pos_normal_f(float x) { return bits_f(x) - 0x00800000u < 0x7f000000u; }
 
@@ -906,7 +917,7 @@ __device__ __forceinline__ double exp_f_internal(double t, const double* __restr
   double r = fma(kd, -ccExpjL1, t);
   r = fma(kd, -ccExpjL2, r);
   double p = fma(r * r, fma(r, ccSixth, 0.5), r);
-  double T = lt[kLtExpHi + (k & 127)];
+  double T = lt[kSlExpHi + (k & 127)];
   double R = fma(T, p, T);
   return __hiloint2double(__double2hiint(R) + ((k >> 7) << 20), __double2loint(R));
 }
