@@ -48,13 +48,15 @@ WORKLOADS = {
     "cfg5": [("sin_d_u10", 5), ("cos_d_u10", 5), ("tan_d_u10", 5), ("atan_d_u10", 5), ("exp_d_u10", 5),
              ("log_d_u10", 5), ("pow_d_u10", 5), ("fmod_d", 5)],
 }
-LOG2N = {"cfg1": 24, "cfg2": 28, "cfg3": 28, "cfg4": 26, "cfg5": 28}
+LOG2N = {"cfg1": 24, "cfg2": 28, "cfg3": 28, "cfg4": 26, "cfg5": 31}
+STRONG = {"cfg5"}  # configs whose element count is the job total (sharded), not per rank
 CONFIG_TEXT = {
     "cfg1": "sin/cos f64 u10, 2^24 x U[-pi,pi] (Cody-Waite path)",
     "cfg2": "exp/log/pow x f32/f64 x u10/u35, 2^28 elements each (BASELINE configs[1] domains)",
     "cfg3": "sin/cos/tan u10 f64+f32, 2^28, |x| log-U[1,1e300]/[1,3e38] +-, forced Payne-Hanek",
     "cfg4": "fmod f64+f32, 2^26 pairs, log-U[1e-300,1e300]/[1e-37,3e38] +-",
-    "cfg5": "8 fns f64 u10, log-U[1e-300,1e300] +- with 1% specials (per-rank 2^28 shard)",
+    "cfg5": "2^31 f64 elements (one shared x array; pow y U[-30,30], fmod y log-U) sharded over the ranks, "
+            "through sin/cos/tan/atan/exp/log/pow/fmod u10; log-U[1e-300,1e300] +- with 1% specials",
 }
 
 
@@ -127,6 +129,23 @@ def device_inputs(fn_name: str, cfg: int, n: int, dev, seed: int):
     if dt == torch.float32:
         xs = [torch.clamp(v, -3.4028234663852886e38, 3.4028234663852886e38).to(dt) for v in xs]
     return [v.to(dt).contiguous() for v in xs]
+
+
+def device_inputs_cfg5(n: int, dev, seed: int, chunk_log2: int = 26):
+    """Config 5: ONE x array (log-U[1e-300,1e300] +-, 1% specials) shared by
+    all eight functions, plus pow's y (U[-30,30]) and fmod's y (same law as
+    x); generated on the device in 2^chunk_log2 chunks to bound temporaries."""
+    import torch
+    x = torch.empty(n, dtype=torch.float64, device=dev)
+    ypow = torch.empty_like(x)
+    yfm = torch.empty_like(x)
+    step = 1 << chunk_log2
+    for c, i in enumerate(range(0, n, step)):
+        m = min(step, n - i)
+        x[i:i + m] = device_inputs("sin_d_u10", 5, m, dev, seed + 1000003 * c)[0]
+        ypow[i:i + m] = device_inputs("pow_d_u10", 5, m, dev, seed + 1000003 * c + 1)[1]
+        yfm[i:i + m] = device_inputs("fmod_d", 5, m, dev, seed + 1000003 * c + 2)[1]
+    return x, ypow, yfm
 
 
 # --------------------------------------------------------------- clocks
@@ -327,11 +346,22 @@ def main():
         keep = set(args.only.split(","))
         work = [w for w in work if w[0] in keep]
     n = 1 << (args.log2n or LOG2N[args.workload])
+    strong = args.workload in STRONG
+    if strong:  # job-total element count, contiguous shard per rank
+        n = n // world
 
     # resident inputs (u10/u35 of one function share inputs)
     cache = {}
     bufs = []
+    if args.workload == "cfg5":
+        x5, ypow5, yfm5 = device_inputs_cfg5(n, dev, seed=0x5EEF0050 + 7919 * rank)
+        cache = {"x": [x5], "ypow": [ypow5], "yfmod": [yfm5]}
+        l_x, l_pow, l_fmod = [x5], [x5, ypow5], [x5, yfm5]  # shared lists: e2e uploads x once
     for name, cfg in work:
+        if args.workload == "cfg5":
+            fn = name.split("_")[0]
+            bufs.append(l_pow if fn == "pow" else (l_fmod if fn == "fmod" else l_x))
+            continue
         base = name.replace("_u35", "_u10") if "_u35" in name else name
         key = (base.split("_")[0], base.split("_")[1], cfg)
         if key not in cache:
@@ -462,7 +492,7 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64/f32 (per entry point)",
+                "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f64/f32 (per entry point)",
                 "data": "synthetic (config-domain inputs generated on device, seeded)",
                 "config": {"workload": args.workload, "text": CONFIG_TEXT[args.workload],
                            "elements_per_entry_point_per_rank": n, "entry_points": [w[0] for w in work],
