@@ -120,12 +120,15 @@ def main():
         f.write("\nTop opcodes per element (thread instructions):\n\n")
         for n, d in out.items():
             f.write(f"- {n}: " + ", ".join(f"{o} {v}" for o, v in list(d.get('mix_per_elem', {}).items())[:14]) + "\n")
-    km_path = os.path.join(ROOT, "profiles", "kernel_metrics.json")
-    km = json.load(open(km_path)) if os.path.exists(km_path) else {}
-    for n, d in out.items():
-        km[n] = {"dram_bytes_per_elem": d["dram_bytes_per_elem"], "fp64_inst_per_elem": d.get("fp64_inst_per_elem"),
-                 "inst_per_elem": d["inst_per_elem"], "source": os.path.basename(prefix)}
-    json.dump(km, open(km_path, "w"), indent=1, sort_keys=True)
+    # only summaries written under profiles/ feed the bench's metrics file
+    if os.path.abspath(prefix).startswith(os.path.join(ROOT, "profiles") + os.sep):
+        km_path = os.path.join(ROOT, "profiles", "kernel_metrics.json")
+        km = json.load(open(km_path)) if os.path.exists(km_path) else {}
+        for n, d in out.items():
+            km[n] = {"dram_bytes_per_elem": d["dram_bytes_per_elem"],
+                     "fp64_inst_per_elem": d.get("fp64_inst_per_elem"),
+                     "inst_per_elem": d["inst_per_elem"], "source": os.path.basename(prefix)}
+        json.dump(km, open(km_path, "w"), indent=1, sort_keys=True)
     print(open(prefix + ".md").read())
 
 
