@@ -266,14 +266,28 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
           if constexpr (NIN == 2) ye[v * W + k] = vget(vb[v], k);
         }
       bool same = true;
+      bool uniform = false;
+      int c_l0 = -1;
+      if constexpr (HasCw1<Op>::value) {
+        // cheap first test: every element of the warp in the CW1 range
+        bool small = true;
 #pragma unroll
-      for (int e = 0; e < NE; e++) {
-        if constexpr (NIN == 2) cl[e] = Op::cls(xe[e], ye[e]);
-        else cl[e] = Op::cls(xe[e]);
-        same = same && (cl[e] == cl[0]);
+        for (int e = 0; e < NE; e++) small = small && Op::is_cw1(xe[e]);
+        if (__all_sync(0xffffffffu, small)) {
+          uniform = true;
+          c_l0 = 0;
+        }
       }
-      const int c_l0 = __shfl_sync(0xffffffffu, cl[0], 0);
-      const bool uniform = __all_sync(0xffffffffu, same && cl[0] == c_l0);
+      if (!uniform) {
+#pragma unroll
+        for (int e = 0; e < NE; e++) {
+          if constexpr (NIN == 2) cl[e] = Op::cls(xe[e], ye[e]);
+          else cl[e] = Op::cls(xe[e]);
+          same = same && (cl[e] == cl[0]);
+        }
+        c_l0 = __shfl_sync(0xffffffffu, cl[0], 0);
+        uniform = __all_sync(0xffffffffu, same && cl[0] == c_l0);
+      }
       auto regroup = [&]() {
         // counting sort of the warp's 32*NE elements by class, heaviest
         // class first: ballots per (row, class), prefix popcounts
@@ -586,6 +600,7 @@ __global__ void __launch_bounds__(kFmodWarps * 32, MINB) k_fmod(const T* __restr
       return FN<kCw1>(x, gPhD __VA_ARGS__);                                              \
     }                                                                                    \
     __device__ __forceinline__ static int cls(double x) { return trig_class(x); }      \
+    __device__ __forceinline__ static bool is_cw1(double x) { return trig_is_cw1(x); } \
   };                                                                                     \
   template <> struct SortsByClass<NAME> {                                                \
     static constexpr bool value = true;                                                  \

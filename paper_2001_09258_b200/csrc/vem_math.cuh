@@ -323,6 +323,11 @@ __device__ __forceinline__ red ph(double x_in, const double* __restrict__ tab) {
   return o;
 }
 
+// |x| < 15 (inside the CW1 range |x| <= 15) from the high word alone
+// (15 = 0x402E0000_00000000); |x| == 15 exactly is left to trig_class
+__device__ __forceinline__ bool trig_is_cw1(double x) {
+  return ((uint32_t)__double2hiint(x) & 0x7fffffffu) < 0x402E0000u;
+}
 // reduction path class of x: 0 = CW1 (|x| <= 15), 1 = CW2 (<= 1e14), 2 = PH
 __device__ __forceinline__ int trig_class(double x) {
   const uint64_t ab = bits_d(x) & 0x7fffffffffffffffull;
@@ -390,14 +395,16 @@ __device__ __forceinline__ double sin_d_u10(double x, const double* tab, const d
   double y = sincos_core_d(r.hi, r.lo, r.q & 1, coef);
   y = neg_if(y, r.q & 2);
   y = is_zero_bits(x) ? x : y;
-  return not_finite_bits(x) ? from_bits_d(kCanonNanD) : y;
+  if constexpr (kMode == kCw1) return y;  // |x| <= 15: finite
+  else return not_finite_bits(x) ? from_bits_d(kCanonNanD) : y;
 }
 template <int kMode>
 __device__ __forceinline__ double cos_d_u10(double x, const double* tab, const double* coef) {
   red r = reduce_mode<kMode>(x, tab);
   double y = sincos_core_d(r.hi, r.lo, (r.q & 1) ^ 1, coef);
   y = neg_if(y, (r.q + 1) & 2);
-  return not_finite_bits(x) ? from_bits_d(kCanonNanD) : y;
+  if constexpr (kMode == kCw1) return y;
+  else return not_finite_bits(x) ? from_bits_d(kCanonNanD) : y;
 }
 
 __device__ __forceinline__ double tan_core_d(double rh, double rl, int odd) {

@@ -176,3 +176,18 @@ def test_tma_pipeline_vs_plain_kernel(cuda, name):
         del got
     del ref, base
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("name", ["sin_d_u10", "cos_d_u10", "tan_d_u10"])
+def test_cw1_boundary_in_small_warps(cuda, name):
+    """Warps whose elements are all |x| < 15 take the branch-free CW1 body;
+    |x| == 15 (still CW1 per reduction.hpp:189) and the next doubles above
+    (CW2) must fall back to the selector without changing any result."""
+    from paper_2001_09258_b200 import inputs as I
+    n = 1 << 16
+    x = I.uniform(77, n, -14.9, 14.9, np.float64)
+    edge = np.array([15.0, -15.0, np.nextafter(15.0, 0.0), np.nextafter(15.0, 16.0), -np.nextafter(15.0, 16.0),
+                     14.999999999999998], dtype=np.float64)
+    idx = np.arange(0, n, 997)
+    x[idx] = edge[np.arange(idx.size) % edge.size]
+    _assert_bit_exact(name, _gpu(name, x), oracle_eval(name, x), x)
