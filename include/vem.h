@@ -77,6 +77,37 @@ int vem_pow_f_u10(const float* x, const float* y2, float* out, size_t n, vem_str
 int vem_pow_f_u35(const float* x, const float* y2, float* out, size_t n, vem_stream_t s);
 int vem_fmod_f(const float* x, const float* y2, float* out, size_t n, vem_stream_t s);
 
+/* ---- SURVEY.md §8(f).1 additions ---------------------------------------
+ * u35 trig/atan (SPEC.md DESIGN DECISIONS: same reductions, shorter
+ * polynomials, single-double reconstruction), asin/acos,
+ * atan2(y, x) (x2 = x, first operand = y), fdim
+ * (exact).  Float32 variants evaluate binary64 internals;
+ * the f32 u35 trig entry points are the u10 kernels (already <= 0.5001 ulp;
+ * the reduction dominates their cost). */
+int vem_sin_d_u35(const double* x, double* y, size_t n, vem_stream_t s);
+int vem_cos_d_u35(const double* x, double* y, size_t n, vem_stream_t s);
+int vem_tan_d_u35(const double* x, double* y, size_t n, vem_stream_t s);
+int vem_atan_d_u35(const double* x, double* y, size_t n, vem_stream_t s);
+int vem_asin_d_u10(const double* x, double* y, size_t n, vem_stream_t s);
+int vem_asin_d_u35(const double* x, double* y, size_t n, vem_stream_t s);
+int vem_acos_d_u10(const double* x, double* y, size_t n, vem_stream_t s);
+int vem_acos_d_u35(const double* x, double* y, size_t n, vem_stream_t s);
+int vem_atan2_d_u10(const double* y, const double* x, double* out, size_t n, vem_stream_t s);
+int vem_atan2_d_u35(const double* y, const double* x, double* out, size_t n, vem_stream_t s);
+int vem_fdim_d(const double* x, const double* y2, double* out, size_t n, vem_stream_t s);
+int vem_sin_f_u35(const float* x, float* y, size_t n, vem_stream_t s);
+int vem_cos_f_u35(const float* x, float* y, size_t n, vem_stream_t s);
+int vem_tan_f_u35(const float* x, float* y, size_t n, vem_stream_t s);
+int vem_atan_f_u10(const float* x, float* y, size_t n, vem_stream_t s);
+int vem_atan_f_u35(const float* x, float* y, size_t n, vem_stream_t s);
+int vem_asin_f_u10(const float* x, float* y, size_t n, vem_stream_t s);
+int vem_asin_f_u35(const float* x, float* y, size_t n, vem_stream_t s);
+int vem_acos_f_u10(const float* x, float* y, size_t n, vem_stream_t s);
+int vem_acos_f_u35(const float* x, float* y, size_t n, vem_stream_t s);
+int vem_atan2_f_u10(const float* y, const float* x, float* out, size_t n, vem_stream_t s);
+int vem_atan2_f_u35(const float* y, const float* x, float* out, size_t n, vem_stream_t s);
+int vem_fdim_f(const float* x, const float* y2, float* out, size_t n, vem_stream_t s);
+
 /* ---- reduction entry points (parity anchors) ------------------------- */
 /* trig_reduce<ScalarFmaDet> (reduction.hpp:189-206): r = hi + lo, q = quadrant mod 4 */
 int vem_trig_reduce_d(const double* x, double* r_hi, double* r_lo, int* q, size_t n, vem_stream_t s);

@@ -43,10 +43,19 @@ VEM_UNARY_PAIR(exp_det, vem_exp_d_u10, vem_exp_f_u10)
 VEM_UNARY_PAIR(log, vem_log_d_u10, vem_log_f_u10)
 VEM_UNARY_PAIR(log_u35, vem_log_d_u35, vem_log_f_u35)
 VEM_UNARY_PAIR(log_det, vem_log_d_u10, vem_log_f_u10)
+VEM_UNARY_PAIR(sin_u35, vem_sin_d_u35, vem_sin_f_u35)
+VEM_UNARY_PAIR(cos_u35, vem_cos_d_u35, vem_cos_f_u35)
+VEM_UNARY_PAIR(tan_u35, vem_tan_d_u35, vem_tan_f_u35)
+VEM_UNARY_PAIR(atan, vem_atan_d_u10, vem_atan_f_u10)
+VEM_UNARY_PAIR(atan_u35, vem_atan_d_u35, vem_atan_f_u35)
+VEM_UNARY_PAIR(atan_det, vem_atan_d_u10, vem_atan_f_u10)
+VEM_UNARY_PAIR(asin, vem_asin_d_u10, vem_asin_f_u10)
+VEM_UNARY_PAIR(asin_u35, vem_asin_d_u35, vem_asin_f_u35)
+VEM_UNARY_PAIR(asin_det, vem_asin_d_u10, vem_asin_f_u10)
+VEM_UNARY_PAIR(acos, vem_acos_d_u10, vem_acos_f_u10)
+VEM_UNARY_PAIR(acos_u35, vem_acos_d_u35, vem_acos_f_u35)
+VEM_UNARY_PAIR(acos_det, vem_acos_d_u10, vem_acos_f_u10)
 #undef VEM_UNARY_PAIR
-
-inline int atan(const double* x, double* y, size_t n, stream_t s = nullptr) { return vem_atan_d_u10(x, y, n, s); }
-inline int atan_det(const double* x, double* y, size_t n, stream_t s = nullptr) { return vem_atan_d_u10(x, y, n, s); }
 
 #define VEM_BINARY_PAIR(NAME, DFN, FFN)                                                                  \
   inline int NAME(const double* x, const double* y, double* o, size_t n, stream_t s = nullptr) {        \
@@ -60,6 +69,11 @@ VEM_BINARY_PAIR(pow_u35, vem_pow_d_u35, vem_pow_f_u35)
 VEM_BINARY_PAIR(pow_det, vem_pow_d_u10, vem_pow_f_u10)
 VEM_BINARY_PAIR(fmod, vem_fmod_d, vem_fmod_f)
 VEM_BINARY_PAIR(fmod_det, vem_fmod_d, vem_fmod_f)
+VEM_BINARY_PAIR(atan2, vem_atan2_d_u10, vem_atan2_f_u10)  // atan2(y, x): first operand y
+VEM_BINARY_PAIR(atan2_u35, vem_atan2_d_u35, vem_atan2_f_u35)
+VEM_BINARY_PAIR(atan2_det, vem_atan2_d_u10, vem_atan2_f_u10)
+VEM_BINARY_PAIR(fdim, vem_fdim_d, vem_fdim_f)
+VEM_BINARY_PAIR(fdim_det, vem_fdim_d, vem_fdim_f)
 #undef VEM_BINARY_PAIR
 
 // reduction.hpp:189 trig_reduce / reduction.hpp:148 cody_waite_reduce /

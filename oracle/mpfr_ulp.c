@@ -39,8 +39,12 @@ extern int mpfr_sgn(const mpfr_s*);
 extern int mpfr_cmpabs(const mpfr_s*, const mpfr_s*);
 extern int mpfr_set_ui_2exp(mpfr_s*, unsigned long, long, rnd_t);
 extern int mpfr_abs(mpfr_s*, const mpfr_s*, rnd_t);
+extern int mpfr_asin(mpfr_s*, const mpfr_s*, rnd_t);
+extern int mpfr_acos(mpfr_s*, const mpfr_s*, rnd_t);
+extern int mpfr_atan2(mpfr_s*, const mpfr_s*, const mpfr_s*, rnd_t);
+extern int mpfr_dim(mpfr_s*, const mpfr_s*, const mpfr_s*, rnd_t);
 
-enum { F_SIN = 0, F_COS, F_TAN, F_ATAN, F_EXP, F_LOG, F_POW, F_FMOD };
+enum { F_SIN = 0, F_COS, F_TAN, F_ATAN, F_EXP, F_LOG, F_POW, F_FMOD, F_ASIN, F_ACOS, F_ATAN2, F_FDIM };
 
 #define PREC 320
 
@@ -54,6 +58,10 @@ static void eval(int fn, mpfr_s* r, mpfr_s* a, mpfr_s* b) {
     case F_LOG: mpfr_log(r, a, RNDN); break;
     case F_POW: mpfr_pow(r, a, b, RNDN); break;
     case F_FMOD: mpfr_fmod(r, a, b, RNDN); break;
+    case F_ASIN: mpfr_asin(r, a, RNDN); break;
+    case F_ACOS: mpfr_acos(r, a, RNDN); break;
+    case F_ATAN2: mpfr_atan2(r, a, b, RNDN); break;
+    case F_FDIM: mpfr_dim(r, a, b, RNDN); break;
   }
 }
 

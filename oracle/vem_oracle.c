@@ -407,7 +407,10 @@ double vo_atan_d_u10(double x) {
   dd_t nn, dn;
   nn.hi = c2 ? -1.0 : (c1 ? ns.hi : a);
   nn.lo = c2 ? 0.0 : (c1 ? ns.lo : 0.0);
-  dn.hi = c2 ? a : (c1 ? ds.hi : 1.0);
+  /* |x| >= 2^60 gives RN(pi/2 - 1/|x|) = pi/2 exactly like |x| = 2^60, and
+   * keeps 1/|x| normal (a subnormal reciprocal takes the GPU division's
+   * slow path) */
+  dn.hi = c2 ? fmin(a, 0x1p60) : (c1 ? ds.hi : 1.0);
   dn.lo = c2 ? 0.0 : (c1 ? ds.lo : 0.0);
   dd_t b = dd_div(nn, dn);
   double z = b.hi * b.hi;
@@ -880,6 +883,217 @@ float vo_fmod_f(float x, float y) {
   return canon_f((float)r);
 }
 
+/* ============================ SURVEY §8(f).1: fdim, atan2, asin/acos, u35
+ * trig/atan (u35 recipe: "same reductions with shorter
+ * polynomials and single-double reconstruction", SPEC.md DESIGN DECISIONS).
+ * Float32 versions evaluate the binary64 routine and round once. */
+static const double C_ASIN_D[] = VEM_ASIN_D_ARR;
+static const double C_ASIN_D_U35[] = VEM_ASIN_D_U35_ARR;
+static const double C_SIN_D_U35[] = VEM_SIN_D_U35_ARR;
+static const double C_COS_D_U35[] = VEM_COS_D_U35_ARR;
+static const double C_ATAN_D_U35[] = VEM_ATAN_D_U35_ARR;
+#define K_PI_HI 0x1.921fb54442d18p+1
+#define K_PI_LO 0x1.1a62633145c07p-53
+#define K_3PIO4_HI 0x1.2d97c7f3321d2p+1
+#define K_3PIO4_LO 0x1.a79394c9e8a0ap-54
+
+/* fdim: x - y if x > y, +0 otherwise; NaN if either is */
+double vo_fdim_d(double x, double y) {
+  double r = (x > y) ? x - y : 0.0;
+  return (x != x || y != y) ? from_bits_d(CANON_NAN_D) : r;
+}
+float vo_fdim_f(float x, float y) {
+  float r = (x > y) ? x - y : 0.0f;
+  return (x != x || y != y) ? from_bits_f(CANON_NAN_F) : r;
+}
+
+/* u35 sin/cos/tan: the u10 reduction, r = hi part only */
+static double sincos_core_d_u35(double r, int cosform) {
+  double z = r * r;
+  if (cosform) {
+    double P = poly(C_COS_D_U35, VEM_COS_D_U35_N, z);
+    return fma(z, fma(z, P, -0.5), 1.0);
+  }
+  double P = poly(C_SIN_D_U35, VEM_SIN_D_U35_N, z);
+  return fma(r * z, P, r);
+}
+double vo_sin_d_u35(double x) {
+  red_t r = trig_reduce(x);
+  double y = sincos_core_d_u35(r.hi, r.q & 1);
+  y = neg_if(y, r.q & 2);
+  y = (x == 0.0) ? x : y;
+  return canon_d(y);
+}
+double vo_cos_d_u35(double x) {
+  red_t r = trig_reduce(x);
+  double y = sincos_core_d_u35(r.hi, (r.q & 1) ^ 1);
+  y = neg_if(y, (r.q + 1) & 2);
+  return canon_d(y);
+}
+/* tan u35: half angle with the u10 polynomial and the reduction's low
+ * part folded in, one binary64 division for both quadrant parities */
+static double tan_core_d_u35(double rh, double rl, int odd) {
+  double h = rh * 0.5, hl = rl * 0.5;
+  double z = h * h;
+  double P = poly(C_TAN_D, VEM_TAN_D_N, z);
+  double t = h + fma(h * z, P, hl);
+  double num = t + t;
+  double den = fma(-t, t, 1.0);
+  double X = odd ? -den : num, Y = odd ? num : den;
+  return X / Y;
+}
+double vo_tan_d_u35(double x) {
+  red_t r = trig_reduce(x);
+  double y = tan_core_d_u35(r.hi, r.lo, r.q & 1);
+  y = (fabs(x) < 0x1p-27) ? x : y;
+  return canon_d(y);
+}
+/* atan u35: the u10 fold with binary64 division, no DD */
+double vo_atan_d_u35(double x) {
+  double a = fabs(x);
+  int c1 = a > K_TAN_PI8;
+  int c2 = a > K_TAN_3PI8;
+  double nn = c2 ? -1.0 : (c1 ? a - 1.0 : a);
+  double dn = c2 ? fmin(a, 0x1p60) : (c1 ? a + 1.0 : 1.0);  /* see vo_atan_d_u10 */
+  double b = nn / dn;
+  double z = b * b;
+  double P = poly(C_ATAN_D_U35, VEM_ATAN_D_U35_N, z);
+  double off = c2 ? K_PIO2_QD0 : (c1 ? K_PIO4_HI : 0.0);
+  double y = off + fma(b * z, P, b);
+  y = copysign_b(y, x);
+  return canon_d(y);
+}
+
+/* asin / acos (§5.3): |x| <= 1/2 directly,
+ * asin t = t + t z P(z), z = t^2; |x| > 1/2 by asin|x| = pi/2 - 2 asin(s),
+ * s = sqrt(z), z = (1-|x|)/2 exact.  u10 carries sqrt's rounding error as
+ * sl = (z - s^2)/(2s) (z - s^2 exact by FMA) and adds pi/2 in DD. */
+typedef struct { double a, z, s, sl, u; int big; } asin_parts_t;
+static asin_parts_t asin_parts(double x, const double* c, int n, int u10) {
+  asin_parts_t o;
+  o.a = fabs(x);
+  o.big = o.a > 0.5;
+  o.z = o.big ? (1.0 - o.a) * 0.5 : o.a * o.a;
+  o.s = sqrt(o.z);
+  double t = o.big ? o.s : o.a;
+  double P = poly(c, n, o.z);
+  o.u = (t * o.z) * P;
+  o.sl = 0.0;
+  if (u10) {
+    double e = fma(-o.s, o.s, o.z);
+    o.sl = (o.z == 0.0) ? 0.0 : e / (o.s + o.s);
+  }
+  return o;
+}
+double vo_asin_d_u10(double x) {
+  asin_parts_t p = asin_parts(x, C_ASIN_D, VEM_ASIN_D_N, 1);
+  dd_t h = two_sum(K_PIO2_QD0, -2.0 * p.s);
+  double yb = h.hi + (h.lo + (K_PIO2_QD1 - 2.0 * (p.sl + p.u)));
+  double y = p.big ? yb : p.a + p.u;
+  y = (p.a > 1.0) ? from_bits_d(CANON_NAN_D) : y;
+  return canon_d(copysign_b(y, x));
+}
+double vo_asin_d_u35(double x) {
+  asin_parts_t p = asin_parts(x, C_ASIN_D_U35, VEM_ASIN_D_U35_N, 0);
+  double yb = (K_PIO2_QD0 - 2.0 * p.s) + (K_PIO2_QD1 - 2.0 * p.u);
+  double y = p.big ? yb : p.a + p.u;
+  y = (p.a > 1.0) ? from_bits_d(CANON_NAN_D) : y;
+  return canon_d(copysign_b(y, x));
+}
+double vo_acos_d_u10(double x) {
+  asin_parts_t p = asin_parts(x, C_ASIN_D, VEM_ASIN_D_N, 1);
+  /* |x| <= 1/2: pi/2 - asin x;  x > 1/2: 2 asin s;  x < -1/2: pi - 2 asin s */
+  double us = copysign_b(p.u, x);
+  dd_t hs = two_sum(K_PIO2_QD0, -x);
+  double ys = hs.hi + (hs.lo + (K_PIO2_QD1 - us));
+  double yp = 2.0 * p.s + 2.0 * (p.sl + p.u);
+  dd_t hn = two_sum(K_PI_HI, -2.0 * p.s);
+  double yn = hn.hi + (hn.lo + (K_PI_LO - 2.0 * (p.sl + p.u)));
+  double y = p.big ? (x > 0.0 ? yp : yn) : ys;
+  y = (p.a > 1.0) ? from_bits_d(CANON_NAN_D) : y;
+  return canon_d(y);
+}
+double vo_acos_d_u35(double x) {
+  asin_parts_t p = asin_parts(x, C_ASIN_D_U35, VEM_ASIN_D_U35_N, 0);
+  double us = copysign_b(p.u, x);
+  double ys = (K_PIO2_QD0 - x) + (K_PIO2_QD1 - us);
+  double yp = 2.0 * (p.s + p.u);
+  double yn = (K_PI_HI - 2.0 * p.s) + (K_PI_LO - 2.0 * p.u);
+  double y = p.big ? (x > 0.0 ? yp : yn) : ys;
+  y = (p.a > 1.0) ? from_bits_d(CANON_NAN_D) : y;
+  return canon_d(y);
+}
+
+/* atan2: num = min(|x|,|y|), den = max(|x|,|y|) (scaled
+ * by a common power of two away from overflow / reciprocal underflow), the
+ * atan fold of num/den -- b = num/den or (num-den)/(num+den), one DD
+ * division -- then result = C + sigma * atan(b) with C in {0, pi/4, pi/2,
+ * 3pi/4, pi} (DD) and sigma = +-1 by (|y| > |x|, x < 0, fold), sign of y.
+ * C99 Annex F.9.1.4 special cases selected at the end. */
+static double atan2_special(double y, double x, double g) {
+  double ax = fabs(x), ay = fabs(y);
+  double r = g;
+  if (ax == INFINITY) r = (ay == INFINITY) ? (x > 0.0 ? K_PIO4_HI : K_3PIO4_HI) : (x > 0.0 ? 0.0 : K_PI_HI);
+  else if (ay == INFINITY) r = K_PIO2_QD0;
+  if (x == 0.0) r = (y == 0.0) ? ((bits_d(x) >> 63) ? K_PI_HI : 0.0) : K_PIO2_QD0;
+  else if (y == 0.0) r = (x > 0.0) ? 0.0 : K_PI_HI;
+  r = copysign_b(r, y);
+  return (x != x || y != y) ? from_bits_d(CANON_NAN_D) : r;
+}
+typedef struct { double num, den, ch, cl; int c1, sig; } atan2_parts_t;
+static atan2_parts_t atan2_parts(double y, double x) {
+  atan2_parts_t o;
+  double ax = fabs(x), ay = fabs(y);
+  int swap = ay > ax;
+  double num = swap ? ax : ay, den = swap ? ay : ax;
+  double sc = den >= 0x1p1000 ? 0x1p-100 : (den < 0x1p-900 ? 0x1p100 : 1.0);
+  o.num = num * sc;
+  o.den = den * sc;
+  o.c1 = o.num > K_TAN_PI8 * o.den;
+  int neg = x < 0.0;
+  /* C = (neg ? pi : 0) + (swap ? (neg ? -pi/2 : pi/2) : 0) + s * (c1 ? pi/4 : 0) */
+  int q = (neg ? 4 : 0) + (swap ? (neg ? -2 : 2) : 0);   /* multiples of pi/4 */
+  o.sig = (swap != neg) ? -1 : 1;
+  q += o.c1 ? o.sig : 0;
+  o.ch = q == 0 ? 0.0 : (q == 1 ? K_PIO4_HI : (q == 2 ? K_PIO2_QD0 : (q == 3 ? K_3PIO4_HI : K_PI_HI)));
+  o.cl = q == 0 ? 0.0 : (q == 1 ? K_PIO4_LO : (q == 2 ? K_PIO2_QD1 : (q == 3 ? K_3PIO4_LO : K_PI_LO)));
+  return o;
+}
+double vo_atan2_d_u10(double y, double x) {
+  atan2_parts_t p = atan2_parts(y, x);
+  dd_t ns = two_sum(p.num, -p.den), ds = two_sum(p.num, p.den);
+  dd_t nn = p.c1 ? ns : (dd_t){p.num, 0.0};
+  dd_t dn = p.c1 ? ds : (dd_t){p.den, 0.0};
+  dd_t b = dd_div(nn, dn);
+  double z = b.hi * b.hi;
+  double P = poly(C_ATAN_D, VEM_ATAN_D_N, z);
+  double corr = fma(b.hi * z, P, fma(-b.lo, z, b.lo));
+  double sg = (double)p.sig;
+  dd_t s = two_sum(p.ch, sg * b.hi);
+  double g = s.hi + (s.lo + (p.cl + sg * corr));
+  return canon_d(atan2_special(y, x, copysign_b(g, y)));
+}
+double vo_atan2_d_u35(double y, double x) {
+  atan2_parts_t p = atan2_parts(y, x);
+  double nn = p.c1 ? p.num - p.den : p.num;
+  double dn = p.c1 ? p.num + p.den : p.den;
+  double b = nn * (1.0 / dn);  /* 1/dn normal after scaling; a tiny quotient stays off the division slow path */
+  double z = b * b;
+  double P = poly(C_ATAN_D_U35, VEM_ATAN_D_U35_N, z);
+  double g = p.ch + (double)p.sig * fma(b * z, P, b);
+  return canon_d(atan2_special(y, x, copysign_b(g, y)));
+}
+
+/* float32: binary64 routine, one rounding */
+float vo_atan_f_u10(float x) { return canon_f((float)vo_atan_d_u10((double)x)); }
+float vo_atan_f_u35(float x) { return canon_f((float)vo_atan_d_u35((double)x)); }
+float vo_asin_f_u10(float x) { return canon_f((float)vo_asin_d_u10((double)x)); }
+float vo_asin_f_u35(float x) { return canon_f((float)vo_asin_d_u35((double)x)); }
+float vo_acos_f_u10(float x) { return canon_f((float)vo_acos_d_u10((double)x)); }
+float vo_acos_f_u35(float x) { return canon_f((float)vo_acos_d_u35((double)x)); }
+float vo_atan2_f_u10(float y, float x) { return canon_f((float)vo_atan2_d_u10((double)y, (double)x)); }
+float vo_atan2_f_u35(float y, float x) { return canon_f((float)vo_atan2_d_u35((double)y, (double)x)); }
+
 /* ============================================ exported array API */
 void vo_trig_reduce_d(const double* x, double* hi, double* lo, int* q, size_t n) {
   for (size_t i = 0; i < n; i++) {
@@ -944,6 +1158,26 @@ UNARY_ARR(vo_log_f_u35, float)
 BINARY_ARR(vo_pow_f_u10, float)
 BINARY_ARR(vo_pow_f_u35, float)
 BINARY_ARR(vo_fmod_f, float)
+UNARY_ARR(vo_sin_d_u35, double)
+UNARY_ARR(vo_cos_d_u35, double)
+UNARY_ARR(vo_tan_d_u35, double)
+UNARY_ARR(vo_atan_d_u35, double)
+UNARY_ARR(vo_asin_d_u10, double)
+UNARY_ARR(vo_asin_d_u35, double)
+UNARY_ARR(vo_acos_d_u10, double)
+UNARY_ARR(vo_acos_d_u35, double)
+BINARY_ARR(vo_atan2_d_u10, double)
+BINARY_ARR(vo_atan2_d_u35, double)
+BINARY_ARR(vo_fdim_d, double)
+UNARY_ARR(vo_atan_f_u10, float)
+UNARY_ARR(vo_atan_f_u35, float)
+UNARY_ARR(vo_asin_f_u10, float)
+UNARY_ARR(vo_asin_f_u35, float)
+UNARY_ARR(vo_acos_f_u10, float)
+UNARY_ARR(vo_acos_f_u35, float)
+BINARY_ARR(vo_atan2_f_u10, float)
+BINARY_ARR(vo_atan2_f_u35, float)
+BINARY_ARR(vo_fdim_f, float)
 
 /* fmod iteration count (for the step-curve property) */
 int vo_fmod_d_iters(double x, double y) {
@@ -966,3 +1200,7 @@ double vo_dbg_exp_dd(double th, double tl) {
 void vo_sin_f_u10_ph_arr(const float* x, float* y, size_t n) { vo_sin_f_u10_arr(x, y, n); }
 void vo_cos_f_u10_ph_arr(const float* x, float* y, size_t n) { vo_cos_f_u10_arr(x, y, n); }
 void vo_tan_f_u10_ph_arr(const float* x, float* y, size_t n) { vo_tan_f_u10_arr(x, y, n); }
+/* f32 u35 trig entry points are the u10 kernels (vem.h §8(f).1 note) */
+void vo_sin_f_u35_arr(const float* x, float* y, size_t n) { vo_sin_f_u10_arr(x, y, n); }
+void vo_cos_f_u35_arr(const float* x, float* y, size_t n) { vo_cos_f_u10_arr(x, y, n); }
+void vo_tan_f_u35_arr(const float* x, float* y, size_t n) { vo_tan_f_u10_arr(x, y, n); }

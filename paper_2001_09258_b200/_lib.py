@@ -21,10 +21,18 @@ UNARY = {
     "sin_f_u10": "f", "cos_f_u10": "f", "tan_f_u10": "f",
     "sin_f_u10_ph": "f", "cos_f_u10_ph": "f", "tan_f_u10_ph": "f",
     "exp_f_u10": "f", "exp_f_u35": "f", "log_f_u10": "f", "log_f_u35": "f",
+    # u35 trig/atan, asin/acos, f32 atan
+    "sin_d_u35": "d", "cos_d_u35": "d", "tan_d_u35": "d", "atan_d_u35": "d",
+    "asin_d_u10": "d", "asin_d_u35": "d", "acos_d_u10": "d", "acos_d_u35": "d",
+    "sin_f_u35": "f", "cos_f_u35": "f", "tan_f_u35": "f", "atan_f_u10": "f", "atan_f_u35": "f",
+    "asin_f_u10": "f", "asin_f_u35": "f", "acos_f_u10": "f", "acos_f_u35": "f",
 }
 BINARY = {
     "pow_d_u10": "d", "pow_d_u35": "d", "fmod_d": "d",
     "pow_f_u10": "f", "pow_f_u35": "f", "fmod_f": "f",
+    # atan2 (first operand y), fdim
+    "atan2_d_u10": "d", "atan2_d_u35": "d", "fdim_d": "d",
+    "atan2_f_u10": "f", "atan2_f_u35": "f", "fdim_f": "f",
 }
 ALL = {**UNARY, **BINARY}
 

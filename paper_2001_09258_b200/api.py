@@ -26,7 +26,7 @@ def _entry(fn: str, acc: str, x: torch.Tensor, ph: bool = False) -> str:
     if x.dtype not in _SUFFIX:
         raise TypeError(f"vem.{fn}: dtype {x.dtype} unsupported (float32/float64)")
     p = _SUFFIX[x.dtype]
-    name = f"{fn}_{p}" if fn == "fmod" else f"{fn}_{p}_{acc}"
+    name = f"{fn}_{p}" if fn in ("fmod", "fdim") else f"{fn}_{p}_{acc}"
     if ph:
         name += "_ph"
     if name not in _lib.ALL:
@@ -84,6 +84,18 @@ log_u35 = _u("log", "u35")
 pow = pow_det = _b("pow")  # noqa: A001
 pow_u35 = _b("pow", "u35")
 fmod = fmod_det = _b("fmod")
+# SURVEY.md §8(f).1
+sin_u35 = _u("sin", "u35")
+cos_u35 = _u("cos", "u35")
+tan_u35 = _u("tan", "u35")
+atan_u35 = _u("atan", "u35")
+asin = asin_det = _u("asin")
+asin_u35 = _u("asin", "u35")
+acos = acos_det = _u("acos")
+acos_u35 = _u("acos", "u35")
+atan2 = atan2_det = _b("atan2")  # atan2(y, x)
+atan2_u35 = _b("atan2", "u35")
+fdim = fdim_det = _b("fdim")
 
 
 def trig_reduce(x: torch.Tensor, kind: str = "trig", level: int = 1):

@@ -41,6 +41,18 @@ const Entry kTable[] = {
     {"log_f_u10", 4, 0, (void*)vem_log_f_u10},       {"log_f_u35", 4, 0, (void*)vem_log_f_u35},
     {"pow_f_u10", 4, 1, (void*)vem_pow_f_u10},       {"pow_f_u35", 4, 1, (void*)vem_pow_f_u35},
     {"fmod_f", 4, 1, (void*)vem_fmod_f},
+    {"sin_d_u35", 8, 0, (void*)vem_sin_d_u35},       {"cos_d_u35", 8, 0, (void*)vem_cos_d_u35},
+    {"tan_d_u35", 8, 0, (void*)vem_tan_d_u35},       {"atan_d_u35", 8, 0, (void*)vem_atan_d_u35},
+    {"asin_d_u10", 8, 0, (void*)vem_asin_d_u10},     {"asin_d_u35", 8, 0, (void*)vem_asin_d_u35},
+    {"acos_d_u10", 8, 0, (void*)vem_acos_d_u10},     {"acos_d_u35", 8, 0, (void*)vem_acos_d_u35},
+    {"atan2_d_u10", 8, 1, (void*)vem_atan2_d_u10},   {"atan2_d_u35", 8, 1, (void*)vem_atan2_d_u35},
+    {"fdim_d", 8, 1, (void*)vem_fdim_d},
+    {"sin_f_u35", 4, 0, (void*)vem_sin_f_u35},       {"cos_f_u35", 4, 0, (void*)vem_cos_f_u35},
+    {"tan_f_u35", 4, 0, (void*)vem_tan_f_u35},       {"atan_f_u10", 4, 0, (void*)vem_atan_f_u10},
+    {"atan_f_u35", 4, 0, (void*)vem_atan_f_u35},     {"asin_f_u10", 4, 0, (void*)vem_asin_f_u10},
+    {"asin_f_u35", 4, 0, (void*)vem_asin_f_u35},     {"acos_f_u10", 4, 0, (void*)vem_acos_f_u10},
+    {"acos_f_u35", 4, 0, (void*)vem_acos_f_u35},     {"atan2_f_u10", 4, 1, (void*)vem_atan2_f_u10},
+    {"atan2_f_u35", 4, 1, (void*)vem_atan2_f_u35},   {"fdim_f", 4, 1, (void*)vem_fdim_f},
 };
 
 const Entry* find(const char* name) {

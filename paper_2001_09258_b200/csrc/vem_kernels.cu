@@ -26,14 +26,14 @@ static std::atomic<uint64_t> g_launches{0};
 // kTableDG: the f64 Payne-Hanek table is read from global memory (L1-resident,
 // __ldg) rather than staged: the 32 KB stage would cost occupancy on inputs
 // that never leave the Cody-Waite range.
-enum TableKind { kNoTable = 0, kTableD = 1, kTableF = 2, kTableLog = 3, kTableDG = 4 };
+enum TableKind { kNoTable = 0, kTableD = 1, kTableF = 2, kTableLog = 3, kTableDG = 4, kTableDG35 = 5 };
 
 template <int TABLE>
 struct TableSize {
   static constexpr int n = TABLE == kTableD   ? 4 * VEM_PH_D_ENTRIES + kSinCosCoefN
                            : TABLE == kTableF ? kPhFDoubles + kSinCosCoefN
                            : TABLE == kTableLog ? kLogTabN
-                           : TABLE == kTableDG ? kSinCosCoefN
+                           : (TABLE == kTableDG || TABLE == kTableDG35) ? kSinCosCoefN
                                                 : 2;
 };
 
@@ -41,8 +41,8 @@ template <int TABLE>
 __device__ __forceinline__ const double* stage_table(double* stab) {
   if constexpr (TABLE == kNoTable) {
     return nullptr;
-  } else if constexpr (TABLE == kTableDG) {
-    if (threadIdx.x < kSinCosCoefN) stab[threadIdx.x] = gSinCosD[threadIdx.x];
+  } else if constexpr (TABLE == kTableDG || TABLE == kTableDG35) {
+    if (threadIdx.x < kSinCosCoefN) stab[threadIdx.x] = (TABLE == kTableDG ? gSinCosD : gSinCosD35)[threadIdx.x];
     __syncthreads();
     return stab;
   } else {
@@ -611,11 +611,25 @@ __global__ void __launch_bounds__(kFmodWarps * 32, MINB) k_fmod(const T* __restr
 VEM_TRIG_OP(OpSinD, sin_d_u10, , tab)
 VEM_TRIG_OP(OpCosD, cos_d_u10, , tab)
 VEM_TRIG_OP(OpTanD, tan_d_u10)
+VEM_TRIG_OP(OpSinDU35, sin_d_u35, , tab)
+VEM_TRIG_OP(OpCosDU35, cos_d_u35, , tab)
+VEM_TRIG_OP(OpTanDU35, tan_d_u35)
 #undef VEM_TRIG_OP
 VEM_UNARY_OP(OpSinDPh, double, (sin_d_u10<kPh>(x, tab, tab + 4 * VEM_PH_D_ENTRIES)))
 VEM_UNARY_OP(OpCosDPh, double, (cos_d_u10<kPh>(x, tab, tab + 4 * VEM_PH_D_ENTRIES)))
 VEM_UNARY_OP(OpTanDPh, double, (tan_d_u10<kPh>(x, tab)))
 VEM_UNARY_OP(OpAtanD, double, ((void)tab, atan_d_u10(x)))
+VEM_UNARY_OP(OpAtanDU35, double, ((void)tab, atan_d_u35(x)))
+VEM_UNARY_OP(OpAsinD, double, ((void)tab, asin_d_u10(x)))
+VEM_UNARY_OP(OpAsinDU35, double, ((void)tab, asin_d_u35(x)))
+VEM_UNARY_OP(OpAcosD, double, ((void)tab, acos_d_u10(x)))
+VEM_UNARY_OP(OpAcosDU35, double, ((void)tab, acos_d_u35(x)))
+VEM_UNARY_OP(OpAtanF, float, ((void)tab, canon_f((float)atan_d_u10((double)x))))
+VEM_UNARY_OP(OpAtanFU35, float, ((void)tab, canon_f((float)atan_d_u35((double)x))))
+VEM_UNARY_OP(OpAsinF, float, ((void)tab, canon_f((float)asin_d_u10((double)x))))
+VEM_UNARY_OP(OpAsinFU35, float, ((void)tab, canon_f((float)asin_d_u35((double)x))))
+VEM_UNARY_OP(OpAcosF, float, ((void)tab, canon_f((float)acos_d_u10((double)x))))
+VEM_UNARY_OP(OpAcosFU35, float, ((void)tab, canon_f((float)acos_d_u35((double)x))))
 // SLOW: value for a flagged element (x, r = fast result, code); `full()`
 // is the out-of-line full function
 #define VEM_SPLIT_UNARY_OP(NAME, T, EXPR, FAST, SLOW)                                    \
@@ -697,6 +711,12 @@ template <> struct SortsByClass<OpFmodF> {
   static constexpr bool value = true;
   static constexpr int classes = kFmodClasses;
 };
+VEM_BINARY_OP(OpAtan2D, double, ((void)tab, atan2_d_u10(x, y)))
+VEM_BINARY_OP(OpAtan2DU35, double, ((void)tab, atan2_d_u35(x, y)))
+VEM_BINARY_OP(OpFdimD, double, ((void)tab, fdim_d(x, y)))
+VEM_BINARY_OP(OpAtan2F, float, ((void)tab, canon_f((float)atan2_d_u10((double)x, (double)y))))
+VEM_BINARY_OP(OpAtan2FU35, float, ((void)tab, canon_f((float)atan2_d_u35((double)x, (double)y))))
+VEM_BINARY_OP(OpFdimF, float, ((void)tab, fdim_f(x, y)))
 #undef VEM_BINARY_OP
 #undef VEM_SPLIT_BINARY_OP
 
@@ -951,6 +971,31 @@ int vem_fmod_f(const float* x, const float* y2, float* o, size_t n, vem_stream_t
   return VEM_STREAM<OpFmodF, float, 2, kNoTable, 2, 2, 4>(x, y2, o, n, s);
 #endif
 }
+
+// ---- SURVEY.md §8(f).1 additions
+int vem_sin_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpSinDU35, double, 1, kTableDG35, 2, 2, 3>(x, nullptr, y, n, s); }
+int vem_cos_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpCosDU35, double, 1, kTableDG35, 2, 2, 3>(x, nullptr, y, n, s); }
+int vem_tan_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpTanDU35, double, 1, kTableDG35, 2, 2, 3>(x, nullptr, y, n, s); }
+int vem_atan_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpAtanDU35, double, 1, kNoTable, 2, 2>(x, nullptr, y, n, s); }
+int vem_asin_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpAsinD, double, 1, kNoTable, 2, 2>(x, nullptr, y, n, s); }
+int vem_asin_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpAsinDU35, double, 1, kNoTable, 2, 2>(x, nullptr, y, n, s); }
+int vem_acos_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpAcosD, double, 1, kNoTable, 2, 2>(x, nullptr, y, n, s); }
+int vem_acos_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpAcosDU35, double, 1, kNoTable, 2, 2>(x, nullptr, y, n, s); }
+int vem_atan2_d_u10(const double* y, const double* x, double* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpAtan2D, double, 2, kNoTable, 2, 2>(y, x, o, n, s); }
+int vem_atan2_d_u35(const double* y, const double* x, double* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpAtan2DU35, double, 2, kNoTable, 2, 2>(y, x, o, n, s); }
+int vem_fdim_d(const double* x, const double* y2, double* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpFdimD, double, 2, kNoTable, 4, 2>(x, y2, o, n, s); }
+int vem_sin_f_u35(const float* x, float* y, size_t n, vem_stream_t s) { return vem_sin_f_u10(x, y, n, s); }
+int vem_cos_f_u35(const float* x, float* y, size_t n, vem_stream_t s) { return vem_cos_f_u10(x, y, n, s); }
+int vem_tan_f_u35(const float* x, float* y, size_t n, vem_stream_t s) { return vem_tan_f_u10(x, y, n, s); }
+int vem_atan_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpAtanF, float, 1, kNoTable, 1, 2>(x, nullptr, y, n, s); }
+int vem_atan_f_u35(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpAtanFU35, float, 1, kNoTable, 1, 2>(x, nullptr, y, n, s); }
+int vem_asin_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpAsinF, float, 1, kNoTable, 1, 2>(x, nullptr, y, n, s); }
+int vem_asin_f_u35(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpAsinFU35, float, 1, kNoTable, 1, 2>(x, nullptr, y, n, s); }
+int vem_acos_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpAcosF, float, 1, kNoTable, 1, 2>(x, nullptr, y, n, s); }
+int vem_acos_f_u35(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpAcosFU35, float, 1, kNoTable, 1, 2>(x, nullptr, y, n, s); }
+int vem_atan2_f_u10(const float* y, const float* x, float* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpAtan2F, float, 2, kNoTable, 1, 2>(y, x, o, n, s); }
+int vem_atan2_f_u35(const float* y, const float* x, float* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpAtan2FU35, float, 2, kNoTable, 1, 2>(y, x, o, n, s); }
+int vem_fdim_f(const float* x, const float* y2, float* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpFdimF, float, 2, kNoTable, 4, 2>(x, y2, o, n, s); }
 
 int vem_trig_reduce_d(const double* x, double* hi, double* lo, int* q, size_t n, vem_stream_t s) {
   return launch_reduce_d<0>(x, hi, lo, q, n, s);

@@ -112,6 +112,16 @@ __device__ const double gSinCosF[kSinCosCoefN] = {
     VEM_SIN_F_C0, VEM_SIN_F_C1, VEM_SIN_F_C2, VEM_SIN_F_C3, 0.0,          0.0, 0.0, 0.0,
     -0.5,         VEM_COS_F_C0, VEM_COS_F_C1, VEM_COS_F_C2, VEM_COS_F_C3, 0.0, 0.0, 0.0};
 
+// u35 sin | cos sets (cos: 5 terms + a zero leading coefficient, so the same
+// 6-step Horner gives the 5-term value exactly: fma(0, z, c4) == c4)
+__device__ const double gSinCosD35[kSinCosCoefN] = {
+    VEM_SIN_D_U35_C0, VEM_SIN_D_U35_C1, VEM_SIN_D_U35_C2, VEM_SIN_D_U35_C3, VEM_SIN_D_U35_C4, VEM_SIN_D_U35_C5,
+    0.0, 0.0,
+    VEM_COS_D_U35_C0, VEM_COS_D_U35_C1, VEM_COS_D_U35_C2, VEM_COS_D_U35_C3, VEM_COS_D_U35_C4, 0.0, 0.0, 0.0};
+__constant__ double cAtanDU35[] = VEM_ATAN_D_U35_ARR;
+__constant__ double cAsinD[] = VEM_ASIN_D_ARR;
+__constant__ double cAsinDU35[] = VEM_ASIN_D_U35_ARR;
+
 // Payne-Hanek tables (global copy; kernels stage them into shared memory).
 __device__ const double gPhD[4 * VEM_PH_D_ENTRIES] = {VEM_PH_D_INIT};
 __device__ __align__(16) const uint32_t gPhF[4 * VEM_PH_F_ENTRIES] = {VEM_PH_F_INIT};
@@ -439,7 +449,7 @@ __device__ __forceinline__ double atan_d_u10(double x) {
   dd nn, dn;
   nn.hi = c2 ? -1.0 : (c1 ? ns.hi : a);
   nn.lo = c2 ? 0.0 : (c1 ? ns.lo : 0.0);
-  dn.hi = c2 ? a : (c1 ? ds.hi : 1.0);
+  dn.hi = c2 ? fmin(a, 0x1p60) : (c1 ? ds.hi : 1.0);  // oracle: normal 1/|x|, same result
   dn.lo = c2 ? 0.0 : (c1 ? ds.lo : 0.0);
   dd b = dd_div(nn, dn);
   double z = b.hi * b.hi;
@@ -978,6 +988,192 @@ __device__ __forceinline__ float pow_f_u35(float x, float y, const double* lt) {
 __device__ __forceinline__ float fmod_f(float x, float y) {
   double r = fmod_core((double)x, (double)y);
   return canon_f((float)r);
+}
+
+// ============================ SURVEY §8(f).1 additions (oracle: same names)
+// fdim, u35 sin/cos/tan/atan, asin/acos, atan2; float32 through binary64.
+constexpr double kPiHi = 0x1.921fb54442d18p+1, kPiLo = 0x1.1a62633145c07p-53;
+constexpr double k3Pio4Hi = 0x1.2d97c7f3321d2p+1, k3Pio4Lo = 0x1.a79394c9e8a0ap-54;
+
+__device__ __forceinline__ double fdim_d(double x, double y) {
+  double r = (x > y) ? x - y : 0.0;
+  return (x != x || y != y) ? from_bits_d(kCanonNanD) : r;
+}
+__device__ __forceinline__ float fdim_f(float x, float y) {
+  float r = (x > y) ? x - y : 0.0f;
+  return (x != x || y != y) ? from_bits_f(kCanonNanF) : r;
+}
+
+// oracle: sincos_core_d_u35 (per-lane coefficient set from the staged block)
+__device__ __forceinline__ double sincos_core_d_u35(double r, int cosform, const double* coef) {
+  const bool cf = cosform != 0;
+  const double z = r * r;
+  const double2* cs = reinterpret_cast<const double2*>(coef + (cf ? 8 : 0));
+  const double2 c01 = cs[0], c23 = cs[1], c45 = cs[2];
+  const double P = fma(fma(fma(fma(fma(c45.y, z, c45.x), z, c23.y), z, c23.x), z, c01.y), z, c01.x);
+  const double A = cf ? z : r * z;
+  const double B = cf ? fma(z, P, -0.5) : P;
+  const double C = cf ? 1.0 : r;
+  return fma(A, B, C);
+}
+template <int kMode>
+__device__ __forceinline__ double sin_d_u35(double x, const double* tab, const double* coef) {
+  red r = reduce_mode<kMode>(x, tab);
+  double y = sincos_core_d_u35(r.hi, r.q & 1, coef);
+  y = neg_if(y, r.q & 2);
+  y = is_zero_bits(x) ? x : y;
+  if constexpr (kMode == kCw1) return y;
+  else return not_finite_bits(x) ? from_bits_d(kCanonNanD) : y;
+}
+template <int kMode>
+__device__ __forceinline__ double cos_d_u35(double x, const double* tab, const double* coef) {
+  red r = reduce_mode<kMode>(x, tab);
+  double y = sincos_core_d_u35(r.hi, (r.q & 1) ^ 1, coef);
+  y = neg_if(y, (r.q + 1) & 2);
+  if constexpr (kMode == kCw1) return y;
+  else return not_finite_bits(x) ? from_bits_d(kCanonNanD) : y;
+}
+__device__ __forceinline__ double tan_core_d_u35(double rh, double rl, int odd) {
+  const double h = rh * 0.5, hl = rl * 0.5;
+  const double z = h * h;
+  const double P = poly<VEM_TAN_D_N>(cTanD, z);
+  const double t = h + fma(h * z, P, hl);
+  const double num = t + t;
+  const double den = fma(-t, t, 1.0);
+  const bool o = odd != 0;
+  return (o ? -den : num) / (o ? num : den);
+}
+template <int kMode>
+__device__ __forceinline__ double tan_d_u35(double x, const double* tab) {
+  red r = reduce_mode<kMode>(x, tab);
+  double y = tan_core_d_u35(r.hi, r.lo, r.q & 1);
+  y = (fabs(x) < 0x1p-27) ? x : y;
+  return canon_d(y);
+}
+__device__ __forceinline__ double atan_d_u35(double x) {
+  const double a = fabs(x);
+  const bool c1 = a > kTanPi8;
+  const bool c2 = a > kTan3Pi8;
+  const double nn = c2 ? -1.0 : (c1 ? a - 1.0 : a);
+  const double dn = c2 ? fmin(a, 0x1p60) : (c1 ? a + 1.0 : 1.0);
+  const double b = nn / dn;
+  const double z = b * b;
+  const double P = poly<VEM_ATAN_D_U35_N>(cAtanDU35, z);
+  const double off = c2 ? kPio2Qd0 : (c1 ? kPio4Hi : 0.0);
+  double y = off + fma(b * z, P, b);
+  y = copysign_b(y, x);
+  return canon_d(y);
+}
+
+// asin / acos (oracle: asin_parts, vo_asin_d_u10, ...)
+struct asin_parts { double a, z, s, sl, u; bool big; };
+template <int N, bool kU10>
+__device__ __forceinline__ asin_parts asin_split(double x, const double* c) {
+  asin_parts o;
+  o.a = fabs(x);
+  o.big = o.a > 0.5;
+  o.z = o.big ? (1.0 - o.a) * 0.5 : o.a * o.a;
+  o.s = sqrt(o.z);
+  const double t = o.big ? o.s : o.a;
+  const double P = poly<N>(c, o.z);
+  o.u = (t * o.z) * P;
+  o.sl = 0.0;
+  if (kU10) {
+    const double e = fma(-o.s, o.s, o.z);
+    o.sl = (o.z == 0.0) ? 0.0 : e / (o.s + o.s);
+  }
+  return o;
+}
+__device__ __forceinline__ double asin_d_u10(double x) {
+  const asin_parts p = asin_split<VEM_ASIN_D_N, true>(x, cAsinD);
+  const dd h = two_sum(kPio2Qd0, -2.0 * p.s);
+  const double yb = h.hi + (h.lo + (kPio2Qd1 - 2.0 * (p.sl + p.u)));
+  double y = p.big ? yb : p.a + p.u;
+  y = (p.a > 1.0) ? from_bits_d(kCanonNanD) : y;
+  return canon_d(copysign_b(y, x));
+}
+__device__ __forceinline__ double asin_d_u35(double x) {
+  const asin_parts p = asin_split<VEM_ASIN_D_U35_N, false>(x, cAsinDU35);
+  const double yb = (kPio2Qd0 - 2.0 * p.s) + (kPio2Qd1 - 2.0 * p.u);
+  double y = p.big ? yb : p.a + p.u;
+  y = (p.a > 1.0) ? from_bits_d(kCanonNanD) : y;
+  return canon_d(copysign_b(y, x));
+}
+__device__ __forceinline__ double acos_d_u10(double x) {
+  const asin_parts p = asin_split<VEM_ASIN_D_N, true>(x, cAsinD);
+  const double us = copysign_b(p.u, x);
+  const dd hs = two_sum(kPio2Qd0, -x);
+  const double ys = hs.hi + (hs.lo + (kPio2Qd1 - us));
+  const double yp = 2.0 * p.s + 2.0 * (p.sl + p.u);
+  const dd hn = two_sum(kPiHi, -2.0 * p.s);
+  const double yn = hn.hi + (hn.lo + (kPiLo - 2.0 * (p.sl + p.u)));
+  double y = p.big ? (x > 0.0 ? yp : yn) : ys;
+  y = (p.a > 1.0) ? from_bits_d(kCanonNanD) : y;
+  return canon_d(y);
+}
+__device__ __forceinline__ double acos_d_u35(double x) {
+  const asin_parts p = asin_split<VEM_ASIN_D_U35_N, false>(x, cAsinDU35);
+  const double us = copysign_b(p.u, x);
+  const double ys = (kPio2Qd0 - x) + (kPio2Qd1 - us);
+  const double yp = 2.0 * (p.s + p.u);
+  const double yn = (kPiHi - 2.0 * p.s) + (kPiLo - 2.0 * p.u);
+  double y = p.big ? (x > 0.0 ? yp : yn) : ys;
+  y = (p.a > 1.0) ? from_bits_d(kCanonNanD) : y;
+  return canon_d(y);
+}
+
+// atan2 (oracle: atan2_special, atan2_parts, vo_atan2_d_u10/u35)
+__device__ __forceinline__ double atan2_special(double y, double x, double g) {
+  const double ax = fabs(x), ay = fabs(y);
+  double r = g;
+  if (ax == kInf) r = (ay == kInf) ? (x > 0.0 ? kPio4Hi : k3Pio4Hi) : (x > 0.0 ? 0.0 : kPiHi);
+  else if (ay == kInf) r = kPio2Qd0;
+  if (x == 0.0) r = (y == 0.0) ? (((bits_d(x) >> 63) != 0) ? kPiHi : 0.0) : kPio2Qd0;
+  else if (y == 0.0) r = (x > 0.0) ? 0.0 : kPiHi;
+  r = copysign_b(r, y);
+  return (x != x || y != y) ? from_bits_d(kCanonNanD) : r;
+}
+struct atan2_parts { double num, den, ch, cl; bool c1; int sig; };
+__device__ __forceinline__ atan2_parts atan2_split(double y, double x) {
+  atan2_parts o;
+  const double ax = fabs(x), ay = fabs(y);
+  const bool swap = ay > ax;
+  const double num = swap ? ax : ay, den = swap ? ay : ax;
+  const double sc = den >= 0x1p1000 ? 0x1p-100 : (den < 0x1p-900 ? 0x1p100 : 1.0);
+  o.num = num * sc;
+  o.den = den * sc;
+  o.c1 = o.num > kTanPi8 * o.den;
+  const bool neg = x < 0.0;
+  int q = (neg ? 4 : 0) + (swap ? (neg ? -2 : 2) : 0);  // multiples of pi/4
+  o.sig = (swap != neg) ? -1 : 1;
+  q += o.c1 ? o.sig : 0;
+  o.ch = q == 0 ? 0.0 : (q == 1 ? kPio4Hi : (q == 2 ? kPio2Qd0 : (q == 3 ? k3Pio4Hi : kPiHi)));
+  o.cl = q == 0 ? 0.0 : (q == 1 ? kPio4Lo : (q == 2 ? kPio2Qd1 : (q == 3 ? k3Pio4Lo : kPiLo)));
+  return o;
+}
+__device__ __forceinline__ double atan2_d_u10(double y, double x) {
+  const atan2_parts p = atan2_split(y, x);
+  const dd ns = two_sum(p.num, -p.den), ds = two_sum(p.num, p.den);
+  const dd nn = p.c1 ? ns : dd{p.num, 0.0};
+  const dd dn = p.c1 ? ds : dd{p.den, 0.0};
+  const dd b = dd_div(nn, dn);
+  const double z = b.hi * b.hi;
+  const double P = poly<VEM_ATAN_D_N>(cAtanD, z);
+  const double corr = fma(b.hi * z, P, fma(-b.lo, z, b.lo));
+  const double sg = (double)p.sig;
+  const dd s = two_sum(p.ch, sg * b.hi);
+  const double g = s.hi + (s.lo + (p.cl + sg * corr));
+  return canon_d(atan2_special(y, x, copysign_b(g, y)));
+}
+__device__ __forceinline__ double atan2_d_u35(double y, double x) {
+  const atan2_parts p = atan2_split(y, x);
+  const double nn = p.c1 ? p.num - p.den : p.num;
+  const double dn = p.c1 ? p.num + p.den : p.den;
+  const double b = nn * (1.0 / dn);
+  const double z = b * b;
+  const double P = poly<VEM_ATAN_D_U35_N>(cAtanDU35, z);
+  const double g = p.ch + (double)p.sig * fma(b * z, P, b);
+  return canon_d(atan2_special(y, x, copysign_b(g, y)));
 }
 
 // ============================================ split fast paths (kernels)

@@ -72,7 +72,8 @@ def overlay_specials(v: np.ndarray, seed: int, frac: float = 0.01) -> np.ndarray
 
 
 # --------------------------------------------------------------- configs
-FN_IDX = {"sin": 0, "cos": 1, "tan": 2, "atan": 3, "exp": 4, "log": 5, "pow": 6, "fmod": 7}
+FN_IDX = {"sin": 0, "cos": 1, "tan": 2, "atan": 3, "exp": 4, "log": 5, "pow": 6, "fmod": 7, "asin": 8, "acos": 9,
+          "atan2": 10, "fdim": 11}
 
 
 def config_inputs(cfg: int, fn: str, prec: str, n: int):
@@ -110,4 +111,12 @@ def config_inputs(cfg: int, fn: str, prec: str, n: int):
             y = overlay_specials(log_uniform(s ^ 0x7777, n, 1e-300, 1e300, dt, signed=True), s ^ 0x7777)
             return (x, y)
         return (x,)
+    if cfg == 6:  # SURVEY.md §8(f).1 functions (no BASELINE config): their natural domains
+        lo, hi = (1e-300, 1e300) if prec == "d" else (1e-37, 3e38)
+        if fn in ("asin", "acos"):
+            return (uniform(s, n, -1.0, 1.0, dt),)
+        if fn in ("atan2", "fdim"):
+            return (log_uniform(s, n, lo, hi, dt, signed=True), log_uniform(s ^ 0x7777, n, lo, hi, dt, signed=True))
+        if fn == "atan":
+            return (log_uniform(s, n, lo, hi, dt, signed=True),)
     raise ValueError(f"no inputs for cfg{cfg} {fn} {prec}")

@@ -33,6 +33,11 @@ def unary_cases(name: str, n: int):
     fn, p = name.split("_")[0], name.split("_")[1]
     dt = D if p == "d" else F
     parts = [SPECIAL_D if dt == D else SPECIAL_F, rnd_bits(11, n, dt)]
+    if fn in ("asin", "acos"):  # domain [-1, 1], both fold regions and the endpoints
+        edge = np.array([1.0, -1.0, 0.5, -0.5, np.nextafter(0.5, 1.0), np.nextafter(1.0, 0.0)], dtype=dt)
+        parts += [edge, I.uniform(13, n, -1.0, 1.0, dt), I.uniform(14, n, 0.49, 1.0, dt),
+                  I.log_uniform(15, n, 1e-300 if dt == D else 1e-37, 1.0, dt, signed=True)]
+        return np.concatenate(parts).astype(dt)
     cfg = {"sin": [1, 3, 5], "cos": [1, 3, 5], "tan": [3, 5], "atan": [5], "exp": [2, 5], "log": [2, 5]}[fn]
     for c in cfg:
         if c == 5 and dt == F:
@@ -51,6 +56,15 @@ def binary_cases(name: str, n: int):
     sp = SPECIAL_D if dt == D else SPECIAL_F
     a, b = _pairs(sp)
     xs, ys = [a, rnd_bits(21, n, dt)], [b, rnd_bits(22, n, dt)]
+    if fn in ("atan2", "fdim"):  # wide magnitudes, both signs, equal pairs
+        lo, hi = (1e-300, 1e300) if dt == D else (1e-37, 3e38)
+        for seed in (31, 33):
+            xs.append(I.log_uniform(seed, n, lo, hi, dt, signed=True))
+            ys.append(I.log_uniform(seed + 1, n, lo, hi, dt, signed=True))
+        u = I.uniform(35, n, -3, 3, dt)
+        xs += [u, I.uniform(36, n, -3, 3, dt)]
+        ys += [u, I.uniform(37, n, -3, 3, dt)]
+        return np.concatenate(xs).astype(dt), np.concatenate(ys).astype(dt)
     cfgs = {"pow": [2, 5], "fmod": [4, 5]}[fn]
     for c in cfgs:
         if c == 5 and dt == F:

@@ -17,7 +17,8 @@ ORACLE_DIR = os.path.join(ROOT, "oracle")
 BUILD = os.path.join(ORACLE_DIR, "_build")
 REF = os.path.join(ORACLE_DIR, "_ref")
 
-FN_ID = {"sin": 0, "cos": 1, "tan": 2, "atan": 3, "exp": 4, "log": 5, "pow": 6, "fmod": 7}
+FN_ID = {"sin": 0, "cos": 1, "tan": 2, "atan": 3, "exp": 4, "log": 5, "pow": 6, "fmod": 7, "asin": 8, "acos": 9,
+         "atan2": 10, "fdim": 11}
 
 _P = ctypes.c_void_p
 _N = ctypes.c_size_t

@@ -65,6 +65,36 @@ DOMAINS = {
 }
 
 
+def _asin_gens(dt):
+    return [lambda n: (I.uniform(1, n, -1, 1, dt),), lambda n: (I.uniform(2, n, 0.45, 1, dt),),
+            lambda n: (I.uniform(3, n, -1, -0.45, dt),), lambda n: (rnd_bits(4, n, dt),)]
+
+
+def _atan2_gens(dt):
+    lo, hi = (1e-300, 1e300) if dt == D else (1e-37, 3e38)
+    return [lambda n: (I.log_uniform(5, n, lo, hi, dt, signed=True), I.log_uniform(6, n, lo, hi, dt, signed=True)),
+            lambda n: (I.uniform(7, n, -3, 3, dt), I.uniform(8, n, -3, 3, dt)),
+            lambda n: (rnd_bits(9, n, dt), rnd_bits(10, n, dt))]
+
+
+# SURVEY.md §8(f).1 additions
+for _dt, _p in ((D, "d"), (F, "f")):
+    for _acc, _b in (("u10", 1.0), ("u35", 3.5)):
+        DOMAINS[f"asin_{_p}_{_acc}"] = ("asin", _b, _asin_gens(_dt))
+        DOMAINS[f"acos_{_p}_{_acc}"] = ("acos", _b, _asin_gens(_dt))
+        DOMAINS[f"atan2_{_p}_{_acc}"] = ("atan2", _b, _atan2_gens(_dt))
+    DOMAINS[f"fdim_{_p}"] = ("fdim", 0.5, [lambda n, dt=_dt: (rnd_bits(13, n, dt), rnd_bits(14, n, dt))])
+DOMAINS["atan_d_u35"] = ("atan", 3.5, [lambda n: (I.uniform(2, n, -3, 3),), lambda n: (rnd_bits(5, n, D),)])
+DOMAINS["atan_f_u10"] = ("atan", 1.0, [lambda n: (I.uniform(2, n, -3, 3, F),), lambda n: (rnd_bits(5, n, F),)])
+DOMAINS["atan_f_u35"] = ("atan", 3.5, [lambda n: (I.uniform(2, n, -3, 3, F),), lambda n: (rnd_bits(5, n, F),)])
+for _fn in ("sin", "cos", "tan"):
+    DOMAINS[f"{_fn}_d_u35"] = (_fn, 3.5, [lambda n: (I.uniform(1, n, -np.pi, np.pi),),
+                                          lambda n: (I.log_uniform(3, n, 1, 1e300, signed=True),),
+                                          lambda n: (I.log_uniform(4, n, 15, 1e14, signed=True),),
+                                          lambda n: (rnd_bits(5, n, D),)])
+    DOMAINS[f"{_fn}_f_u35"] = (_fn, 3.5, [lambda n: (I.log_uniform(1, n, 1, 3e38, F, signed=True),)])
+
+
 @pytest.mark.parametrize("name", sorted(DOMAINS))
 def test_ulp_bound_vs_mpfr(name):
     fn, bound, gens = DOMAINS[name]
@@ -143,6 +173,43 @@ def test_pow_special_table_matches_libm():
                 assert abs(float(g) - float(r)) <= 2 * np.spacing(np.abs(r)), (name, x, y, g, r)
 
 
+def test_atan2_special_table_matches_libm():
+    """C99 Annex F.9.1.4: every pair of {+-0, +-inf, NaN, +-1, +-2.5, +-1e300} vs glibc atan2."""
+    vals = [0.0, -0.0, np.inf, -np.inf, np.nan, 1.0, -1.0, 2.5, -2.5, 1e300, -1e300]
+    ys, xs = np.meshgrid(np.array(vals), np.array(vals), indexing="ij")
+    ys, xs = ys.ravel(), xs.ravel()
+    for name, dt in (("atan2_d_u10", D), ("atan2_d_u35", D), ("atan2_f_u10", F), ("atan2_f_u35", F)):
+        yy, xx = ys.astype(dt), xs.astype(dt)
+        out = oracle_eval(name, yy, xx)
+        ref = np.arctan2(yy, xx)
+        for y, x, g, r in zip(yy, xx, out, ref):
+            special = not np.isfinite(x) or not np.isfinite(y) or x == 0 or y == 0
+            if special:
+                assert _same(float(r), float(g)), (name, y, x, g, r)
+
+
+def test_asin_acos_fdim_specials():
+    for p, dt in (("d", D), ("f", F)):
+        sp = np.array([0.0, -0.0, 1.0, -1.0, 1.5, -1.5, np.inf, -np.inf, np.nan, 0.5, -0.5], dtype=dt)
+        with np.errstate(all="ignore"):
+            for fn, ref in (("asin", np.arcsin), ("acos", np.arccos)):
+                for acc in ("u10", "u35"):
+                    out = oracle_eval(f"{fn}_{p}_{acc}", sp)
+                    r = ref(sp)
+                    for x, g, e in zip(sp, out, r):
+                        if np.isnan(e) or x == 0 or abs(x) == 1:
+                            assert _same(float(e), float(g)), (fn, acc, x, g, e)
+                        else:
+                            assert abs(float(g) - float(e)) <= 2 * np.spacing(np.abs(e)), (fn, acc, x, g, e)
+        a = np.array([3.0, 1.0, np.inf, np.inf, -np.inf, np.nan, 1.0, 0.0, -0.0, 1e308], dtype=dt)
+        b = np.array([1.0, 3.0, np.inf, -np.inf, -np.inf, 1.0, np.nan, -0.0, 0.0, -1e308], dtype=dt)
+        out = oracle_eval(f"fdim_{p}", a, b)
+        with np.errstate(all="ignore"):
+            ref = np.where(np.isnan(a) | np.isnan(b), np.nan, np.where(a > b, a - b, 0.0)).astype(dt)
+        for x, y, g, r in zip(a, b, out, ref):
+            assert _same(float(r), float(g)), ("fdim", p, x, y, g, r)
+
+
 def test_known_answers_from_spec():
     """SPEC.md examples (the only pinned answers the reference ships)."""
     assert oracle_eval("exp_d_u10", np.array([0.0]))[0] == 1.0           # SPEC.md:409
@@ -159,6 +226,14 @@ def test_known_answers_from_spec():
     fm = oracle_eval("fmod_d", np.array([1e40, 5.5, 3.7, 3.7, 1e300]), np.array([0.75, 2.0, 3.7, np.inf, 3e-300]))
     assert fm[0] == 0.25 and fm[1] == 1.5 and fm[2] == 0.0 and fm[3] == 3.7
     assert fm[4] == np.fmod(1e300, 3e-300)  # beyond SLEEF: ratio > DBL_MAX
+    asn = oracle_eval("asin_d_u10", np.array([0.0, 0.5, 1.0]))
+    assert asn[0] == 0.0 and abs(asn[1] - np.pi / 6) <= np.spacing(np.pi / 6) and asn[2] == np.float64(np.pi / 2)
+    acs = oracle_eval("acos_d_u10", np.array([1.0, -1.0]))
+    assert acs[0] == 0.0 and acs[1] == np.float64(np.pi)
+    fd = oracle_eval("fdim_d", np.array([3.0, 1.0, 1e308]), np.array([1.0, 3.0, -1e308]))
+    assert fd[0] == 2.0 and fd[1] == 0.0 and not np.signbit(fd[1]) and fd[2] == np.inf
+    a2 = oracle_eval("atan2_d_u10", np.array([0.0, 1.0, 0.0, -0.0]), np.array([1.0, 1.0, -1.0, -1.0]))
+    assert a2[0] == 0.0 and abs(a2[1] - np.pi / 4) <= np.spacing(np.pi / 4) and a2[2] == np.pi and a2[3] == -np.pi
 
 
 def test_special_inputs_are_canonical_nan():
@@ -173,7 +248,7 @@ def test_special_inputs_are_canonical_nan():
 def test_special_grid_runs_everywhere():
     for name in DOMAINS:
         fn = name.split("_")[0]
-        if fn == "pow":
+        if fn in ("pow", "atan2", "fdim"):
             continue
         sp = SPECIAL_D if "_d_" in name else SPECIAL_F
         out = oracle_eval(name, sp)

@@ -164,6 +164,17 @@ SPECS = {
               "exp(r) = 1 + r + r^2*P(r), |r|<=ln2/2 (13 terms)"),
     "exp_d_u35": (exp_target(), exp_weight(), -R_EXP, R_EXP, list(range(10)), 0,
                   "exp(r) = 1 + r + r^2*P(r), |r|<=ln2/2 (12 terms)"),
+    # ---- float64, SPEC.md 8(f) additions (asin/acos fold, u35 trig/atan)
+    "asin_d": (odd_target(mp.asin, 1 / mp.mpf(6)), odd_weight(mp.asin), 0, mp.mpf("0.2501"), list(range(13)), 0,
+               "asin(t) = t + t*z*P(z), z=t^2, |t|<=0.5 (asin/acos fold)"),
+    "asin_d_u35": (odd_target(mp.asin, 1 / mp.mpf(6)), odd_weight(mp.asin), 0, mp.mpf("0.2501"), list(range(12)), 0,
+                   "asin(t) = t + t*z*P(z), z=t^2, |t|<=0.5 (u35)"),
+    "sin_d_u35": (odd_target(mp.sin, -1 / mp.mpf(6)), odd_weight(mp.sin), 0, R_TRIG ** 2, list(range(6)), 0,
+                  "sin(r) = r + r*z*P(z), z=r^2, |r|<=0.80 (u35)"),
+    "cos_d_u35": (cos_target(), cos_weight(), 0, R_TRIG ** 2, list(range(5)), 0,
+                  "cos(r) = 1 - z/2 + z^2*P(z), z=r^2, |r|<=0.80 (u35)"),
+    "atan_d_u35": (odd_target(mp.atan, -1 / mp.mpf(3)), odd_weight(mp.atan), 0, T_PI8 ** 2, list(range(10)), 0,
+                   "atan(b) = b + b*z*P(z), z=b^2, |b|<=tan(pi/8) (u35)"),
     # ---- float32 (binary64 internals)
     "sin_f": (odd_target(mp.sin, -1 / mp.mpf(6)), odd_weight(mp.sin), 0, R_TRIG_F ** 2, list(range(4)), 0,
               "f32 sin(r) = r + r*z*P(z), |r|<=pi/4"),

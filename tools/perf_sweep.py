@@ -17,7 +17,8 @@ sys.path.insert(0, ROOT)
 from paper_2001_09258_b200 import _lib, api, build  # noqa: E402
 from paper_2001_09258_b200 import inputs as I  # noqa: E402
 
-CFG = {"sin": 3, "cos": 3, "tan": 3, "atan": 5, "exp": 2, "log": 2, "pow": 2, "fmod": 4}
+CFG = {"sin": 3, "cos": 3, "tan": 3, "atan": 5, "exp": 2, "log": 2, "pow": 2, "fmod": 4, "asin": 6, "acos": 6,
+       "atan2": 6, "fdim": 6}
 
 
 def main():
@@ -34,6 +35,8 @@ def main():
         cfg = CFG[fn]
         if name.startswith(("sin_d", "cos_d")) and not name.endswith("_ph"):
             cfg = 1
+        if name.startswith("atan_f"):
+            cfg = 6
         arrs = I.config_inputs(cfg, fn, p, n)
         ts = [torch.from_numpy(a).cuda() for a in arrs]
         out = torch.empty_like(ts[0])

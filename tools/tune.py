@@ -24,7 +24,8 @@ sys.path.insert(0, ROOT)
 from paper_2001_09258_b200 import _lib, build  # noqa: E402
 from paper_2001_09258_b200 import inputs as I  # noqa: E402
 
-CFG = {"sin": 1, "cos": 1, "tan": 3, "atan": 5, "exp": 2, "log": 2, "pow": 2, "fmod": 4}
+CFG = {"sin": 1, "cos": 1, "tan": 3, "atan": 5, "exp": 2, "log": 2, "pow": 2, "fmod": 4, "asin": 6, "acos": 6,
+       "atan2": 6, "fdim": 6}
 
 
 def build_tune():
