@@ -832,15 +832,19 @@ __device__ __forceinline__ redf ph_f(float xf, const double* __restrict__ tab) {
   return o;
 }
 
+// oracle: sincos_core_f.  Both forms from constant-bank coefficients and a
+// per-lane select of the result: the FP64 pipe has room in these
+// integer-reduction kernels, the shared-memory pipe does not.  Same values
+// as the selected 5-term Horner (the sin set's leading 0 is exact:
+// fma(0, z, c3) == c3; the cos form's A*z is 1.0*z == z).
 __device__ __forceinline__ double sincos_core_f(double r, int cosform, const double* tab) {
-  bool cf = cosform != 0;
-  const double2* cs = reinterpret_cast<const double2*>(tab + kPhFDoubles + (cf ? 8 : 0));
-  const double2 c01 = cs[0], c23 = cs[1];
-  const double c4 = tab[kPhFDoubles + (cf ? 12 : 4)];
-  double z = r * r;
-  double P = fma(fma(fma(fma(c4, z, c23.y), z, c23.x), z, c01.y), z, c01.x);
-  double A = cf ? 1.0 : r;
-  return fma(A * z, P, A);
+  (void)tab;
+  const double z = r * r;
+  const double Ps = fma(fma(fma(cSinF[3], z, cSinF[2]), z, cSinF[1]), z, cSinF[0]);
+  const double Pc = fma(fma(fma(fma(cCosF[3], z, cCosF[2]), z, cCosF[1]), z, cCosF[0]), z, -0.5);
+  const double ys = fma(r * z, Ps, r);
+  const double yc = fma(z, Pc, 1.0);
+  return cosform != 0 ? yc : ys;
 }
 
 __device__ __forceinline__ float sin_f_u10(float x, const double* tab) {
