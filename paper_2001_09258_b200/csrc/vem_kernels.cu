@@ -987,14 +987,14 @@ int vem_fdim_d(const double* x, const double* y2, double* o, size_t n, vem_strea
 int vem_sin_f_u35(const float* x, float* y, size_t n, vem_stream_t s) { return vem_sin_f_u10(x, y, n, s); }
 int vem_cos_f_u35(const float* x, float* y, size_t n, vem_stream_t s) { return vem_cos_f_u10(x, y, n, s); }
 int vem_tan_f_u35(const float* x, float* y, size_t n, vem_stream_t s) { return vem_tan_f_u10(x, y, n, s); }
-int vem_atan_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpAtanF, float, 1, kNoTable, 1, 2>(x, nullptr, y, n, s); }
-int vem_atan_f_u35(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpAtanFU35, float, 1, kNoTable, 1, 2>(x, nullptr, y, n, s); }
+int vem_atan_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpAtanF, float, 1, kNoTable, 2, 2>(x, nullptr, y, n, s); }
+int vem_atan_f_u35(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpAtanFU35, float, 1, kNoTable, 2, 2>(x, nullptr, y, n, s); }
 int vem_asin_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpAsinF, float, 1, kNoTable, 1, 2>(x, nullptr, y, n, s); }
-int vem_asin_f_u35(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpAsinFU35, float, 1, kNoTable, 1, 2>(x, nullptr, y, n, s); }
+int vem_asin_f_u35(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpAsinFU35, float, 1, kNoTable, 2, 2>(x, nullptr, y, n, s); }
 int vem_acos_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpAcosF, float, 1, kNoTable, 1, 2>(x, nullptr, y, n, s); }
-int vem_acos_f_u35(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpAcosFU35, float, 1, kNoTable, 1, 2>(x, nullptr, y, n, s); }
-int vem_atan2_f_u10(const float* y, const float* x, float* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpAtan2F, float, 2, kNoTable, 1, 2>(y, x, o, n, s); }
-int vem_atan2_f_u35(const float* y, const float* x, float* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpAtan2FU35, float, 2, kNoTable, 1, 2>(y, x, o, n, s); }
+int vem_acos_f_u35(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpAcosFU35, float, 1, kNoTable, 2, 2>(x, nullptr, y, n, s); }
+int vem_atan2_f_u10(const float* y, const float* x, float* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpAtan2F, float, 2, kNoTable, 2, 2>(y, x, o, n, s); }
+int vem_atan2_f_u35(const float* y, const float* x, float* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpAtan2FU35, float, 2, kNoTable, 2, 2>(y, x, o, n, s); }
 int vem_fdim_f(const float* x, const float* y2, float* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpFdimF, float, 2, kNoTable, 4, 2>(x, y2, o, n, s); }
 
 int vem_trig_reduce_d(const double* x, double* hi, double* lo, int* q, size_t n, vem_stream_t s) {
