@@ -1230,11 +1230,9 @@ __device__ __forceinline__ double pow_fast_d(double x, double y, const double* c
   const double R = exp_dd_core(t.hi, t.lo, lt, e);
   const uint32_t th = (uint32_t)__double2hiint(t.hi);
   const uint32_t ht = th & 0x7fffffffu;
-  int c = ((int)hx < 0) ? 2 : 0;
-  if (ht >= kExpFastHi) {
-    const bool neg = (int)th < 0;
-    c |= (!neg && ht >= 0x40862E43u) ? 4 : ((neg && ht >= 0x40874911u) ? 8 : 1);
-  }
+  const bool neg = (int)th < 0;  // selects only: no branch between the elements' chains
+  const int sat = (!neg && ht >= 0x40862E43u) ? 4 : ((neg && ht >= 0x40874911u) ? 8 : 1);
+  const int c = (((int)hx < 0) ? 2 : 0) | ((ht >= kExpFastHi) ? sat : 0);
   code = (fx && fy) ? c : 1;
   return __hiloint2double(__double2hiint(R) + (e << 20), __double2loint(R));
 }
