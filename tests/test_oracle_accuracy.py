@@ -292,3 +292,15 @@ def test_f32_reduction_accuracy_vs_f64_payne_hanek():
     assert np.array_equal(q[big], qd[big] & 3)
     rel = np.abs((r[big] - hi[big]) - lo[big]) / np.abs(hi[big])
     assert rel.max() < 2.0 ** -51
+
+
+def test_oracle_digest_file_reproduces():
+    """Spot-check tests/golden/oracle_digests.json against the oracle (two
+    cheap entry points; the full file is regenerated by tools/gen_digests.py)."""
+    import hashlib
+    import json
+    from digest_inputs import digest_inputs
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "oracle_digests.json")))
+    for name in ("exp_f_u10", "fdim_d"):
+        r = oracle_eval(name, *digest_inputs(name, gold[name]["n"]))
+        assert hashlib.md5(r.tobytes()).hexdigest() == gold[name]["md5"], name
