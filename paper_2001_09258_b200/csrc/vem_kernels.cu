@@ -452,6 +452,229 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
   }
 }
 
+// ------------------------------------------------------- fmod: step queue
+// fmod's cost is data dependent: ceil(E/50) exact 50-bit long-division steps
+// (E = exponent gap, config 4 f64: 0 for the half of the pairs with |x| < |y|,
+// up to 42 otherwise).  Per TMA tile (TILE_E pairs):
+//   1. triage on the operand bits, every element: NaN / Inf / zero divisor /
+//      |x| <= |y| are finished at once into the tile's output block in
+//      shared memory; the others get a sort key (steps estimated from the
+//      biased exponents) and a rank from a shared-memory histogram atomic;
+//   2. one warp-level suffix scan of the histogram (every warp redundantly:
+//      no extra barrier) gives each key its queue offset, heaviest first;
+//      the pending pairs are written to the queue in that order;
+//   3. the warps take queue rows of 32 (snake order over the 8 warps for
+//      balance): the lanes of a row hold pairs of (nearly) the same step
+//      count, so the long division runs converged with no idle lanes;
+//      results go back into the output block at their tile slots;
+//   4. the output block is stored coalesced (16-byte st.global.cs).
+// Per element the math is fmod_setup / fmod_step50 / fmod_finish (exact),
+// so results are bit-identical to the oracle and to glibc.
+constexpr int kFmodKeys = 64;
+
+// Pending pair (|x| > |y| > 0, both finite) after setup: r = (mn 2^s0) mod md
+// with `steps` full 50-bit steps to go; result = +-r 2^ed.
+struct fmod_pend {
+  double r, md, rmd;
+  int steps, ed;
+  uint32_t sx;  // sign word of x
+};
+__device__ __forceinline__ fmod_pend fmod_pend_setup(double x, double y) {
+  fmod_pend p;
+  const uint32_t hx = (uint32_t)__double2hiint(x), hy = (uint32_t)__double2hiint(y);
+  const int bx = (int)((hx >> 20) & 0x7ffu), by = (int)((hy >> 20) & 0x7ffu);
+  p.sx = hx & 0x80000000u;
+  double mn, md;
+  int E;
+  if (bx != 0 && by != 0) {  // normal operands: mantissas by bit surgery
+    mn = __hiloint2double((int)((hx & 0x000fffffu) | 0x3ff00000u), __double2loint(x));
+    md = __hiloint2double((int)((hy & 0x000fffffu) | 0x3ff00000u), __double2loint(y));
+    E = bx - by;
+    p.ed = by - 1023;
+  } else {  // a subnormal operand (rare)
+    const double n = fabs(x), d = fabs(y);
+    const int en = ilogb_pos(n), ed = ilogb_pos(d);
+    mn = mant_1_2(n, en);
+    md = mant_1_2(d, ed);
+    E = en - ed;
+    p.ed = ed;
+  }
+  p.md = md;
+  p.rmd = toward0_pos(1.0 / md);  // <= 1/md (1.0/md is correctly rounded)
+  // E >= 0; (E - 1) / 50 for E - 1 in [0, 2100] (and 0 for E = 0)
+  p.steps = E == 0 ? 0 : (int)(((uint32_t)(E - 1) * 1311u) >> 16);
+  p.r = fmod_step(mn, E - 50 * p.steps, md, p.rmd);  // E = 0: one 0-bit step, mn - md
+  return p;
+}
+__device__ __forceinline__ double fmod_pend_finish(const fmod_pend& p) {
+  // r in [0, md) is a multiple of 2^-52: r 2^ed is normal when ed >= -970
+  const double m = p.ed >= -970 ? p.r * __hiloint2double((p.ed + 1023) << 20, 0) : ldexp2(p.r, p.ed);
+  return __hiloint2double(__double2hiint(m) | (int)p.sx, __double2loint(m));
+}
+
+template <class T, int VPT, int STAGES, int MINB, int ROWS>
+__global__ void __launch_bounds__(kThreads, MINB) k_fmod_q(const T* __restrict__ a, const T* __restrict__ b,
+                                                           T* __restrict__ out, size_t n) {
+  using V = typename Vec16<T>::type;
+  constexpr int W = Vec16<T>::n;
+  constexpr int TILE_V = kThreads * VPT;
+  constexpr uint32_t TILE_BYTES = TILE_V * 16;
+  constexpr int TILE_E = TILE_V * W;
+  constexpr int NE = VPT * W;
+  constexpr int kExpShift = sizeof(T) == 8 ? 20 : 23;
+  constexpr uint32_t kExpMask = sizeof(T) == 8 ? 0x7ffu : 0xffu;
+  extern __shared__ __align__(128) unsigned char dsm[];
+  __shared__ uint64_t bars[STAGES];
+  __shared__ __align__(16) T so[TILE_E];  // output block (tile order)
+  __shared__ unsigned short qi[TILE_E];
+  __shared__ int hist[kFmodKeys + 1];  // + the row-fetch counter
+  V* buf = reinterpret_cast<V*>(dsm);
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; s++) tma::mbar_init(&bars[s], 1);
+    tma::fence_barrier_init();
+  }
+  if (tid <= kFmodKeys) hist[tid] = 0;
+  __syncthreads();
+  const size_t ntiles = n / TILE_E;
+  const size_t G = gridDim.x;
+  const size_t my = ntiles > blockIdx.x ? (ntiles - blockIdx.x + G - 1) / G : 0;
+  uint64_t pol = 0;
+  auto issue = [&](int s, size_t tile) {
+    tma::mbar_expect_tx(&bars[s], 2 * TILE_BYTES);
+    tma::bulk_g2s(buf + (size_t)(s * 2) * TILE_V, reinterpret_cast<const V*>(a) + tile * TILE_V, TILE_BYTES,
+                  &bars[s], pol);
+    tma::bulk_g2s(buf + (size_t)(s * 2 + 1) * TILE_V, reinterpret_cast<const V*>(b) + tile * TILE_V, TILE_BYTES,
+                  &bars[s], pol);
+  };
+  if (tid == 0) {
+    pol = tma::policy_evict_first();
+    for (int s = 0; s < STAGES && (size_t)s < my; s++) issue(s, blockIdx.x + (size_t)s * G);
+  }
+  for (size_t j = 0; j < my; j++) {
+    const int s = (int)(j % STAGES);
+    tma::mbar_wait(&bars[s], (uint32_t)((j / STAGES) & 1));
+    T xe[NE], ye[NE];
+#pragma unroll
+    for (int v = 0; v < VPT; v++) {
+      V va = buf[(size_t)(s * 2) * TILE_V + v * kThreads + tid];
+      V vb = buf[(size_t)(s * 2 + 1) * TILE_V + v * kThreads + tid];
+#pragma unroll
+      for (int k = 0; k < W; k++) {
+        xe[v * W + k] = vget(va, k);
+        ye[v * W + k] = vget(vb, k);
+      }
+    }
+    __syncthreads();  // stage consumed (it holds the queue until step 3 ends)
+    T* qx = reinterpret_cast<T*>(buf + (size_t)(s * 2) * TILE_V);
+    T* qy = reinterpret_cast<T*>(buf + (size_t)(s * 2 + 1) * TILE_V);
+    // ---- 1. triage: every slot gets its trivial result (pending slots are
+    // overwritten in step 3); pending pairs get a key and a histogram rank
+    int key[NE], rank[NE];
+#pragma unroll
+    for (int e = 0; e < NE; e++) {
+      const int slot = ((e / W) * kThreads + tid) * W + (e % W);
+      const T nx = fabs(xe[e]), ny = fabs(ye[e]);
+      const bool nan_res = !(nx < (T)kInf) || !(ny > (T)0);  // x NaN/Inf, y NaN/0
+      const bool ret_x = nx < ny;                            // incl. y = +-Inf
+      T res = ret_x ? xe[e] : copysign((T)0, xe[e]);         // |x| == |y| -> +-0
+      res = nan_res ? (sizeof(T) == 8 ? (T)from_bits_d(kCanonNanD) : (T)from_bits_f(kCanonNanF)) : res;
+      so[slot] = res;
+      key[e] = -1;
+      if (!nan_res && !ret_x && nx != ny) {
+        uint32_t hx, hy;
+        if constexpr (sizeof(T) == 8) {
+          hx = (uint32_t)__double2hiint((double)xe[e]);
+          hy = (uint32_t)__double2hiint((double)ye[e]);
+        } else {
+          hx = bits_f((float)xe[e]);
+          hy = bits_f((float)ye[e]);
+        }
+        const int gap = (int)((hx >> kExpShift) & kExpMask) - (int)((hy >> kExpShift) & kExpMask);
+        key[e] = gap <= 0 ? 0 : min((int)(((uint32_t)(gap - 1) * 1311u) >> 16), kFmodKeys - 1);
+        rank[e] = atomicAdd(&hist[key[e]], 1);
+      }
+    }
+    __syncthreads();
+    // ---- 2. queue offsets: suffix scan over keys (heaviest first), per warp
+    const int h0 = hist[2 * lane], h1 = hist[2 * lane + 1];
+    int suf = h0 + h1;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int t = __shfl_down_sync(0xffffffffu, suf, off);
+      if (lane + off < 32) suf += t;
+    }
+    const int Q = __shfl_sync(0xffffffffu, suf, 0);
+    const int base_odd = suf - h0 - h1;  // keys > 2*lane+1
+    const int base_even = base_odd + h1;
+#pragma unroll
+    for (int e = 0; e < NE; e++) {
+      const int k = key[e] < 0 ? 0 : key[e];
+      const int bo = __shfl_sync(0xffffffffu, base_odd, k >> 1);
+      const int be = __shfl_sync(0xffffffffu, base_even, k >> 1);
+      if (key[e] >= 0) {
+        const int pos = ((k & 1) ? bo : be) + rank[e];
+        qx[pos] = xe[e];
+        qy[pos] = ye[e];
+        qi[pos] = (unsigned short)(((e / W) * kThreads + tid) * W + (e % W));
+      }
+    }
+    __syncthreads();
+    // ---- 3. converged long division over the sorted queue: units of ROWS
+    // adjacent rows (ROWS independent chains per lane), fetched dynamically
+    // heaviest first (list scheduling balances the warps)
+    const int nunits = (Q + 32 * ROWS - 1) / (32 * ROWS);
+    while (true) {
+      int u = 0;
+      if (lane == 0) u = atomicAdd(&hist[kFmodKeys], 1);
+      u = __shfl_sync(0xffffffffu, u, 0);
+      if (u >= nunits) break;
+      if constexpr (ROWS == 1) {
+        const int pa = u * 32 + lane;
+        if (pa < Q) {
+          fmod_pend A = fmod_pend_setup((double)qx[pa], (double)qy[pa]);
+          for (int k = 0; k < A.steps; k++) A.r = fmod_step50(A.r, A.md, A.rmd);
+          so[qi[pa]] = (T)fmod_pend_finish(A);
+        }
+      } else {
+        const int pa = u * 64 + lane, pb = pa + 32;
+        const bool va = pa < Q, vb = pb < Q;
+        // invalid lanes run a dummy pair (2 mod 1.5: zero steps)
+        fmod_pend A = fmod_pend_setup(va ? (double)qx[pa] : 2.0, va ? (double)qy[pa] : 1.5);
+        fmod_pend B = fmod_pend_setup(vb ? (double)qx[pb] : 2.0, vb ? (double)qy[pb] : 1.5);
+        const int c = min(A.steps, B.steps);
+        int i = 0;
+        for (; i < c; i++) {
+          A.r = fmod_step50(A.r, A.md, A.rmd);
+          B.r = fmod_step50(B.r, B.md, B.rmd);
+        }
+        for (int k = i; k < A.steps; k++) A.r = fmod_step50(A.r, A.md, A.rmd);
+        for (int k = i; k < B.steps; k++) B.r = fmod_step50(B.r, B.md, B.rmd);
+        if (va) so[qi[pa]] = (T)fmod_pend_finish(A);
+        if (vb) so[qi[pb]] = (T)fmod_pend_finish(B);
+      }
+    }
+    __syncthreads();
+    if (tid <= kFmodKeys) hist[tid] = 0;  // for the next tile (ranks and fetches consumed)
+    if (tid == 0 && j + STAGES < my) {    // the queue's stage is free: refill it
+      tma::fence_proxy_async_smem();
+      issue(s, blockIdx.x + (j + STAGES) * G);
+    }
+    // ---- 4. coalesced store of the output block
+    V* ov = reinterpret_cast<V*>(out) + (blockIdx.x + j * G) * TILE_V;
+    const V* sv = reinterpret_cast<const V*>(so);
+#pragma unroll
+    for (int v = 0; v < VPT; v++) __stcs(ov + v * kThreads + tid, sv[v * kThreads + tid]);
+  }
+  // remainder (< one tile)
+  const size_t done = ntiles * TILE_E;
+  for (size_t i = done + (size_t)blockIdx.x * kThreads + tid; i < n; i += G * kThreads) {
+    if constexpr (sizeof(T) == 8) out[i] = fmod_d(a[i], b[i]);
+    else out[i] = fmod_f(a[i], b[i]);
+  }
+}
+
 #ifdef VEM_TUNE
 // Work-ring fmod kernel (superseded by the regrouped streaming kernel,
 // OpFmodD/OpFmodF below; kept in the tuning build for comparison).
@@ -811,6 +1034,29 @@ static int launch_stream(const T* a, const T* b, T* out, size_t n, vem_stream_t 
   return (int)cudaGetLastError();
 }
 
+template <class T, int VPT, int STAGES, int MINB = 1, int ROWS = 2>
+static int launch_fmod_q(const T* a, const T* b, T* out, size_t n, vem_stream_t s) {
+  using OpF = typename std::conditional<sizeof(T) == 8, OpFmodD, OpFmodF>::type;
+  if (n == 0) return 0;
+  if (!(aligned16(a) && aligned16(b) && aligned16(out))) return launch_binary<OpF, T, kNoTable, 1>(a, b, out, n, s);
+  auto k = k_fmod_q<T, VPT, STAGES, MINB, ROWS>;
+  constexpr int smem = STAGES * 2 * kThreads * VPT * 16;
+  static const int occ = [k] {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int bpm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpm, k, kThreads, smem) != cudaSuccess || bpm < 1) bpm = 1;
+    return bpm;
+  }();
+  constexpr size_t tile_e = (size_t)kThreads * VPT * Vec16<T>::n;
+  size_t tiles = n / tile_e;
+  size_t cap = (size_t)num_sms() * occ;
+  size_t g = tiles < cap ? tiles : cap;
+  if (g < 1) g = 1;
+  k<<<(int)g, kThreads, smem, (cudaStream_t)s>>>(a, b, out, n);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return (int)cudaGetLastError();
+}
+
 #ifdef VEM_TUNE
 template <class T, int MINB = 1>
 static int launch_fmod(const T* a, const T* b, T* out, size_t n, vem_stream_t s) {
@@ -910,14 +1156,16 @@ template <class T>
 static int launch_fmod_tuned(const T* a, const T* b, T* o, size_t n, vem_stream_t s) {
   using OpF = typename std::conditional<sizeof(T) == 8, OpFmodD, OpFmodF>::type;
   switch (g_tune) {
-    case 1: return launch_fmod<T, 8>(a, b, o, n, s);
-    case 2: return launch_fmod<T, 12>(a, b, o, n, s);
-    case 3: return launch_fmod<T, 16>(a, b, o, n, s);
-    case 4: return launch_stream<OpF, T, 2, kNoTable, 1, 2>(a, b, o, n, s);
-    case 5: return launch_stream<OpF, T, 2, kNoTable, 2, 2, 4>(a, b, o, n, s);
-    case 6: return launch_stream<OpF, T, 2, kNoTable, 4, 2>(a, b, o, n, s);
+    case 0: return launch_fmod_q<T, 1, 2, 1, 1>(a, b, o, n, s);
+    case 1: return launch_fmod_q<T, 2, 2, 1, 1>(a, b, o, n, s);
+    case 2: return launch_fmod_q<T, 4, 2, 1, 1>(a, b, o, n, s);
+    case 3: return launch_fmod_q<T, 2, 3, 1, 2>(a, b, o, n, s);
+    case 4: return launch_fmod_q<T, 4, 2, 1, 2>(a, b, o, n, s);
+    case 5: return launch_fmod_q<T, 1, 2, 1, 2>(a, b, o, n, s);
+    case 6: return launch_fmod_q<T, 2, 2, 1, 2>(a, b, o, n, s);
     case 7: return launch_stream<OpF, T, 2, kNoTable, 2, 2>(a, b, o, n, s);
-    default: return launch_fmod<T>(a, b, o, n, s);
+    case 8: return launch_fmod<T>(a, b, o, n, s);
+    default: return launch_fmod_q<T, 2, 2, 1, 1>(a, b, o, n, s);
   }
 }
 #define VEM_FMOD launch_fmod_tuned
@@ -947,7 +1195,7 @@ int vem_fmod_d(const double* x, const double* y2, double* o, size_t n, vem_strea
 #ifdef VEM_TUNE
   return VEM_FMOD<double>(x, y2, o, n, s);
 #else
-  return VEM_STREAM<OpFmodD, double, 2, kNoTable, 2, 2>(x, y2, o, n, s);
+  return launch_fmod_q<double, 2, 2, 1, 1>(x, y2, o, n, s);
 #endif
 }
 
@@ -968,7 +1216,7 @@ int vem_fmod_f(const float* x, const float* y2, float* o, size_t n, vem_stream_t
 #ifdef VEM_TUNE
   return VEM_FMOD<float>(x, y2, o, n, s);
 #else
-  return VEM_STREAM<OpFmodF, float, 2, kNoTable, 2, 2, 4>(x, y2, o, n, s);
+  return launch_fmod_q<float, 2, 2, 1, 1>(x, y2, o, n, s);
 #endif
 }
 

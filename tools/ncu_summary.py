@@ -49,6 +49,9 @@ def ncu(*args):
 
 
 def entry_of(kname):
+    q = re.search(r"k_fmod_q<(double|float)", kname)
+    if q:
+        return "fmod_d" if q.group(1) == "double" else "fmod_f"
     m = re.search(r"vem::(Op\w+)|<(Op\w+)", kname)
     if not m:
         return kname

@@ -6,9 +6,9 @@ paper_2001_09258_b200/_tune/libvem_tune.so, then times every entry point
 (filtered by argv[2]) at 2^argv[1] elements for each (VPT, STAGES) variant:
  0:(1,2) 1:(1,4) 2:(2,2) 3:(2,3) 4:(2,4) 5:(4,2), -1 = the shipped choice, and
  6/7/8 = the shipped shape with __launch_bounds__ min-blocks 2/3/4.
-fmod: -1 shipped ring kernel, 1/2/3 = ring kernel with min-blocks 8/12/16,
-4/5/6/7 = the streaming kernel with step-class regrouping, shapes (1,2),
-(2,2,minb 4), (4,2), (2,2).
+fmod: -1 shipped step-queue kernel, 0-6 = step-queue shapes
+(VPT,STAGES,ROWS): (1,2,1) (2,2,1) (4,2,1) (2,3,2) (4,2,2) (1,2,2) (2,2,2); 7 = the streaming kernel with
+warp step-class regrouping (2,2); 8 = the work-ring kernel.
 Prints one JSON line per entry point with Gelem/s per variant.
 """
 import ctypes
@@ -66,7 +66,7 @@ def main():
             f.argtypes = [ctypes.c_void_p] * 2 + [ctypes.c_size_t, ctypes.c_void_p]
             call = lambda: f(ts[0].data_ptr(), out.data_ptr(), n, stream)  # noqa: E731
         res = {}
-        for v in ((-1, 1, 4, 5, 6, 7) if name.startswith("fmod") else (-1, 0, 1, 2, 3, 4, 5, 6, 7, 8)):
+        for v in ((-1, 0, 1, 2, 3, 4, 5, 6, 7, 8) if name.startswith("fmod") else (-1, 0, 1, 2, 3, 4, 5, 6, 7, 8)):
             L.vem_tune_set(v)
             for _ in range(3):
                 call()
