@@ -470,8 +470,6 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
 //   4. the output block is stored coalesced (16-byte st.global.cs).
 // Per element the math is fmod_setup / fmod_step50 / fmod_finish (exact),
 // so results are bit-identical to the oracle and to glibc.
-constexpr int kFmodKeys = 64;
-
 // Pending pair (|x| > |y| > 0, both finite) after setup: r = (mn 2^s0) mod md
 // with `steps` full 50-bit steps to go; result = +-r 2^ed.
 struct fmod_pend {
@@ -512,22 +510,95 @@ __device__ __forceinline__ double fmod_pend_finish(const fmod_pend& p) {
   return __hiloint2double(__double2hiint(m) | (int)p.sx, __double2loint(m));
 }
 
-template <class T, int VPT, int STAGES, int MINB, int ROWS>
-__global__ void __launch_bounds__(kThreads, MINB) k_fmod_q(const T* __restrict__ a, const T* __restrict__ b,
-                                                           T* __restrict__ out, size_t n) {
+// Queue ops for fmod (the binary kernel below): triage on the operand bits,
+// key = estimated 50-bit steps, exact long division for the queue rows.
+template <class T>
+struct FmodQ {
+  static constexpr int kDirect = 0;
+  __device__ static bool direct_ok(T) { return false; }
+  __device__ static T direct(T x, T, const double*) { return x; }
+  // every slot gets its trivial result (pending slots are overwritten later)
+  __device__ static bool triage(T x, T y, T& res, int& key) {
+    const T nx = fabs(x), ny = fabs(y);
+    const bool nan_res = !(nx < (T)kInf) || !(ny > (T)0);  // x NaN/Inf, y NaN/0
+    const bool ret_x = nx < ny;                            // incl. y = +-Inf
+    res = ret_x ? x : copysign((T)0, x);                   // |x| == |y| -> +-0
+    res = nan_res ? (sizeof(T) == 8 ? (T)from_bits_d(kCanonNanD) : (T)from_bits_f(kCanonNanF)) : res;
+    if (nan_res || ret_x || nx == ny) return false;
+    uint32_t hx, hy;
+    int gap;
+    if constexpr (sizeof(T) == 8) {
+      hx = (uint32_t)__double2hiint((double)x);
+      hy = (uint32_t)__double2hiint((double)y);
+      gap = (int)((hx >> 20) & 0x7ffu) - (int)((hy >> 20) & 0x7ffu);
+    } else {
+      hx = bits_f((float)x);
+      hy = bits_f((float)y);
+      gap = (int)((hx >> 23) & 0xffu) - (int)((hy >> 23) & 0xffu);
+    }
+    key = gap <= 0 ? 0 : min((int)(((uint32_t)(gap - 1) * 1311u) >> 16), 63);
+    return true;
+  }
+  __device__ static T eval_full(T x, T y, const double*) {
+    if constexpr (sizeof(T) == 8) return fmod_d(x, y);
+    else return fmod_f(x, y);
+  }
+  __device__ static T eval1(T x, T y, const double*) {
+    fmod_pend A = fmod_pend_setup((double)x, (double)y);
+    for (int k = 0; k < A.steps; k++) A.r = fmod_step50(A.r, A.md, A.rmd);
+    return (T)fmod_pend_finish(A);
+  }
+  __device__ static void eval2(T xa, T ya, T xb, T yb, T& ra, T& rb, const double*) {
+    fmod_pend A = fmod_pend_setup((double)xa, (double)ya);
+    fmod_pend B = fmod_pend_setup((double)xb, (double)yb);
+    const int c = min(A.steps, B.steps);
+    int i = 0;
+    for (; i < c; i++) {
+      A.r = fmod_step50(A.r, A.md, A.rmd);
+      B.r = fmod_step50(B.r, B.md, B.rmd);
+    }
+    for (int k = i; k < A.steps; k++) A.r = fmod_step50(A.r, A.md, A.rmd);
+    for (int k = i; k < B.steps; k++) B.r = fmod_step50(B.r, B.md, B.rmd);
+    ra = (T)fmod_pend_finish(A);
+    rb = (T)fmod_pend_finish(B);
+  }
+};
+
+// ------------------------------------------------ tile work-queue kernel
+// For entry points whose per-element cost is data dependent (fmod: step
+// count; the trig selector: Cody-Waite 1 / 2 / Payne-Hanek).  Per TMA tile:
+//   0. (Q::kDirect) if every element of the tile takes the cheap path
+//      (trig: |x| < 15), evaluate it branch-free in registers and store;
+//   1. triage: Q::triage finishes trivial elements into the tile's output
+//      block in shared memory and gives the others a key (cost class) and a
+//      rank from a shared-memory histogram atomic;
+//   2. a warp-level suffix scan of the histogram (every warp redundantly: no
+//      extra barrier) gives each key its queue offset, heaviest first; the
+//      pending elements are written to the queue, which lives in the
+//      consumed TMA stage (its refill is issued after step 3);
+//   3. warps fetch units of ROWS x 32 queue entries dynamically (heaviest
+//      first: list scheduling balances the warps); the lanes of a row hold
+//      elements of (nearly) the same cost, so they run converged; ROWS = 2
+//      gives each lane two independent chains (Q::eval2);
+//   4. the output block is stored coalesced (16-byte st.global.cs).
+// Results per element are the op's own (bit-identical to the oracle).
+constexpr int kQKeys = 64;
+
+template <class Q, class T, int NIN, int TABLE, int VPT, int STAGES, int MINB, int ROWS>
+__global__ void __launch_bounds__(kThreads, MINB) k_queue(const T* __restrict__ a, const T* __restrict__ b,
+                                                          T* __restrict__ out, size_t n) {
   using V = typename Vec16<T>::type;
   constexpr int W = Vec16<T>::n;
   constexpr int TILE_V = kThreads * VPT;
   constexpr uint32_t TILE_BYTES = TILE_V * 16;
   constexpr int TILE_E = TILE_V * W;
   constexpr int NE = VPT * W;
-  constexpr int kExpShift = sizeof(T) == 8 ? 20 : 23;
-  constexpr uint32_t kExpMask = sizeof(T) == 8 ? 0x7ffu : 0xffu;
   extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ uint64_t bars[STAGES];
+  __shared__ __align__(16) double stab[TableSize<TABLE>::n];
   __shared__ __align__(16) T so[TILE_E];  // output block (tile order)
   __shared__ unsigned short qi[TILE_E];
-  __shared__ int hist[kFmodKeys + 1];  // + the row-fetch counter
+  __shared__ int hist[kQKeys + 1];  // + the unit-fetch counter
   V* buf = reinterpret_cast<V*>(dsm);
   const int tid = threadIdx.x, lane = tid & 31;
   if (tid == 0) {
@@ -535,18 +606,20 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fmod_q(const T* __restrict__
     for (int s = 0; s < STAGES; s++) tma::mbar_init(&bars[s], 1);
     tma::fence_barrier_init();
   }
-  if (tid <= kFmodKeys) hist[tid] = 0;
-  __syncthreads();
+  if (tid <= kQKeys) hist[tid] = 0;
+  const double* tab = stage_table<TABLE>(stab);  // includes __syncthreads()
+  if constexpr (TABLE == kNoTable) __syncthreads();
   const size_t ntiles = n / TILE_E;
   const size_t G = gridDim.x;
   const size_t my = ntiles > blockIdx.x ? (ntiles - blockIdx.x + G - 1) / G : 0;
   uint64_t pol = 0;
   auto issue = [&](int s, size_t tile) {
-    tma::mbar_expect_tx(&bars[s], 2 * TILE_BYTES);
-    tma::bulk_g2s(buf + (size_t)(s * 2) * TILE_V, reinterpret_cast<const V*>(a) + tile * TILE_V, TILE_BYTES,
+    tma::mbar_expect_tx(&bars[s], NIN * TILE_BYTES);
+    tma::bulk_g2s(buf + (size_t)(s * NIN) * TILE_V, reinterpret_cast<const V*>(a) + tile * TILE_V, TILE_BYTES,
                   &bars[s], pol);
-    tma::bulk_g2s(buf + (size_t)(s * 2 + 1) * TILE_V, reinterpret_cast<const V*>(b) + tile * TILE_V, TILE_BYTES,
-                  &bars[s], pol);
+    if constexpr (NIN == 2)
+      tma::bulk_g2s(buf + (size_t)(s * NIN + 1) * TILE_V, reinterpret_cast<const V*>(b) + tile * TILE_V,
+                    TILE_BYTES, &bars[s], pol);
   };
   if (tid == 0) {
     pol = tma::policy_evict_first();
@@ -558,43 +631,52 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fmod_q(const T* __restrict__
     T xe[NE], ye[NE];
 #pragma unroll
     for (int v = 0; v < VPT; v++) {
-      V va = buf[(size_t)(s * 2) * TILE_V + v * kThreads + tid];
-      V vb = buf[(size_t)(s * 2 + 1) * TILE_V + v * kThreads + tid];
+      V va = buf[(size_t)(s * NIN) * TILE_V + v * kThreads + tid];
+      V vb;
+      if constexpr (NIN == 2) vb = buf[(size_t)(s * NIN + 1) * TILE_V + v * kThreads + tid];
 #pragma unroll
       for (int k = 0; k < W; k++) {
         xe[v * W + k] = vget(va, k);
-        ye[v * W + k] = vget(vb, k);
+        ye[v * W + k] = NIN == 2 ? vget(vb, k) : (T)0;
       }
     }
-    __syncthreads();  // stage consumed (it holds the queue until step 3 ends)
-    T* qx = reinterpret_cast<T*>(buf + (size_t)(s * 2) * TILE_V);
-    T* qy = reinterpret_cast<T*>(buf + (size_t)(s * 2 + 1) * TILE_V);
-    // ---- 1. triage: every slot gets its trivial result (pending slots are
-    // overwritten in step 3); pending pairs get a key and a histogram rank
+    V* ov = reinterpret_cast<V*>(out) + (blockIdx.x + j * G) * TILE_V;
+    if constexpr (Q::kDirect) {
+      bool ok = true;
+#pragma unroll
+      for (int e = 0; e < NE; e++) ok = ok && Q::direct_ok(xe[e]);
+      if (__syncthreads_and(ok)) {  // also releases the stage
+        if (tid == 0 && j + STAGES < my) {
+          tma::fence_proxy_async_smem();
+          issue(s, blockIdx.x + (j + STAGES) * G);
+        }
+#pragma unroll
+        for (int v = 0; v < VPT; v++) {
+          V o;
+#pragma unroll
+          for (int k = 0; k < W; k++) vget(o, k) = Q::direct(xe[v * W + k], ye[v * W + k], tab);
+          __stcs(ov + v * kThreads + tid, o);
+        }
+        continue;
+      }
+    } else {
+      __syncthreads();  // stage consumed; previous tile's output block stored
+    }
+    T* qx = reinterpret_cast<T*>(buf + (size_t)(s * NIN) * TILE_V);
+    T* qy = reinterpret_cast<T*>(buf + (size_t)(s * NIN + (NIN - 1)) * TILE_V);
+    // ---- 1. triage
     int key[NE], rank[NE];
 #pragma unroll
     for (int e = 0; e < NE; e++) {
       const int slot = ((e / W) * kThreads + tid) * W + (e % W);
-      const T nx = fabs(xe[e]), ny = fabs(ye[e]);
-      const bool nan_res = !(nx < (T)kInf) || !(ny > (T)0);  // x NaN/Inf, y NaN/0
-      const bool ret_x = nx < ny;                            // incl. y = +-Inf
-      T res = ret_x ? xe[e] : copysign((T)0, xe[e]);         // |x| == |y| -> +-0
-      res = nan_res ? (sizeof(T) == 8 ? (T)from_bits_d(kCanonNanD) : (T)from_bits_f(kCanonNanF)) : res;
-      so[slot] = res;
+      T res;
       key[e] = -1;
-      if (!nan_res && !ret_x && nx != ny) {
-        uint32_t hx, hy;
-        if constexpr (sizeof(T) == 8) {
-          hx = (uint32_t)__double2hiint((double)xe[e]);
-          hy = (uint32_t)__double2hiint((double)ye[e]);
-        } else {
-          hx = bits_f((float)xe[e]);
-          hy = bits_f((float)ye[e]);
-        }
-        const int gap = (int)((hx >> kExpShift) & kExpMask) - (int)((hy >> kExpShift) & kExpMask);
-        key[e] = gap <= 0 ? 0 : min((int)(((uint32_t)(gap - 1) * 1311u) >> 16), kFmodKeys - 1);
-        rank[e] = atomicAdd(&hist[key[e]], 1);
+      int k;
+      if (Q::triage(xe[e], ye[e], res, k)) {
+        key[e] = k;
+        rank[e] = atomicAdd(&hist[k], 1);
       }
+      so[slot] = res;
     }
     __syncthreads();
     // ---- 2. queue offsets: suffix scan over keys (heaviest first), per warp
@@ -605,7 +687,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fmod_q(const T* __restrict__
       const int t = __shfl_down_sync(0xffffffffu, suf, off);
       if (lane + off < 32) suf += t;
     }
-    const int Q = __shfl_sync(0xffffffffu, suf, 0);
+    const int Qn = __shfl_sync(0xffffffffu, suf, 0);
     const int base_odd = suf - h0 - h1;  // keys > 2*lane+1
     const int base_even = base_odd + h1;
 #pragma unroll
@@ -616,63 +698,179 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fmod_q(const T* __restrict__
       if (key[e] >= 0) {
         const int pos = ((k & 1) ? bo : be) + rank[e];
         qx[pos] = xe[e];
-        qy[pos] = ye[e];
+        if constexpr (NIN == 2) qy[pos] = ye[e];
         qi[pos] = (unsigned short)(((e / W) * kThreads + tid) * W + (e % W));
       }
     }
     __syncthreads();
-    // ---- 3. converged long division over the sorted queue: units of ROWS
-    // adjacent rows (ROWS independent chains per lane), fetched dynamically
-    // heaviest first (list scheduling balances the warps)
-    const int nunits = (Q + 32 * ROWS - 1) / (32 * ROWS);
+    // ---- 3. queue units, fetched dynamically heaviest first; lanes past the
+    // end duplicate the unit's first entry (same cost class, result dropped)
+    const int nunits = (Qn + 32 * ROWS - 1) / (32 * ROWS);
     while (true) {
       int u = 0;
-      if (lane == 0) u = atomicAdd(&hist[kFmodKeys], 1);
+      if (lane == 0) u = atomicAdd(&hist[kQKeys], 1);
       u = __shfl_sync(0xffffffffu, u, 0);
       if (u >= nunits) break;
+      const int p0 = u * 32 * ROWS;
+      const int pa = p0 + lane, ca = pa < Qn ? pa : p0;
       if constexpr (ROWS == 1) {
-        const int pa = u * 32 + lane;
-        if (pa < Q) {
-          fmod_pend A = fmod_pend_setup((double)qx[pa], (double)qy[pa]);
-          for (int k = 0; k < A.steps; k++) A.r = fmod_step50(A.r, A.md, A.rmd);
-          so[qi[pa]] = (T)fmod_pend_finish(A);
-        }
+        const T r = Q::eval1(qx[ca], NIN == 2 ? qy[ca] : (T)0, tab);
+        if (pa < Qn) so[qi[pa]] = r;
       } else {
-        const int pa = u * 64 + lane, pb = pa + 32;
-        const bool va = pa < Q, vb = pb < Q;
-        // invalid lanes run a dummy pair (2 mod 1.5: zero steps)
-        fmod_pend A = fmod_pend_setup(va ? (double)qx[pa] : 2.0, va ? (double)qy[pa] : 1.5);
-        fmod_pend B = fmod_pend_setup(vb ? (double)qx[pb] : 2.0, vb ? (double)qy[pb] : 1.5);
-        const int c = min(A.steps, B.steps);
-        int i = 0;
-        for (; i < c; i++) {
-          A.r = fmod_step50(A.r, A.md, A.rmd);
-          B.r = fmod_step50(B.r, B.md, B.rmd);
-        }
-        for (int k = i; k < A.steps; k++) A.r = fmod_step50(A.r, A.md, A.rmd);
-        for (int k = i; k < B.steps; k++) B.r = fmod_step50(B.r, B.md, B.rmd);
-        if (va) so[qi[pa]] = (T)fmod_pend_finish(A);
-        if (vb) so[qi[pb]] = (T)fmod_pend_finish(B);
+        const int pb = pa + 32, cb = pb < Qn ? pb : p0;
+        T ra, rb;
+        Q::eval2(qx[ca], NIN == 2 ? qy[ca] : (T)0, qx[cb], NIN == 2 ? qy[cb] : (T)0, ra, rb, tab);
+        if (pa < Qn) so[qi[pa]] = ra;
+        if (pb < Qn) so[qi[pb]] = rb;
       }
     }
     __syncthreads();
-    if (tid <= kFmodKeys) hist[tid] = 0;  // for the next tile (ranks and fetches consumed)
-    if (tid == 0 && j + STAGES < my) {    // the queue's stage is free: refill it
+    if (tid <= kQKeys) hist[tid] = 0;  // for the next tile (ranks and fetches consumed)
+    if (tid == 0 && j + STAGES < my) {  // the queue's stage is free: refill it
       tma::fence_proxy_async_smem();
       issue(s, blockIdx.x + (j + STAGES) * G);
     }
     // ---- 4. coalesced store of the output block
-    V* ov = reinterpret_cast<V*>(out) + (blockIdx.x + j * G) * TILE_V;
     const V* sv = reinterpret_cast<const V*>(so);
 #pragma unroll
     for (int v = 0; v < VPT; v++) __stcs(ov + v * kThreads + tid, sv[v * kThreads + tid]);
   }
-  // remainder (< one tile)
+  // remainder (< one tile): the full per-element function
   const size_t done = ntiles * TILE_E;
-  for (size_t i = done + (size_t)blockIdx.x * kThreads + tid; i < n; i += G * kThreads) {
-    if constexpr (sizeof(T) == 8) out[i] = fmod_d(a[i], b[i]);
-    else out[i] = fmod_f(a[i], b[i]);
+  for (size_t i = done + (size_t)blockIdx.x * kThreads + tid; i < n; i += G * kThreads)
+    out[i] = Q::eval_full(a[i], NIN == 2 ? b[i] : (T)0, tab);
+}
+
+// ------------------------------------------- warp-private work queue
+// Same four steps as k_queue, but every warp owns its chunks (32 x NE
+// elements), TMA stages, mbarriers, histogram and queue: no CTA barriers, so
+// a warp with a heavy queue never holds the others back.
+template <class Q, class T, int NIN, int VPT, int STAGES, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_wqueue(const T* __restrict__ a, const T* __restrict__ b,
+                                                           T* __restrict__ out, size_t n) {
+  using V = typename Vec16<T>::type;
+  constexpr int W = Vec16<T>::n;
+  constexpr int NW = kThreads / 32;
+  constexpr int CH_V = 32 * VPT;  // 16-byte vectors per input per chunk
+  constexpr uint32_t CH_BYTES = CH_V * 16;
+  constexpr int CH_E = CH_V * W;
+  constexpr int NE = VPT * W;
+  extern __shared__ __align__(128) unsigned char dsm[];
+  __shared__ uint64_t bars[NW][STAGES];
+  __shared__ __align__(16) T so_all[NW][CH_E];
+  __shared__ unsigned short qi_all[NW][CH_E];
+  __shared__ int hist_all[NW][kQKeys];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  V* buf = reinterpret_cast<V*>(dsm) + (size_t)warp * STAGES * NIN * CH_V;
+  T* so = so_all[warp];
+  unsigned short* qi = qi_all[warp];
+  int* hist = hist_all[warp];
+  uint64_t* bar = bars[warp];
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; s++) tma::mbar_init(&bar[s], 1);
+    tma::fence_barrier_init();
   }
+  hist[lane] = 0;
+  hist[lane + 32] = 0;
+  __syncwarp();
+  const size_t nch = n / CH_E;
+  const size_t GW = (size_t)gridDim.x * NW;
+  const size_t gw = (size_t)blockIdx.x * NW + warp;
+  const size_t my = nch > gw ? (nch - gw + GW - 1) / GW : 0;
+  uint64_t pol = 0;
+  auto issue = [&](int s, size_t ch) {
+    tma::mbar_expect_tx(&bar[s], NIN * CH_BYTES);
+    tma::bulk_g2s(buf + (size_t)(s * NIN) * CH_V, reinterpret_cast<const V*>(a) + ch * CH_V, CH_BYTES, &bar[s], pol);
+    if constexpr (NIN == 2)
+      tma::bulk_g2s(buf + (size_t)(s * NIN + 1) * CH_V, reinterpret_cast<const V*>(b) + ch * CH_V, CH_BYTES, &bar[s],
+                    pol);
+  };
+  if (lane == 0) {
+    pol = tma::policy_evict_first();
+    for (int s = 0; s < STAGES && (size_t)s < my; s++) issue(s, gw + (size_t)s * GW);
+  }
+  for (size_t j = 0; j < my; j++) {
+    const int s = (int)(j % STAGES);
+    tma::mbar_wait(&bar[s], (uint32_t)((j / STAGES) & 1));
+    T xe[NE], ye[NE];
+#pragma unroll
+    for (int v = 0; v < VPT; v++) {
+      V va = buf[(size_t)(s * NIN) * CH_V + v * 32 + lane];
+      V vb;
+      if constexpr (NIN == 2) vb = buf[(size_t)(s * NIN + 1) * CH_V + v * 32 + lane];
+#pragma unroll
+      for (int k = 0; k < W; k++) {
+        xe[v * W + k] = vget(va, k);
+        ye[v * W + k] = NIN == 2 ? vget(vb, k) : (T)0;
+      }
+    }
+    __syncwarp();  // stage consumed (it holds the queue until the rows are done)
+    T* qx = reinterpret_cast<T*>(buf + (size_t)(s * NIN) * CH_V);
+    T* qy = reinterpret_cast<T*>(buf + (size_t)(s * NIN + (NIN - 1)) * CH_V);
+    int key[NE], rank[NE];
+#pragma unroll
+    for (int e = 0; e < NE; e++) {
+      const int slot = ((e / W) * 32 + lane) * W + (e % W);
+      T res;
+      key[e] = -1;
+      int k;
+      if (Q::triage(xe[e], ye[e], res, k)) {
+        key[e] = k;
+        rank[e] = atomicAdd(&hist[k], 1);
+      }
+      so[slot] = res;
+    }
+    __syncwarp();
+    const int h0 = hist[2 * lane], h1 = hist[2 * lane + 1];
+    int suf = h0 + h1;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int t = __shfl_down_sync(0xffffffffu, suf, off);
+      if (lane + off < 32) suf += t;
+    }
+    const int Qn = __shfl_sync(0xffffffffu, suf, 0);
+    const int base_odd = suf - h0 - h1;
+    const int base_even = base_odd + h1;
+    hist[2 * lane] = 0;  // this lane's two counters are read: reset for the next chunk
+    hist[2 * lane + 1] = 0;
+#pragma unroll
+    for (int e = 0; e < NE; e++) {
+      const int k = key[e] < 0 ? 0 : key[e];
+      const int bo = __shfl_sync(0xffffffffu, base_odd, k >> 1);
+      const int be = __shfl_sync(0xffffffffu, base_even, k >> 1);
+      if (key[e] >= 0) {
+        const int pos = ((k & 1) ? bo : be) + rank[e];
+        qx[pos] = xe[e];
+        if constexpr (NIN == 2) qy[pos] = ye[e];
+        qi[pos] = (unsigned short)(((e / W) * 32 + lane) * W + (e % W));
+      }
+    }
+    __syncwarp();
+    // rows in pairs, heaviest first; lanes past the end duplicate entry p0
+    for (int p0 = 0; p0 < Qn; p0 += 64) {
+      const int pa = p0 + lane, pb = pa + 32;
+      const int ca = pa < Qn ? pa : p0, cb = pb < Qn ? pb : p0;
+      T ra, rb;
+      Q::eval2(qx[ca], NIN == 2 ? qy[ca] : (T)0, qx[cb], NIN == 2 ? qy[cb] : (T)0, ra, rb, nullptr);
+      if (pa < Qn) so[qi[pa]] = ra;
+      if (pb < Qn) so[qi[pb]] = rb;
+    }
+    __syncwarp();
+    if (lane == 0 && j + STAGES < my) {
+      tma::fence_proxy_async_smem();
+      issue(s, gw + (j + STAGES) * GW);
+    }
+    V* ov = reinterpret_cast<V*>(out) + (gw + j * GW) * CH_V;
+    const V* sv = reinterpret_cast<const V*>(so);
+#pragma unroll
+    for (int v = 0; v < VPT; v++) __stcs(ov + v * 32 + lane, sv[v * 32 + lane]);
+    __syncwarp();
+  }
+  const size_t done = nch * CH_E;
+  const size_t tg = (size_t)blockIdx.x * kThreads + tid;
+  for (size_t i = done + tg; i < n; i += (size_t)gridDim.x * kThreads)
+    out[i] = Q::eval_full(a[i], NIN == 2 ? b[i] : (T)0, nullptr);
 }
 
 #ifdef VEM_TUNE
@@ -1034,13 +1232,15 @@ static int launch_stream(const T* a, const T* b, T* out, size_t n, vem_stream_t 
   return (int)cudaGetLastError();
 }
 
-template <class T, int VPT, int STAGES, int MINB = 1, int ROWS = 2>
-static int launch_fmod_q(const T* a, const T* b, T* out, size_t n, vem_stream_t s) {
-  using OpF = typename std::conditional<sizeof(T) == 8, OpFmodD, OpFmodF>::type;
+template <class Q, class Op, class T, int NIN, int TABLE, int VPT, int STAGES, int MINB = 1, int ROWS = 1>
+static int launch_queue(const T* a, const T* b, T* out, size_t n, vem_stream_t s) {
   if (n == 0) return 0;
-  if (!(aligned16(a) && aligned16(b) && aligned16(out))) return launch_binary<OpF, T, kNoTable, 1>(a, b, out, n, s);
-  auto k = k_fmod_q<T, VPT, STAGES, MINB, ROWS>;
-  constexpr int smem = STAGES * 2 * kThreads * VPT * 16;
+  if (!(aligned16(a) && aligned16(out) && (NIN == 1 || aligned16(b)))) {
+    if constexpr (NIN == 2) return launch_binary<Op, T, TABLE, 1>(a, b, out, n, s);
+    else return launch_unary<Op, T, TABLE, 1>(a, out, n, s);
+  }
+  auto k = k_queue<Q, T, NIN, TABLE, VPT, STAGES, MINB, ROWS>;
+  constexpr int smem = STAGES * NIN * kThreads * VPT * 16;
   static const int occ = [k] {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int bpm = 0;
@@ -1055,6 +1255,34 @@ static int launch_fmod_q(const T* a, const T* b, T* out, size_t n, vem_stream_t 
   k<<<(int)g, kThreads, smem, (cudaStream_t)s>>>(a, b, out, n);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return (int)cudaGetLastError();
+}
+template <class T, int VPT, int STAGES, int MINB = 1>
+static int launch_fmod_w(const T* a, const T* b, T* out, size_t n, vem_stream_t s) {
+  using OpF = typename std::conditional<sizeof(T) == 8, OpFmodD, OpFmodF>::type;
+  if (n == 0) return 0;
+  if (!(aligned16(a) && aligned16(out) && aligned16(b))) return launch_binary<OpF, T, kNoTable, 1>(a, b, out, n, s);
+  auto k = k_wqueue<FmodQ<T>, T, 2, VPT, STAGES, MINB>;
+  constexpr int smem = (kThreads / 32) * STAGES * 2 * 32 * VPT * 16;
+  static const int occ = [k] {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int bpm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpm, k, kThreads, smem) != cudaSuccess || bpm < 1) bpm = 1;
+    return bpm;
+  }();
+  constexpr size_t ch_e = (size_t)32 * VPT * Vec16<T>::n;
+  size_t warps = n / ch_e;
+  size_t cap = (size_t)num_sms() * occ * (kThreads / 32);
+  size_t w = warps < cap ? warps : cap;
+  size_t g = (w + kThreads / 32 - 1) / (kThreads / 32);
+  if (g < 1) g = 1;
+  k<<<(int)g, kThreads, smem, (cudaStream_t)s>>>(a, b, out, n);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return (int)cudaGetLastError();
+}
+template <class T, int VPT, int STAGES, int MINB = 1, int ROWS = 1>
+static int launch_fmod_q(const T* a, const T* b, T* out, size_t n, vem_stream_t s) {
+  using OpF = typename std::conditional<sizeof(T) == 8, OpFmodD, OpFmodF>::type;
+  return launch_queue<FmodQ<T>, OpF, T, 2, kNoTable, VPT, STAGES, MINB, ROWS>(a, b, out, n, s);
 }
 
 #ifdef VEM_TUNE
@@ -1156,13 +1384,13 @@ template <class T>
 static int launch_fmod_tuned(const T* a, const T* b, T* o, size_t n, vem_stream_t s) {
   using OpF = typename std::conditional<sizeof(T) == 8, OpFmodD, OpFmodF>::type;
   switch (g_tune) {
-    case 0: return launch_fmod_q<T, 1, 2, 1, 1>(a, b, o, n, s);
-    case 1: return launch_fmod_q<T, 2, 2, 1, 1>(a, b, o, n, s);
-    case 2: return launch_fmod_q<T, 4, 2, 1, 1>(a, b, o, n, s);
-    case 3: return launch_fmod_q<T, 2, 3, 1, 2>(a, b, o, n, s);
-    case 4: return launch_fmod_q<T, 4, 2, 1, 2>(a, b, o, n, s);
-    case 5: return launch_fmod_q<T, 1, 2, 1, 2>(a, b, o, n, s);
-    case 6: return launch_fmod_q<T, 2, 2, 1, 2>(a, b, o, n, s);
+    case 0: return launch_fmod_w<T, 2, 2>(a, b, o, n, s);
+    case 1: return launch_fmod_w<T, 4, 2>(a, b, o, n, s);
+    case 2: return launch_fmod_w<T, 2, 3>(a, b, o, n, s);
+    case 3: return launch_fmod_w<T, 4, 2, 2>(a, b, o, n, s);
+    case 4: return launch_fmod_w<T, 2, 2, 3>(a, b, o, n, s);
+    case 5: return launch_fmod_q<T, 2, 2, 1, 2>(a, b, o, n, s);
+    case 6: return launch_fmod_q<T, 4, 2, 1, 1>(a, b, o, n, s);
     case 7: return launch_stream<OpF, T, 2, kNoTable, 2, 2>(a, b, o, n, s);
     case 8: return launch_fmod<T>(a, b, o, n, s);
     default: return launch_fmod_q<T, 2, 2, 1, 1>(a, b, o, n, s);
@@ -1216,7 +1444,7 @@ int vem_fmod_f(const float* x, const float* y2, float* o, size_t n, vem_stream_t
 #ifdef VEM_TUNE
   return VEM_FMOD<float>(x, y2, o, n, s);
 #else
-  return launch_fmod_q<float, 2, 2, 1, 1>(x, y2, o, n, s);
+  return launch_fmod_w<float, 2, 2>(x, y2, o, n, s);
 #endif
 }
 

@@ -6,9 +6,10 @@ paper_2001_09258_b200/_tune/libvem_tune.so, then times every entry point
 (filtered by argv[2]) at 2^argv[1] elements for each (VPT, STAGES) variant:
  0:(1,2) 1:(1,4) 2:(2,2) 3:(2,3) 4:(2,4) 5:(4,2), -1 = the shipped choice, and
  6/7/8 = the shipped shape with __launch_bounds__ min-blocks 2/3/4.
-fmod: -1 shipped step-queue kernel, 0-6 = step-queue shapes
-(VPT,STAGES,ROWS): (1,2,1) (2,2,1) (4,2,1) (2,3,2) (4,2,2) (1,2,2) (2,2,2); 7 = the streaming kernel with
+fmod: -1 shipped step-queue kernel; 0-4 warp-private queue (VPT,STAGES[,MINB]) (2,2) (4,2) (2,3) (4,2,2) (2,2,3);
+5-6 CTA queue (VPT,STAGES,ROWS) (2,2,2) (4,2,1); 7 = the streaming kernel with
 warp step-class regrouping (2,2); 8 = the work-ring kernel.
+VEM_TUNE_CFG=k overrides the BASELINE config whose inputs are used.
 Prints one JSON line per entry point with Gelem/s per variant.
 """
 import ctypes
@@ -55,6 +56,8 @@ def main():
             continue
         fn, p = name.split("_")[0], name.split("_")[1]
         cfg = 3 if name.endswith("_ph") else CFG[fn]
+        if os.environ.get("VEM_TUNE_CFG"):
+            cfg = int(os.environ["VEM_TUNE_CFG"])
         arrs = I.config_inputs(cfg, fn, p, n)
         ts = [torch.from_numpy(a).cuda() for a in arrs]
         out = torch.empty_like(ts[0])
@@ -79,7 +82,7 @@ def main():
             torch.cuda.synchronize()
             res[v] = round(n / (e0.elapsed_time(e1) / 10) / 1e6, 1)
         best = max(res, key=res.get)
-        print(json.dumps({"fn": name, "gelem_s": res, "best": best}), flush=True)
+        print(json.dumps({"fn": name, "cfg": cfg, "gelem_s": res, "best": best}), flush=True)
         del ts, out
         torch.cuda.empty_cache()
 
