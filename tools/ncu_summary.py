@@ -49,7 +49,7 @@ def ncu(*args):
 
 
 def entry_of(kname):
-    q = re.search(r"k_fmod_q<(double|float)", kname)
+    q = re.search(r"FmodQ<(double|float)>", kname)
     if q:
         return "fmod_d" if q.group(1) == "double" else "fmod_f"
     m = re.search(r"vem::(Op\w+)|<(Op\w+)", kname)

@@ -1,0 +1,38 @@
+#!/usr/bin/env python3
+"""Run one entry point on one BASELINE config's inputs (dev tool for ncu).
+
+Usage: python tools/prof_one.py NAME CFG [log2_n=24] [reps=3]
+e.g.  ncu --set full -k regex:OpSinD python tools/prof_one.py sin_d_u10 5 24
+Prints Gelem/s (CUDA events) so the same command also runs without ncu.
+"""
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2001_09258_b200 import api  # noqa: E402
+from paper_2001_09258_b200 import inputs as I  # noqa: E402
+
+
+def main():
+    name, cfg = sys.argv[1], int(sys.argv[2])
+    n = 1 << (int(sys.argv[3]) if len(sys.argv) > 3 else 24)
+    reps = int(sys.argv[4]) if len(sys.argv) > 4 else 3
+    fn, p = name.split("_")[0], name.split("_")[1]
+    ts = [torch.from_numpy(a).cuda() for a in I.config_inputs(cfg, fn, p, n)]
+    out = torch.empty_like(ts[0])
+    api.call(name, *ts, out=out)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        api.call(name, *ts, out=out)
+    e1.record()
+    torch.cuda.synchronize()
+    print(f"{name} cfg{cfg} n={n}: {n / (e0.elapsed_time(e1) / reps) / 1e6:.1f} Gelem/s")
+
+
+if __name__ == "__main__":
+    main()
