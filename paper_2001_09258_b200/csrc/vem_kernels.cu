@@ -219,6 +219,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
   }
   const double* tab = stage_table<TABLE>(stab);  // includes __syncthreads()
   if constexpr (TABLE == kNoTable) __syncthreads();
+  tma::griddep_wait();  // inputs / outputs may belong to the previous grid
+  tma::griddep_launch_dependents();
   Op op;
   const size_t ntiles = n / TILE_E;
   const size_t G = gridDim.x;
@@ -609,6 +611,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_queue(const T* __restrict__ 
   if (tid <= kQKeys) hist[tid] = 0;
   const double* tab = stage_table<TABLE>(stab);  // includes __syncthreads()
   if constexpr (TABLE == kNoTable) __syncthreads();
+  tma::griddep_wait();
+  tma::griddep_launch_dependents();
   const size_t ntiles = n / TILE_E;
   const size_t G = gridDim.x;
   const size_t my = ntiles > blockIdx.x ? (ntiles - blockIdx.x + G - 1) / G : 0;
@@ -774,6 +778,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_wqueue(const T* __restrict__
   hist[lane] = 0;
   hist[lane + 32] = 0;
   __syncwarp();
+  tma::griddep_wait();
+  tma::griddep_launch_dependents();
   const size_t nch = n / CH_E;
   const size_t GW = (size_t)gridDim.x * NW;
   const size_t gw = (size_t)blockIdx.x * NW + warp;
@@ -1169,6 +1175,23 @@ static int grid_for(int occ, size_t work_items, int per_thread) {
 
 static inline bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
+// Launch with programmatic stream serialization (see tma::griddep_wait): the
+// kernel may start while the previous grid in the stream drains.
+template <class K, class... Args>
+static void launch_pdl(K kernel, int grid, int smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 template <class Op, class T, int TABLE, int U>
 static int launch_unary(const T* x, T* y, size_t n, vem_stream_t s) {
   if (n == 0) return 0;
@@ -1227,7 +1250,7 @@ static int launch_stream(const T* a, const T* b, T* out, size_t n, vem_stream_t 
   size_t cap = (size_t)num_sms() * occ;
   size_t g = tiles < cap ? tiles : cap;
   if (g < 1) g = 1;
-  k<<<(int)g, kThreads, smem, (cudaStream_t)s>>>(a, b, out, n);
+  launch_pdl(k, (int)g, smem, (cudaStream_t)s, a, b, out, n);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return (int)cudaGetLastError();
 }
@@ -1252,7 +1275,7 @@ static int launch_queue(const T* a, const T* b, T* out, size_t n, vem_stream_t s
   size_t cap = (size_t)num_sms() * occ;
   size_t g = tiles < cap ? tiles : cap;
   if (g < 1) g = 1;
-  k<<<(int)g, kThreads, smem, (cudaStream_t)s>>>(a, b, out, n);
+  launch_pdl(k, (int)g, smem, (cudaStream_t)s, a, b, out, n);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return (int)cudaGetLastError();
 }
@@ -1275,7 +1298,7 @@ static int launch_fmod_w(const T* a, const T* b, T* out, size_t n, vem_stream_t 
   size_t w = warps < cap ? warps : cap;
   size_t g = (w + kThreads / 32 - 1) / (kThreads / 32);
   if (g < 1) g = 1;
-  k<<<(int)g, kThreads, smem, (cudaStream_t)s>>>(a, b, out, n);
+  launch_pdl(k, (int)g, smem, (cudaStream_t)s, a, b, out, n);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return (int)cudaGetLastError();
 }

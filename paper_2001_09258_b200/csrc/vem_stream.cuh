@@ -74,5 +74,17 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   return p;
 }
 
+// Programmatic dependent launch (the streaming kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization): `wait` blocks until
+// the previous grid in the stream has completed and its memory operations
+// are visible (a no-op without the attribute), so everything before it may
+// only touch kernel-private state (barrier init, constant-table staging);
+// `launch_dependents` lets the next grid's CTAs be scheduled as this grid's
+// CTAs exit, overlapping its launch and prologue with this grid's tail.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 }  // namespace tma
 }  // namespace vem

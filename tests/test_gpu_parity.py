@@ -191,3 +191,51 @@ def test_cw1_boundary_in_small_warps(cuda, name):
     idx = np.arange(0, n, 997)
     x[idx] = edge[np.arange(idx.size) % edge.size]
     _assert_bit_exact(name, _gpu(name, x), oracle_eval(name, x), x)
+
+
+def test_chained_launches_in_place(cuda):
+    """Programmatic dependent launch (tma::griddep_wait): a grid may start while
+    the previous one in the stream drains, so every read of an input written
+    by the previous grid must wait for it.  A chain of dependent, in-place
+    calls on one stream (each reads the previous call's output) must equal
+    the oracle composed the same way, over 2^24 elements (many tiles per CTA,
+    back-to-back launches with no host synchronisation in between)."""
+    import torch
+    from paper_2001_09258_b200 import api
+    n = 1 << 24
+    x = unary_cases("sin_d_u10", n)[:n].copy()
+    x = np.where(np.isfinite(x), np.clip(x, -700.0, 700.0), 0.5)
+    buf = torch.from_numpy(x).cuda()
+    chain = ["sin_d_u10", "exp_d_u10", "log_d_u35", "cos_d_u10", "exp_d_u35", "tan_d_u10"]
+    for name in chain:
+        api.call(name, buf, out=buf)  # in place: reads what the previous grid wrote
+    sub = np.arange(0, n, 61)  # the oracle on a sample of the lanes
+    exp = x[sub]
+    for name in chain:
+        exp = oracle_eval(name, exp)
+    got = buf.cpu().numpy()[sub]
+    _assert_bit_exact("chain", got, exp, x[sub])
+
+
+def test_chained_launches_mixed_kernels(cuda):
+    """Dependent calls across the three streaming kernel families (TMA stream,
+    CTA work queue, warp-private work queue) on one stream."""
+    import torch
+    from paper_2001_09258_b200 import api
+    n = (1 << 22) + 77
+    x, y = binary_cases("fmod_d", n)
+    x, y = x[:n].copy(), y[:n].copy()
+    tx, ty = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    t1 = api.call("fmod_d", tx, ty)            # CTA work queue
+    t2 = api.call("exp_d_u10", t1)             # TMA stream, reads t1
+    t3 = api.call("fmod_d", t2, ty)            # reads t2
+    f1 = api.call("fmod_f", t3.float(), ty.float())  # warp-private queue
+    f2 = api.call("log_f_u10", f1)
+    sub = np.arange(0, n, 7)
+    e1 = oracle_eval("fmod_d", x[sub], y[sub])
+    e2 = oracle_eval("exp_d_u10", e1)
+    e3 = oracle_eval("fmod_d", e2, y[sub])
+    g1 = oracle_eval("fmod_f", e3.astype(np.float32), y[sub].astype(np.float32))
+    g2 = oracle_eval("log_f_u10", g1)
+    _assert_bit_exact("chain_d", t3.cpu().numpy()[sub], e3, x[sub])
+    _assert_bit_exact("chain_f", f2.cpu().numpy()[sub], g2, x[sub])
