@@ -12,6 +12,10 @@ __m512d Sleef_sind8_u10avx512f(__m512d);
 __m512d Sleef_cosd8_u10avx512f(__m512d);
 __m512d Sleef_tand8_u10avx512f(__m512d);
 __m512d Sleef_atand8_u10avx512f(__m512d);
+__m512d Sleef_sind8_u35avx512f(__m512d);
+__m512d Sleef_cosd8_u35avx512f(__m512d);
+__m512d Sleef_tand8_u35avx512f(__m512d);
+__m512d Sleef_atand8_u35avx512f(__m512d);
 __m512d Sleef_expd8_u10avx512f(__m512d);
 __m512d Sleef_logd8_u10avx512f(__m512d);
 __m512d Sleef_logd8_u35avx512f(__m512d);
@@ -48,6 +52,8 @@ static void* pick(const char* n, int* kind) {
   M("log_f_u10", Sleef_logf16_u10avx512f, 2) M("log_f_u35", Sleef_logf16_u35avx512f, 2)
   M("pow_f_u10", Sleef_powf16_u10avx512f, 3) M("pow_f_u35", Sleef_powf16_u10avx512f, 3)
   M("fmod_f", Sleef_fmodf16_avx512f, 3)
+  M("sin_d_u35", Sleef_sind8_u35avx512f, 0) M("cos_d_u35", Sleef_cosd8_u35avx512f, 0)
+  M("tan_d_u35", Sleef_tand8_u35avx512f, 0) M("atan_d_u35", Sleef_atand8_u35avx512f, 0)
 #undef M
   return 0;
 }
