@@ -1110,8 +1110,9 @@ VEM_SPLIT_BINARY_OP(OpPowD, double, pow_d_u10(x, y, tab), (pow_fast_d<VEM_LOG1P_
                     pow_slow_split_d(y, r, code, full))
 VEM_SPLIT_BINARY_OP(OpPowDU35, double, pow_d_u35(x, y, tab),
                     (pow_fast_d<VEM_LOG1P_D_U35_N>(x, y, cLog1pDU35, tab, code)), pow_slow_split_d(y, r, code, full))
-// fmod: regrouped by step class (exponent gap / 50 in 6 ranges) so the
-// lanes of a row run similar long-division trip counts
+// fmod functors: operator() is the full function (unaligned pointers, tails);
+// the step-class regrouping traits serve only the tuning build's variant 7
+// (the shipped entry points use the tile work queue, FmodQ)
 struct OpFmodD {
   __device__ __forceinline__ double operator()(double x, double y, const double* tab) const {
     (void)tab;

@@ -677,8 +677,11 @@ __device__ __forceinline__ double pow_d_u35(double x, double y, const double* lt
 }
 
 // fmod: normalised-mantissa FP long division (oracle: fmod_core).  The
-// per-element state is split into setup / step / finish so the kernel can
-// refill lanes (vem_kernels.cu: k_fmod).
+// shipped kernels (vem_kernels.cu: k_queue / k_wqueue with FmodQ) triage on
+// the operand bits and run fmod_pend_setup / fmod_step50 / fmod_pend_finish
+// on sorted queue rows; fmod_core is the full per-element function (tails,
+// unaligned pointers); the setup / step / finish split below also serves the
+// tuning build's work-ring kernel.
 __device__ __forceinline__ int ilogb_pos(double x) {
   uint64_t b = bits_d(x);
   int e = (int)(b >> 52);
@@ -763,7 +766,8 @@ __device__ __forceinline__ double fmod_core(double x, double y) {
   return fmod_finish(st);
 }
 __device__ __forceinline__ double fmod_d(double x, double y) { return fmod_core(x, y); }
-// Work class of a pair for the kernels' regrouping: the number of 50-bit
+// Work class of a pair for the warp regrouping of k_stream (tuning build
+// variant only since the tile work queue replaced it): the number of 50-bit
 // steps from the biased exponents (subnormals counted as exponent 0; only a
 // scheduling hint, results do not depend on it), bucketed into 6 ranges.
 constexpr int kFmodClasses = 6;
