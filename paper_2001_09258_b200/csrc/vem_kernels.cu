@@ -178,6 +178,9 @@ template <class Op> struct SortsByClass {
 };
 // ops with a branch-free Cody-Waite-level-1 body for all-small warps
 template <class Op> struct HasCw1 { static constexpr bool value = false; };
+// ops with a closed-form result for "trivial" inputs (trig: |x| < 2^-27 and
+// non-finite x), which the class regrouping leaves out of the sorted rows
+template <class Op> struct HasTrivial { static constexpr bool value = false; };
 
 // Ops with a split fast path (vem_math.cuh "split fast paths"): the kernel
 // evaluates a tile's elements with Op::fast (branch-free, interleavable)
@@ -290,6 +293,19 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
         c_l0 = __shfl_sync(0xffffffffu, cl[0], 0);
         uniform = __all_sync(0xffffffffu, same && cl[0] == c_l0);
       }
+      bool triv[NE];
+      T tres[NE];
+#pragma unroll
+      for (int e = 0; e < NE; e++) {
+        if constexpr (HasTrivial<Op>::value) {
+          triv[e] = Op::is_trivial(xe[e]);
+          tres[e] = Op::trivial(xe[e]);
+        } else {
+          triv[e] = false;
+          tres[e] = xe[e];
+        }
+      }
+      int nplaced = 32 * NE;
       auto regroup = [&]() {
         // counting sort of the warp's 32*NE elements by class, heaviest
         // class first: ballots per (row, class), prefix popcounts
@@ -297,30 +313,37 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
         T* sy = wscr2 + (tid >> 5) * (32 * NE);
         unsigned short* si = widx + (tid >> 5) * (32 * NE);
         if constexpr (K == 3) {
-          // trig: two ballots per row, explicit three-way positions
-          unsigned m2[NE], m1[NE];
+          // trig: two ballots per row, explicit three-way positions;
+          // trivial elements (HasTrivial) are not placed: their results
+          // stay in registers and the rows past the last placed one are
+          // skipped
+          unsigned m2[NE], m1[NE], m0[NE];
           int n2 = 0, n1 = 0;
 #pragma unroll
           for (int e = 0; e < NE; e++) {
-            m2[e] = __ballot_sync(0xffffffffu, cl[e] == 2);
-            m1[e] = __ballot_sync(0xffffffffu, cl[e] == 1);
+            const bool pl = !triv[e];
+            m2[e] = __ballot_sync(0xffffffffu, pl && cl[e] == 2);
+            m1[e] = __ballot_sync(0xffffffffu, pl && cl[e] == 1);
+            m0[e] = HasTrivial<Op>::value ? __ballot_sync(0xffffffffu, pl && cl[e] == 0) : ~(m2[e] | m1[e]);
             n2 += __popc(m2[e]);
             n1 += __popc(m1[e]);
           }
           int a2 = 0, a1 = n2, a0 = n2 + n1;  // heaviest class first
 #pragma unroll
           for (int e = 0; e < NE; e++) {
-            const unsigned m0 = ~(m2[e] | m1[e]);
             const int pos = cl[e] == 2 ? a2 + __popc(m2[e] & lt_mask)
                           : cl[e] == 1 ? a1 + __popc(m1[e] & lt_mask)
-                                       : a0 + __popc(m0 & lt_mask);
+                                       : a0 + __popc(m0[e] & lt_mask);
             a2 += __popc(m2[e]);
             a1 += __popc(m1[e]);
-            a0 += __popc(m0);
-            sx[pos] = xe[e];
-            if constexpr (NIN == 2) sy[pos] = ye[e];
-            si[pos] = (unsigned short)(e * 32 + lane);
+            a0 += __popc(m0[e]);
+            if (!triv[e]) {
+              sx[pos] = xe[e];
+              if constexpr (NIN == 2) sy[pos] = ye[e];
+              si[pos] = (unsigned short)(e * 32 + lane);
+            }
           }
+          nplaced = a0;
         } else {
           // K classes: per-warp class cursors in shared memory; lanes of one
           // class in a row are ranked by match_any, the group's lowest lane
@@ -360,22 +383,29 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
         int ids[NE];
 #pragma unroll
         for (int r = 0; r < NE; r++) {
-          xs[r] = sx[r * 32 + lane];
-          if constexpr (NIN == 2) ys[r] = sy[r * 32 + lane];
-          ids[r] = si[r * 32 + lane];
+          // past the last placed element a lane repeats its row's first
+          // entry (same class: no divergence); its result is not written
+          const int i = r * 32 + lane < nplaced ? r * 32 + lane : r * 32;
+          xs[r] = sx[i];
+          if constexpr (NIN == 2) ys[r] = sy[i];
+          ids[r] = r * 32 + lane < nplaced ? si[i] : -1;
         }
         __syncwarp();
 #pragma unroll
         for (int r = 0; r < NE; r++) {
-          if constexpr (NIN == 2) sx[ids[r]] = op(xs[r], ys[r], tab);
-          else sx[ids[r]] = op(xs[r], tab);
+          if (r * 32 < nplaced) {  // warp-uniform
+            T yv;
+            if constexpr (NIN == 2) yv = op(xs[r], ys[r], tab);
+            else yv = op(xs[r], tab);
+            if (ids[r] >= 0) sx[ids[r]] = yv;
+          }
         }
         __syncwarp();
 #pragma unroll
         for (int v = 0; v < VPT; v++) {
           V o;
 #pragma unroll
-          for (int k = 0; k < W; k++) vget(o, k) = sx[(v * W + k) * 32 + lane];
+          for (int k = 0; k < W; k++) vget(o, k) = triv[v * W + k] ? tres[v * W + k] : sx[(v * W + k) * 32 + lane];
           __stcs(ov + v * kThreads + tid, o);
         }
         __syncwarp();
@@ -1018,6 +1048,16 @@ __global__ void __launch_bounds__(kFmodWarps * 32, MINB) k_fmod(const T* __restr
   struct NAME {                                                                       \
     __device__ __forceinline__ T operator()(T x, const double* tab) const { return EXPR; } \
   };
+// Trivial trig inputs: |x| < 2^-27 (incl. zeros and subnormals) and non-finite
+// x.  For |x| < 2^-27 every sin/tan form returns x exactly and every cos form
+// 1.0 (the polynomial terms are below half an ulp: |x|^3/6 < 2^-54 |x|,
+// x^2/2 < 2^-55), and the selector's own finals give +-0 -> x / 1.0 and
+// Inf/NaN -> the canonical NaN; the GPU parity and digest tests pin this on
+// random bit patterns.
+__device__ __forceinline__ bool trig_is_trivial(double x) {
+  const uint32_t h = (uint32_t)__double2hiint(x) & 0x7fffffffu;
+  return h < 0x3E400000u || h >= 0x7ff00000u;
+}
 #define VEM_TRIG_OP(NAME, FN, ...)                                                       \
   struct NAME {                                                                          \
     __device__ __forceinline__ double operator()(double x, const double* tab) const {   \
@@ -1028,6 +1068,8 @@ __global__ void __launch_bounds__(kFmodWarps * 32, MINB) k_fmod(const T* __restr
     }                                                                                    \
     __device__ __forceinline__ static int cls(double x) { return trig_class(x); }      \
     __device__ __forceinline__ static bool is_cw1(double x) { return trig_is_cw1(x); } \
+    __device__ __forceinline__ static bool is_trivial(double x) { return trig_is_trivial(x); } \
+    __device__ static double trivial(double x);                                          \
   };                                                                                     \
   template <> struct SortsByClass<NAME> {                                                \
     static constexpr bool value = true;                                                  \
@@ -1042,6 +1084,19 @@ VEM_TRIG_OP(OpSinDU35, sin_d_u35, , tab)
 VEM_TRIG_OP(OpCosDU35, cos_d_u35, , tab)
 VEM_TRIG_OP(OpTanDU35, tan_d_u35)
 #undef VEM_TRIG_OP
+// TINY: the result for a finite trivial x
+#define VEM_TRIG_TINY(NAME, TINY)                                                         \
+  template <> struct HasTrivial<NAME> { static constexpr bool value = true; };           \
+  __device__ __forceinline__ double NAME::trivial(double x) {                              \
+    return ((uint32_t)__double2hiint(x) & 0x7fffffffu) >= 0x7ff00000u ? from_bits_d(kCanonNanD) : (TINY); \
+  }
+VEM_TRIG_TINY(OpSinD, x)
+VEM_TRIG_TINY(OpCosD, 1.0)
+VEM_TRIG_TINY(OpTanD, x)
+VEM_TRIG_TINY(OpSinDU35, x)
+VEM_TRIG_TINY(OpCosDU35, 1.0)
+VEM_TRIG_TINY(OpTanDU35, x)
+#undef VEM_TRIG_TINY
 VEM_UNARY_OP(OpSinDPh, double, (sin_d_u10<kPh>(x, tab, tab + 4 * VEM_PH_D_ENTRIES)))
 VEM_UNARY_OP(OpCosDPh, double, (cos_d_u10<kPh>(x, tab, tab + 4 * VEM_PH_D_ENTRIES)))
 VEM_UNARY_OP(OpTanDPh, double, (tan_d_u10<kPh>(x, tab)))

@@ -239,3 +239,22 @@ def test_chained_launches_mixed_kernels(cuda):
     g2 = oracle_eval("log_f_u10", g1)
     _assert_bit_exact("chain_d", t3.cpu().numpy()[sub], e3, x[sub])
     _assert_bit_exact("chain_f", f2.cpu().numpy()[sub], g2, x[sub])
+
+
+@pytest.mark.parametrize("name", ["sin_d_u10", "cos_d_u10", "tan_d_u10", "sin_d_u35", "cos_d_u35", "tan_d_u35"])
+def test_trig_trivial_elements_in_mixed_warps(cuda, name):
+    """The class regrouping keeps |x| < 2^-27, zeros, subnormals and Inf/NaN
+    out of the sorted rows and writes their closed-form result (x, 1.0 or the
+    canonical NaN).  Warps mixing them with Payne-Hanek, CW2 and CW1 lanes,
+    and values straddling 2^-27, must still equal the oracle bit for bit."""
+    from paper_2001_09258_b200 import inputs as I
+    n = 1 << 18
+    rng = np.random.default_rng(2027)
+    t = 2.0 ** -27
+    pool = np.array([t, -t, np.nextafter(t, 0.0), -np.nextafter(t, 0.0), np.nextafter(t, 1.0), 0.0, -0.0,
+                     5e-324, -5e-324, 2.2250738585072014e-308, np.inf, -np.inf, np.nan, 1e-300, 3e-9, 7.4e-9,
+                     7.5e-9, 1e100, -1e300, 123456.789, 1e13, 2.0, -14.9, 15.0], dtype=np.float64)
+    x = I.log_uniform(91, n, 1e-300, 1e300, np.float64, signed=True)
+    sel = rng.random(n) < 0.3
+    x[sel] = pool[rng.integers(0, pool.size, int(sel.sum()))]
+    _assert_bit_exact(name, _gpu(name, x), oracle_eval(name, x), x)
