@@ -512,10 +512,12 @@ def e2e_leg(work, bufs, outs, n, args, dev, stream, world):
     entry points of one function read the same arrays, so each input array is
     uploaded once), runs every entry point, and reads every result back
     device->host into its own pinned buffer; chunked over three streams so
-    copies in both directions overlap the kernels."""
+    copies in both directions overlap the kernels (4 streams, 2^24-element
+    chunks: the best of a chunk x stream sweep, profiles/r01_e2e_sweep.log)."""
     import torch
     from paper_2001_09258_b200 import api
-    chunk = 1 << 24
+    chunk = 1 << int(os.environ.get("VEM_E2E_CHUNK_LOG2", "24"))
+    nstreams = int(os.environ.get("VEM_E2E_STREAMS", "4"))
     n = min(n, 1 << 26)  # 2^26 elements per entry point per rank (bounded pinned memory)
     groups = []  # (device input list, [(entry name, work index)])
     for i, (name, _) in enumerate(work):
@@ -528,7 +530,7 @@ def e2e_leg(work, bufs, outs, n, args, dev, stream, world):
     host_in = {id(g[0]): [t[:n].to("cpu").pin_memory() for t in g[0]] for g in groups}
     host_out = [torch.empty(n, dtype=bufs[i][0].dtype).pin_memory() for i in range(len(work))]
     dev_out = [torch.empty(n, dtype=bufs[i][0].dtype, device=dev) for i in range(len(work))]
-    streams = [torch.cuda.Stream(dev) for _ in range(3)]
+    streams = [torch.cuda.Stream(dev) for _ in range(nstreams)]
     h2d = sum(t.numel() * t.element_size() for v in host_in.values() for t in v)
     d2h = sum(h.numel() * h.element_size() for h in host_out)
 
@@ -537,7 +539,7 @@ def e2e_leg(work, bufs, outs, n, args, dev, stream, world):
             hin = host_in[id(dins)]
             for j, c0 in enumerate(range(0, n, chunk)):
                 c1 = min(n, c0 + chunk)
-                s = streams[j % 3]  # a given range always uses the same stream
+                s = streams[j % nstreams]  # a given range always uses the same stream
                 with torch.cuda.stream(s):
                     for hd, dd_ in zip(hin, dins):
                         dd_[c0:c1].copy_(hd[c0:c1], non_blocking=True)
@@ -556,7 +558,7 @@ def e2e_leg(work, bufs, outs, n, args, dev, stream, world):
     return {"value": round(len(work) * n * world / dt / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": round(dt * 1e3, 2), "steps": steps,
             "elements_per_entry_point_per_rank": n,
-            "path": "pinned host -> H2D (each distinct input once, chunked 2^24, 3 streams) -> vem C ABI "
+            "path": "pinned host -> H2D (each distinct input once, chunked 2^24, 4 streams) -> vem C ABI "
                     "(every entry point) -> D2H of every result, host wall clock"}
 
 
