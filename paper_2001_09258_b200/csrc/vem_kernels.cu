@@ -1455,6 +1455,8 @@ static int launch_tuned(const T* a, const T* b, T* o, size_t n, vem_stream_t s) 
     case 6: return launch_stream<Op, T, NIN, TAB, VPT, ST, 2>(a, b, o, n, s);
     case 7: return launch_stream<Op, T, NIN, TAB, VPT, ST, 3>(a, b, o, n, s);
     case 8: return launch_stream<Op, T, NIN, TAB, VPT, ST, 4>(a, b, o, n, s);
+    case 9: return launch_stream<Op, T, NIN, TAB, 4, 2, 2>(a, b, o, n, s);
+    case 10: return launch_stream<Op, T, NIN, TAB, 4, 2, 3>(a, b, o, n, s);
     default: return launch_stream<Op, T, NIN, TAB, VPT, ST, MINB>(a, b, o, n, s);
   }
 }
@@ -1486,8 +1488,8 @@ static int launch_fmod_tuned(const T* a, const T* b, T* o, size_t n, vem_stream_
 extern "C" {
 
 int vem_sin_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpSinD, double, 1, kTableDG, 2, 2, 4>(x, nullptr, y, n, s); }
-int vem_cos_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpCosD, double, 1, kTableDG, 2, 2, 4>(x, nullptr, y, n, s); }
-int vem_tan_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpTanD, double, 1, kTableDG, 4, 2>(x, nullptr, y, n, s); }
+int vem_cos_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpCosD, double, 1, kTableDG, 4, 2, 3>(x, nullptr, y, n, s); }
+int vem_tan_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpTanD, double, 1, kTableDG, 4, 2, 3>(x, nullptr, y, n, s); }
 int vem_sin_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpSinDPh, double, 1, kTableD, 2, 2>(x, nullptr, y, n, s); }
 int vem_cos_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpCosDPh, double, 1, kTableD, 2, 2>(x, nullptr, y, n, s); }
 int vem_tan_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpTanDPh, double, 1, kTableD, 2, 2>(x, nullptr, y, n, s); }
@@ -1528,9 +1530,9 @@ int vem_fmod_f(const float* x, const float* y2, float* o, size_t n, vem_stream_t
 }
 
 // ---- SURVEY.md §8(f).1 additions
-int vem_sin_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpSinDU35, double, 1, kTableDG35, 2, 2, 3>(x, nullptr, y, n, s); }
-int vem_cos_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpCosDU35, double, 1, kTableDG35, 2, 2, 3>(x, nullptr, y, n, s); }
-int vem_tan_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpTanDU35, double, 1, kTableDG35, 2, 2, 3>(x, nullptr, y, n, s); }
+int vem_sin_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpSinDU35, double, 1, kTableDG35, 4, 2, 3>(x, nullptr, y, n, s); }
+int vem_cos_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpCosDU35, double, 1, kTableDG35, 4, 2, 3>(x, nullptr, y, n, s); }
+int vem_tan_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpTanDU35, double, 1, kTableDG35, 4, 2, 3>(x, nullptr, y, n, s); }
 int vem_atan_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpAtanDU35, double, 1, kNoTable, 2, 2>(x, nullptr, y, n, s); }
 int vem_asin_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpAsinD, double, 1, kNoTable, 2, 2>(x, nullptr, y, n, s); }
 int vem_asin_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpAsinDU35, double, 1, kNoTable, 2, 2>(x, nullptr, y, n, s); }
