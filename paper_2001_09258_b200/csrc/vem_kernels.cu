@@ -1162,9 +1162,9 @@ VEM_SPLIT_UNARY_OP(OpLogFU35, float, (log_f_u35(x, tab)), (log_fast_f<VEM_LOG1P_
   };                                                                              \
   template <> struct HasFast<NAME> { static constexpr bool value = true; };
 VEM_SPLIT_BINARY_OP(OpPowD, double, pow_d_u10(x, y, tab), (pow_fast_d<VEM_LOG1P_D_N>(x, y, cLog1pD, tab, code)),
-                    pow_slow_split_d(y, r, code, full))
+                    pow_slow_split_d(x, y, r, code, full))
 VEM_SPLIT_BINARY_OP(OpPowDU35, double, pow_d_u35(x, y, tab),
-                    (pow_fast_d<VEM_LOG1P_D_U35_N>(x, y, cLog1pDU35, tab, code)), pow_slow_split_d(y, r, code, full))
+                    (pow_fast_d<VEM_LOG1P_D_U35_N>(x, y, cLog1pDU35, tab, code)), pow_slow_split_d(x, y, r, code, full))
 // fmod functors: operator() is the full function (unaligned pointers, tails);
 // the step-class regrouping traits serve only the tuning build's variant 7
 // (the shipped entry points use the tile work queue, FmodQ)

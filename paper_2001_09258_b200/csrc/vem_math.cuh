@@ -1244,9 +1244,29 @@ __device__ __forceinline__ double pow_fast_d(double x, double y, const double* c
 __device__ __forceinline__ double pow_neg_fix_d(double R, double y) {
   return is_int_d(y) ? (is_odd_d(y) ? -R : R) : from_bits_d(kCanonNanD);
 }
+// x in {+-0, +-Inf, NaN} with y finite and nonzero: pow_slow_d's C99 Annex F
+// results, selected inline (these are most of the flagged specials; the
+// out-of-line call costs the warp ~150 instructions per occurrence)
+__device__ __forceinline__ double pow_special_x_d(double x, double y) {
+  const bool yodd = is_odd_d(y);
+  double res;
+  if (x == 0.0) res = (y < 0.0) ? (yodd ? copysign_b(kInf, x) : kInf) : (yodd ? x : 0.0);
+  else res = (y < 0.0) ? ((yodd && x < 0.0) ? -0.0 : 0.0) : ((yodd && x < 0.0) ? -kInf : kInf);
+  return (x != x) ? from_bits_d(kCanonNanD) : res;
+}
 template <class F>
-__device__ __forceinline__ double pow_slow_split_d(double y, double r, int code, F full) {
-  if (code & 1) return full();
+__device__ __forceinline__ double pow_slow_split_d(double x, double y, double r, int code, F full) {
+  if (code & 1) {
+    // x in {+-0, +-Inf, NaN} with an ordinary y: inline; everything else
+    // flagged here (subnormal x, special y, t in the saturation margin)
+    // needs the full function
+    const uint32_t hx = (uint32_t)__double2hiint(x) & 0x7fffffffu;
+    const uint32_t hy = (uint32_t)__double2hiint(y) & 0x7fffffffu, ly = (uint32_t)__double2loint(y);
+    const bool fy = (hy < 0x7ff00000u) && ((hy | ly) != 0u);
+    const bool sx = hx >= 0x7ff00000u || is_zero_bits(x);
+    if (fy && sx) return pow_special_x_d(x, y);
+    return full();
+  }
   r = (code & 4) ? kInf : ((code & 8) ? 0.0 : r);
   return (code & 2) ? pow_neg_fix_d(r, y) : r;
 }
