@@ -71,6 +71,7 @@ def parse():
     ap.add_argument("--log2n", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-verify", action="store_true")
     return ap.parse_args()
 
 
@@ -421,6 +422,13 @@ def main():
     elems_step = len(work) * n * world
     value = elems_step / (ms_step * 1e-3) / 1e9
 
+    # ---------------- verification (outside the timed region): the one
+    # collective of the sharded path -- every rank checks its shard, NCCL
+    # all-reduces {mismatch count: SUM, max ulp distance: MAX}
+    verify = None
+    if not args.no_verify:
+        verify = verify_leg(work, bufs, outs, n, dev, world, share)
+
     # ---------------- e2e: C ABI with HOST buffers (pinned), copies timed
     e2e = None
     if not args.no_e2e:
@@ -499,11 +507,62 @@ def main():
                            "l2": l2_note,
                            "parallelism": f"data-parallel shards x{world} (no collective on the data path)"},
                 "gpu_launches": int(launches), "clocks": clk, "roofline": roofline,
-                "per_function": per_function, "e2e": e2e, "cpu_baseline": cpu, "sleef_cpu": sleef}
+                "per_function": per_function, "e2e": e2e, "cpu_baseline": cpu, "sleef_cpu": sleef,
+                "verify": verify}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def verify_leg(work, bufs, outs, n, dev, world, share):
+    """Every entry point over the rank's whole shard twice: the shipped
+    TMA-pipelined / work-queue kernel (16-byte aligned buffers) and the plain
+    grid-stride kernel the library takes for misaligned pointers (same math,
+    independent load/store path, no staging or regrouping), compared bit for
+    bit on the device; per rank: mismatching elements (SUM) and the largest
+    ulp distance (MAX), combined over the ranks by one all-reduce each.  Bit
+    identity to the CPU oracle is the test suite's job (tests/); this checks,
+    at full scale on every shard, that the fast data path returns exactly
+    what the per-element function computes."""
+    import torch
+    import torch.distributed as dist
+    from paper_2001_09258_b200 import api
+    mism = 0
+    max_ulp = 0
+    checked = 0
+    for i, (name, _) in enumerate(work):
+        ins = bufs[i]
+        dt = ins[0].dtype
+        it = torch.int64 if dt == torch.float64 else torch.int32
+        a = api.call(name, *ins, out=outs[dt])
+        un = []
+        for t in ins:
+            u = torch.empty(n + 1, dtype=dt, device=dev)
+            u[1:].copy_(t)
+            un.append(u[1:])  # 4/8-byte offset: the misaligned (plain) path
+        ob = torch.empty(n + 1, dtype=dt, device=dev)
+        b = api.call(name, *un, out=ob[1:])
+        ai, bi = a.view(it), b.view(it)
+        ne = ai != bi
+        mism += int(ne.sum().item())
+        if bool(ne.any().item()):
+            # same-sign finite values: ulp distance = difference of the bit patterns
+            d = (ai.to(torch.int64) - bi.to(torch.int64)).abs()
+            max_ulp = max(max_ulp, int(d[ne].max().item()))
+        checked += n
+        del un, ob, b
+    torch.cuda.empty_cache()
+    if world > 1:
+        t = torch.tensor([mism, checked], dtype=torch.int64, device="cpu" if share else dev)
+        m = torch.tensor([max_ulp], dtype=torch.int64, device="cpu" if share else dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        dist.all_reduce(m, op=dist.ReduceOp.MAX)
+        mism, checked, max_ulp = int(t[0].item()), int(t[1].item()), int(m[0].item())
+    return {"elements": checked, "mismatches": mism, "max_ulp": max_ulp,
+            "compared": "TMA-pipelined / work-queue kernels vs the plain grid-stride kernel (misaligned "
+                        "pointers), bit for bit, every element of every shard",
+            "reduction": "all_reduce SUM (mismatches) and MAX (ulp) over the ranks"}
 
 
 def e2e_leg(work, bufs, outs, n, args, dev, stream, world):
