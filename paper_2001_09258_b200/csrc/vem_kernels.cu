@@ -1460,6 +1460,16 @@ static int launch_tuned(const T* a, const T* b, T* o, size_t n, vem_stream_t s) 
     default: return launch_stream<Op, T, NIN, TAB, VPT, ST, MINB>(a, b, o, n, s);
   }
 }
+// fmod without regrouping or queue (every lane loops to its warp's largest
+// step count): comparison only
+template <class T>
+struct OpFmodPlain {
+  __device__ __forceinline__ T operator()(T x, T y, const double* tab) const {
+    (void)tab;
+    if constexpr (sizeof(T) == 8) return fmod_d(x, y);
+    else return fmod_f(x, y);
+  }
+};
 #define VEM_STREAM launch_tuned
 template <class T>
 static int launch_fmod_tuned(const T* a, const T* b, T* o, size_t n, vem_stream_t s) {
@@ -1473,6 +1483,8 @@ static int launch_fmod_tuned(const T* a, const T* b, T* o, size_t n, vem_stream_
     case 5: return launch_fmod_q<T, 2, 2, 1, 2>(a, b, o, n, s);
     case 6: return launch_fmod_q<T, 4, 2, 1, 1>(a, b, o, n, s);
     case 7: return launch_stream<OpF, T, 2, kNoTable, 2, 2>(a, b, o, n, s);
+    case 9: return launch_stream<OpFmodPlain<T>, T, 2, kNoTable, 2, 2>(a, b, o, n, s);
+    case 10: return launch_stream<OpFmodPlain<T>, T, 2, kNoTable, 1, 2>(a, b, o, n, s);
     case 8: return launch_fmod<T>(a, b, o, n, s);
     default: return launch_fmod_q<T, 2, 2, 1, 1>(a, b, o, n, s);
   }
