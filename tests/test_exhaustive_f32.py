@@ -16,7 +16,8 @@ from oracle_lib import oracle_eval
 pytestmark = [pytest.mark.gpu,
               pytest.mark.skipif(os.environ.get("VEM_EXHAUSTIVE") != "1", reason="set VEM_EXHAUSTIVE=1")]
 
-FUNCS = ["sin_f_u10", "cos_f_u10", "tan_f_u10", "exp_f_u10", "exp_f_u35", "log_f_u10", "log_f_u35"]
+FUNCS = ["sin_f_u10", "cos_f_u10", "tan_f_u10", "exp_f_u10", "exp_f_u35", "log_f_u10", "log_f_u35",
+         "atan_f_u10", "atan_f_u35", "asin_f_u10", "asin_f_u35", "acos_f_u10", "acos_f_u35"]
 CHUNK = 1 << 28
 
 
