@@ -453,7 +453,10 @@ def main():
     prof = os.path.join(ROOT, "profiles", "kernel_metrics.json")
     if os.path.exists(prof):
         try:
-            km = json.load(open(prof)).get(dname, {})
+            allm = json.load(open(prof))
+            # metrics depend on the input mix: a capture of this workload's
+            # inputs (key "name@cfgN") wins over the entry point's default
+            km = allm.get(f"{dname}@{args.workload}", allm.get(dname, {}))
             if km.get("dram_bytes_per_elem") is not None:
                 traffic = km["dram_bytes_per_elem"] * n
             fp64_per_elem = km.get("fp64_inst_per_elem")

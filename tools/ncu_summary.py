@@ -1,7 +1,10 @@
 #!/usr/bin/env python3
 """Summarise an ncu report into per-kernel JSON + markdown (profiles/).
 
-Usage: python tools/ncu_summary.py REPORT.ncu-rep ELEMS_PER_LAUNCH OUT_PREFIX
+Usage: python tools/ncu_summary.py REPORT.ncu-rep ELEMS_PER_LAUNCH OUT_PREFIX [KEY_SUFFIX]
+
+KEY_SUFFIX (e.g. "@cfg5") is appended to the entry-point keys merged into
+kernel_metrics.json, for captures whose input mix is workload specific.
 
 For every profiled kernel: duration, DRAM bytes (read+write) per element,
 executed instructions per element, the dynamic SASS opcode mix (from the
@@ -61,6 +64,7 @@ def entry_of(kname):
 
 def main():
     rep, elems, prefix = sys.argv[1], int(sys.argv[2]), sys.argv[3]
+    suffix = sys.argv[4] if len(sys.argv) > 4 else ""
     raw = list(csv.reader(io.StringIO(ncu("-i", rep, "--page", "raw", "--csv"))))
     hdr, units, data = raw[0], raw[1], raw[2:]
     col = {k: hdr.index(v) for k, v in RAW.items() if v in hdr}
@@ -128,7 +132,7 @@ def main():
         km_path = os.path.join(ROOT, "profiles", "kernel_metrics.json")
         km = json.load(open(km_path)) if os.path.exists(km_path) else {}
         for n, d in out.items():
-            km[n] = {"dram_bytes_per_elem": d["dram_bytes_per_elem"],
+            km[n + suffix] = {"dram_bytes_per_elem": d["dram_bytes_per_elem"],
                      "fp64_inst_per_elem": d.get("fp64_inst_per_elem"),
                      "inst_per_elem": d["inst_per_elem"], "source": os.path.basename(prefix)}
         json.dump(km, open(km_path, "w"), indent=1, sort_keys=True)

@@ -1,8 +1,10 @@
 #!/usr/bin/env python3
 """Run one entry point on one BASELINE config's inputs (dev tool for ncu).
 
-Usage: python tools/prof_one.py NAME CFG [log2_n=24] [reps=3]
-e.g.  ncu --set full -k regex:OpSinD python tools/prof_one.py sin_d_u10 5 24
+Usage: python tools/prof_one.py NAME[,NAME...] CFG [log2_n=24] [reps=3]
+e.g.  ncu --set full -k regex:k_stream -s 1 -c 1 python tools/prof_one.py sin_d_u10 5 24
+reps=0: each entry point runs exactly once, no warm-up (one ncu capture per
+entry point with -c <number of names>).
 Prints Gelem/s (CUDA events) so the same command also runs without ncu.
 """
 import os
@@ -17,12 +19,22 @@ from paper_2001_09258_b200 import inputs as I  # noqa: E402
 
 
 def main():
-    name, cfg = sys.argv[1], int(sys.argv[2])
+    cfg = int(sys.argv[2])
     n = 1 << (int(sys.argv[3]) if len(sys.argv) > 3 else 24)
     reps = int(sys.argv[4]) if len(sys.argv) > 4 else 3
+    for name in sys.argv[1].split(","):
+        run(name, cfg, n, reps)
+
+
+def run(name, cfg, n, reps):
     fn, p = name.split("_")[0], name.split("_")[1]
     ts = [torch.from_numpy(a).cuda() for a in I.config_inputs(cfg, fn, p, n)]
     out = torch.empty_like(ts[0])
+    if reps == 0:
+        api.call(name, *ts, out=out)
+        torch.cuda.synchronize()
+        print(f"{name} cfg{cfg} n={n}: ran once")
+        return
     api.call(name, *ts, out=out)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
