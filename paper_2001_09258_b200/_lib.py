@@ -9,7 +9,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libvem.so")
+# VEM_LIB: an alternative build of the same library (A/B timing of two builds)
+LIB_PATH = os.environ.get("VEM_LIB") or os.path.join(HERE, "libvem.so")
 
 _P = ctypes.c_void_p
 _N = ctypes.c_size_t

@@ -209,9 +209,11 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
   extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ uint64_t bars[STAGES];
   __shared__ __align__(16) double stab[TableSize<TABLE>::n];
-  __shared__ __align__(16) T wscr[kSort ? kThreads * NE : 1];
-  __shared__ __align__(16) T wscr2[kSort && NIN == 2 ? kThreads * NE : 1];
-  __shared__ unsigned short widx[kSort ? kThreads * NE : 1];
+  // + 32 junk slots at the end: unplaced (trivial) elements store there
+  // unconditionally instead of branching around the store
+  __shared__ __align__(16) T wscr[kSort ? kThreads * NE + 32 : 1];
+  __shared__ __align__(16) T wscr2[kSort && NIN == 2 ? kThreads * NE + 32 : 1];
+  __shared__ unsigned short widx[kSort ? kThreads * NE + 32 : 1];
   __shared__ int wcur[kSort ? kThreads / 32 * 8 : 1];
   V* buf = reinterpret_cast<V*>(dsm);
   const int tid = threadIdx.x;
@@ -329,19 +331,19 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
             n1 += __popc(m1[e]);
           }
           int a2 = 0, a1 = n2, a0 = n2 + n1;  // heaviest class first
+          // junk slot of this lane (past every warp's block), relative to sx
+          const int junk = kThreads * NE + lane - (tid >> 5) * (32 * NE);
 #pragma unroll
           for (int e = 0; e < NE; e++) {
-            const int pos = cl[e] == 2 ? a2 + __popc(m2[e] & lt_mask)
-                          : cl[e] == 1 ? a1 + __popc(m1[e] & lt_mask)
-                                       : a0 + __popc(m0[e] & lt_mask);
+            const unsigned mk = cl[e] == 2 ? m2[e] : (cl[e] == 1 ? m1[e] : m0[e]);
+            const int base = cl[e] == 2 ? a2 : (cl[e] == 1 ? a1 : a0);
+            const int pos = triv[e] ? junk : base + __popc(mk & lt_mask);
             a2 += __popc(m2[e]);
             a1 += __popc(m1[e]);
             a0 += __popc(m0[e]);
-            if (!triv[e]) {
-              sx[pos] = xe[e];
-              if constexpr (NIN == 2) sy[pos] = ye[e];
-              si[pos] = (unsigned short)(e * 32 + lane);
-            }
+            sx[pos] = xe[e];
+            if constexpr (NIN == 2) sy[pos] = ye[e];
+            si[pos] = (unsigned short)(e * 32 + lane);
           }
           nplaced = a0;
         } else {
