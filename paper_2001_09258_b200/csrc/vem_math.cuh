@@ -250,7 +250,12 @@ __device__ __forceinline__ red cw1(double x) {
   double r0 = fma(qd, -kCw1P0, x);
   dd tail = two_prod(qd, -kCw1T1);
   tail.lo = fma(qd, -kCw1T2, tail.lo);
-  dd r = dd_normalize(dd_add2(dd{r0, 0.0}, tail));
+  // dd_add2({r0, 0}, tail) without the "+ 0.0": that add only turns a -0
+  // tail.lo into +0, which changes no result bit of any caller (the residual
+  // lo only enters sums with nonzero terms; tests pin CW1 bit for bit)
+  double s = r0 + tail.hi, v = s - r0;
+  double e = (r0 - (s - v)) + (tail.hi - v);
+  dd r = dd_normalize(dd{s, e + tail.lo});
   return {r.hi, r.lo, (int)qd & 3};  // |qd| <= 10
 }
 
@@ -693,21 +698,19 @@ __device__ __forceinline__ double mant_1_2(double x, int e) {
   return from_bits_d(m | 0x3ff0000000000000ull);
 }
 // One step of up to 50 bits: (r * 2^s) mod md, exactly (r < md, md in
-// [1,2), rmd <= 1/md within 2 ulps).  The quotient estimate
-// Q = trunc(RZ(rs * rmd)) is floor(rs/md) or one less (relative error
-// < 2^-51 on a quotient < 2^50), so the true remainders V1 = rs - Q*md in
-// [0, 2 md) and V2 = V1 - md satisfy: V2 >= 0 exactly when Q is one short.
-// Each FMA is exact whenever its value is selected: rs and Q*md are
-// multiples of 2^-52, so V1 (< md < 2 when kept) and V2 (in [0, md)) are
-// representable; a rounded V1 >= 2 or a negative V2 only feeds the
-// comparison, whose sign RN preserves.  Every step is exact, so the result
-// equals the oracle's (vem_oracle.c fmod_step: two_prod, 50-bit steps from
-// the top) bit for bit although the step split differs.
+// [1,2), rmd <= 1/md within 2 ulps).  Q1 = trunc(RZ(rs * rmd + 1)) equals
+// floor(rs * rmd) + 1 (one DFMA.RZ: RZ never rounds below the integer
+// floor(rs*rmd) + 1, which is representable), and floor(rs * rmd) is
+// floor(rs/md) or one less (relative error < 2^-51 on a quotient < 2^50), so
+// Q1 is floor(rs/md) or one more and V = rs - Q1*md lies in [-md, md).  rs
+// and Q1*md are multiples of 2^-52, so V (|V| < 2) is representable and the
+// FMA exact; V < 0 takes V + md, exact in [0, md).  Every step is exact, so
+// the result equals the oracle's (vem_oracle.c fmod_step: two_prod, 50-bit
+// steps from the top) bit for bit although the step split differs.
 __device__ __forceinline__ double fmod_step_rs(double rs, double md, double rmd) {
-  const double Q = trunc(__dmul_rz(rs, rmd));
-  const double V1 = fma(-Q, md, rs);
-  const double V2 = fma(-(Q + 1.0), md, rs);
-  return (V2 >= 0.0) ? V2 : V1;
+  const double Q1 = trunc(__fma_rz(rs, rmd, 1.0));
+  const double V = fma(-Q1, md, rs);
+  return (V < 0.0) ? V + md : V;
 }
 __device__ __forceinline__ double fmod_step(double r, int s, double md, double rmd) {
   return fmod_step_rs(r * __hiloint2double((1023 + s) << 20, 0), md, rmd);
