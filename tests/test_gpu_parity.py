@@ -258,3 +258,38 @@ def test_trig_trivial_elements_in_mixed_warps(cuda, name):
     sel = rng.random(n) < 0.3
     x[sel] = pool[rng.integers(0, pool.size, int(sel.sum()))]
     _assert_bit_exact(name, _gpu(name, x), oracle_eval(name, x), x)
+
+
+def test_cuda_graph_capture_and_replay(cuda):
+    """A chain of vem calls captured in a CUDA graph (the launches carry the
+    programmatic-serialization attribute) and replayed must reproduce the
+    eager results bit for bit, across replays with new input data."""
+    import torch
+    from paper_2001_09258_b200 import api
+    n = (1 << 20) + 3
+    x = torch.from_numpy(unary_cases("exp_d_u10", n)[:n].copy()).cuda()
+    y = torch.from_numpy(binary_cases("pow_d_u10", n)[1][:n].copy()).cuda()
+    o1, o2, o3 = torch.empty_like(x), torch.empty_like(x), torch.empty_like(x)
+
+    def chain():
+        api.call("exp_d_u10", x, out=o1)
+        api.call("pow_d_u10", o1, y, out=o2)
+        api.call("fmod_d", o2, y, out=o3)
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        chain()  # warm-up (occupancy queries, attributes) outside the capture
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        chain()
+    for seed in range(3):
+        with np.errstate(over="ignore"):
+            x.copy_(torch.from_numpy(unary_cases("exp_d_u10", n)[:n].copy() * (1.0 + seed)).cuda())
+        g.replay()
+        torch.cuda.synchronize()
+        got = o3.clone()
+        chain()
+        torch.cuda.synchronize()
+        assert torch.equal(got.view(torch.int64), o3.view(torch.int64)), seed
