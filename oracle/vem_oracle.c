@@ -70,6 +70,7 @@ static inline float canon_f(float y) { return (y != y) ? from_bits_f(CANON_NAN_F
 #define K_FOUR_THIRDS 0x1.5555555555555p+0
 
 static const double PH_D[4 * VEM_PH_D_ENTRIES] = {VEM_PH_D_INIT};
+static const uint64_t PH_DI[4 * VEM_PH_DI_ENTRIES] = {VEM_PH_DI_INIT};
 static const uint32_t PH_F[4 * VEM_PH_F_ENTRIES] = {VEM_PH_F_INIT};
 static const double LOGT_INVC[256] = {VEM_LOGT_INVC_INIT};
 static const double LOGT_HI[256] = {VEM_LOGT_HI_INIT};
@@ -292,12 +293,102 @@ static red_t ph(double x_in) {
   return o;
 }
 
+/* Integer Payne-Hanek for binary64 (own design; SURVEY.md §8(a) a9 allows
+ * "an own design validated to 2^-60 abs"; the function kernels use it, the
+ * reference algorithm above stays the parity anchor of vem_ph_reduce_d).
+ * |x| = M 2^E, M in [2^52, 2^53): P = M W(E) mod 2^192 with
+ * W(E) = floor((2^E 2/pi mod 4) 2^190) (tools/genphtable.py) is x 2/pi mod 4
+ * in units of 2^-190, short by less than M units (2^-137).  Adding half a
+ * unit of the quadrant (2^189) and taking the top two bits gives
+ * q = round(x 2/pi) mod 4; the 190 fraction bits, one's-complemented when the
+ * first is set (|fraction| < 1/2, one unit of 2^-192 off), are normalised by
+ * a leading-zero count and converted into h (53 bits, exact) + l (the next
+ * 64 bits, rounded), and r = (h 2^-(53+lz) + l 2^-(117+lz)) (pi/2) is formed
+ * as p + e with pi/2 = C0 + C1, the scalings folded exactly into the
+ * constants.  Binary64 never comes closer than ~2^-62 to a multiple of
+ * pi/2 (relative), so r keeps >= 70 correct bits (tests check it against
+ * mpmath, worst cases included).  |x| < 1/2: r = x, q = 0. */
+static int clz64(uint64_t v) { return __builtin_clzll(v); }
+static uint64_t shl_pair(uint64_t hi, uint64_t lo, int s) { return s ? (hi << s) | (lo >> (64 - s)) : hi; }
+static double scale_pow2(double c, int k) { return from_bits_d(bits_d(c) - ((uint64_t)k << 52)); }
+static red_t ph_int(double x) {
+  const uint64_t b = bits_d(x), ab = b & 0x7fffffffffffffffull;
+  red_t o;
+  if (ab >= 0x7ff0000000000000ull) {
+    o.hi = from_bits_d(CANON_NAN_D);
+    o.lo = from_bits_d(CANON_NAN_D);
+    o.q = 0;
+    return o;
+  }
+  const int ue = (int)(ab >> 52) - 1023;
+  if (ue < VEM_PH_DI_UEMIN) {
+    o.hi = x;
+    o.lo = 0.0;
+    o.q = 0;
+    return o;
+  }
+  const uint64_t M = (ab & 0x000fffffffffffffull) | 0x0010000000000000ull;
+  const uint64_t* w = PH_DI + 4 * (ue - VEM_PH_DI_UEMIN);
+  const unsigned __int128 t0 = (unsigned __int128)M * w[0];
+  const unsigned __int128 t1 = (unsigned __int128)M * w[1];
+  const uint64_t P0 = (uint64_t)t0;
+  const uint64_t h0 = (uint64_t)(t0 >> 64), l1 = (uint64_t)t1, h1 = (uint64_t)(t1 >> 64);
+  const uint64_t P1 = h0 + l1;
+  const uint64_t P2 = M * w[2] + h1 + (uint64_t)(P1 < l1);
+  int q = (int)((P2 + 0x2000000000000000ull) >> 62);
+  const uint64_t U2 = (P2 << 2) | (P1 >> 62), U1 = (P1 << 2) | (P0 >> 62), U0 = P0 << 2;
+  const uint64_t mask = (uint64_t)((int64_t)U2 >> 63);
+  const uint64_t V2 = U2 ^ mask, V1 = U1 ^ mask, V0 = U0 ^ mask;
+  int lz;
+  uint64_t nh, nl;
+  if (V2) {
+    lz = clz64(V2);
+    nh = shl_pair(V2, V1, lz);
+    nl = shl_pair(V1, V0, lz);
+  } else if (V1) {
+    lz = 64 + clz64(V1);
+    nh = shl_pair(V1, V0, lz - 64);
+    nl = V0 << (lz - 64);
+  } else if (V0) {
+    lz = 128 + clz64(V0);
+    nh = V0 << (lz - 128);
+    nl = 0;
+  } else {
+    lz = 0;
+    nh = 0;
+    nl = 0;
+  }
+  const double hd = (double)(nh >> 11);
+  const double ld = (double)(((nh & 0x7ffull) << 53) | (nl >> 11));
+  const double c0s = scale_pow2(K_PIO2_QD0, 53 + lz), c1s = scale_pow2(K_PIO2_QD1, 53 + lz);
+  const double c0t = scale_pow2(K_PIO2_QD0, 117 + lz);
+  const double p = hd * c0s;
+  double e = fma(hd, c0s, -p);
+  e = fma(hd, c1s, e);
+  e = fma(ld, c0t, e);
+  const int neg = (int)((mask ^ b) >> 63);
+  o.hi = neg ? -p : p;
+  o.lo = neg ? -e : e;
+  if (b >> 63) q = -q;
+  o.q = q & 3;
+  return o;
+}
+
 /* reduction.hpp:189-206, deterministic policy, per lane */
 static red_t trig_reduce(double x) {
   double ax = fabs(x);
   if (ax <= K_CW1_MAX) return cw1(x);
   if (ax <= K_CW2_MAX) return cw2(x);
   return ph(x);
+}
+
+/* the functions' selector: CW1 / CW2 (the reference's, bit for bit) and the
+ * integer Payne-Hanek above for |x| > 1e14 */
+static red_t trig_reduce_fn(double x) {
+  double ax = fabs(x);
+  if (ax <= K_CW1_MAX) return cw1(x);
+  if (ax <= K_CW2_MAX) return cw2(x);
+  return ph_int(x);
 }
 
 /* ======================================================= f64 kernels */
@@ -329,27 +420,27 @@ static double sincos_core_d(double rh, double rl, int cosform) {
 }
 
 double vo_sin_d_u10(double x) {
-  red_t r = trig_reduce(x);
+  red_t r = trig_reduce_fn(x);
   double y = sincos_core_d(r.hi, r.lo, r.q & 1);
   y = neg_if(y, r.q & 2);
   y = (x == 0.0) ? x : y;
   return canon_d(y);
 }
 double vo_cos_d_u10(double x) {
-  red_t r = trig_reduce(x);
+  red_t r = trig_reduce_fn(x);
   double y = sincos_core_d(r.hi, r.lo, (r.q & 1) ^ 1);
   y = neg_if(y, (r.q + 1) & 2);
   return canon_d(y);
 }
 double vo_sin_d_u10_ph(double x) {
-  red_t r = ph(x);
+  red_t r = ph_int(x);
   double y = sincos_core_d(r.hi, r.lo, r.q & 1);
   y = neg_if(y, r.q & 2);
   y = (x == 0.0) ? x : y;
   return canon_d(y);
 }
 double vo_cos_d_u10_ph(double x) {
-  red_t r = ph(x);
+  red_t r = ph_int(x);
   double y = sincos_core_d(r.hi, r.lo, (r.q & 1) ^ 1);
   y = neg_if(y, (r.q + 1) & 2);
   return canon_d(y);
@@ -377,13 +468,13 @@ static double tan_core_d(double rh, double rl, int odd) {
   return q.hi + q.lo;
 }
 double vo_tan_d_u10(double x) {
-  red_t r = trig_reduce(x);
+  red_t r = trig_reduce_fn(x);
   double y = tan_core_d(r.hi, r.lo, r.q & 1);
   y = (fabs(x) < 0x1p-27) ? x : y;
   return canon_d(y);
 }
 double vo_tan_d_u10_ph(double x) {
-  red_t r = ph(x);
+  red_t r = ph_int(x);
   double y = tan_core_d(r.hi, r.lo, r.q & 1);
   y = (fabs(x) < 0x1p-27) ? x : y;
   return canon_d(y);
@@ -918,14 +1009,14 @@ static double sincos_core_d_u35(double r, int cosform) {
   return fma(r * z, P, r);
 }
 double vo_sin_d_u35(double x) {
-  red_t r = trig_reduce(x);
+  red_t r = trig_reduce_fn(x);
   double y = sincos_core_d_u35(r.hi, r.q & 1);
   y = neg_if(y, r.q & 2);
   y = (x == 0.0) ? x : y;
   return canon_d(y);
 }
 double vo_cos_d_u35(double x) {
-  red_t r = trig_reduce(x);
+  red_t r = trig_reduce_fn(x);
   double y = sincos_core_d_u35(r.hi, (r.q & 1) ^ 1);
   y = neg_if(y, (r.q + 1) & 2);
   return canon_d(y);
@@ -943,7 +1034,7 @@ static double tan_core_d_u35(double rh, double rl, int odd) {
   return X / Y;
 }
 double vo_tan_d_u35(double x) {
-  red_t r = trig_reduce(x);
+  red_t r = trig_reduce_fn(x);
   double y = tan_core_d_u35(r.hi, r.lo, r.q & 1);
   y = (fabs(x) < 0x1p-27) ? x : y;
   return canon_d(y);
@@ -1095,6 +1186,14 @@ float vo_atan2_f_u10(float y, float x) { return canon_f((float)vo_atan2_d_u10((d
 float vo_atan2_f_u35(float y, float x) { return canon_f((float)vo_atan2_d_u35((double)y, (double)x)); }
 
 /* ============================================ exported array API */
+void vo_ph_int_reduce_d(const double* x, double* hi, double* lo, int* q, size_t n) {
+  for (size_t i = 0; i < n; i++) {
+    red_t r = ph_int(x[i]);
+    hi[i] = r.hi;
+    lo[i] = r.lo;
+    q[i] = r.q;
+  }
+}
 void vo_trig_reduce_d(const double* x, double* hi, double* lo, int* q, size_t n) {
   for (size_t i = 0; i < n; i++) {
     red_t r = trig_reduce(x[i]);

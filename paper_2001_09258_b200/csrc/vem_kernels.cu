@@ -26,11 +26,14 @@ static std::atomic<uint64_t> g_launches{0};
 // kTableDG: the f64 Payne-Hanek table is read from global memory (L1-resident,
 // __ldg) rather than staged: the 32 KB stage would cost occupancy on inputs
 // that never leave the Cody-Waite range.
-enum TableKind { kNoTable = 0, kTableD = 1, kTableF = 2, kTableLog = 3, kTableDG = 4, kTableDG35 = 5 };
+// kTableD: the reference-algorithm PH table (reduction entry points);
+// kTableDI: the integer PH table (function kernels) + sin|cos coefficients
+enum TableKind { kNoTable = 0, kTableD = 1, kTableF = 2, kTableLog = 3, kTableDG = 4, kTableDG35 = 5, kTableDI = 6 };
 
 template <int TABLE>
 struct TableSize {
   static constexpr int n = TABLE == kTableD   ? 4 * VEM_PH_D_ENTRIES + kSinCosCoefN
+                           : TABLE == kTableDI ? 4 * VEM_PH_DI_ENTRIES + kSinCosCoefN
                            : TABLE == kTableF ? kPhFDoubles + kSinCosCoefN
                            : TABLE == kTableLog ? kLogTabN
                            : (TABLE == kTableDG || TABLE == kTableDG35) ? kSinCosCoefN
@@ -58,14 +61,16 @@ __device__ __forceinline__ const double* stage_table(double* stab) {
         }
       }
     } else {
-      const double* src = TABLE == kTableD ? gPhD : reinterpret_cast<const double*>(gPhF);
+      const double* src = TABLE == kTableD    ? gPhD
+                          : TABLE == kTableDI ? reinterpret_cast<const double*>(gPhDI)
+                                              : reinterpret_cast<const double*>(gPhF);
       constexpr int n2 = (TableSize<TABLE>::n - kSinCosCoefN) / 2;
       const double2* s2 = reinterpret_cast<const double2*>(src);
       double2* d2 = reinterpret_cast<double2*>(stab);
       for (int i = threadIdx.x; i < n2; i += blockDim.x) d2[i] = __ldg(s2 + i);
     }
-    if constexpr (TABLE == kTableD || TABLE == kTableF) {  // per-lane coefficient sets (sin | cos)
-      const double* cs = TABLE == kTableD ? gSinCosD : gSinCosF;
+    if constexpr (TABLE == kTableD || TABLE == kTableDI || TABLE == kTableF) {  // per-lane sin|cos coefficients
+      const double* cs = TABLE == kTableF ? gSinCosF : gSinCosD;
       if (threadIdx.x < kSinCosCoefN) stab[TableSize<TABLE>::n - kSinCosCoefN + threadIdx.x] = cs[threadIdx.x];
     }
     __syncthreads();
@@ -1063,10 +1068,10 @@ __device__ __forceinline__ bool trig_is_trivial(double x) {
 #define VEM_TRIG_OP(NAME, FN, ...)                                                       \
   struct NAME {                                                                          \
     __device__ __forceinline__ double operator()(double x, const double* tab) const {   \
-      return FN<kSel>(x, gPhD __VA_ARGS__);                                              \
+      return FN<kSel>(x, reinterpret_cast<const double*>(gPhDI) __VA_ARGS__);             \
     }                                                                                    \
     __device__ __forceinline__ double cw1(double x, const double* tab) const {          \
-      return FN<kCw1>(x, gPhD __VA_ARGS__);                                              \
+      return FN<kCw1>(x, reinterpret_cast<const double*>(gPhDI) __VA_ARGS__);             \
     }                                                                                    \
     __device__ __forceinline__ static int cls(double x) { return trig_class(x); }      \
     __device__ __forceinline__ static bool is_cw1(double x) { return trig_is_cw1(x); } \
@@ -1099,8 +1104,8 @@ VEM_TRIG_TINY(OpSinDU35, x)
 VEM_TRIG_TINY(OpCosDU35, 1.0)
 VEM_TRIG_TINY(OpTanDU35, x)
 #undef VEM_TRIG_TINY
-VEM_UNARY_OP(OpSinDPh, double, (sin_d_u10<kPh>(x, tab, tab + 4 * VEM_PH_D_ENTRIES)))
-VEM_UNARY_OP(OpCosDPh, double, (cos_d_u10<kPh>(x, tab, tab + 4 * VEM_PH_D_ENTRIES)))
+VEM_UNARY_OP(OpSinDPh, double, (sin_d_u10<kPh>(x, tab, tab + 4 * VEM_PH_DI_ENTRIES)))
+VEM_UNARY_OP(OpCosDPh, double, (cos_d_u10<kPh>(x, tab, tab + 4 * VEM_PH_DI_ENTRIES)))
 VEM_UNARY_OP(OpTanDPh, double, (tan_d_u10<kPh>(x, tab)))
 VEM_UNARY_OP(OpAtanD, double, ((void)tab, atan_d_u10(x)))
 VEM_UNARY_OP(OpAtanDU35, double, ((void)tab, atan_d_u35(x)))
@@ -1504,9 +1509,9 @@ extern "C" {
 int vem_sin_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpSinD, double, 1, kTableDG, 2, 2, 4>(x, nullptr, y, n, s); }
 int vem_cos_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpCosD, double, 1, kTableDG, 4, 2, 3>(x, nullptr, y, n, s); }
 int vem_tan_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpTanD, double, 1, kTableDG, 4, 2, 3>(x, nullptr, y, n, s); }
-int vem_sin_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpSinDPh, double, 1, kTableD, 2, 2>(x, nullptr, y, n, s); }
-int vem_cos_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpCosDPh, double, 1, kTableD, 2, 2>(x, nullptr, y, n, s); }
-int vem_tan_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpTanDPh, double, 1, kTableD, 2, 2>(x, nullptr, y, n, s); }
+int vem_sin_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpSinDPh, double, 1, kTableDI, 2, 2>(x, nullptr, y, n, s); }
+int vem_cos_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpCosDPh, double, 1, kTableDI, 2, 2>(x, nullptr, y, n, s); }
+int vem_tan_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpTanDPh, double, 1, kTableDI, 2, 2>(x, nullptr, y, n, s); }
 int vem_atan_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpAtanD, double, 1, kNoTable, 2, 2>(x, nullptr, y, n, s); }
 int vem_exp_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpExpD, double, 1, kNoTable, 1, 2, 3>(x, nullptr, y, n, s); }
 int vem_exp_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpExpDU35, double, 1, kNoTable, 4, 2>(x, nullptr, y, n, s); }

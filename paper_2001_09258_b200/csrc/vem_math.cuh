@@ -124,6 +124,8 @@ __constant__ double cAsinDU35[] = VEM_ASIN_D_U35_ARR;
 
 // Payne-Hanek tables (global copy; kernels stage them into shared memory).
 __device__ const double gPhD[4 * VEM_PH_D_ENTRIES] = {VEM_PH_D_INIT};
+// integer Payne-Hanek table (ph_int): [w0, w1, w2, 0] per exponent
+__device__ const unsigned long long gPhDI[4 * VEM_PH_DI_ENTRIES] = {VEM_PH_DI_INIT};
 __device__ __align__(16) const uint32_t gPhF[4 * VEM_PH_F_ENTRIES] = {VEM_PH_F_INIT};
 constexpr int kPhFDoubles = 2 * VEM_PH_F_ENTRIES;  // staged size of gPhF in doubles
 // log / exp tables (tools/genlogtables.py).  Global copy: structure of
@@ -338,6 +340,71 @@ __device__ __forceinline__ red ph(double x_in, const double* __restrict__ tab) {
   return o;
 }
 
+// Integer Payne-Hanek for binary64 (oracle: ph_int, which documents the
+// method): 64 x 192-bit product mod 2^192 in 64-bit limbs, quadrant from the
+// top two bits, one's-complemented fraction normalised by a leading-zero
+// count, converted to h (53 bits, exact) + l (rounded) and multiplied by
+// pi/2 = C0 + C1 with the 2^-(53+lz) / 2^-(117+lz) scalings folded exactly
+// into the constants.  Moves the reduction from the FP64 pipe (the cascaded
+// double-double form of reduction.hpp:89-137 takes ~90 FP64 instructions)
+// to the integer pipes (6 FP64 instructions).  `tab` = gPhDI (staged or
+// global), read as 2 x 16 bytes per element.
+__device__ __forceinline__ uint64_t shl_pair(uint64_t hi, uint64_t lo, int s) {
+  return s ? (hi << s) | (lo >> (64 - s)) : hi;
+}
+__device__ __forceinline__ double scale_pow2(double c, int k) {
+  return __hiloint2double(__double2hiint(c) - (k << 20), __double2loint(c));
+}
+__device__ __forceinline__ red ph_int(double x, const double* __restrict__ tab) {
+  const uint64_t b = bits_d(x), ab = b & 0x7fffffffffffffffull;
+  const int ue = (int)(ab >> 52) - 1023;
+  const bool small = ue < VEM_PH_DI_UEMIN;
+  const bool bad = ab >= 0x7ff0000000000000ull;
+  int idx = ue - VEM_PH_DI_UEMIN;
+  idx = small ? 0 : (idx > VEM_PH_DI_ENTRIES - 1 ? VEM_PH_DI_ENTRIES - 1 : idx);
+  const uint64_t M = (ab & 0x000fffffffffffffull) | 0x0010000000000000ull;
+  const ulonglong2* wt = reinterpret_cast<const ulonglong2*>(tab) + 2 * idx;
+  const ulonglong2 w01 = wt[0], w2p = wt[1];
+  const uint64_t P0 = M * w01.x, h0 = __umul64hi(M, w01.x);
+  const uint64_t l1 = M * w01.y, h1 = __umul64hi(M, w01.y);
+  const uint64_t P1 = h0 + l1;
+  const uint64_t P2 = M * w2p.x + h1 + (uint64_t)(P1 < l1);
+  int q = (int)((P2 + 0x2000000000000000ull) >> 62);
+  const uint64_t U2 = (P2 << 2) | (P1 >> 62), U1 = (P1 << 2) | (P0 >> 62), U0 = P0 << 2;
+  const uint64_t mask = (uint64_t)((int64_t)U2 >> 63);
+  const uint64_t V2 = U2 ^ mask, V1 = U1 ^ mask, V0 = U0 ^ mask;
+  int lz;
+  uint64_t nh, nl;
+  if (V2) {
+    lz = __clzll((long long)V2);
+    nh = shl_pair(V2, V1, lz);
+    nl = shl_pair(V1, V0, lz);
+  } else if (V1) {  // |fraction| < 2^-62: not reached by any binary64 (rare paths)
+    lz = 64 + __clzll((long long)V1);
+    nh = shl_pair(V1, V0, lz - 64);
+    nl = V0 << (lz - 64);
+  } else {
+    lz = V0 ? 128 + __clzll((long long)V0) : 0;
+    nh = V0 ? V0 << (lz - 128) : 0ull;
+    nl = 0;
+  }
+  const double hd = (double)(nh >> 11);
+  const double ld = __ull2double_rn(((nh & 0x7ffull) << 53) | (nl >> 11));
+  const double c0s = scale_pow2(kPio2Qd0, 53 + lz), c1s = scale_pow2(kPio2Qd1, 53 + lz);
+  const double c0t = scale_pow2(kPio2Qd0, 117 + lz);
+  const double p = hd * c0s;
+  double e = fma(hd, c0s, -p);
+  e = fma(hd, c1s, e);
+  e = fma(ld, c0t, e);
+  const bool neg = ((mask ^ b) >> 63) != 0;
+  if (b >> 63) q = -q;
+  red o;
+  o.hi = bad ? from_bits_d(kCanonNanD) : (small ? x : (neg ? -p : p));
+  o.lo = bad ? from_bits_d(kCanonNanD) : (small ? 0.0 : (neg ? -e : e));
+  o.q = (bad || small) ? 0 : (q & 3);
+  return o;
+}
+
 // |x| < 15 (inside the CW1 range |x| <= 15) from the high word alone
 // (15 = 0x402E0000_00000000); |x| == 15 exactly is left to trig_class
 __device__ __forceinline__ bool trig_is_cw1(double x) {
@@ -361,6 +428,21 @@ __device__ __forceinline__ red trig_reduce(double x, const double* __restrict__ 
     r = cw2(x);
   } else {
     r = ph(x, tab);
+  }
+  return r;
+}
+
+// the functions' selector (oracle: trig_reduce_fn): CW1 / CW2 as the
+// reference, the integer Payne-Hanek above 1e14; `tab` = gPhDI
+__device__ __forceinline__ red trig_reduce_fn(double x, const double* __restrict__ tab) {
+  const int c = trig_class(x);
+  red r;
+  if (c == 0) {
+    r = cw1(x);
+  } else if (c == 1) {
+    r = cw2(x);
+  } else {
+    r = ph_int(x, tab);
   }
   return r;
 }
@@ -395,11 +477,12 @@ __device__ __forceinline__ bool not_finite_bits(double x) {
 // kernels use it for warps whose elements are all |x| <= 15, where the
 // selector takes that path anyway: same values, no branches).
 enum RedMode { kSel = 0, kPh = 1, kCw1 = 2 };
+// `tab` is the integer Payne-Hanek table gPhDI (staged or global)
 template <int kMode>
 __device__ __forceinline__ red reduce_mode(double x, const double* tab) {
-  if constexpr (kMode == kPh) return ph(x, tab);
+  if constexpr (kMode == kPh) return ph_int(x, tab);
   else if constexpr (kMode == kCw1) return cw1(x);
-  else return trig_reduce(x, tab);
+  else return trig_reduce_fn(x, tab);
 }
 
 // NaN can only come from a non-finite input: canonicalised by an integer test

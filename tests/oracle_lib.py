@@ -93,6 +93,8 @@ def reduce_oracle(kind: str, x: np.ndarray, level: int = 1):
         f = L.vo_trig_reduce_d; f.argtypes = [_P, _P, _P, _P, _N]; f(ptr(x), ptr(hi), ptr(lo), ptr(q), n)
     elif kind == "ph":
         f = L.vo_ph_reduce_d; f.argtypes = [_P, _P, _P, _P, _N]; f(ptr(x), ptr(hi), ptr(lo), ptr(q), n)
+    elif kind == "ph_int":
+        f = L.vo_ph_int_reduce_d; f.argtypes = [_P, _P, _P, _P, _N]; f(ptr(x), ptr(hi), ptr(lo), ptr(q), n)
     elif kind == "cw":
         f = L.vo_cw_reduce_d; f.argtypes = [_P, _P, _P, _P, _N, ctypes.c_int]
         f(ptr(x), ptr(hi), ptr(lo), ptr(q), n, level)

@@ -25,6 +25,11 @@ quadrant in its top two bits and the fraction below; `tools/phf_margin.c`
 shows (exhaustively over every M and E) that the rounded fraction is never
 below 2^-30, so 126 fraction bits leave >= 70 bits of relative precision.
 
+The f64 integer table (new, for the kernels' own binary64 Payne-Hanek; the
+reference-algorithm table above stays the parity anchor of vem_ph_reduce_d):
+1025 entries for ue in [-1, 1023], W(E) = floor((2^E 2/pi mod 4) 2^190) as
+three little-endian 64-bit words plus a zero pad (32800 bytes).
+
 2/pi itself comes from mpmath at 3400 bits (no constants are copied from the
 reference's embedded kTwoOverPiBits, ph_table.cpp:15-26; a test checks that the
 first 2560 fractional bits agree with them).
@@ -124,6 +129,29 @@ def table_f32_words():
     return out
 
 
+PH_DI_ENTRIES = 1025
+PH_DI_UEMIN = -1
+
+
+def table_f64_int():
+    """[w0, w1, w2, 0] per entry (64-bit LE words): W(E) = floor((2^E * 2/pi mod 4)
+    * 2^190) for |x| = M * 2^E, M in [2^52, 2^53), E = ue - 52, ue in [-1, 1023]
+    (unbiased exponent of x).  M * W(E) mod 2^192 holds the quadrant in its top
+    two bits and 190 fraction bits below (integer Payne-Hanek for binary64)."""
+    out = []
+    for i in range(PH_DI_ENTRIES):
+        E = i + PH_DI_UEMIN - 52
+        sh = NBITS - E - 190
+        v = (TOP >> sh) if sh >= 0 else (TOP << -sh)
+        v &= (1 << 192) - 1
+        out.extend([v & (2**64 - 1), (v >> 64) & (2**64 - 1), (v >> 128) & (2**64 - 1), 0])
+    return out
+
+
+def serialize_u64(words):
+    return b"".join(struct.pack("<Q", w) for w in words)
+
+
 def serialize_words(words):
     return b"".join(struct.pack("<I", w) for w in words)
 
@@ -136,14 +164,16 @@ def md5(limbs):
     return hashlib.md5(serialize(limbs)).hexdigest()
 
 
-def emit_header(path, t64, t32):
+def emit_header(path, t64, t32, tdi):
     m32 = hashlib.md5(serialize_words(t32)).hexdigest()
+    mdi = hashlib.md5(serialize_u64(tdi)).hexdigest()
     lines = [
         "/* GENERATED by tools/genphtable.py -- do not edit.",
         " * Repaired Payne-Hanek tables (centred 2^E*2/pi mod 4, cascaded nearest",
         " * doubles); layout follows ph_table.hpp:8-15 (entry E+52, 4 limbs).",
         f" * md5(f64 table, 32768 B LE) = {md5(t64)}",
-        f" * md5(f32 table,  2064 B LE) = {m32} */",
+        f" * md5(f32 table,  2064 B LE) = {m32}",
+        f" * md5(f64 integer table, {8 * len(tdi)} B LE) = {mdi} */",
         "#ifndef VEM_PH_TABLES_H",
         "#define VEM_PH_TABLES_H",
         "#define VEM_PH_D_ENTRIES 1024",
@@ -152,6 +182,9 @@ def emit_header(path, t64, t32):
         f"#define VEM_PH_F_EMIN ({PH_F_EMIN})",
         f'#define VEM_PH_D_MD5 "{md5(t64)}"',
         f'#define VEM_PH_F_MD5 "{m32}"',
+        f"#define VEM_PH_DI_ENTRIES {PH_DI_ENTRIES}",
+        f"#define VEM_PH_DI_UEMIN ({PH_DI_UEMIN})",
+        f'#define VEM_PH_DI_MD5 "{mdi}"',
         "#define VEM_PH_D_INIT \\",
     ]
     for i in range(0, len(t64), 4):
@@ -163,6 +196,11 @@ def emit_header(path, t64, t32):
         row = ", ".join(f"0x{w:08x}u" for w in t32[i:i + 4])
         lines.append(f"  {row}, \\")
     lines.append("")
+    lines.append("#define VEM_PH_DI_INIT \\")
+    for i in range(0, len(tdi), 4):
+        row = ", ".join(f"0x{w:016x}ull" for w in tdi[i:i + 4])
+        lines.append(f"  {row}, \\")
+    lines.append("")
     lines.append("#endif")
     with open(path, "w") as f:
         f.write("\n".join(lines) + "\n")
@@ -171,15 +209,18 @@ def emit_header(path, t64, t32):
 def main():
     t64 = table_f64_mod4()
     t32 = table_f32_words()
+    tdi = table_f64_int()
     tfr = table_f64_frac()
     print("f64 mod4 md5", md5(t64))
     print("f64 frac md5", md5(tfr))
     m32 = hashlib.md5(serialize_words(t32)).hexdigest()
     print("f32 int md5", m32)
-    emit_header(os.path.join(ROOT, "paper_2001_09258_b200", "csrc", "vem_ph_tables.h"), t64, t32)
+    mdi = hashlib.md5(serialize_u64(tdi)).hexdigest()
+    print("f64 int md5", mdi)
+    emit_header(os.path.join(ROOT, "paper_2001_09258_b200", "csrc", "vem_ph_tables.h"), t64, t32, tdi)
     os.makedirs(os.path.join(ROOT, "tests", "golden"), exist_ok=True)
     with open(os.path.join(ROOT, "tests", "golden", "ph_table_digests.txt"), "w") as f:
-        f.write(f"f64_mod4 {md5(t64)}\nf64_frac {md5(tfr)}\nf32_int {m32}\n")
+        f.write(f"f64_mod4 {md5(t64)}\nf64_frac {md5(tfr)}\nf32_int {m32}\nf64_int {mdi}\n")
 
 
 if __name__ == "__main__":
