@@ -355,11 +355,24 @@ __device__ __forceinline__ uint64_t shl_pair(uint64_t hi, uint64_t lo, int s) {
 __device__ __forceinline__ double scale_pow2(double c, int k) {
   return __hiloint2double(__double2hiint(c) - (k << 20), __double2loint(c));
 }
+struct ph_norm { uint64_t nh, nl; int lz; };
+__device__ __noinline__ ph_norm ph_int_norm_rare(uint64_t V1, uint64_t V0) {
+  ph_norm o;
+  if (V1) {
+    o.lz = 64 + __clzll((long long)V1);
+    o.nh = shl_pair(V1, V0, o.lz - 64);
+    o.nl = V0 << (o.lz - 64);
+  } else {
+    o.lz = V0 ? 128 + __clzll((long long)V0) : 0;
+    o.nh = V0 ? V0 << (o.lz - 128) : 0ull;
+    o.nl = 0;
+  }
+  return o;
+}
 __device__ __forceinline__ red ph_int(double x, const double* __restrict__ tab) {
   const uint64_t b = bits_d(x), ab = b & 0x7fffffffffffffffull;
   const int ue = (int)(ab >> 52) - 1023;
   const bool small = ue < VEM_PH_DI_UEMIN;
-  const bool bad = ab >= 0x7ff0000000000000ull;
   int idx = ue - VEM_PH_DI_UEMIN;
   idx = small ? 0 : (idx > VEM_PH_DI_ENTRIES - 1 ? VEM_PH_DI_ENTRIES - 1 : idx);
   const uint64_t M = (ab & 0x000fffffffffffffull) | 0x0010000000000000ull;
@@ -373,20 +386,16 @@ __device__ __forceinline__ red ph_int(double x, const double* __restrict__ tab) 
   const uint64_t U2 = (P2 << 2) | (P1 >> 62), U1 = (P1 << 2) | (P0 >> 62), U0 = P0 << 2;
   const uint64_t mask = (uint64_t)((int64_t)U2 >> 63);
   const uint64_t V2 = U2 ^ mask, V1 = U1 ^ mask, V0 = U0 ^ mask;
-  int lz;
-  uint64_t nh, nl;
-  if (V2) {
-    lz = __clzll((long long)V2);
-    nh = shl_pair(V2, V1, lz);
-    nl = shl_pair(V1, V0, lz);
-  } else if (V1) {  // |fraction| < 2^-62: not reached by any binary64 (rare paths)
-    lz = 64 + __clzll((long long)V1);
-    nh = shl_pair(V1, V0, lz - 64);
-    nl = V0 << (lz - 64);
-  } else {
-    lz = V0 ? 128 + __clzll((long long)V0) : 0;
-    nh = V0 ? V0 << (lz - 128) : 0ull;
-    nl = 0;
+  // V2's top bit is clear (the fraction's first bit was folded into mask),
+  // so lz in [1, 63] whenever V2 != 0: plain funnel shifts
+  int lz = __clzll((long long)V2);
+  uint64_t nh = (V2 << lz) | (V1 >> (64 - lz));
+  uint64_t nl = (V1 << lz) | (V0 >> (64 - lz));
+  if (V2 == 0ull) {  // |fraction| < 2^-64: no binary64 gets here
+    const ph_norm o = ph_int_norm_rare(V1, V0);
+    lz = o.lz;
+    nh = o.nh;
+    nl = o.nl;
   }
   const double hd = (double)(nh >> 11);
   const double ld = __ull2double_rn(((nh & 0x7ffull) << 53) | (nl >> 11));
@@ -396,12 +405,15 @@ __device__ __forceinline__ red ph_int(double x, const double* __restrict__ tab) 
   double e = fma(hd, c0s, -p);
   e = fma(hd, c1s, e);
   e = fma(ld, c0t, e);
-  const bool neg = ((mask ^ b) >> 63) != 0;
+  // negation by the sign bit; a non-finite x gets a meaningless r here (the
+  // functions select the canonical NaN from x itself, as the oracle's NaN r
+  // yields)
+  const int sflip = (int)((uint32_t)((mask ^ b) >> 32) & 0x80000000u);
   if (b >> 63) q = -q;
   red o;
-  o.hi = bad ? from_bits_d(kCanonNanD) : (small ? x : (neg ? -p : p));
-  o.lo = bad ? from_bits_d(kCanonNanD) : (small ? 0.0 : (neg ? -e : e));
-  o.q = (bad || small) ? 0 : (q & 3);
+  o.hi = small ? x : __hiloint2double(__double2hiint(p) ^ sflip, __double2loint(p));
+  o.lo = small ? 0.0 : __hiloint2double(__double2hiint(e) ^ sflip, __double2loint(e));
+  o.q = small ? 0 : (q & 3);
   return o;
 }
 
@@ -526,7 +538,8 @@ __device__ __forceinline__ double tan_d_u10(double x, const double* tab) {
   red r = reduce_mode<kMode>(x, tab);
   double y = tan_core_d(r.hi, r.lo, r.q & 1);
   y = (fabs(x) < 0x1p-27) ? x : y;
-  return canon_d(y);
+  // finite x never gives a NaN y: the oracle's canon_d(y) is this select
+  return not_finite_bits(x) ? from_bits_d(kCanonNanD) : y;
 }
 
 __device__ __forceinline__ double atan_d_u10(double x) {
@@ -1142,7 +1155,7 @@ __device__ __forceinline__ double tan_d_u35(double x, const double* tab) {
   red r = reduce_mode<kMode>(x, tab);
   double y = tan_core_d_u35(r.hi, r.lo, r.q & 1);
   y = (fabs(x) < 0x1p-27) ? x : y;
-  return canon_d(y);
+  return not_finite_bits(x) ? from_bits_d(kCanonNanD) : y;
 }
 __device__ __forceinline__ double atan_d_u35(double x) {
   const double a = fabs(x);
