@@ -300,17 +300,15 @@ static red_t ph(double x_in) {
  * W(E) = floor((2^E 2/pi mod 4) 2^190) (tools/genphtable.py) is x 2/pi mod 4
  * in units of 2^-190, short by less than M units (2^-137).  Adding half a
  * unit of the quadrant (2^189) and taking the top two bits gives
- * q = round(x 2/pi) mod 4; the 190 fraction bits, one's-complemented when the
- * first is set (|fraction| < 1/2, one unit of 2^-192 off), are normalised by
- * a leading-zero count and converted into h (53 bits, exact) + l (the next
- * 64 bits, rounded), and r = (h 2^-(53+lz) + l 2^-(117+lz)) (pi/2) is formed
- * as p + e with pi/2 = C0 + C1, the scalings folded exactly into the
- * constants.  Binary64 never comes closer than ~2^-62 to a multiple of
- * pi/2 (relative), so r keeps >= 70 correct bits (tests check it against
- * mpmath, worst cases included).  |x| < 1/2: r = x, q = 0. */
-static int clz64(uint64_t v) { return __builtin_clzll(v); }
-static uint64_t shl_pair(uint64_t hi, uint64_t lo, int s) { return s ? (hi << s) | (lo >> (64 - s)) : hi; }
-static double scale_pow2(double c, int k) { return from_bits_d(bits_d(c) - ((uint64_t)k << 52)); }
+ * q = round(x 2/pi) mod 4.  The centred fraction F = frac - [frac >= 1/2]
+ * is summed from P's 32-bit words p5 (30 fraction bits) .. p1 as doubles
+ * (each exact) with fast two-sums: every partial sum is 0 or at least 2^-63
+ * in magnitude, because binary64 never comes closer than ~2^-61 (relative)
+ * to a multiple of pi/2, so every step is exact and only the error terms'
+ * sum rounds (~2^-104 relative).  r = F (pi/2) as p + e with pi/2 = C0 + C1
+ * and the sign of x folded into the constants.  r keeps >= 70 correct bits
+ * (tests check it against mpmath, worst cases included).  |x| < 1/2: r = x,
+ * q = 0; non-finite x: NaN. */
 static red_t ph_int(double x) {
   const uint64_t b = bits_d(x), ab = b & 0x7fffffffffffffffull;
   red_t o;
@@ -335,41 +333,34 @@ static red_t ph_int(double x) {
   const uint64_t h0 = (uint64_t)(t0 >> 64), l1 = (uint64_t)t1, h1 = (uint64_t)(t1 >> 64);
   const uint64_t P1 = h0 + l1;
   const uint64_t P2 = M * w[2] + h1 + (uint64_t)(P1 < l1);
-  int q = (int)((P2 + 0x2000000000000000ull) >> 62);
-  const uint64_t U2 = (P2 << 2) | (P1 >> 62), U1 = (P1 << 2) | (P0 >> 62), U0 = P0 << 2;
-  const uint64_t mask = (uint64_t)((int64_t)U2 >> 63);
-  const uint64_t V2 = U2 ^ mask, V1 = U1 ^ mask, V0 = U0 ^ mask;
-  int lz;
-  uint64_t nh, nl;
-  if (V2) {
-    lz = clz64(V2);
-    nh = shl_pair(V2, V1, lz);
-    nl = shl_pair(V1, V0, lz);
-  } else if (V1) {
-    lz = 64 + clz64(V1);
-    nh = shl_pair(V1, V0, lz - 64);
-    nl = V0 << (lz - 64);
-  } else if (V0) {
-    lz = 128 + clz64(V0);
-    nh = V0 << (lz - 128);
-    nl = 0;
-  } else {
-    lz = 0;
-    nh = 0;
-    nl = 0;
-  }
-  const double hd = (double)(nh >> 11);
-  const double ld = (double)(((nh & 0x7ffull) << 53) | (nl >> 11));
-  const double c0s = scale_pow2(K_PIO2_QD0, 53 + lz), c1s = scale_pow2(K_PIO2_QD1, 53 + lz);
-  const double c0t = scale_pow2(K_PIO2_QD0, 117 + lz);
-  const double p = hd * c0s;
-  double e = fma(hd, c0s, -p);
-  e = fma(hd, c1s, e);
-  e = fma(ld, c0t, e);
-  const int neg = (int)((mask ^ b) >> 63);
-  o.hi = neg ? -p : p;
-  o.lo = neg ? -e : e;
+  const uint32_t p5 = (uint32_t)(P2 >> 32), p4 = (uint32_t)P2;
+  const uint32_t p3 = (uint32_t)(P1 >> 32), p2 = (uint32_t)P1, p1 = (uint32_t)(P0 >> 32);
+  int q = (int)((p5 + 0x20000000u) >> 30);
+  const uint32_t f5 = p5 & 0x3fffffffu;
+  const double s0 = fma((double)f5, 0x1p-30, -(double)(f5 >> 29));
+  double t = (double)p4 * 0x1p-62;
+  const double s1 = s0 + t;
+  double e = t - (s1 - s0);
+  t = (double)p3 * 0x1p-94;
+  const double s2 = s1 + t;
+  e = e + (t - (s2 - s1));
+  t = (double)p2 * 0x1p-126;
+  const double s3 = s2 + t;
+  e = e + (t - (s3 - s2));
+  t = (double)p1 * 0x1p-158;
+  const double s4 = s3 + t;
+  e = e + (t - (s4 - s3));
+  const double fh = s4 + e;
+  const double fl = e - (fh - s4);
+  const double c0 = (b >> 63) ? -K_PIO2_QD0 : K_PIO2_QD0;
+  const double c1 = (b >> 63) ? -K_PIO2_QD1 : K_PIO2_QD1;
+  const double p = fh * c0;
+  double ee = fma(fh, c0, -p);
+  ee = fma(fh, c1, ee);
+  ee = fma(fl, c0, ee);
   if (b >> 63) q = -q;
+  o.hi = p;
+  o.lo = ee;
   o.q = q & 3;
   return o;
 }

@@ -341,34 +341,14 @@ __device__ __forceinline__ red ph(double x_in, const double* __restrict__ tab) {
 }
 
 // Integer Payne-Hanek for binary64 (oracle: ph_int, which documents the
-// method): 64 x 192-bit product mod 2^192 in 64-bit limbs, quadrant from the
-// top two bits, one's-complemented fraction normalised by a leading-zero
-// count, converted to h (53 bits, exact) + l (rounded) and multiplied by
-// pi/2 = C0 + C1 with the 2^-(53+lz) / 2^-(117+lz) scalings folded exactly
-// into the constants.  Moves the reduction from the FP64 pipe (the cascaded
-// double-double form of reduction.hpp:89-137 takes ~90 FP64 instructions)
-// to the integer pipes (6 FP64 instructions).  `tab` = gPhDI (staged or
-// global), read as 2 x 16 bytes per element.
-__device__ __forceinline__ uint64_t shl_pair(uint64_t hi, uint64_t lo, int s) {
-  return s ? (hi << s) | (lo >> (64 - s)) : hi;
-}
-__device__ __forceinline__ double scale_pow2(double c, int k) {
-  return __hiloint2double(__double2hiint(c) - (k << 20), __double2loint(c));
-}
-struct ph_norm { uint64_t nh, nl; int lz; };
-__device__ __noinline__ ph_norm ph_int_norm_rare(uint64_t V1, uint64_t V0) {
-  ph_norm o;
-  if (V1) {
-    o.lz = 64 + __clzll((long long)V1);
-    o.nh = shl_pair(V1, V0, o.lz - 64);
-    o.nl = V0 << (o.lz - 64);
-  } else {
-    o.lz = V0 ? 128 + __clzll((long long)V0) : 0;
-    o.nh = V0 ? V0 << (o.lz - 128) : 0ull;
-    o.nl = 0;
-  }
-  return o;
-}
+// method): 53 x 192-bit product mod 2^192 (IMAD.WIDE chains), the quadrant
+// from its top two bits, and the centred fraction summed straight from the
+// product's 32-bit words as an exact floating-point expansion (each word
+// converts exactly; fast two-sums, no leading-zero shifts), then times pi/2
+// in double-double with the sign of x folded into the constant.  The
+// cascaded double-double form of reduction.hpp:89-137 takes ~90 FP64
+// instructions per element; this takes ~30 and a few integer ones.
+// `tab` = gPhDI (staged or global), read as 2 x 16 bytes per element.
 __device__ __forceinline__ red ph_int(double x, const double* __restrict__ tab) {
   const uint64_t b = bits_d(x), ab = b & 0x7fffffffffffffffull;
   const int ue = (int)(ab >> 52) - 1023;
@@ -382,37 +362,42 @@ __device__ __forceinline__ red ph_int(double x, const double* __restrict__ tab) 
   const uint64_t l1 = M * w01.y, h1 = __umul64hi(M, w01.y);
   const uint64_t P1 = h0 + l1;
   const uint64_t P2 = M * w2p.x + h1 + (uint64_t)(P1 < l1);
-  int q = (int)((P2 + 0x2000000000000000ull) >> 62);
-  const uint64_t U2 = (P2 << 2) | (P1 >> 62), U1 = (P1 << 2) | (P0 >> 62), U0 = P0 << 2;
-  const uint64_t mask = (uint64_t)((int64_t)U2 >> 63);
-  const uint64_t V2 = U2 ^ mask, V1 = U1 ^ mask, V0 = U0 ^ mask;
-  // V2's top bit is clear (the fraction's first bit was folded into mask),
-  // so lz in [1, 63] whenever V2 != 0: plain funnel shifts
-  int lz = __clzll((long long)V2);
-  uint64_t nh = (V2 << lz) | (V1 >> (64 - lz));
-  uint64_t nl = (V1 << lz) | (V0 >> (64 - lz));
-  if (V2 == 0ull) {  // |fraction| < 2^-64: no binary64 gets here
-    const ph_norm o = ph_int_norm_rare(V1, V0);
-    lz = o.lz;
-    nh = o.nh;
-    nl = o.nl;
-  }
-  const double hd = (double)(nh >> 11);
-  const double ld = __ull2double_rn(((nh & 0x7ffull) << 53) | (nl >> 11));
-  const double c0s = scale_pow2(kPio2Qd0, 53 + lz), c1s = scale_pow2(kPio2Qd1, 53 + lz);
-  const double c0t = scale_pow2(kPio2Qd0, 117 + lz);
-  const double p = hd * c0s;
-  double e = fma(hd, c0s, -p);
-  e = fma(hd, c1s, e);
-  e = fma(ld, c0t, e);
-  // negation by the sign bit; a non-finite x gets a meaningless r here (the
-  // functions select the canonical NaN from x itself, as the oracle's NaN r
-  // yields)
-  const int sflip = (int)((uint32_t)((mask ^ b) >> 32) & 0x80000000u);
+  const uint32_t p5 = (uint32_t)(P2 >> 32), p4 = (uint32_t)P2;
+  const uint32_t p3 = (uint32_t)(P1 >> 32), p2 = (uint32_t)P1, p1 = (uint32_t)(P0 >> 32);
+  int q = (int)((p5 + 0x20000000u) >> 30);
+  const uint32_t f5 = p5 & 0x3fffffffu;
+  // centred fraction F = frac - [frac >= 1/2] as an exact expansion: every
+  // partial sum is 0 or at least 2^-63 in magnitude (no binary64 is closer
+  // than ~2^-61 to a multiple of pi/2), so each fast two-sum is exact
+  const double s0 = fma((double)f5, 0x1p-30, -(double)(f5 >> 29));
+  double t = (double)p4 * 0x1p-62;
+  const double s1 = s0 + t;
+  double e = t - (s1 - s0);
+  t = (double)p3 * 0x1p-94;
+  const double s2 = s1 + t;
+  e = e + (t - (s2 - s1));
+  t = (double)p2 * 0x1p-126;
+  const double s3 = s2 + t;
+  e = e + (t - (s3 - s2));
+  t = (double)p1 * 0x1p-158;
+  const double s4 = s3 + t;
+  e = e + (t - (s4 - s3));
+  const double fh = s4 + e;
+  const double fl = e - (fh - s4);
+  // r = F (pi/2) sign(x), pi/2 = C0 + C1
+  const int sx = (int)(uint32_t)(b >> 32) & (int)0x80000000u;
+  const double c0 = __hiloint2double(__double2hiint(kPio2Qd0) ^ sx, __double2loint(kPio2Qd0));
+  const double c1 = __hiloint2double(__double2hiint(kPio2Qd1) ^ sx, __double2loint(kPio2Qd1));
+  const double p = fh * c0;
+  double ee = fma(fh, c0, -p);
+  ee = fma(fh, c1, ee);
+  ee = fma(fl, c0, ee);
   if (b >> 63) q = -q;
   red o;
-  o.hi = small ? x : __hiloint2double(__double2hiint(p) ^ sflip, __double2loint(p));
-  o.lo = small ? 0.0 : __hiloint2double(__double2hiint(e) ^ sflip, __double2loint(e));
+  // non-finite x: a meaningless r (the functions select the canonical NaN
+  // from x itself, as the oracle's NaN r yields)
+  o.hi = small ? x : p;
+  o.lo = small ? 0.0 : ee;
   o.q = small ? 0 : (q & 3);
   return o;
 }
