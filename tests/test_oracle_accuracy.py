@@ -304,3 +304,39 @@ def test_oracle_digest_file_reproduces():
     for name in ("exp_f_u10", "fdim_d"):
         r = oracle_eval(name, *digest_inputs(name, gold[name]["n"]))
         assert hashlib.md5(r.tobytes()).hexdigest() == gold[name]["md5"], name
+
+
+def test_integer_payne_hanek_vs_mpmath():
+    """The functions' own binary64 Payne-Hanek (oracle ph_int, mirrored on
+    the GPU bit for bit): quadrant exact and r = x - q pi/2 within 2^-70
+    relative of a 2600-bit mpmath reduction, on log-uniform |x| up to
+    DBL_MAX, neighbours of multiples of pi/2, and the binary64 argument
+    closest to a multiple of pi/2 (6381956970095103 * 2^797)."""
+    import mpmath as mp
+    from oracle_lib import reduce_oracle
+    mp.mp.prec = 2600
+    pio2 = mp.pi / 2
+    rng = np.random.default_rng(7)
+    xs = list(10.0 ** rng.uniform(-0.3, 308, 1500) * rng.choice([-1.0, 1.0], 1500))
+    worst = 6381956970095103 * 2.0 ** 797
+    xs += [worst, -worst, np.nextafter(worst, 0), 0.5, 0.75, 1.0, np.pi / 4, 1e14, 1.7976931348623157e308,
+           2.0 ** 1023, 1e22, 5e15]
+    for k in [1, 2, 3, 10 ** 6, 10 ** 12, 10 ** 15, 2 ** 60, 3 ** 30]:
+        v = float(mp.mpf(k) * pio2)
+        xs += [v, np.nextafter(v, 0.0), np.nextafter(v, np.inf)]
+    x = np.array(xs, dtype=np.float64)
+    hi, lo, q = reduce_oracle("ph_int", x)
+    worst_rel = mp.mpf(0)
+    for i in range(x.size):
+        t = mp.mpf(float(x[i])) / pio2
+        k = mp.nint(t)
+        r = (t - k) * pio2
+        assert int(q[i]) == int(k) % 4, (x[i], q[i], int(k) % 4)
+        if r != 0:
+            worst_rel = max(worst_rel, abs((mp.mpf(float(hi[i])) + mp.mpf(float(lo[i])) - r) / r))
+    assert worst_rel < mp.mpf(2) ** -70, float(mp.log(worst_rel, 2))
+    # specials: |x| < 1/2 returns x itself, non-finite x NaN
+    sp = np.array([0.0, -0.0, 1e-300, -0.25, np.inf, -np.inf, np.nan])
+    h2, l2, q2 = reduce_oracle("ph_int", sp)
+    assert np.array_equal(h2[:4].view(np.uint64), sp[:4].view(np.uint64)) and (q2[:4] == 0).all()
+    assert np.isnan(h2[4:]).all()
