@@ -509,7 +509,9 @@ __device__ __forceinline__ double tan_core_d(double rh, double rl, int odd) {
   double corr = fma(hh * z, P, fma(hl, z, hl));
   dd t = two_sum_fast(hh, corr);
   dd t2 = dd_squ(t);
-  dd den = two_sum(1.0, -t2.hi);
+  // |t2| <= tan^2(pi/8) < 1: the fast two-sum gives the same exact pair
+  // as the oracle's two_sum, three adds fewer
+  dd den = two_sum_fast(1.0, -t2.hi);
   den.lo = den.lo - t2.lo;
   dd num = {t.hi * 2.0, t.lo * 2.0};
   bool o = odd != 0;
@@ -543,7 +545,8 @@ __device__ __forceinline__ double atan_d_u10(double x) {
   double corr = fma(b.hi * z, P, fma(-b.lo, z, b.lo));
   double offh = c2 ? kPio2Qd0 : (c1 ? kPio4Hi : 0.0);
   double offl = c2 ? kPio2Qd1 : (c1 ? kPio4Lo : 0.0);
-  dd s = two_sum(offh, b.hi);
+  // offh is 0 or >= pi/4 > tan(pi/8) >= |b|: fast two-sum, same exact pair
+  dd s = two_sum_fast(offh, b.hi);
   double y = s.hi + (s.lo + (offl + corr));
   y = (a == kInf) ? kPio2Qd0 : y;
   y = copysign_b(y, x);
@@ -1253,7 +1256,7 @@ __device__ __forceinline__ double atan2_d_u10(double y, double x) {
   const double P = poly<VEM_ATAN_D_N>(cAtanD, z);
   const double corr = fma(b.hi * z, P, fma(-b.lo, z, b.lo));
   const double sg = (double)p.sig;
-  const dd s = two_sum(p.ch, sg * b.hi);
+  const dd s = two_sum_fast(p.ch, sg * b.hi);  // p.ch is 0 or >= pi/4 > |b|
   const double g = s.hi + (s.lo + (p.cl + sg * corr));
   return canon_d(atan2_special(y, x, copysign_b(g, y)));
 }
