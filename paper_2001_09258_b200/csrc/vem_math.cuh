@@ -1181,7 +1181,7 @@ __device__ __forceinline__ asin_parts asin_split(double x, const double* c) {
 }
 __device__ __forceinline__ double asin_d_u10(double x) {
   const asin_parts p = asin_split<VEM_ASIN_D_N, true>(x, cAsinD);
-  const dd h = two_sum(kPio2Qd0, -2.0 * p.s);
+  const dd h = two_sum_fast(kPio2Qd0, -2.0 * p.s);  // 2s <= 1 < pi/2 where used: same exact pair
   const double yb = h.hi + (h.lo + (kPio2Qd1 - 2.0 * (p.sl + p.u)));
   double y = p.big ? yb : p.a + p.u;
   y = (p.a > 1.0) ? from_bits_d(kCanonNanD) : y;
@@ -1197,10 +1197,10 @@ __device__ __forceinline__ double asin_d_u35(double x) {
 __device__ __forceinline__ double acos_d_u10(double x) {
   const asin_parts p = asin_split<VEM_ASIN_D_N, true>(x, cAsinD);
   const double us = copysign_b(p.u, x);
-  const dd hs = two_sum(kPio2Qd0, -x);
+  const dd hs = two_sum_fast(kPio2Qd0, -x);  // |x| <= 1 < pi/2 where used
   const double ys = hs.hi + (hs.lo + (kPio2Qd1 - us));
   const double yp = 2.0 * p.s + 2.0 * (p.sl + p.u);
-  const dd hn = two_sum(kPiHi, -2.0 * p.s);
+  const dd hn = two_sum_fast(kPiHi, -2.0 * p.s);
   const double yn = hn.hi + (hn.lo + (kPiLo - 2.0 * (p.sl + p.u)));
   double y = p.big ? (x > 0.0 ? yp : yn) : ys;
   y = (p.a > 1.0) ? from_bits_d(kCanonNanD) : y;
