@@ -509,10 +509,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
 //   4. the output block is stored coalesced (16-byte st.global.cs).
 // Per element the math is fmod_setup / fmod_step50 / fmod_finish (exact),
 // so results are bit-identical to the oracle and to glibc.
-// Pending pair (|x| > |y| > 0, both finite) after setup: r = (mn 2^s0) mod md
-// with `steps` full 50-bit steps to go; result = +-r 2^ed.
+// Pending pair (|x| > |y| > 0, both finite) after setup: r == (mn 2^s0) mod md, signed,
+// with `steps` full 50-bit steps to go (fmod_stepn50); result = +-(r mod md) 2^ed.
 struct fmod_pend {
-  double r, md, rmd;
+  double r, md, rmd;  // r signed in (-md, md); rmd = RN(1/md) 2^50
   int steps, ed;
   uint32_t sx;  // sign word of x
 };
@@ -537,15 +537,19 @@ __device__ __forceinline__ fmod_pend fmod_pend_setup(double x, double y) {
     p.ed = ed;
   }
   p.md = md;
-  p.rmd = toward0_pos(1.0 / md);  // <= 1/md (1.0/md is correctly rounded)
+  const double rmd = 1.0 / md;  // RN(1/md): the signed step's bound (fmod_stepn_rs)
+  p.rmd = rmd * 0x1p50;
   // E >= 0; (E - 1) / 50 for E - 1 in [0, 2100] (and 0 for E = 0)
   p.steps = E == 0 ? 0 : (int)(((uint32_t)(E - 1) * 1311u) >> 16);
-  p.r = fmod_step(mn, E - 50 * p.steps, md, p.rmd);  // E = 0: one 0-bit step, mn - md
+  // first step of s0 = E - 50 steps in [1, 50] bits (E = 0: 0 bits, mn - {1,2} md)
+  p.r = fmod_stepn_rs(mn * __hiloint2double((1023 + E - 50 * p.steps) << 20, 0), md, rmd);
   return p;
 }
 __device__ __forceinline__ double fmod_pend_finish(const fmod_pend& p) {
-  // r in [0, md) is a multiple of 2^-52: r 2^ed is normal when ed >= -970
-  const double m = p.ed >= -970 ? p.r * __hiloint2double((p.ed + 1023) << 20, 0) : ldexp2(p.r, p.ed);
+  // signed r in (-md, md) -> [0, md), a multiple of 2^-52: r 2^ed is normal
+  // when ed >= -970
+  const double r = p.r < 0.0 ? p.r + p.md : p.r;
+  const double m = p.ed >= -970 ? r * __hiloint2double((p.ed + 1023) << 20, 0) : ldexp2(r, p.ed);
   return __hiloint2double(__double2hiint(m) | (int)p.sx, __double2loint(m));
 }
 
@@ -584,7 +588,7 @@ struct FmodQ {
   }
   __device__ static T eval1(T x, T y, const double*) {
     fmod_pend A = fmod_pend_setup((double)x, (double)y);
-    for (int k = 0; k < A.steps; k++) A.r = fmod_step50(A.r, A.md, A.rmd);
+    for (int k = 0; k < A.steps; k++) A.r = fmod_stepn50(A.r, A.md, A.rmd);
     return (T)fmod_pend_finish(A);
   }
   __device__ static void eval2(T xa, T ya, T xb, T yb, T& ra, T& rb, const double*) {
@@ -593,11 +597,11 @@ struct FmodQ {
     const int c = min(A.steps, B.steps);
     int i = 0;
     for (; i < c; i++) {
-      A.r = fmod_step50(A.r, A.md, A.rmd);
-      B.r = fmod_step50(B.r, B.md, B.rmd);
+      A.r = fmod_stepn50(A.r, A.md, A.rmd);
+      B.r = fmod_stepn50(B.r, B.md, B.rmd);
     }
-    for (int k = i; k < A.steps; k++) A.r = fmod_step50(A.r, A.md, A.rmd);
-    for (int k = i; k < B.steps; k++) B.r = fmod_step50(B.r, B.md, B.rmd);
+    for (int k = i; k < A.steps; k++) A.r = fmod_stepn50(A.r, A.md, A.rmd);
+    for (int k = i; k < B.steps; k++) B.r = fmod_stepn50(B.r, B.md, B.rmd);
     ra = (T)fmod_pend_finish(A);
     rb = (T)fmod_pend_finish(B);
   }

@@ -802,6 +802,25 @@ __device__ __forceinline__ double fmod_step(double r, int s, double md, double r
 __device__ __forceinline__ double fmod_step50(double r, double md, double rmd) {
   return fmod_step_rs(r * 0x1p50, md, rmd);
 }
+// Signed-remainder step (the shipped queue kernels, vem_kernels.cu FmodQ):
+// V = rs - rint(rs * rmd) md with rmd = RN(1/md), no sign fix-up inside the
+// loop (4 FP64 instructions instead of 8).  With r = b md (|b| <= 1 after
+// the first step) and an s-bit step, rs * rmd = (rs/md)(1 + e), |e| <=
+// 2^-52 + 2^-106, so |rint(rs*rmd) - rs/md| <= 1/2 + |b| 2^(s-52) + tiny:
+// s = 50 keeps |b| <= 1/2 + 1/4 + ... < 1 and the first step (mn / md < 2,
+// s0 <= 50) gives |b| <= 1 + 2^-55, i.e. |V| <= md as V and md are
+// multiples of 2^-52.  So |V| < 2 is a multiple of 2^-52, representable, and
+// the FMA (exact product Q md) is exact: V == rs (mod md) at every step.  The
+// final r in (-md, md) takes r + md when negative (exact), giving the same
+// r in [0, md) as fmod_step_rs -- results are identical bit for bit.
+__device__ __forceinline__ double fmod_stepn_rs(double rs, double md, double rmd) {
+  return fma(-rint(rs * rmd), md, rs);
+}
+// 50-bit step on r; rmd50 = rmd 2^50 (exact) so r * rmd50 == rs * rmd and the
+// two products are independent.
+__device__ __forceinline__ double fmod_stepn50(double r, double md, double rmd50) {
+  return fma(-rint(r * rmd50), md, r * 0x1p50);
+}
 // After setup: r = (mn * 2^s0) mod md with s0 = E - 50*E50 in [1, 50], and
 // E = E50 full 50-bit steps still to go (the kernels' ring holds only
 // elements with E > 0).

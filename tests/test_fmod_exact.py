@@ -83,3 +83,18 @@ def test_fmod_first_step_matches_paper_example_value():
     """Fig. 2 (PAPER.md:929-934): 1e40 mod 0.75 = 0.25 (final value pinned;
     the printed intermediate depends on the quotient rule)."""
     assert oracle_eval("fmod_d", np.array([1e40]), np.array([0.75]))[0] == 0.25
+
+
+def test_fmod_signed_step_schedule_model(tmp_path):
+    """The device step (vem_math.cuh fmod_stepn_rs: signed remainders,
+    Q = rint(rs RN(1/md)), one fix-up at the end) restated in C: every step
+    exact (binary128 check) with |V| <= md, and 10^6 pending pairs (random
+    bits, config-4-like, extreme divisor mantissas, subnormals) equal to
+    glibc fmod bit for bit."""
+    import subprocess
+    src = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cpp", "fmod_signed_step.c")
+    exe = str(tmp_path / "fss")
+    subprocess.run(["gcc", "-O2", "-ffp-contract=off", src, "-o", exe, "-lm", "-lquadmath"], check=True)
+    out = subprocess.run([exe, "1600000"], capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "mismatches=0 bad_steps=0" in out.stdout
