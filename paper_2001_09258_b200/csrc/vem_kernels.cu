@@ -507,7 +507,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
 //      count, so the long division runs converged with no idle lanes;
 //      results go back into the output block at their tile slots;
 //   4. the output block is stored coalesced (16-byte st.global.cs).
-// Per element the math is fmod_setup / fmod_step50 / fmod_finish (exact),
+// Per element the math is fmod_pend_setup / fmod_stepn50 / fmod_pend_finish (exact),
 // so results are bit-identical to the oracle and to glibc.
 // Pending pair (|x| > |y| > 0, both finite) after setup: r == (mn 2^s0) mod md, signed,
 // with `steps` full 50-bit steps to go (fmod_stepn50); result = +-(r mod md) 2^ed.
@@ -961,7 +961,7 @@ __global__ void __launch_bounds__(kFmodWarps * 32, MINB) k_fmod(const T* __restr
 
   auto step_all = [&]() {
     if (active) {
-      st.r = fmod_step50(st.r, st.md, st.rmd);
+      st.r = fmod_stepn50(st.r, st.md, st.rmd);
       if (--st.E == 0) {
         active = false;
         pend = true;

@@ -767,7 +767,7 @@ __device__ __forceinline__ double pow_d_u35(double x, double y, const double* lt
 
 // fmod: normalised-mantissa FP long division (oracle: fmod_core).  The
 // shipped kernels (vem_kernels.cu: k_queue / k_wqueue with FmodQ) triage on
-// the operand bits and run fmod_pend_setup / fmod_step50 / fmod_pend_finish
+// the operand bits and run fmod_pend_setup / fmod_stepn50 / fmod_pend_finish
 // on sorted queue rows; fmod_core is the full per-element function (tails,
 // unaligned pointers); the setup / step / finish split below also serves the
 // tuning build's work-ring kernel.
@@ -781,38 +781,20 @@ __device__ __forceinline__ double mant_1_2(double x, int e) {
   uint64_t m = (e >= -1022) ? (b & 0x000fffffffffffffull) : ((b << (-1022 - e)) & 0x000fffffffffffffull);
   return from_bits_d(m | 0x3ff0000000000000ull);
 }
-// One step of up to 50 bits: (r * 2^s) mod md, exactly (r < md, md in
-// [1,2), rmd <= 1/md within 2 ulps).  Q1 = trunc(RZ(rs * rmd + 1)) equals
-// floor(rs * rmd) + 1 (one DFMA.RZ: RZ never rounds below the integer
-// floor(rs*rmd) + 1, which is representable), and floor(rs * rmd) is
-// floor(rs/md) or one less (relative error < 2^-51 on a quotient < 2^50), so
-// Q1 is floor(rs/md) or one more and V = rs - Q1*md lies in [-md, md).  rs
-// and Q1*md are multiples of 2^-52, so V (|V| < 2) is representable and the
-// FMA exact; V < 0 takes V + md, exact in [0, md).  Every step is exact, so
-// the result equals the oracle's (vem_oracle.c fmod_step: two_prod, 50-bit
-// steps from the top) bit for bit although the step split differs.
-__device__ __forceinline__ double fmod_step_rs(double rs, double md, double rmd) {
-  const double Q1 = trunc(__fma_rz(rs, rmd, 1.0));
-  const double V = fma(-Q1, md, rs);
-  return (V < 0.0) ? V + md : V;
-}
-__device__ __forceinline__ double fmod_step(double r, int s, double md, double rmd) {
-  return fmod_step_rs(r * __hiloint2double((1023 + s) << 20, 0), md, rmd);
-}
-__device__ __forceinline__ double fmod_step50(double r, double md, double rmd) {
-  return fmod_step_rs(r * 0x1p50, md, rmd);
-}
-// Signed-remainder step (the shipped queue kernels, vem_kernels.cu FmodQ):
-// V = rs - rint(rs * rmd) md with rmd = RN(1/md), no sign fix-up inside the
-// loop (4 FP64 instructions instead of 8).  With r = b md (|b| <= 1 after
-// the first step) and an s-bit step, rs * rmd = (rs/md)(1 + e), |e| <=
-// 2^-52 + 2^-106, so |rint(rs*rmd) - rs/md| <= 1/2 + |b| 2^(s-52) + tiny:
-// s = 50 keeps |b| <= 1/2 + 1/4 + ... < 1 and the first step (mn / md < 2,
-// s0 <= 50) gives |b| <= 1 + 2^-55, i.e. |V| <= md as V and md are
+// One long-division step of up to 50 bits: V == r 2^s (mod md), exactly,
+// with signed remainders: V = rs - rint(rs * rmd) md, rmd = RN(1/md), and no
+// sign fix-up inside the loop (4 FP64 instructions; the round-1 unsigned
+// form trunc(RZ(rs rmd + 1)) / fma / compare / add took 8).  With r = b md
+// (|b| <= 1 after the first step) and an s-bit step, rs * rmd = (rs/md)(1 +
+// e), |e| <= 2^-52 + 2^-106, so |rint(rs*rmd) - rs/md| <= 1/2 + |b| 2^(s-52)
+// + tiny: s = 50 keeps |b| <= 1/2 + 1/4 + ... < 1, and the first step (mn /
+// md < 2, s0 <= 50) gives |b| <= 1 + 2^-55, i.e. |V| <= md as V and md are
 // multiples of 2^-52.  So |V| < 2 is a multiple of 2^-52, representable, and
-// the FMA (exact product Q md) is exact: V == rs (mod md) at every step.  The
-// final r in (-md, md) takes r + md when negative (exact), giving the same
-// r in [0, md) as fmod_step_rs -- results are identical bit for bit.
+// the FMA (exact product Q md) is exact at every step.  The final r in (-md,
+// md) takes r + md when negative (exact), giving r 2^s mod md in [0, md):
+// the exact remainder, equal to the oracle's (vem_oracle.c fmod_step:
+// two_prod, 50-bit steps from the top) bit for bit although the steps differ.
+// CPU model with a per-step exactness check: tests/cpp/fmod_signed_step.c.
 __device__ __forceinline__ double fmod_stepn_rs(double rs, double md, double rmd) {
   return fma(-rint(rs * rmd), md, rs);
 }
@@ -821,13 +803,14 @@ __device__ __forceinline__ double fmod_stepn_rs(double rs, double md, double rmd
 __device__ __forceinline__ double fmod_stepn50(double r, double md, double rmd50) {
   return fma(-rint(r * rmd50), md, r * 0x1p50);
 }
-// After setup: r = (mn * 2^s0) mod md with s0 = E - 50*E50 in [1, 50], and
+// After setup: r == (mn * 2^s0) mod md (signed) with s0 = E - 50*E50 in [1, 50], and
 // E = E50 full 50-bit steps still to go (the kernels' ring holds only
 // elements with E > 0).
 struct fmod_state {
   double r, md, rmd, x;
   int E, ed;
 };
+__device__ __forceinline__ double fmod_finish(const fmod_state& st);
 // returns true when the element is finished already (result in `res`)
 __device__ __forceinline__ bool fmod_setup(double x, double y, fmod_state& st, double& res) {
   double n = fabs(x), d = fabs(y);
@@ -843,7 +826,8 @@ __device__ __forceinline__ bool fmod_setup(double x, double y, fmod_state& st, d
   double mn = mant_1_2(n, en), md = mant_1_2(d, ed);
   int E = en - ed;
   st.md = md;
-  st.rmd = toward0_pos(1.0 / md);  // <= 1/md (1.0/md is correctly rounded)
+  const double rmd = 1.0 / md;  // RN(1/md): signed steps (fmod_stepn_rs)
+  st.rmd = rmd * 0x1p50;
   st.ed = ed;
   st.x = x;
   if (E == 0) {  // mn >= md: one exact subtraction finishes it
@@ -853,22 +837,24 @@ __device__ __forceinline__ bool fmod_setup(double x, double y, fmod_state& st, d
     return true;
   }
   const int E50 = (E - 1) / 50;
-  st.r = fmod_step(mn, E - 50 * E50, md, st.rmd);
+  st.r = fmod_stepn_rs(mn * __hiloint2double((1023 + E - 50 * E50) << 20, 0), md, rmd);
   st.E = E50;
   if (E50 == 0) {
-    res = copysign_b(ldexp2(st.r, ed), x);
+    res = fmod_finish(st);
     return true;
   }
   return false;
 }
+// signed r in (-md, md) -> [0, md), scaled, sign of x
 __device__ __forceinline__ double fmod_finish(const fmod_state& st) {
-  return copysign_b(ldexp2(st.r, st.ed), st.x);
+  const double r = st.r < 0.0 ? st.r + st.md : st.r;
+  return copysign_b(ldexp2(r, st.ed), st.x);
 }
 __device__ __forceinline__ double fmod_core(double x, double y) {
   fmod_state st;
   double res;
   if (fmod_setup(x, y, st, res)) return res;
-  for (int i = 0; i < st.E; i++) st.r = fmod_step50(st.r, st.md, st.rmd);
+  for (int i = 0; i < st.E; i++) st.r = fmod_stepn50(st.r, st.md, st.rmd);
   return fmod_finish(st);
 }
 __device__ __forceinline__ double fmod_d(double x, double y) { return fmod_core(x, y); }
