@@ -627,7 +627,7 @@ struct FmodQ {
 // Results per element are the op's own (bit-identical to the oracle).
 constexpr int kQKeys = 64;
 
-template <class Q, class T, int NIN, int TABLE, int VPT, int STAGES, int MINB, int ROWS>
+template <class Q, class T, int NIN, int TABLE, int VPT, int STAGES, int MINB, int ROWS, int FETCH = 1>
 __global__ void __launch_bounds__(kThreads, MINB) k_queue(const T* __restrict__ a, const T* __restrict__ b,
                                                           T* __restrict__ out, size_t n) {
   using V = typename Vec16<T>::type;
@@ -750,23 +750,26 @@ __global__ void __launch_bounds__(kThreads, MINB) k_queue(const T* __restrict__ 
     __syncthreads();
     // ---- 3. queue units, fetched dynamically heaviest first; lanes past the
     // end duplicate the unit's first entry (same cost class, result dropped)
+    // (FETCH units per atomic: consecutive units have nearly the same cost)
     const int nunits = (Qn + 32 * ROWS - 1) / (32 * ROWS);
-    while (true) {
-      int u = 0;
-      if (lane == 0) u = atomicAdd(&hist[kQKeys], 1);
-      u = __shfl_sync(0xffffffffu, u, 0);
-      if (u >= nunits) break;
-      const int p0 = u * 32 * ROWS;
-      const int pa = p0 + lane, ca = pa < Qn ? pa : p0;
-      if constexpr (ROWS == 1) {
-        const T r = Q::eval1(qx[ca], NIN == 2 ? qy[ca] : (T)0, tab);
-        if (pa < Qn) so[qi[pa]] = r;
-      } else {
-        const int pb = pa + 32, cb = pb < Qn ? pb : p0;
-        T ra, rb;
-        Q::eval2(qx[ca], NIN == 2 ? qy[ca] : (T)0, qx[cb], NIN == 2 ? qy[cb] : (T)0, ra, rb, tab);
-        if (pa < Qn) so[qi[pa]] = ra;
-        if (pb < Qn) so[qi[pb]] = rb;
+    for (int u0 = 0;;) {
+      if (lane == 0) u0 = atomicAdd(&hist[kQKeys], FETCH);
+      u0 = __shfl_sync(0xffffffffu, u0, 0);
+      if (u0 >= nunits) break;
+#pragma unroll 1
+      for (int u = u0; u < u0 + FETCH && u < nunits; u++) {
+        const int p0 = u * 32 * ROWS;
+        const int pa = p0 + lane, ca = pa < Qn ? pa : p0;
+        if constexpr (ROWS == 1) {
+          const T r = Q::eval1(qx[ca], NIN == 2 ? qy[ca] : (T)0, tab);
+          if (pa < Qn) so[qi[pa]] = r;
+        } else {
+          const int pb = pa + 32, cb = pb < Qn ? pb : p0;
+          T ra, rb;
+          Q::eval2(qx[ca], NIN == 2 ? qy[ca] : (T)0, qx[cb], NIN == 2 ? qy[cb] : (T)0, ra, rb, tab);
+          if (pa < Qn) so[qi[pa]] = ra;
+          if (pb < Qn) so[qi[pb]] = rb;
+        }
       }
     }
     __syncthreads();
@@ -1322,14 +1325,15 @@ static int launch_stream(const T* a, const T* b, T* out, size_t n, vem_stream_t 
   return (int)cudaGetLastError();
 }
 
-template <class Q, class Op, class T, int NIN, int TABLE, int VPT, int STAGES, int MINB = 1, int ROWS = 1>
+template <class Q, class Op, class T, int NIN, int TABLE, int VPT, int STAGES, int MINB = 1, int ROWS = 1,
+          int FETCH = 1>
 static int launch_queue(const T* a, const T* b, T* out, size_t n, vem_stream_t s) {
   if (n == 0) return 0;
   if (!(aligned16(a) && aligned16(out) && (NIN == 1 || aligned16(b)))) {
     if constexpr (NIN == 2) return launch_binary<Op, T, TABLE, 1>(a, b, out, n, s);
     else return launch_unary<Op, T, TABLE, 1>(a, out, n, s);
   }
-  auto k = k_queue<Q, T, NIN, TABLE, VPT, STAGES, MINB, ROWS>;
+  auto k = k_queue<Q, T, NIN, TABLE, VPT, STAGES, MINB, ROWS, FETCH>;
   constexpr int smem = STAGES * NIN * kThreads * VPT * 16;
   static const int occ = [k] {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1369,10 +1373,10 @@ static int launch_fmod_w(const T* a, const T* b, T* out, size_t n, vem_stream_t 
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return (int)cudaGetLastError();
 }
-template <class T, int VPT, int STAGES, int MINB = 1, int ROWS = 1>
+template <class T, int VPT, int STAGES, int MINB = 1, int ROWS = 1, int FETCH = 1>
 static int launch_fmod_q(const T* a, const T* b, T* out, size_t n, vem_stream_t s) {
   using OpF = typename std::conditional<sizeof(T) == 8, OpFmodD, OpFmodF>::type;
-  return launch_queue<FmodQ<T>, OpF, T, 2, kNoTable, VPT, STAGES, MINB, ROWS>(a, b, out, n, s);
+  return launch_queue<FmodQ<T>, OpF, T, 2, kNoTable, VPT, STAGES, MINB, ROWS, FETCH>(a, b, out, n, s);
 }
 
 #ifdef VEM_TUNE
@@ -1496,6 +1500,9 @@ static int launch_fmod_tuned(const T* a, const T* b, T* o, size_t n, vem_stream_
     case 7: return launch_stream<OpF, T, 2, kNoTable, 2, 2>(a, b, o, n, s);
     case 9: return launch_stream<OpFmodPlain<T>, T, 2, kNoTable, 2, 2>(a, b, o, n, s);
     case 10: return launch_stream<OpFmodPlain<T>, T, 2, kNoTable, 1, 2>(a, b, o, n, s);
+    case 11: return launch_fmod_q<T, 2, 2, 1, 1, 2>(a, b, o, n, s);
+    case 12: return launch_fmod_q<T, 2, 2, 1, 1, 4>(a, b, o, n, s);
+    case 13: return launch_fmod_q<T, 2, 2, 2, 1, 2>(a, b, o, n, s);
     case 8: return launch_fmod<T>(a, b, o, n, s);
     default: return launch_fmod_q<T, 2, 2, 1, 1>(a, b, o, n, s);
   }
