@@ -183,6 +183,13 @@ template <class Op> struct SortsByClass {
 };
 // ops with a branch-free Cody-Waite-level-1 body for all-small warps
 template <class Op> struct HasCw1 { static constexpr bool value = false; };
+// Leading Payne-Hanek rows evaluated as interleaved branch-free bodies
+// (Op::ph, same values as the selector for class-2 elements) when the
+// warp's sorted block starts with at least this many full class-2 rows.
+#ifndef VEM_PH_ROWS
+#define VEM_PH_ROWS 3
+#endif
+template <class Op> struct PhRows { static constexpr int value = 0; };
 // ops with a closed-form result for "trivial" inputs (trig: |x| < 2^-27 and
 // non-finite x), which the class regrouping leaves out of the sorted rows
 template <class Op> struct HasTrivial { static constexpr bool value = false; };
@@ -313,6 +320,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
         }
       }
       int nplaced = 32 * NE;
+      int nph = 0;  // placed class-2 (Payne-Hanek) elements: rows [0, nph) of the block
       auto regroup = [&]() {
         // counting sort of the warp's 32*NE elements by class, heaviest
         // class first: ballots per (row, class), prefix popcounts
@@ -351,6 +359,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
             si[pos] = (unsigned short)(e * 32 + lane);
           }
           nplaced = a0;
+          nph = n2;
         } else {
           // K classes: per-warp class cursors in shared memory; lanes of one
           // class in a row are ranked by match_any, the group's lowest lane
@@ -398,9 +407,21 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
           ids[r] = r * 32 + lane < nplaced ? si[i] : -1;
         }
         __syncwarp();
+        int r0 = 0;
+        if constexpr (PhRows<Op>::value > 1 && PhRows<Op>::value <= NE) {
+          constexpr int P = PhRows<Op>::value;
+          if (nph >= P * 32) {  // warp-uniform: rows 0..P-1 all Payne-Hanek
+            T yp[P];
+#pragma unroll
+            for (int r = 0; r < P; r++) yp[r] = op.ph(xs[r], tab);
+#pragma unroll
+            for (int r = 0; r < P; r++) sx[ids[r]] = yp[r];
+            r0 = P;
+          }
+        }
 #pragma unroll
         for (int r = 0; r < NE; r++) {
-          if (r * 32 < nplaced) {  // warp-uniform
+          if (r >= r0 && r * 32 < nplaced) {  // warp-uniform
             T yv;
             if constexpr (NIN == 2) yv = op(xs[r], ys[r], tab);
             else yv = op(xs[r], tab);
@@ -1080,6 +1101,9 @@ __device__ __forceinline__ bool trig_is_trivial(double x) {
     __device__ __forceinline__ double cw1(double x, const double* tab) const {          \
       return FN<kCw1>(x, reinterpret_cast<const double*>(gPhDI) __VA_ARGS__);             \
     }                                                                                    \
+    __device__ __forceinline__ double ph(double x, const double* tab) const {           \
+      return FN<kPh>(x, reinterpret_cast<const double*>(gPhDI) __VA_ARGS__);              \
+    }                                                                                    \
     __device__ __forceinline__ static int cls(double x) { return trig_class(x); }      \
     __device__ __forceinline__ static bool is_cw1(double x) { return trig_is_cw1(x); } \
     __device__ __forceinline__ static bool is_trivial(double x) { return trig_is_trivial(x); } \
@@ -1089,7 +1113,8 @@ __device__ __forceinline__ bool trig_is_trivial(double x) {
     static constexpr bool value = true;                                                  \
     static constexpr int classes = 3;                                                    \
   };                                                                                     \
-  template <> struct HasCw1<NAME> { static constexpr bool value = true; };
+  template <> struct HasCw1<NAME> { static constexpr bool value = true; };              \
+  template <> struct PhRows<NAME> { static constexpr int value = VEM_PH_ROWS; };
 // selector variants: PH table from global memory (L1), coefficients staged
 VEM_TRIG_OP(OpSinD, sin_d_u10, , tab)
 VEM_TRIG_OP(OpCosD, cos_d_u10, , tab)
