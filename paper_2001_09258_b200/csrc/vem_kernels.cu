@@ -1542,8 +1542,8 @@ static int launch_fmod_tuned(const T* a, const T* b, T* o, size_t n, vem_stream_
 // vectors in flight, FP64-pipe-bound ones 2 (register pressure).
 extern "C" {
 
-int vem_sin_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpSinD, double, 1, kTableDG, 4, 2, 3>(x, nullptr, y, n, s); }
-int vem_cos_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpCosD, double, 1, kTableDG, 4, 2, 3>(x, nullptr, y, n, s); }
+int vem_sin_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpSinD, double, 1, kTableDG, 4, 2, 2>(x, nullptr, y, n, s); }
+int vem_cos_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpCosD, double, 1, kTableDG, 4, 2, 2>(x, nullptr, y, n, s); }
 int vem_tan_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpTanD, double, 1, kTableDG, 4, 2, 3>(x, nullptr, y, n, s); }
 int vem_sin_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpSinDPh, double, 1, kTableDI, 4, 2, 2>(x, nullptr, y, n, s); }
 int vem_cos_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpCosDPh, double, 1, kTableDI, 4, 2, 2>(x, nullptr, y, n, s); }
