@@ -1404,6 +1404,30 @@ static int launch_fmod_q(const T* a, const T* b, T* out, size_t n, vem_stream_t 
   return launch_queue<FmodQ<T>, OpF, T, 2, kNoTable, VPT, STAGES, MINB, ROWS, FETCH>(a, b, out, n, s);
 }
 
+// fmodf as one straight-line streaming body (fmod_f_flat; no work queue)
+struct OpFmodFFlat {
+  __device__ __forceinline__ float operator()(float x, float y, const double* tab) const {
+    (void)tab;
+    return fmod_f_flat(x, y);
+  }
+};
+struct OpFmodFFixed {
+  __device__ __forceinline__ float operator()(float x, float y, const double* tab) const {
+    (void)tab;
+    return fmod_f_fixed(x, y);
+  }
+};
+template <class T, int VPT, int STAGES, int MINB = 1>
+static int launch_fmod_fixed(const T* a, const T* b, T* out, size_t n, vem_stream_t s) {
+  if constexpr (sizeof(T) == 4) return launch_stream<OpFmodFFixed, float, 2, kNoTable, VPT, STAGES, MINB>(a, b, out, n, s);
+  else return launch_fmod_q<double, 2, 2, 1, 1>(a, b, out, n, s);
+}
+template <class T, int VPT, int STAGES, int MINB = 1>
+static int launch_fmod_flat(const T* a, const T* b, T* out, size_t n, vem_stream_t s) {
+  if constexpr (sizeof(T) == 4) return launch_stream<OpFmodFFlat, float, 2, kNoTable, VPT, STAGES, MINB>(a, b, out, n, s);
+  else return launch_fmod_q<double, 2, 2, 1, 1>(a, b, out, n, s);
+}
+
 #ifdef VEM_TUNE
 template <class T, int MINB = 1>
 static int launch_fmod(const T* a, const T* b, T* out, size_t n, vem_stream_t s) {
@@ -1528,6 +1552,15 @@ static int launch_fmod_tuned(const T* a, const T* b, T* o, size_t n, vem_stream_
     case 11: return launch_fmod_q<T, 2, 2, 1, 1, 2>(a, b, o, n, s);
     case 12: return launch_fmod_q<T, 2, 2, 1, 1, 4>(a, b, o, n, s);
     case 13: return launch_fmod_q<T, 2, 2, 2, 1, 2>(a, b, o, n, s);
+    case 14: return launch_fmod_flat<T, 2, 2>(a, b, o, n, s);
+    case 15: return launch_fmod_flat<T, 4, 2>(a, b, o, n, s);
+    case 16: return launch_fmod_flat<T, 1, 2>(a, b, o, n, s);
+    case 17: return launch_fmod_flat<T, 2, 2, 4>(a, b, o, n, s);
+    case 18: return launch_fmod_flat<T, 4, 2, 3>(a, b, o, n, s);
+    case 19: return launch_fmod_fixed<T, 2, 2>(a, b, o, n, s);
+    case 20: return launch_fmod_fixed<T, 1, 2>(a, b, o, n, s);
+    case 21: return launch_fmod_fixed<T, 2, 2, 2>(a, b, o, n, s);
+    case 22: return launch_fmod_fixed<T, 1, 4>(a, b, o, n, s);
     case 8: return launch_fmod<T>(a, b, o, n, s);
     default: return launch_fmod_q<T, 2, 2, 1, 1>(a, b, o, n, s);
   }
@@ -1580,7 +1613,7 @@ int vem_fmod_f(const float* x, const float* y2, float* o, size_t n, vem_stream_t
 #ifdef VEM_TUNE
   return VEM_FMOD<float>(x, y2, o, n, s);
 #else
-  return launch_fmod_w<float, 2, 2>(x, y2, o, n, s);
+  return launch_fmod_flat<float, 2, 2>(x, y2, o, n, s);
 #endif
 }
 

@@ -1089,6 +1089,63 @@ __device__ __forceinline__ float fmod_f(float x, float y) {
   double r = fmod_core((double)x, (double)y);
   return canon_f((float)r);
 }
+// fmodf without a work queue (the shipped vem_fmod_f): binary32 exponent
+// gaps are <= 277, i.e. <= 5 signed 50-bit steps (fmod_stepn50), so every
+// lane runs the same straight-line body plus a loop whose trip count varies
+// by at most 5 across the warp; trivial pairs and specials are selected at
+// the end.  |x| and |y| are exact normal binary64 values (subnormal floats
+// included), the remainder r 2^ed is exact and a binary32 value, so the
+// result equals fmod_f / glibc fmodf bit for bit.
+__device__ __forceinline__ float fmod_f_flat(float x, float y) {
+  const uint32_t bx = bits_f(x) & 0x7fffffffu, by = bits_f(y) & 0x7fffffffu;
+  const bool pend = bx > by && bx < 0x7f800000u && by != 0u;  // |x| > |y| > 0, x finite (so y finite)
+  const uint64_t nb = bits_d((double)from_bits_f(pend ? bx : 0x3f800000u));
+  const uint64_t db = bits_d((double)from_bits_f(pend ? by : 0x3f800000u));
+  const int en = (int)(nb >> 52), ed = (int)(db >> 52);
+  const double mn = from_bits_d((nb & 0x000fffffffffffffull) | 0x3ff0000000000000ull);
+  const double md = from_bits_d((db & 0x000fffffffffffffull) | 0x3ff0000000000000ull);
+  const int E = en - ed;  // 0 when not pending
+  const int steps = E == 0 ? 0 : (int)(((uint32_t)(E - 1) * 1311u) >> 16);
+  const double rmd = 1.0 / md;
+  const double rmd50 = rmd * 0x1p50;
+  double r = fmod_stepn_rs(mn * __hiloint2double((1023 + E - 50 * steps) << 20, 0), md, rmd);
+#pragma unroll 1
+  for (int k = 0; k < steps; k++) r = fmod_stepn50(r, md, rmd50);
+  r = r < 0.0 ? r + md : r;
+  const float m = (float)(r * __hiloint2double(ed << 20, 0));  // r 2^(ed-1023), exact
+  float res = pend ? m : (bx < by ? x : 0.0f);                 // |x| < |y| -> x; |x| == |y| -> 0
+  res = from_bits_f((bits_f(res) & 0x7fffffffu) | (bits_f(x) & 0x80000000u));
+  const bool nan = bx >= 0x7f800000u || by > 0x7f800000u || by == 0u;
+  return nan ? from_bits_f(kCanonNanF) : res;
+}
+// Branch-free fmodf: the exponent gap E <= 277 is split into exactly six
+// signed steps of s_i = floor((E + i) / 6) <= 47 bits (sum E, Hermite), so
+// every element runs the same straight-line body and the kernel's elements
+// interleave.  Each step: rs = r 2^s_i (exact), V = rs - rint(rs RN(1/md)) md
+// with |rint(..) - rs/md| <= 1/2 + 2^-4 |r/md| (fmod_stepn_rs' bound for s <=
+// 47), so every step is exact; same result as fmod_f bit for bit.
+__device__ __forceinline__ float fmod_f_fixed(float x, float y) {
+  const uint32_t bx = bits_f(x) & 0x7fffffffu, by = bits_f(y) & 0x7fffffffu;
+  const bool pend = bx > by && bx < 0x7f800000u && by != 0u;
+  const uint64_t nb = bits_d((double)from_bits_f(pend ? bx : 0x3f800000u));
+  const uint64_t db = bits_d((double)from_bits_f(pend ? by : 0x3f800000u));
+  const int en = (int)(nb >> 52), ed = (int)(db >> 52);
+  double r = from_bits_d((nb & 0x000fffffffffffffull) | 0x3ff0000000000000ull);
+  const double md = from_bits_d((db & 0x000fffffffffffffull) | 0x3ff0000000000000ull);
+  const int E = en - ed;  // [0, 277]; 0 when not pending
+  const double rmd = 1.0 / md;
+#pragma unroll
+  for (int i = 0; i < 6; i++) {
+    const int s = (int)(((uint32_t)(E + i) * 10923u) >> 16);  // (E + i) / 6 for E + i <= 282
+    r = fmod_stepn_rs(r * __hiloint2double((1023 + s) << 20, 0), md, rmd);
+  }
+  r = r < 0.0 ? r + md : r;
+  const float m = (float)(r * __hiloint2double(ed << 20, 0));  // r 2^(ed-1023), exact
+  float res = pend ? m : (bx < by ? x : 0.0f);
+  res = from_bits_f((bits_f(res) & 0x7fffffffu) | (bits_f(x) & 0x80000000u));
+  const bool nan = bx >= 0x7f800000u || by > 0x7f800000u || by == 0u;
+  return nan ? from_bits_f(kCanonNanF) : res;
+}
 
 // ============================ SURVEY §8(f).1 additions (oracle: same names)
 // fdim, u35 sin/cos/tan/atan, asin/acos, atan2; float32 through binary64.

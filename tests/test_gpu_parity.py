@@ -293,3 +293,26 @@ def test_cuda_graph_capture_and_replay(cuda):
         chain()
         torch.cuda.synchronize()
         assert torch.equal(got.view(torch.int64), o3.view(torch.int64)), seed
+
+
+@pytest.mark.gpu
+def test_fmod_f_every_exponent_pair(cuda):
+    """fmod_f (one straight-line streaming body, fmod_f_flat) on every
+    (exponent of x, exponent of y) pair of binary32, subnormals included,
+    random mantissas and signs, plus |x| == |y| and mantissa-equal pairs:
+    bit-identical to the oracle (== glibc fmodf)."""
+    rng = np.random.default_rng(0x5EEF)
+    ex, ey = np.meshgrid(np.arange(0, 255, dtype=np.uint32), np.arange(0, 255, dtype=np.uint32))
+    ex, ey = np.repeat(ex.ravel(), 4), np.repeat(ey.ravel(), 4)
+    k = ex.size
+    mx = rng.integers(0, 1 << 23, size=k, dtype=np.uint32)
+    my = rng.integers(0, 1 << 23, size=k, dtype=np.uint32)
+    my[::4] = mx[::4]  # same mantissa: E-bit shifts of one value
+    sx = rng.integers(0, 2, size=k, dtype=np.uint32) << 31
+    sy = rng.integers(0, 2, size=k, dtype=np.uint32) << 31
+    x = (sx | (ex << 23) | mx).view(np.float32)
+    y = (sy | (ey << 23) | my).view(np.float32)
+    x = np.concatenate([x, x[: k // 4]])
+    y = np.concatenate([y, -x[: k // 4]])  # |x| == |y|
+    got = _gpu("fmod_f", x, y)
+    _assert_bit_exact("fmod_f", got, oracle_eval("fmod_f", x, y), x, y)

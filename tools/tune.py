@@ -10,7 +10,7 @@ paper_2001_09258_b200/_tune/libvem_tune.so, then times every entry point
 fmod: -1 shipped step-queue kernel; 0-4 warp-private queue (VPT,STAGES[,MINB]) (2,2) (4,2) (2,3) (4,2,2) (2,2,3);
 5-6 CTA queue (VPT,STAGES,ROWS) (2,2,2) (4,2,1); 7 = the streaming kernel with
 warp step-class regrouping (2,2); 8 = the work-ring kernel; 9/10 = the
-streaming kernel with no regrouping (2,2) / (1,2); 11/12/13 = CTA queue (2,2,1) claiming 2/4 units per atomic, and 2 with min-blocks 2.
+streaming kernel with no regrouping (2,2) / (1,2); 11/12/13 = CTA queue (2,2,1) claiming 2/4 units per atomic, and 2 with min-blocks 2; 14-18 = fmodf as one flat streaming body (VPT,STAGES[,MINB]) (2,2) (4,2) (1,2) (2,2,4) (4,2,3); 19-22 = fmodf branch-free six-step body (2,2) (1,2) (2,2,2) (1,4).
 VEM_TUNE_CFG=k overrides the BASELINE config whose inputs are used.
 Prints one JSON line per entry point with Gelem/s per variant.
 """
@@ -71,7 +71,7 @@ def main():
             f.argtypes = [ctypes.c_void_p] * 2 + [ctypes.c_size_t, ctypes.c_void_p]
             call = lambda: f(ts[0].data_ptr(), out.data_ptr(), n, stream)  # noqa: E731
         res = {}
-        for v in ((-1, 0, 5, 11, 12, 13) if name.startswith("fmod") else (-1, 0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10)):
+        for v in ((0, 14, 17, 19, 20, 21, 22) if name.startswith("fmod") else (-1, 0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10)):
             L.vem_tune_set(v)
             for _ in range(3):
                 call()
