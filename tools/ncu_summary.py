@@ -43,7 +43,7 @@ ENTRY = {  # kernel functor -> C-ABI entry point
     "OpExpDU35": "exp_d_u35", "OpLogD": "log_d_u10", "OpLogDU35": "log_d_u35", "OpPowD": "pow_d_u10",
     "OpPowDU35": "pow_d_u35", "OpFmodD": "fmod_d", "OpSinF": "sin_f_u10", "OpCosF": "cos_f_u10",
     "OpTanF": "tan_f_u10", "OpExpF": "exp_f_u10", "OpExpFU35": "exp_f_u35", "OpLogF": "log_f_u10",
-    "OpLogFU35": "log_f_u35", "OpPowF": "pow_f_u10", "OpPowFU35": "pow_f_u35", "OpFmodF": "fmod_f",
+    "OpLogFU35": "log_f_u35", "OpPowF": "pow_f_u10", "OpPowFU35": "pow_f_u35", "OpFmodF": "fmod_f", "OpFmodFFlat": "fmod_f",
 }
 
 
