@@ -811,6 +811,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_queue(const T* __restrict__ 
 }
 
 // ------------------------------------------- warp-private work queue
+// (tuning build only: fmod_f shipped it until the straight-line fmod_f_flat)
 // Same four steps as k_queue, but every warp owns its chunks (32 x NE
 // elements), TMA stages, mbarriers, histogram and queue: no CTA barriers, so
 // a warp with a heavy queue never holds the others back.

@@ -218,8 +218,8 @@ def test_chained_launches_in_place(cuda):
 
 
 def test_chained_launches_mixed_kernels(cuda):
-    """Dependent calls across the three streaming kernel families (TMA stream,
-    CTA work queue, warp-private work queue) on one stream."""
+    """Dependent calls across the kernel families (TMA stream,
+    CTA work queue, straight-line fmodf) on one stream."""
     import torch
     from paper_2001_09258_b200 import api
     n = (1 << 22) + 77
@@ -229,7 +229,7 @@ def test_chained_launches_mixed_kernels(cuda):
     t1 = api.call("fmod_d", tx, ty)            # CTA work queue
     t2 = api.call("exp_d_u10", t1)             # TMA stream, reads t1
     t3 = api.call("fmod_d", t2, ty)            # reads t2
-    f1 = api.call("fmod_f", t3.float(), ty.float())  # warp-private queue
+    f1 = api.call("fmod_f", t3.float(), ty.float())  # straight-line streaming body
     f2 = api.call("log_f_u10", f1)
     sub = np.arange(0, n, 7)
     e1 = oracle_eval("fmod_d", x[sub], y[sub])
