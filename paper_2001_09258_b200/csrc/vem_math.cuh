@@ -533,7 +533,10 @@ __device__ __forceinline__ double atan_d_u10(double x) {
   double a = fabs(x);
   bool c1 = a > kTanPi8;
   bool c2 = a > kTan3Pi8;
-  dd ns = two_sum(a, -1.0), ds = two_sum(a, 1.0);
+  // ns/ds are used for a in (tan(pi/8), tan(3pi/8)]: there a -+ 1 is exact
+  // or |a| < 1, and 1 is a multiple of ulp(a), so the fast two-sums with
+  // the constant first give the oracle's exact two_sum pairs
+  dd ns = two_sum_fast(-1.0, a), ds = two_sum_fast(1.0, a);
   dd nn, dn;
   nn.hi = c2 ? -1.0 : (c1 ? ns.hi : a);
   nn.lo = c2 ? 0.0 : (c1 ? ns.lo : 0.0);
@@ -1314,7 +1317,8 @@ __device__ __forceinline__ atan2_parts atan2_split(double y, double x) {
 }
 __device__ __forceinline__ double atan2_d_u10(double y, double x) {
   const atan2_parts p = atan2_split(y, x);
-  const dd ns = two_sum(p.num, -p.den), ds = two_sum(p.num, p.den);
+  // den >= num >= 0: fast two-sums (den first), same exact pairs
+  const dd ns = two_sum_fast(-p.den, p.num), ds = two_sum_fast(p.den, p.num);
   const dd nn = p.c1 ? ns : dd{p.num, 0.0};
   const dd dn = p.c1 ? ds : dd{p.den, 0.0};
   const dd b = dd_div(nn, dn);
