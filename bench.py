@@ -7,15 +7,25 @@ Workload (default, BASELINE.json configs[1] -- the config the metric is
 quoted on): exp / log / pow x {f32, f64} x {u10, u35}, 2^28 elements each,
 inputs drawn from the config's domains.  One STEP = one pass of all 12 entry
 points over their resident 2^28-element inputs (12 x 2^28 elements).
-  value      = elements processed by all ranks / max-over-ranks step time
-  e2e        = same metric through the C ABI with HOST buffers (pinned
-               H2D + kernel + D2H inside the timed region, every step)
-  roofline   = dominant kernel (largest share of the step): algorithmic bytes
-               per launch / its CUDA-event duration vs measured HBM peak;
-               plus its FP64-pipe roofline against the measured DFMA peak
-  cpu_baseline = the CPU oracle port (oracle/, all host threads) on a bounded
-               sample; SLEEF 3.8 AVX-512 timed beside it for context
-Inputs are 2-4 GiB per array (>> 126 MB L2), so no L2 flush is needed.
+  value        = elements processed by all ranks / max-over-ranks step time
+  e2e          = same metric through the C ABI with HOST buffers (pinned
+                 H2D + kernel + D2H inside the timed region, every step)
+  roofline     = dominant kernel (largest share of the step): algorithmic
+                 bytes per launch / its CUDA-event duration vs the measured HBM
+                 peak; plus its FP64-pipe roofline against the measured DFMA peak
+  per_config   = configs 1, 3, 4, 5 timed the same way (config 5: the 2^31
+                 element job sharded over the ranks -- strong scaling), each
+                 with per-function Gelem/s and roofline fraction
+  verify       = every result of every timed workload checked against the CPU
+                 ORACLE's checksums of the same full config arrays
+                 (tests/golden/config_checksums.json): per-rank partial chunk
+                 checksums, one all-reduce (SUM), compared on rank 0
+  cpu_baseline = the CPU oracle port (oracle/, all host threads + 1 thread) on
+                 a bounded sample; SLEEF 3.8 AVX-512 timed beside it for context
+Inputs: the config generator (paper_2001_09258_b200/inputs.py) evaluated on the
+device (csrc/vem_aux.cu, bit-identical to the host generator -- verified), rank
+r of N taking its own slice of the config's global index space.  Inputs are
+1-16 GiB per array (>> 126 MB L2), so no L2 flush is needed.
 `--impl reference` times the reference CPU path (oracle port, all host
 threads) on the same workload instead (rank 0 only).
 """
@@ -24,129 +34,37 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import platform
 import subprocess
 import sys
 import tempfile
 import time
-import zlib
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+from paper_2001_09258_b200 import configs as C  # noqa: E402
+
 METRIC = "Gelements/s per function (f32/f64, u10/u35) at 1-8 B200 + roofline fraction"
 UNIT = "Gelem/s"
-
-# (entry point, config, fn, prec)
-WORKLOADS = {
-    "cfg2": [("exp_d_u10", 2), ("exp_d_u35", 2), ("log_d_u10", 2), ("log_d_u35", 2), ("pow_d_u10", 2),
-             ("pow_d_u35", 2), ("exp_f_u10", 2), ("exp_f_u35", 2), ("log_f_u10", 2), ("log_f_u35", 2),
-             ("pow_f_u10", 2), ("pow_f_u35", 2)],
-    "cfg1": [("sin_d_u10", 1), ("cos_d_u10", 1)],
-    "cfg3": [("sin_d_u10_ph", 3), ("cos_d_u10_ph", 3), ("tan_d_u10_ph", 3), ("sin_f_u10_ph", 3),
-             ("cos_f_u10_ph", 3), ("tan_f_u10_ph", 3)],
-    "cfg4": [("fmod_d", 4), ("fmod_f", 4)],
-    "cfg5": [("sin_d_u10", 5), ("cos_d_u10", 5), ("tan_d_u10", 5), ("atan_d_u10", 5), ("exp_d_u10", 5),
-             ("log_d_u10", 5), ("pow_d_u10", 5), ("fmod_d", 5)],
-}
-LOG2N = {"cfg1": 24, "cfg2": 28, "cfg3": 28, "cfg4": 26, "cfg5": 31}
-STRONG = {"cfg5"}  # configs whose element count is the job total (sharded), not per rank
-CONFIG_TEXT = {
-    "cfg1": "sin/cos f64 u10, 2^24 x U[-pi,pi] (Cody-Waite path)",
-    "cfg2": "exp/log/pow x f32/f64 x u10/u35, 2^28 elements each (BASELINE configs[1] domains)",
-    "cfg3": "sin/cos/tan u10 f64+f32, 2^28, |x| log-U[1,1e300]/[1,3e38] +-, forced Payne-Hanek",
-    "cfg4": "fmod f64+f32, 2^26 pairs, log-U[1e-300,1e300]/[1e-37,3e38] +-",
-    "cfg5": "2^31 f64 elements (one shared x array; pow y U[-30,30], fmod y log-U) sharded over the ranks, "
-            "through sin/cos/tan/atan/exp/log/pow/fmod u10; log-U[1e-300,1e300] +- with 1% specials",
-}
+GOLDEN = os.path.join(ROOT, "tests", "golden", "config_checksums.json")
+M64 = (1 << 64) - 1
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="vem", choices=["vem", "reference"])
-    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="cfg2", choices=sorted(C.WORKLOADS))
     ap.add_argument("--only", default="", help="comma list of entry points (profiling)")
     ap.add_argument("--log2n", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-verify", action="store_true")
+    ap.add_argument("--no-per-config", action="store_true")
     return ap.parse_args()
-
-
-# --------------------------------------------------------------- inputs
-def device_inputs(fn_name: str, cfg: int, n: int, dev, seed: int):
-    """Config-domain inputs generated ON the device (torch Philox): same
-    distributions as paper_2001_09258_b200.inputs (the host generator used by
-    the parity tests), without shipping 2-4 GiB from the host."""
-    import torch
-    fn, p = fn_name.split("_")[0], fn_name.split("_")[1]
-    dt = torch.float64 if p == "d" else torch.float32
-    g = torch.Generator(device=dev)
-    g.manual_seed(seed)
-
-    def U(a, b):
-        return (a + (b - a) * torch.rand(n, dtype=torch.float64, device=dev, generator=g))
-
-    def LU(a, b, signed=False):
-        import math
-        la, lb = math.log10(a), math.log10(b)
-        v = torch.pow(10.0, U(la, lb))
-        if signed:
-            s = torch.rand(n, device=dev, generator=g) < 0.5
-            v = torch.where(s, -v, v)
-        return v
-
-    def specials(v):
-        pick = torch.rand(n, device=dev, generator=g) < 0.01
-        which = torch.randint(0, 9, (n,), device=dev, generator=g)
-        sp = torch.tensor([0.0, -0.0, float("inf"), float("-inf"), float("nan"), 5e-324, 1e-310,
-                           1.7976931348623157e308, -1.7976931348623157e308], dtype=torch.float64, device=dev)
-        return torch.where(pick, sp[which], v)
-
-    if cfg == 1:
-        xs = [U(-3.141592653589793, 3.141592653589793)]
-    elif cfg == 2:
-        if p == "d":
-            xs = {"exp": lambda: [U(-700, 700)], "log": lambda: [LU(1e-300, 1e300)],
-                  "pow": lambda: [LU(1e-10, 1e10), U(-30, 30)]}[fn]()
-        else:
-            xs = {"exp": lambda: [U(-87, 88)], "log": lambda: [LU(1e-37, 3e38)],
-                  "pow": lambda: [LU(1e-3, 1e3), U(-10, 10)]}[fn]()
-    elif cfg == 3:
-        xs = [LU(1.0, 1e300 if p == "d" else 3e38, signed=True)]
-    elif cfg == 4:
-        lo, hi = (1e-300, 1e300) if p == "d" else (1e-37, 3e38)
-        xs = [LU(lo, hi, True), LU(lo, hi, True)]
-    else:
-        x = specials(LU(1e-300, 1e300, True))
-        if fn == "pow":
-            xs = [x, U(-30, 30)]
-        elif fn == "fmod":
-            xs = [x, specials(LU(1e-300, 1e300, True))]
-        else:
-            xs = [x]
-    if dt == torch.float32:
-        xs = [torch.clamp(v, -3.4028234663852886e38, 3.4028234663852886e38).to(dt) for v in xs]
-    return [v.to(dt).contiguous() for v in xs]
-
-
-def device_inputs_cfg5(n: int, dev, seed: int, chunk_log2: int = 26):
-    """Config 5: ONE x array (log-U[1e-300,1e300] +-, 1% specials) shared by
-    all eight functions, plus pow's y (U[-30,30]) and fmod's y (same law as
-    x); generated on the device in 2^chunk_log2 chunks to bound temporaries."""
-    import torch
-    x = torch.empty(n, dtype=torch.float64, device=dev)
-    ypow = torch.empty_like(x)
-    yfm = torch.empty_like(x)
-    step = 1 << chunk_log2
-    for c, i in enumerate(range(0, n, step)):
-        m = min(step, n - i)
-        x[i:i + m] = device_inputs("sin_d_u10", 5, m, dev, seed + 1000003 * c)[0]
-        ypow[i:i + m] = device_inputs("pow_d_u10", 5, m, dev, seed + 1000003 * c + 1)[1]
-        yfm[i:i + m] = device_inputs("fmod_d", 5, m, dev, seed + 1000003 * c + 2)[1]
-    return x, ypow, yfm
 
 
 # --------------------------------------------------------------- clocks
@@ -209,30 +127,39 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------- CPU legs
-def cpu_oracle_rate(work, sample_log2: int, threads: int, budget_s: float = 0.0):
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
+
+
+def cpu_oracle_rate(workload, names, sample_log2: int, threads: int, budget_s: float = 0.0):
     """Oracle port (oracle/vem_oracle.c, OpenMP on `threads` host threads) over a
-    bounded host sample of every entry point: 2^sample_log2 elements, passes
-    repeated until each entry point has run budget_s/len(work) seconds (at
-    least one pass); returns (Gelem/s, seconds, elements, per-function)."""
+    bounded host sample of every entry point: the first 2^sample_log2 elements
+    of the config arrays (host generator), passes repeated until each entry
+    point has run budget_s/len(names) seconds (at least one pass); returns
+    (Gelem/s, seconds, elements, per-function Gelem/s)."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from oracle_lib import oracle_eval
-    from paper_2001_09258_b200 import inputs as I
-    os.environ["OMP_NUM_THREADS"] = str(threads)
+    import oracle_lib as O
+    set_omp_threads(threads)
     n = 1 << sample_log2
     total_t = 0.0
     total_n = 0
     per = {}
-    for name, cfg in work:
-        fn, p = name.split("_")[0], name.split("_")[1]
-        arrs = I.config_inputs(cfg, fn, p, n)
-        oracle_eval(name, *[a[:4096] for a in arrs])  # warm (threads, pages)
+    for name in names:
+        arrs = [O.gen_fill(r, n, 0) for r in C.recipes(workload, name)]
+        O.oracle_eval(name, *[a[:4096] for a in arrs])  # warm (threads, pages)
         reps = 0
         t0 = time.perf_counter()
         while True:
-            oracle_eval(name, *arrs)
+            O.oracle_eval(name, *arrs)
             reps += 1
             dt = time.perf_counter() - t0
-            if dt >= budget_s / max(1, len(work)):
+            if dt >= budget_s / max(1, len(names)):
                 break
         per[name] = round(reps * n / dt / 1e9, 4)
         total_t += dt
@@ -240,37 +167,43 @@ def cpu_oracle_rate(work, sample_log2: int, threads: int, budget_s: float = 0.0)
     return total_n / total_t / 1e9, total_t, total_n, per
 
 
-def cpu_sleef_rate(work, sample_log2: int, threads: int):
+def cpu_sleef_rate(workload, names, sample_log2: int, threads: int):
     """Upstream SLEEF 3.8 AVX-512 (torch's libtorch_cpu.so) on the same sample."""
-    import ctypes
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
     import numpy as np
-    path = os.path.join(ROOT, "oracle", "_build", "libvem_sleef.so")
-    if not os.path.exists(path):
-        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")], check=False)
-    if not os.path.exists(path):
-        return None
-    L = ctypes.CDLL(path)
-    L.sleef_run.restype = ctypes.c_double
-    L.sleef_run.argtypes = [ctypes.c_char_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
-                            ctypes.c_int]
-    from paper_2001_09258_b200 import inputs as I
+    import oracle_lib as O
+    import sleef_lib as S
+    why = S.available()
+    if why:
+        return {"unavailable": why}
     n = 1 << sample_log2
     tt = 0.0
     per = {}
-    for name, cfg in work:
-        fn, p = name.split("_")[0], name.split("_")[1]
-        arrs = I.config_inputs(cfg, fn, p, n)
+    L = S.lib()
+    for name in names:
+        arrs = [O.gen_fill(r, n, 0) for r in C.recipes(workload, name)]
         out = np.empty_like(arrs[0])
         y = arrs[1].ctypes.data if len(arrs) > 1 else None
         best = None
         for _ in range(3):
             t = L.sleef_run(name.encode(), arrs[0].ctypes.data, y, out.ctypes.data, n, threads)
             best = t if best is None or t < best else best
+        if best is None or best < 0:
+            continue
         per[name] = round(n / best / 1e9, 4)
         tt += best
-    return {"value": round(len(work) * n / tt / 1e9, 4), "unit": UNIT, "cores": threads,
+    return {"value": round(len(per) * n / tt / 1e9, 4) if tt else None, "unit": UNIT, "cores": threads,
             "kind": "sleef-3.8-avx512", "per_function": per,
             "note": "SLEEF has no u35 exp/pow: those rows time the u10 entry"}
+
+
+def set_omp_threads(k: int):
+    os.environ["OMP_NUM_THREADS"] = str(k)
+    try:
+        import ctypes
+        ctypes.CDLL("libgomp.so.1").omp_set_num_threads(k)
+    except OSError:
+        pass
 
 
 def run_reference(args, rank, world):
@@ -278,19 +211,17 @@ def run_reference(args, rank, world):
     has no function kernels) on all host threads."""
     if rank != 0:
         return
-    work = WORKLOADS[args.workload]
-    if args.only:
-        keep = set(args.only.split(","))
-        work = [w for w in work if w[0] in keep]
+    names = select(args)
     threads = os.cpu_count() or 1
+    set_omp_threads(threads)
     lg = 22
     for _ in range(args.warmup):
-        cpu_oracle_rate(work[:1], 16, threads)
+        cpu_oracle_rate(args.workload, names[:1], 16, threads)
     vals = []
     t_all = 0.0
     per = {}
     for _ in range(args.steps):
-        v, t, n, per = cpu_oracle_rate(work, lg, threads, budget_s=3.0)
+        v, t, n, per = cpu_oracle_rate(args.workload, names, lg, threads, budget_s=3.0)
         vals.append(v)
         t_all += t
     value = sum(vals) / len(vals)
@@ -298,18 +229,181 @@ def run_reference(args, rank, world):
     line = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64/f32", "data": "synthetic",
-            "config": {"workload": args.workload, "text": CONFIG_TEXT[args.workload],
-                       "sample": f"2^{lg}-element host arrays per entry point, passes repeated for ~3 s "
-                                 f"of CPU work per step"},
+            "config": {"workload": args.workload, "text": C.CONFIG_TEXT[args.workload],
+                       "sample": f"the first 2^{lg} elements of each config array (host generator), passes "
+                                 f"repeated for ~3 s of CPU work per step"},
             "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": threads, "kind": "port",
-                             "sample": f"{len(work)} entry points x 2^{lg}-element arrays, ~3 s of CPU work "
+                             "cpu_model": cpu_model(),
+                             "sample": f"{len(names)} entry points x 2^{lg}-element arrays, ~3 s of CPU work "
                                        f"per step, oracle/vem_oracle.c (OpenMP, {threads} threads)",
                              "per_function": per},
             "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
+def select(args, workload=None):
+    names = C.WORKLOADS[workload or args.workload]
+    if args.only:
+        keep = set(args.only.split(","))
+        names = [w for w in names if w in keep]
+    return names
+
+
 # --------------------------------------------------------------- GPU arm
+class Dist:
+    def __init__(self, rank, world, local, share, dev):
+        self.rank, self.world, self.local, self.share, self.dev = rank, world, local, share, dev
+
+    def tensor(self, vals, dtype):
+        import torch
+        return torch.tensor(vals, dtype=dtype, device="cpu" if self.share else self.dev)
+
+    def all_reduce(self, t, op):
+        import torch.distributed as dist
+        if self.world > 1:
+            dist.all_reduce(t, op=op)
+        return t
+
+    def barrier(self):
+        import torch.distributed as dist
+        if self.world > 1:
+            dist.barrier()
+
+
+def make_inputs(workload, names, n_log2, D):
+    """Device-generated operands of this rank's slice: {entry: [tensors]},
+    operands with the same recipe are one tensor (u10/u35 pairs, config 5's
+    shared x)."""
+    import torch
+    from paper_2001_09258_b200 import _aux
+    if n_log2:
+        off, n = (D.rank << n_log2, 1 << n_log2)
+    else:
+        off, n = C.shard(workload, D.rank, D.world)
+    cache = {}
+    bufs = {}
+    for name in names:
+        ts = []
+        for r in C.recipes(workload, name):
+            key = (r["kind"], r["seed"], r["a"], r["b"], r["sign"], r["specials"], r["f32"])
+            if key not in cache:
+                t = torch.empty(n, dtype=torch.float32 if r["f32"] else torch.float64, device=D.dev)
+                cache[key] = _aux.fill(r, t, off)
+            ts.append(cache[key])
+        bufs[name] = ts
+    torch.cuda.synchronize()
+    return bufs, off, n
+
+
+def time_workload(workload, names, bufs, n, steps, warmup, D, clocks=False):
+    """Warm-up, then `steps` timed passes over every entry point (CUDA events
+    on the launching stream, barrier + synchronize on both sides, max over
+    ranks).  Returns timing dict and the last outputs."""
+    import torch
+    import torch.distributed as dist
+    from paper_2001_09258_b200 import _lib, api
+    outs = {name: torch.empty_like(bufs[name][0]) for name in names}
+    stream = torch.cuda.current_stream()
+
+    def step(evs=None):
+        for i, name in enumerate(names):
+            if evs is not None:
+                evs[i][0].record(stream)
+            api.call(name, *bufs[name], out=outs[name])
+            if evs is not None:
+                evs[i][1].record(stream)
+
+    for _ in range(max(warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in names]
+           for _ in range(steps)]
+    sampler = ClockSampler(D.local) if clocks else None
+    if sampler:
+        sampler.start()
+        time.sleep(0.3)
+    D.barrier()
+    torch.cuda.synchronize()
+    launches0 = _lib.launch_count()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    # a short device-side spin ahead of the timed region keeps the GPU busy
+    # while the host enqueues the first launches, so host launch latency
+    # (Python + ctypes) does not appear as device idle time inside it
+    torch.cuda._sleep(int(2e6))
+    t0.record(stream)
+    for s in range(steps):
+        step(evs[s])
+    t1.record(stream)
+    torch.cuda.synchronize()
+    launches = _lib.launch_count() - launches0
+    D.barrier()
+    clk = sampler.stop() if sampler else None
+    ms_total = t0.elapsed_time(t1)
+    per_ms = [sum(evs[s][i][0].elapsed_time(evs[s][i][1]) for s in range(steps)) / steps for i in range(len(names))]
+    t = D.tensor([ms_total] + per_ms, torch.float64)
+    D.all_reduce(t, dist.ReduceOp.MAX)
+    ms_total, per_ms = float(t[0]), [float(v) for v in t[1:]]
+    ms_step = ms_total / steps
+    return {"ms_step": ms_step, "per_ms": per_ms, "launches": int(launches), "clocks": clk}, outs
+
+
+def verify_workload(workload, names, bufs, outs, off, n, D, gold):
+    """Result (and operand) chunk checksums of this rank's slice, all-reduced
+    (SUM) over the ranks -- the path's one collective -- and compared on
+    rank 0 with the CPU oracle's checksums of the same config arrays."""
+    import torch
+    import torch.distributed as dist
+    from paper_2001_09258_b200 import _aux
+    g = (gold or {}).get("configs", {}).get(workload)
+    if g is None:
+        return {"skipped": f"no golden checksums for {workload}"}
+    lc = C.LOG2CHUNK
+    nchunks = len(next(iter(g["outputs"].values())))
+    items = [("out", name, outs[name]) for name in names]
+    groups = {}
+    for name in names:
+        groups.setdefault(C.input_key(workload, name), []).append(name)
+    for members in groups.values():
+        for k, t in enumerate(bufs[members[0]]):
+            items.append(("in", f"{members[0]}#{k}", t))
+    mine = [C.chunk_vector(_aux.checksum(t, off, lc), nchunks) for _, _, t in items]
+    tot = D.tensor(mine, torch.int64)
+    D.all_reduce(tot, dist.ReduceOp.SUM)
+    # chunks covered by the ranks that ran, within the golden file's range:
+    # weak configs [0, world * n), config 5 the whole job
+    c_lo = 0
+    c_hi = nchunks if workload in C.STRONG else min(nchunks, (D.world * n) >> lc)
+    bad = {}
+    for (kind, key, _), row in zip(items, tot.cpu().tolist()):
+        ref = (g["outputs"] if kind == "out" else g["inputs"]).get(key)
+        if ref is None:
+            continue
+        mis = C.mismatching_chunks(row, ref, c_lo, c_hi)
+        if mis:
+            bad[f"{kind}:{key}"] = mis[:8]
+    checked = (c_hi - c_lo) << lc
+    return {"elements_per_entry_point": checked, "entry_points": len(names),
+            "mismatching_chunks": sum(len(v) for v in bad.values()), "bad": bad,
+            "compared": "chunk checksums (2^24 elements) of every result and operand vs the CPU oracle's over the "
+                        "same config arrays (tests/golden/config_checksums.json, tools/make_config_digests.py)",
+            "reduction": "per-rank partial checksums, all_reduce SUM over the ranks"}
+
+
+def roofline_entry(name, workload, n, ms, esz, nops, hbm_peak, fp64_peak, km):
+    g = n / (ms * 1e-3) / 1e9
+    bpe = esz * (nops + 1)
+    hbm_roof = hbm_peak / bpe
+    m = km.get(f"{name}@{workload}", km.get(name, {}))
+    f64 = m.get("fp64_inst_per_elem")
+    fp_roof = fp64_peak / f64 if f64 else None
+    roof = min(hbm_roof, fp_roof) if fp_roof else hbm_roof
+    return {"gelem_s": round(g, 2), "ms": round(ms, 4), "hbm_frac": round(g * bpe / hbm_peak, 4),
+            "roof_gelem_s": round(roof, 1), "roof_frac": round(g / roof, 4),
+            "bound": "hbm" if not fp_roof or hbm_roof <= fp_roof else "fp64",
+            "fp64_inst_per_elem": f64, "inst_per_elem": m.get("inst_per_elem"), "metrics_source": m.get("source")}
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -321,11 +415,12 @@ def main():
 
     import torch
     import torch.distributed as dist
-    from paper_2001_09258_b200 import _lib, api, build
+    from paper_2001_09258_b200 import _lib, build
 
     # VEM_BENCH_SHARE_GPU=1 (testing only): map every rank to the visible
     # device(s) round-robin and reduce over gloo -- exercises the multi-rank
-    # bookkeeping on a box with fewer GPUs than ranks.
+    # bookkeeping on a box with fewer GPUs than ranks (no kernel waits on
+    # another rank: the data path has no collective).
     share = os.environ.get("VEM_BENCH_SHARE_GPU") == "1"
     ndev = max(1, torch.cuda.device_count())
     local = local % ndev if share else local
@@ -336,105 +431,13 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    D = Dist(rank, world, local, share, dev)
     if rank == 0:
         build.build()
-    if world > 1:
-        dist.barrier()
+    D.barrier()
     _lib.lib()
+    gold = json.load(open(GOLDEN)) if os.path.exists(GOLDEN) else None
 
-    work = WORKLOADS[args.workload]
-    if args.only:
-        keep = set(args.only.split(","))
-        work = [w for w in work if w[0] in keep]
-    n = 1 << (args.log2n or LOG2N[args.workload])
-    strong = args.workload in STRONG
-    if strong:  # job-total element count, contiguous shard per rank
-        n = n // world
-
-    # resident inputs (u10/u35 of one function share inputs)
-    cache = {}
-    bufs = []
-    if args.workload == "cfg5":
-        x5, ypow5, yfm5 = device_inputs_cfg5(n, dev, seed=0x5EEF0050 + 7919 * rank)
-        cache = {"x": [x5], "ypow": [ypow5], "yfmod": [yfm5]}
-        l_x, l_pow, l_fmod = [x5], [x5, ypow5], [x5, yfm5]  # shared lists: e2e uploads x once
-    for name, cfg in work:
-        if args.workload == "cfg5":
-            fn = name.split("_")[0]
-            bufs.append(l_pow if fn == "pow" else (l_fmod if fn == "fmod" else l_x))
-            continue
-        base = name.replace("_u35", "_u10") if "_u35" in name else name
-        key = (base.split("_")[0], base.split("_")[1], cfg)
-        if key not in cache:
-            cache[key] = device_inputs(name, cfg, n, dev, seed=zlib.crc32(repr(key).encode()) + 7919 * rank)
-        bufs.append(cache[key])
-    outs = {}
-    for ins in bufs:
-        outs.setdefault(ins[0].dtype, torch.empty_like(ins[0]))
-    stream = torch.cuda.current_stream()
-
-    def step(evs=None):
-        for i, (name, _) in enumerate(work):
-            ins = bufs[i]
-            if evs is not None:
-                evs[i][0].record(stream)
-            api.call(name, *ins, out=outs[ins[0].dtype])
-            if evs is not None:
-                evs[i][1].record(stream)
-
-    for _ in range(max(args.warmup, 0)):
-        step()
-    torch.cuda.synchronize()
-
-    # per-kernel event pairs for every timed step
-    evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in work]
-           for _ in range(args.steps)]
-    clocks = ClockSampler(local)
-    clocks.start()
-    time.sleep(0.3)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    launches0 = _lib.launch_count()
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    # a short device-side spin ahead of the timed region keeps the GPU busy
-    # while the host enqueues the first launches, so host launch latency
-    # (Python + ctypes) does not appear as device idle time inside it
-    torch.cuda._sleep(int(2e6))
-    t0.record(stream)
-    for s in range(args.steps):
-        step(evs[s])
-    t1.record(stream)
-    torch.cuda.synchronize()
-    launches = _lib.launch_count() - launches0
-    if world > 1:
-        dist.barrier()
-    clk = clocks.stop()
-    ms_total = t0.elapsed_time(t1)
-    per_kernel_ms = [sum(evs[s][i][0].elapsed_time(evs[s][i][1]) for s in range(args.steps)) / args.steps
-                     for i in range(len(work))]
-    if world > 1:
-        t = torch.tensor([ms_total], dtype=torch.float64, device="cpu" if share else dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_total = float(t.item())
-    ms_step = ms_total / args.steps
-    elems_step = len(work) * n * world
-    value = elems_step / (ms_step * 1e-3) / 1e9
-
-    # ---------------- verification (outside the timed region): the one
-    # collective of the sharded path -- every rank checks its shard, NCCL
-    # all-reduces {mismatch count: SUM, max ulp distance: MAX}
-    verify = None
-    if not args.no_verify:
-        verify = verify_leg(work, bufs, outs, n, dev, world, share)
-
-    # ---------------- e2e: C ABI with HOST buffers (pinned), copies timed
-    e2e = None
-    if not args.no_e2e:
-        e2e = e2e_leg(work, bufs, outs, n, args, dev, stream, world)
-
-    # ---------------- roofline of the dominant kernel
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -442,138 +445,121 @@ def main():
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     hbm_src = "measured (MEASURED_PEAKS.json)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
-    dom = max(range(len(work)), key=lambda i: per_kernel_ms[i])
-    dname = work[dom][0]
-    esz = bufs[dom][0].element_size()
-    bytes_per_launch = n * esz * (len(bufs[dom]) + 1)
-    ach = bytes_per_launch / (per_kernel_ms[dom] * 1e-3) / 1e9
     fp64_peak = _lib.probe_peak("fp64")
-    traffic = None
-    fp64_per_elem = None
-    prof = os.path.join(ROOT, "profiles", "kernel_metrics.json")
-    if os.path.exists(prof):
-        try:
-            allm = json.load(open(prof))
-            # metrics depend on the input mix: a capture of this workload's
-            # inputs (key "name@cfgN") wins over the entry point's default
-            km = allm.get(f"{dname}@{args.workload}", allm.get(dname, {}))
-            if km.get("dram_bytes_per_elem") is not None:
-                traffic = km["dram_bytes_per_elem"] * n
-            fp64_per_elem = km.get("fp64_inst_per_elem")
-        except Exception:
-            pass
+    km = {}
+    try:
+        km = json.load(open(os.path.join(ROOT, "profiles", "kernel_metrics.json")))
+    except Exception:
+        pass
+
+    # ---------------- headline workload
+    names = select(args)
+    bufs, off, n = make_inputs(args.workload, names, args.log2n, D)
+    tim, outs = time_workload(args.workload, names, bufs, n, args.steps, args.warmup, D, clocks=True)
+    ms_step = tim["ms_step"]
+    value = len(names) * n * world / (ms_step * 1e-3) / 1e9
+    verify = None
+    if not args.no_verify and not args.log2n:
+        verify = verify_workload(args.workload, names, bufs, outs, off, n, D, gold)
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_leg(names, bufs, outs, n, args, dev, world)
+    per_function = {}
+    for i, name in enumerate(names):
+        per_function[name] = roofline_entry(name, args.workload, n, tim["per_ms"][i], bufs[name][0].element_size(),
+                                            len(bufs[name]), hbm_peak, fp64_peak, km)
+    dom = max(range(len(names)), key=lambda i: tim["per_ms"][i])
+    dname = names[dom]
+    esz = bufs[dname][0].element_size()
+    bpl = n * esz * (len(bufs[dname]) + 1)
+    ach = bpl / (tim["per_ms"][dom] * 1e-3) / 1e9
+    m = km.get(f"{dname}@{args.workload}", km.get(dname, {}))
+    traffic = m["dram_bytes_per_elem"] * n if m.get("dram_bytes_per_elem") is not None else None
     pipe = None
-    if fp64_per_elem:
-        ach_ops = fp64_per_elem * n / (per_kernel_ms[dom] * 1e-3) / 1e9
+    if m.get("fp64_inst_per_elem"):
+        ach_ops = m["fp64_inst_per_elem"] * n / (tim["per_ms"][dom] * 1e-3) / 1e9
         pipe = {"pipe": "fp64", "achieved": round(ach_ops, 1), "peak": round(fp64_peak, 1), "unit": "Ginst/s",
-                "frac": round(ach_ops / fp64_peak, 4), "fp64_inst_per_elem": fp64_per_elem,
+                "frac": round(ach_ops / fp64_peak, 4), "fp64_inst_per_elem": m["fp64_inst_per_elem"],
                 "peak_source": "measured (vem_probe_peak DFMA microbenchmark, this run)"}
     roofline = {"bound": "hbm", "kernel": dname, "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
-                "frac": round(ach / hbm_peak, 4), "traffic": traffic, "bytes_per_launch": bytes_per_launch,
-                "bytes_per_elem": esz * (len(bufs[dom]) + 1), "elems_per_launch": n,
-                "ms_per_launch": round(per_kernel_ms[dom], 4), "peak_source": hbm_src,
-                "fp64_pipe": pipe, "fp64_dfma_peak_ginst_s": round(fp64_peak, 1)}
+                "frac": round(ach / hbm_peak, 4), "traffic": traffic, "bytes_per_launch": bpl,
+                "bytes_per_elem": esz * (len(bufs[dname]) + 1), "elems_per_launch": n,
+                "ms_per_launch": round(tim["per_ms"][dom], 4), "peak_source": hbm_src,
+                "traffic_source": m.get("source"), "fp64_pipe": pipe,
+                "fp64_dfma_peak_ginst_s": round(fp64_peak, 1)}
+    ws = sum(t.numel() * t.element_size() for t in {id(t): t for v in bufs.values() for t in v}.values())
+    ws += sum(t.numel() * t.element_size() for t in outs.values())
+    del bufs, outs
+    torch.cuda.empty_cache()
 
-    per_function = {}
-    for i, (name, cfg) in enumerate(work):
-        esz_i = bufs[i][0].element_size() * (len(bufs[i]) + 1)
-        g = n / (per_kernel_ms[i] * 1e-3) / 1e9
-        per_function[name] = {"gelem_s": round(g, 2), "ms": round(per_kernel_ms[i], 4),
-                              "hbm_frac": round(g * esz_i / hbm_peak, 4)}
+    # ---------------- the other BASELINE configs (same timing rules)
+    per_config = None
+    if args.workload == "cfg2" and not args.no_per_config and not args.only and not args.log2n:
+        per_config = {}
+        for w in ("cfg1", "cfg3", "cfg4", "cfg5"):
+            nm = C.WORKLOADS[w]
+            b, o, nn = make_inputs(w, nm, 0, D)
+            st = max(3, args.steps // 2)
+            tw, ow = time_workload(w, nm, b, nn, st, max(3, args.warmup), D)
+            vw = None if args.no_verify else verify_workload(w, nm, b, ow, o, nn, D, gold)
+            pf = {name: roofline_entry(name, w, nn, tw["per_ms"][i], b[name][0].element_size(), len(b[name]),
+                                       hbm_peak, fp64_peak, km) for i, name in enumerate(nm)}
+            per_config[w] = {"value": round(len(nm) * nn * world / (tw["ms_step"] * 1e-3) / 1e9, 3), "unit": UNIT,
+                             "ms_per_step": round(tw["ms_step"], 4), "steps": st,
+                             "scaling": "strong" if w in C.STRONG else "weak",
+                             "elements_per_entry_point_per_rank": nn, "text": C.CONFIG_TEXT[w],
+                             "gpu_launches": tw["launches"], "per_function": pf, "verify": vw}
+            del b, ow
+            torch.cuda.empty_cache()
 
     cpu = None
     sleef = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
-        v, t, cn, per = cpu_oracle_rate(work, 23, threads, budget_s=12.0)
-        cpu = {"value": round(v, 4), "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"{len(work)} entry points x 2^23-element arrays of the same config domains, repeated "
-                         f"passes: {cn / 1e9:.2f} G elements in {t:.1f} s of CPU work, oracle/vem_oracle.c, "
-                         f"OpenMP {threads} threads",
+        set_omp_threads(threads)
+        v, t, cn, per = cpu_oracle_rate(args.workload, names, 23, threads, budget_s=12.0)
+        set_omp_threads(1)
+        v1, t1, cn1, _ = cpu_oracle_rate(args.workload, names, 20, 1, budget_s=3.0)
+        set_omp_threads(threads)
+        cpu = {"value": round(v, 4), "unit": UNIT, "cores": threads, "kind": "port", "cpu_model": cpu_model(),
+               "value_1core": round(v1, 4),
+               "sample": f"{len(names)} entry points x the first 2^23 elements of the same config arrays (host "
+                         f"generator), repeated passes: {cn / 1e9:.2f} G elements in {t:.1f} s of CPU work, "
+                         f"oracle/vem_oracle.c, OpenMP {threads} threads; value_1core: 2^20-element samples, "
+                         f"{t1:.1f} s on 1 thread",
                "per_function": per}
         try:
-            sleef = cpu_sleef_rate(work, 23, threads)
+            sleef = cpu_sleef_rate(args.workload, names, 23, threads)
         except Exception as ex:  # context only
             sleef = {"error": str(ex)}
 
-    ws = sum(t.numel() * t.element_size() for ins in cache.values() for t in ins) + \
-        sum(t.numel() * t.element_size() for t in outs.values())
-    l2_note = (f"no flush: per-step working set {ws / 2**20:.0f} MiB (distinct inputs {n}-element arrays + "
-               f"outputs) > 126 MB L2, each input re-read only after the other kernels' traffic")
+    l2_note = (f"no flush: per-step working set {ws / 2**20:.0f} MiB (distinct inputs + outputs of "
+               f"{n}-element arrays) > 126 MB L2, each input re-read only after the other kernels' traffic")
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
-                "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f64/f32 (per entry point)",
-                "data": "synthetic (config-domain inputs generated on device, seeded)",
-                "config": {"workload": args.workload, "text": CONFIG_TEXT[args.workload],
-                           "elements_per_entry_point_per_rank": n, "entry_points": [w[0] for w in work],
-                           "l2": l2_note,
+                "scaling": "strong" if args.workload in C.STRONG else "weak", "vs_baseline": None,
+                "dtype": "f64/f32 (per entry point)",
+                "data": "synthetic (config-domain inputs, counter-based generator evaluated on the device, "
+                        "bit-identical to the host generator)",
+                "config": {"workload": args.workload, "text": C.CONFIG_TEXT[args.workload],
+                           "elements_per_entry_point_per_rank": n, "entry_points": names, "l2": l2_note,
                            "parallelism": f"data-parallel shards x{world} (no collective on the data path)"},
-                "gpu_launches": int(launches), "clocks": clk, "roofline": roofline,
+                "gpu_launches": tim["launches"], "clocks": tim["clocks"], "roofline": roofline,
                 "per_function": per_function, "e2e": e2e, "cpu_baseline": cpu, "sleef_cpu": sleef,
-                "verify": verify}
+                "verify": verify, "per_config": per_config}
         print(json.dumps(line), flush=True)
     if world > 1:
-        dist.barrier()
+        D.barrier()
         dist.destroy_process_group()
 
 
-def verify_leg(work, bufs, outs, n, dev, world, share):
-    """Every entry point over the rank's whole shard twice: the shipped
-    TMA-pipelined / work-queue kernel (16-byte aligned buffers) and the plain
-    grid-stride kernel the library takes for misaligned pointers (same math,
-    independent load/store path, no staging or regrouping), compared bit for
-    bit on the device; per rank: mismatching elements (SUM) and the largest
-    ulp distance (MAX), combined over the ranks by one all-reduce each.  Bit
-    identity to the CPU oracle is the test suite's job (tests/); this checks,
-    at full scale on every shard, that the fast data path returns exactly
-    what the per-element function computes."""
-    import torch
-    import torch.distributed as dist
-    from paper_2001_09258_b200 import api
-    mism = 0
-    max_ulp = 0
-    checked = 0
-    for i, (name, _) in enumerate(work):
-        ins = bufs[i]
-        dt = ins[0].dtype
-        it = torch.int64 if dt == torch.float64 else torch.int32
-        a = api.call(name, *ins, out=outs[dt])
-        un = []
-        for t in ins:
-            u = torch.empty(n + 1, dtype=dt, device=dev)
-            u[1:].copy_(t)
-            un.append(u[1:])  # 4/8-byte offset: the misaligned (plain) path
-        ob = torch.empty(n + 1, dtype=dt, device=dev)
-        b = api.call(name, *un, out=ob[1:])
-        ai, bi = a.view(it), b.view(it)
-        ne = ai != bi
-        mism += int(ne.sum().item())
-        if bool(ne.any().item()):
-            # same-sign finite values: ulp distance = difference of the bit patterns
-            d = (ai.to(torch.int64) - bi.to(torch.int64)).abs()
-            max_ulp = max(max_ulp, int(d[ne].max().item()))
-        checked += n
-        del un, ob, b
-    torch.cuda.empty_cache()
-    if world > 1:
-        t = torch.tensor([mism, checked], dtype=torch.int64, device="cpu" if share else dev)
-        m = torch.tensor([max_ulp], dtype=torch.int64, device="cpu" if share else dev)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        dist.all_reduce(m, op=dist.ReduceOp.MAX)
-        mism, checked, max_ulp = int(t[0].item()), int(t[1].item()), int(m[0].item())
-    return {"elements": checked, "mismatches": mism, "max_ulp": max_ulp,
-            "compared": "TMA-pipelined / work-queue kernels vs the plain grid-stride kernel (misaligned "
-                        "pointers), bit for bit, every element of every shard",
-            "reduction": "all_reduce SUM (mismatches) and MAX (ulp) over the ranks"}
-
-
-def e2e_leg(work, bufs, outs, n, args, dev, stream, world):
+def e2e_leg(names, bufs, outs, n, args, dev, world):
     """Same step through the C ABI with HOST buffers: every step uploads that
     step's distinct inputs host->device from pinned memory (the u10 and u35
     entry points of one function read the same arrays, so each input array is
     uploaded once), runs every entry point, and reads every result back
-    device->host into its own pinned buffer; chunked over three streams so
+    device->host into its own pinned buffer; chunked over four streams so
     copies in both directions overlap the kernels (4 streams, 2^24-element
     chunks: the best of a chunk x stream sweep, profiles/r01_e2e_sweep.log)."""
     import torch
@@ -582,31 +568,32 @@ def e2e_leg(work, bufs, outs, n, args, dev, stream, world):
     nstreams = int(os.environ.get("VEM_E2E_STREAMS", "4"))
     n = min(n, 1 << 26)  # 2^26 elements per entry point per rank (bounded pinned memory)
     groups = []  # (device input list, [(entry name, work index)])
-    for i, (name, _) in enumerate(work):
+    for i, name in enumerate(names):
         for g in groups:
-            if g[0] is bufs[i]:
+            if all(a is b for a, b in zip(g[0], bufs[name])) and len(g[0]) == len(bufs[name]):
                 g[1].append((name, i))
                 break
         else:
-            groups.append((bufs[i], [(name, i)]))
+            groups.append((bufs[name], [(name, i)]))
     host_in = {id(g[0]): [t[:n].to("cpu").pin_memory() for t in g[0]] for g in groups}
-    host_out = [torch.empty(n, dtype=bufs[i][0].dtype).pin_memory() for i in range(len(work))]
-    dev_out = [torch.empty(n, dtype=bufs[i][0].dtype, device=dev) for i in range(len(work))]
+    dev_in = {id(g[0]): [torch.empty(n, dtype=t.dtype, device=dev) for t in g[0]] for g in groups}
+    host_out = [torch.empty(n, dtype=bufs[name][0].dtype).pin_memory() for name in names]
+    dev_out = [torch.empty(n, dtype=bufs[name][0].dtype, device=dev) for name in names]
     streams = [torch.cuda.Stream(dev) for _ in range(nstreams)]
     h2d = sum(t.numel() * t.element_size() for v in host_in.values() for t in v)
     d2h = sum(h.numel() * h.element_size() for h in host_out)
 
     def one_step():
         for dins, members in groups:
-            hin = host_in[id(dins)]
+            hin, din = host_in[id(dins)], dev_in[id(dins)]
             for j, c0 in enumerate(range(0, n, chunk)):
                 c1 = min(n, c0 + chunk)
                 s = streams[j % nstreams]  # a given range always uses the same stream
                 with torch.cuda.stream(s):
-                    for hd, dd_ in zip(hin, dins):
+                    for hd, dd_ in zip(hin, din):
                         dd_[c0:c1].copy_(hd[c0:c1], non_blocking=True)
                     for name, i in members:
-                        api.call(name, *[d[c0:c1] for d in dins], out=dev_out[i][c0:c1])
+                        api.call(name, *[d[c0:c1] for d in din], out=dev_out[i][c0:c1])
                         host_out[i][c0:c1].copy_(dev_out[i][c0:c1], non_blocking=True)
 
     one_step()
@@ -617,7 +604,13 @@ def e2e_leg(work, bufs, outs, n, args, dev, stream, world):
         one_step()
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) / steps
-    return {"value": round(len(work) * n * world / dt / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+    # the results that crossed PCIe are the device results (spot check)
+    for i, name in enumerate(names):
+        if not torch.equal(host_out[i][:4096].view(torch.int32 if host_out[i].dtype == torch.float32 else torch.int64),
+                           outs[name][:4096].cpu().view(torch.int32 if host_out[i].dtype == torch.float32
+                                                        else torch.int64)):
+            raise RuntimeError(f"e2e: {name} host result differs from the device result")
+    return {"value": round(len(names) * n * world / dt / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": round(dt * 1e3, 2), "steps": steps,
             "elements_per_entry_point_per_rank": n,
             "path": "pinned host -> H2D (each distinct input once, chunked 2^24, 4 streams) -> vem C ABI "

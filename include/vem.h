@@ -17,9 +17,12 @@
  *    errors stay in-band exactly as in the reference: NaN/Inf, no errno, no FP
  *    exceptions; NaN results are the
  *    canonical quiet NaN (0x7ff8000000000000 / 0x7fc00000);
- *  - reentrant from any host thread; the Payne-Hanek table is a device
- *    constant staged per CTA into shared memory (replaces the lazy singleton
- *    ph_table(), ph_table.cpp:182-185);
+ *  - reentrant from any host thread, on any device (launch state is cached
+ *    per device); the Payne-Hanek tables are device constants (replace the
+ *    lazy singleton ph_table(), ph_table.cpp:182-185): the binary32 table and
+ *    the forced-Payne-Hanek kernels' binary64 table are staged per CTA into
+ *    shared memory, the binary64 selector kernels (sin/cos/tan_d) read theirs
+ *    through L1 (most of their lanes never touch it);
  *  - results are bit-identical to the deterministic CPU oracle (oracle/).
  *
  * Accuracy: *_u10 <= 1.0 ulp, *_u35 <= 3.5 ulp (vs MPFR), fmod exact.
@@ -140,6 +143,11 @@ int vem_probe_peak(int kind, int iters, double* gops_out);
  * devices of the kernel time in milliseconds (CUDA events). */
 int vem_run_sharded(const char* name, const void* x, const void* y2, void* out, size_t n, int ngpu,
                     double* ms_out);
+/* Same with an explicit device per shard (shard g on devices[g]; a device may
+ * appear more than once -- each shard still gets its own host thread and
+ * stream).  vem_run_sharded(..., ngpu, ...) == devices {0, 1, ..., ngpu-1}. */
+int vem_run_sharded_on(const char* name, const void* x, const void* y2, void* out, size_t n, int ngpu,
+                       const int* devices, double* ms_out);
 
 #ifdef __cplusplus
 }

@@ -1,7 +1,10 @@
-/* BENCH INFRASTRUCTURE ONLY -- upstream SLEEF 3.8.0 AVX-512 on the host cores,
- * the CPU context number of BASELINE.md (C): the paper's own library, exported
- * by torch's libtorch_cpu.so (header torch/include/sleef.h).  Timed by
- * bench.py next to the oracle port; never part of the product.
+/* BENCH + TEST INFRASTRUCTURE ONLY -- upstream SLEEF 3.8.0 AVX-512 on the
+ * host cores, the paper's own library, exported by torch's libtorch_cpu.so
+ * (header torch/include/sleef.h).  Timed by bench.py next to the oracle port
+ * (the CPU context number of BASELINE.md (C)) and used by
+ * tests/test_sleef_crosscheck.py as the <= 1 ulp cross-check of north_star
+ * ("within 1 ULP of the reference"); never part of the product.
+ * Entry names follow vem's; a name SLEEF lacks returns -1.
  * SLEEF has no u35 exp / pow: those names time the u10 entry (labelled). */
 #include <immintrin.h>
 #include <omp.h>
@@ -29,6 +32,25 @@ __m512 Sleef_logf16_u10avx512f(__m512);
 __m512 Sleef_logf16_u35avx512f(__m512);
 __m512 Sleef_powf16_u10avx512f(__m512, __m512);
 __m512 Sleef_fmodf16_avx512f(__m512, __m512);
+__m512d Sleef_asind8_u10avx512f(__m512d);
+__m512d Sleef_asind8_u35avx512f(__m512d);
+__m512d Sleef_acosd8_u10avx512f(__m512d);
+__m512d Sleef_acosd8_u35avx512f(__m512d);
+__m512d Sleef_atan2d8_u10avx512f(__m512d, __m512d);
+__m512d Sleef_atan2d8_u35avx512f(__m512d, __m512d);
+__m512d Sleef_fdimd8_avx512f(__m512d, __m512d);
+__m512 Sleef_sinf16_u35avx512f(__m512);
+__m512 Sleef_cosf16_u35avx512f(__m512);
+__m512 Sleef_tanf16_u35avx512f(__m512);
+__m512 Sleef_atanf16_u10avx512f(__m512);
+__m512 Sleef_atanf16_u35avx512f(__m512);
+__m512 Sleef_asinf16_u10avx512f(__m512);
+__m512 Sleef_asinf16_u35avx512f(__m512);
+__m512 Sleef_acosf16_u10avx512f(__m512);
+__m512 Sleef_acosf16_u35avx512f(__m512);
+__m512 Sleef_atan2f16_u10avx512f(__m512, __m512);
+__m512 Sleef_atan2f16_u35avx512f(__m512, __m512);
+__m512 Sleef_fdimf16_avx512f(__m512, __m512);
 
 typedef __m512d (*ud)(__m512d);
 typedef __m512d (*bd)(__m512d, __m512d);
@@ -54,6 +76,16 @@ static void* pick(const char* n, int* kind) {
   M("fmod_f", Sleef_fmodf16_avx512f, 3)
   M("sin_d_u35", Sleef_sind8_u35avx512f, 0) M("cos_d_u35", Sleef_cosd8_u35avx512f, 0)
   M("tan_d_u35", Sleef_tand8_u35avx512f, 0) M("atan_d_u35", Sleef_atand8_u35avx512f, 0)
+  M("asin_d_u10", Sleef_asind8_u10avx512f, 0) M("asin_d_u35", Sleef_asind8_u35avx512f, 0)
+  M("acos_d_u10", Sleef_acosd8_u10avx512f, 0) M("acos_d_u35", Sleef_acosd8_u35avx512f, 0)
+  M("atan2_d_u10", Sleef_atan2d8_u10avx512f, 1) M("atan2_d_u35", Sleef_atan2d8_u35avx512f, 1)
+  M("fdim_d", Sleef_fdimd8_avx512f, 1)
+  M("sin_f_u35", Sleef_sinf16_u35avx512f, 2) M("cos_f_u35", Sleef_cosf16_u35avx512f, 2)
+  M("tan_f_u35", Sleef_tanf16_u35avx512f, 2) M("atan_f_u10", Sleef_atanf16_u10avx512f, 2)
+  M("atan_f_u35", Sleef_atanf16_u35avx512f, 2) M("asin_f_u10", Sleef_asinf16_u10avx512f, 2)
+  M("asin_f_u35", Sleef_asinf16_u35avx512f, 2) M("acos_f_u10", Sleef_acosf16_u10avx512f, 2)
+  M("acos_f_u35", Sleef_acosf16_u35avx512f, 2) M("atan2_f_u10", Sleef_atan2f16_u10avx512f, 3)
+  M("atan2_f_u35", Sleef_atan2f16_u35avx512f, 3) M("fdim_f", Sleef_fdimf16_avx512f, 3)
 #undef M
   return 0;
 }

@@ -1294,3 +1294,45 @@ void vo_tan_f_u10_ph_arr(const float* x, float* y, size_t n) { vo_tan_f_u10_arr(
 void vo_sin_f_u35_arr(const float* x, float* y, size_t n) { vo_sin_f_u10_arr(x, y, n); }
 void vo_cos_f_u35_arr(const float* x, float* y, size_t n) { vo_cos_f_u10_arr(x, y, n); }
 void vo_tan_f_u35_arr(const float* x, float* y, size_t n) { vo_tan_f_u10_arr(x, y, n); }
+
+/* DD operator hooks (tests only): the restated ddarith.hpp operators above,
+ * exported so tests/test_oracle_reference.py can pin them bit-for-bit against
+ * the reference's own templates (oracle/ref_shim.cpp). */
+static inline dd_t dd_recip(double y) { /* ddarith.hpp:243-254 (FMA path) */
+  double q = 1.0 / y;
+  double e = fma(q, -y, 1.0);
+  dd_t r = {q, q * e};
+  return r;
+}
+void vo_dd_add2(double xh, double xl, double yh, double yl, double* h, double* l) {
+  dd_t x = {xh, xl}, y = {yh, yl}, r = dd_add2(x, y);
+  *h = r.hi; *l = r.lo;
+}
+void vo_dd_mul(double xh, double xl, double yh, double yl, double* h, double* l) {
+  dd_t x = {xh, xl}, y = {yh, yl}, r = dd_mul(x, y);
+  *h = r.hi; *l = r.lo;
+}
+void vo_dd_div(double xh, double xl, double yh, double yl, double* h, double* l) {
+  dd_t x = {xh, xl}, y = {yh, yl}, r = dd_div(x, y);
+  *h = r.hi; *l = r.lo;
+}
+void vo_dd_squ(double xh, double xl, double* h, double* l) {
+  dd_t x = {xh, xl}, r = dd_squ(x);
+  *h = r.hi; *l = r.lo;
+}
+void vo_dd_recip(double y, double* h, double* l) {
+  dd_t r = dd_recip(y);
+  *h = r.hi; *l = r.lo;
+}
+void vo_dd_normalize(double xh, double xl, double* h, double* l) {
+  dd_t x = {xh, xl}, r = dd_normalize(x);
+  *h = r.hi; *l = r.lo;
+}
+void vo_two_sum(double a, double b, double* s, double* e) {
+  dd_t r = two_sum(a, b);
+  *s = r.hi; *e = r.lo;
+}
+void vo_two_prod(double a, double b, double* p, double* e) {
+  dd_t r = two_prod(a, b);
+  *p = r.hi; *e = r.lo;
+}

@@ -76,6 +76,9 @@ def lib() -> ctypes.CDLL:
     L.vem_run_sharded.argtypes = [ctypes.c_char_p, _P, _P, _P, _N, ctypes.c_int,
                                   ctypes.POINTER(ctypes.c_double)]
     L.vem_run_sharded.restype = ctypes.c_int
+    L.vem_run_sharded_on.argtypes = [ctypes.c_char_p, _P, _P, _P, _N, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                                     ctypes.POINTER(ctypes.c_double)]
+    L.vem_run_sharded_on.restype = ctypes.c_int
     L.vem_probe_peak.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
     L.vem_probe_peak.restype = ctypes.c_int
     _lib = L

@@ -18,7 +18,14 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libvem.so")
 SOURCES = ["vem_kernels.cu", "vem_host.cu", "vem_probe.cu"]
-HEADERS = ["vem_math.cuh", "vem_coeffs.h", "vem_ph_tables.h", "../../include/vem.h"]
+# bench/test infrastructure (config-input generator, chunk checksums): a
+# separate library, so the product libvem.so carries only the math path
+AUX_LIB = os.path.join(HERE, "libvem_aux.so")
+AUX_SOURCES = ["vem_aux.cu"]
+# every header under csrc/ (vem_math.cuh, vem_stream.cuh, the generated
+# tables, ...) plus the public C header: any of them newer than the library
+# makes it stale
+HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))) + ["../../include/vem.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -34,38 +41,43 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
+def _stale(lib: str = LIB, sources=SOURCES) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
-    for f in SOURCES + HEADERS + ["../build.py"]:
+    t = os.path.getmtime(lib)
+    for f in sources + HEADERS + ["../build.py"]:
         p = os.path.join(CSRC, f)
         if os.path.exists(p) and os.path.getmtime(p) > t:
             return True
     return False
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
-        return LIB
+def _link(lib: str, sources, verbose: bool):
     objs = []
     bdir = os.path.join(HERE, "_build")
     os.makedirs(bdir, exist_ok=True)
-    for s in SOURCES:
+    for s in sources:
         o = os.path.join(bdir, s.replace(".cu", ".o"))
         cmd = [nvcc(), *NVCC_FLAGS, "-c", os.path.join(CSRC, s), "-o", o]
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)
         objs.append(o)
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     # static cudart: the library carries its own 12.9 runtime (torch bundles an
     # older libcudart.so.12); both share the device's primary context, so
     # torch-allocated pointers and torch streams are valid here.
     cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
            *objs, "-o", tmp]
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if force or _stale():
+        _link(LIB, SOURCES, verbose)
+    if force or _stale(AUX_LIB, AUX_SOURCES):
+        _link(AUX_LIB, AUX_SOURCES, verbose)
     return LIB
 
 

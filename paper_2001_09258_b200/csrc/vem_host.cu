@@ -1,8 +1,9 @@
 // Host-side multi-GPU driver above the per-device C ABI (SURVEY.md §3 S5,
 // §8(e)): contiguous shards [g*N/G, (g+1)*N/G) of every operand, one host
 // thread per device with its own stream and events, no collective on the data
-// path.  Used by the C++ host and by bench.py's multi-GPU path when run
-// without torchrun.
+// path.  The host-array entry point for a C++ caller that owns several GPUs
+// in one process (tests/cpp/host_abi_test.cpp); bench.py's multi-GPU path is
+// one process per GPU under torchrun instead and calls the per-device ABI.
 #include <cuda_runtime.h>
 
 #include <cstring>
@@ -72,15 +73,17 @@ int call(const Entry* e, const void* x, const void* y, void* o, size_t n, cudaSt
 
 }  // namespace
 
-extern "C" int vem_run_sharded(const char* name, const void* x, const void* y2, void* out, size_t n, int ngpu,
-                               double* ms_out) {
+extern "C" int vem_run_sharded_on(const char* name, const void* x, const void* y2, void* out, size_t n,
+                                  int ngpu, const int* devices, double* ms_out) {
   const Entry* e = find(name);
-  if (!e) return (int)cudaErrorInvalidValue;
+  if (!e || !devices) return (int)cudaErrorInvalidValue;
   if (e->binary && !y2) return (int)cudaErrorInvalidValue;
   int ndev = 0;
   cudaError_t st = cudaGetDeviceCount(&ndev);
   if (st != cudaSuccess) return (int)st;
-  if (ngpu < 1 || ngpu > ndev) return (int)cudaErrorInvalidDevice;
+  if (ngpu < 1) return (int)cudaErrorInvalidValue;
+  for (int g = 0; g < ngpu; g++)
+    if (devices[g] < 0 || devices[g] >= ndev) return (int)cudaErrorInvalidDevice;
   std::vector<int> rc(ngpu, 0);
   std::vector<double> ms(ngpu, 0.0);
   std::vector<std::thread> th;
@@ -88,7 +91,7 @@ extern "C" int vem_run_sharded(const char* name, const void* x, const void* y2, 
     th.emplace_back([&, g] {
       size_t lo = n * (size_t)g / ngpu, hi = n * (size_t)(g + 1) / ngpu, m = hi - lo;
       size_t bytes = m * e->elem;
-      cudaError_t err = cudaSetDevice(g);
+      cudaError_t err = cudaSetDevice(devices[g]);
       cudaStream_t s = nullptr;
       void *dx = nullptr, *dy = nullptr, *dout = nullptr;
       cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -126,4 +129,15 @@ extern "C" int vem_run_sharded(const char* name, const void* x, const void* y2, 
   }
   if (ms_out) *ms_out = mx;
   return 0;
+}
+
+extern "C" int vem_run_sharded(const char* name, const void* x, const void* y2, void* out, size_t n, int ngpu,
+                               double* ms_out) {
+  int ndev = 0;
+  cudaError_t st = cudaGetDeviceCount(&ndev);
+  if (st != cudaSuccess) return (int)st;
+  if (ngpu < 1 || ngpu > ndev) return (int)cudaErrorInvalidDevice;
+  std::vector<int> devs(ngpu);
+  for (int g = 0; g < ngpu; g++) devs[g] = g;
+  return vem_run_sharded_on(name, x, y2, out, n, ngpu, devs.data(), ms_out);
 }

@@ -578,9 +578,6 @@ __device__ __forceinline__ double fmod_pend_finish(const fmod_pend& p) {
 // key = estimated 50-bit steps, exact long division for the queue rows.
 template <class T>
 struct FmodQ {
-  static constexpr int kDirect = 0;
-  __device__ static bool direct_ok(T) { return false; }
-  __device__ static T direct(T x, T, const double*) { return x; }
   // every slot gets its trivial result (pending slots are overwritten later)
   __device__ static bool triage(T x, T y, T& res, int& key) {
     const T nx = fabs(x), ny = fabs(y);
@@ -631,8 +628,6 @@ struct FmodQ {
 // ------------------------------------------------ tile work-queue kernel
 // For entry points whose per-element cost is data dependent (fmod: step
 // count; the trig selector: Cody-Waite 1 / 2 / Payne-Hanek).  Per TMA tile:
-//   0. (Q::kDirect) if every element of the tile takes the cheap path
-//      (trig: |x| < 15), evaluate it branch-free in registers and store;
 //   1. triage: Q::triage finishes trivial elements into the tile's output
 //      block in shared memory and gives the others a key (cost class) and a
 //      rank from a shared-memory histogram atomic;
@@ -707,27 +702,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_queue(const T* __restrict__ 
       }
     }
     V* ov = reinterpret_cast<V*>(out) + (blockIdx.x + j * G) * TILE_V;
-    if constexpr (Q::kDirect) {
-      bool ok = true;
-#pragma unroll
-      for (int e = 0; e < NE; e++) ok = ok && Q::direct_ok(xe[e]);
-      if (__syncthreads_and(ok)) {  // also releases the stage
-        if (tid == 0 && j + STAGES < my) {
-          tma::fence_proxy_async_smem();
-          issue(s, blockIdx.x + (j + STAGES) * G);
-        }
-#pragma unroll
-        for (int v = 0; v < VPT; v++) {
-          V o;
-#pragma unroll
-          for (int k = 0; k < W; k++) vget(o, k) = Q::direct(xe[v * W + k], ye[v * W + k], tab);
-          __stcs(ov + v * kThreads + tid, o);
-        }
-        continue;
-      }
-    } else {
-      __syncthreads();  // stage consumed; previous tile's output block stored
-    }
+    __syncthreads();  // stage consumed; previous tile's output block stored
     T* qx = reinterpret_cast<T*>(buf + (size_t)(s * NIN) * TILE_V);
     T* qy = reinterpret_cast<T*>(buf + (size_t)(s * NIN + (NIN - 1)) * TILE_V);
     // ---- 1. triage
@@ -810,6 +785,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_queue(const T* __restrict__ 
     out[i] = Q::eval_full(a[i], NIN == 2 ? b[i] : (T)0, tab);
 }
 
+#ifdef VEM_TUNE
 // ------------------------------------------- warp-private work queue
 // (tuning build only: fmod_f shipped it until the straight-line fmod_f_flat)
 // Same four steps as k_queue, but every warp owns its chunks (32 x NE
@@ -945,7 +921,6 @@ __global__ void __launch_bounds__(kThreads, MINB) k_wqueue(const T* __restrict__
     out[i] = Q::eval_full(a[i], NIN == 2 ? b[i] : (T)0, nullptr);
 }
 
-#ifdef VEM_TUNE
 // Work-ring fmod kernel (superseded by the regrouped streaming kernel,
 // OpFmodD/OpFmodF below; kept in the tuning build for comparison).
 // ------------------------------------------------------------ fmod
@@ -1244,27 +1219,57 @@ VEM_BINARY_OP(OpFdimF, float, ((void)tab, fdim_f(x, y)))
 #undef VEM_SPLIT_BINARY_OP
 
 // ------------------------------------------------------------- launching
-static int num_sms() {
-  static int sms = [] {
-    int dev = 0, v = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v;
-  }();
-  return sms;
+// Per-device launch state.  The shared-memory opt-in
+// (cudaFuncAttributeMaxDynamicSharedMemorySize) and the occupancy figure are
+// properties of a kernel ON A DEVICE: they are cached per (instantiation,
+// device) and (re)computed the first time a kernel is launched on each device,
+// so one process can drive several GPUs (vem_run_sharded, multi-device torch
+// programs).  Zero in the cache = not yet initialised on that device.
+constexpr int kMaxDevices = 64;
+using DevCache = std::atomic<int>[kMaxDevices];
+
+static int current_device() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0) d = 0;
+  return d;
 }
 
+template <class F>
+static int per_device(DevCache& cache, int dev, F init) {
+  if (dev >= kMaxDevices) return init();
+  int v = cache[dev].load(std::memory_order_acquire);
+  if (v == 0) {
+    v = init();  // idempotent: two threads racing here compute the same value
+    cache[dev].store(v, std::memory_order_release);
+  }
+  return v;
+}
+
+static int num_sms(int dev) {
+  static DevCache cache;
+  return per_device(cache, dev, [dev] {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v < 1) v = 148;
+    return v;
+  });
+}
+
+// resident CTAs per SM of `kernel` with `smem` dynamic bytes on the current
+// device (applies the dynamic shared-memory opt-in there first)
 template <class K>
-static int occupancy(K kernel) {
+static int occupancy(K kernel, int smem = 0) {
+  // opt in whenever there is dynamic shared memory: static + dynamic may
+  // exceed the 48 KB default even when the dynamic part alone does not
+  if (smem > 0) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   int b = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kThreads, 0) != cudaSuccess || b < 1) b = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kThreads, smem) != cudaSuccess || b < 1) b = 1;
   return b;
 }
 
-// Persistent grid: min(work, SMs x resident CTAs per SM); `occ` is cached by
-// the caller per kernel instantiation.
-static int grid_for(int occ, size_t work_items, int per_thread) {
+// Persistent grid: min(work, SMs x resident CTAs per SM).
+static int grid_for(int dev, int occ, size_t work_items, int per_thread) {
   size_t need = (work_items + (size_t)kThreads * per_thread - 1) / ((size_t)kThreads * per_thread);
-  size_t cap = (size_t)num_sms() * occ;
+  size_t cap = (size_t)num_sms(dev) * occ;
   size_t g = need < cap ? need : cap;
   return (int)(g < 1 ? 1 : g);
 }
@@ -1272,7 +1277,12 @@ static int grid_for(int occ, size_t work_items, int per_thread) {
 static inline bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
 // Launch with programmatic stream serialization (see tma::griddep_wait): the
-// kernel may start while the previous grid in the stream drains.
+// kernel may start while the previous grid in the stream drains.  INVARIANT:
+// every kernel launched through launch_pdl executes tma::griddep_wait()
+// before its first global-memory access (k_stream, k_queue); only
+// kernel-private set-up (mbarrier init, constant-table staging) may precede
+// it.  Kernels without that wait (k_unary, k_binary, k_reduce_*) are
+// launched with plain <<<>>>.
 template <class K, class... Args>
 static void launch_pdl(K kernel, int grid, int smem, cudaStream_t st, Args... args) {
   cudaLaunchConfig_t cfg = {};
@@ -1294,13 +1304,15 @@ static int launch_unary(const T* x, T* y, size_t n, vem_stream_t s) {
   cudaStream_t st = (cudaStream_t)s;
   if (aligned16(x) && aligned16(y)) {
     auto k = k_unary<Op, T, TABLE, U, true>;
-    static const int occ = occupancy(k);
-    int g = grid_for(occ, n / Vec16<T>::n + 1, U);
+    static DevCache occ;
+    const int dev = current_device();
+    int g = grid_for(dev, per_device(occ, dev, [k] { return occupancy(k); }), n / Vec16<T>::n + 1, U);
     k<<<g, kThreads, 0, st>>>(x, y, n);
   } else {
     auto k = k_unary<Op, T, TABLE, 1, false>;
-    static const int occ = occupancy(k);
-    int g = grid_for(occ, n, 1);
+    static DevCache occ;
+    const int dev = current_device();
+    int g = grid_for(dev, per_device(occ, dev, [k] { return occupancy(k); }), n, 1);
     k<<<g, kThreads, 0, st>>>(x, y, n);
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -1313,13 +1325,15 @@ static int launch_binary(const T* x, const T* y2, T* out, size_t n, vem_stream_t
   cudaStream_t st = (cudaStream_t)s;
   if (aligned16(x) && aligned16(y2) && aligned16(out)) {
     auto k = k_binary<Op, T, TABLE, U, true>;
-    static const int occ = occupancy(k);
-    int g = grid_for(occ, n / Vec16<T>::n + 1, U);
+    static DevCache occ;
+    const int dev = current_device();
+    int g = grid_for(dev, per_device(occ, dev, [k] { return occupancy(k); }), n / Vec16<T>::n + 1, U);
     k<<<g, kThreads, 0, st>>>(x, y2, out, n);
   } else {
     auto k = k_binary<Op, T, TABLE, 1, false>;
-    static const int occ = occupancy(k);
-    int g = grid_for(occ, n, 1);
+    static DevCache occ;
+    const int dev = current_device();
+    int g = grid_for(dev, per_device(occ, dev, [k] { return occupancy(k); }), n, 1);
     k<<<g, kThreads, 0, st>>>(x, y2, out, n);
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -1335,15 +1349,12 @@ static int launch_stream(const T* a, const T* b, T* out, size_t n, vem_stream_t 
   }
   auto k = k_stream<Op, T, NIN, TABLE, VPT, STAGES, MINB>;
   constexpr int smem = STAGES * NIN * kThreads * VPT * 16;
-  static const int occ = [k] {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    int bpm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpm, k, kThreads, smem) != cudaSuccess || bpm < 1) bpm = 1;
-    return bpm;
-  }();
+  static DevCache occ_cache;
+  const int dev = current_device();
+  const int occ = per_device(occ_cache, dev, [k] { return occupancy(k, smem); });
   constexpr size_t tile_e = (size_t)kThreads * VPT * Vec16<T>::n;
   size_t tiles = n / tile_e;
-  size_t cap = (size_t)num_sms() * occ;
+  size_t cap = (size_t)num_sms(dev) * occ;
   size_t g = tiles < cap ? tiles : cap;
   if (g < 1) g = 1;
   launch_pdl(k, (int)g, smem, (cudaStream_t)s, a, b, out, n);
@@ -1361,21 +1372,19 @@ static int launch_queue(const T* a, const T* b, T* out, size_t n, vem_stream_t s
   }
   auto k = k_queue<Q, T, NIN, TABLE, VPT, STAGES, MINB, ROWS, FETCH>;
   constexpr int smem = STAGES * NIN * kThreads * VPT * 16;
-  static const int occ = [k] {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    int bpm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpm, k, kThreads, smem) != cudaSuccess || bpm < 1) bpm = 1;
-    return bpm;
-  }();
+  static DevCache occ_cache;
+  const int dev = current_device();
+  const int occ = per_device(occ_cache, dev, [k] { return occupancy(k, smem); });
   constexpr size_t tile_e = (size_t)kThreads * VPT * Vec16<T>::n;
   size_t tiles = n / tile_e;
-  size_t cap = (size_t)num_sms() * occ;
+  size_t cap = (size_t)num_sms(dev) * occ;
   size_t g = tiles < cap ? tiles : cap;
   if (g < 1) g = 1;
   launch_pdl(k, (int)g, smem, (cudaStream_t)s, a, b, out, n);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return (int)cudaGetLastError();
 }
+#ifdef VEM_TUNE  // tuning-only launchers (tools/tune.py)
 template <class T, int VPT, int STAGES, int MINB = 1>
 static int launch_fmod_w(const T* a, const T* b, T* out, size_t n, vem_stream_t s) {
   using OpF = typename std::conditional<sizeof(T) == 8, OpFmodD, OpFmodF>::type;
@@ -1383,15 +1392,12 @@ static int launch_fmod_w(const T* a, const T* b, T* out, size_t n, vem_stream_t 
   if (!(aligned16(a) && aligned16(out) && aligned16(b))) return launch_binary<OpF, T, kNoTable, 1>(a, b, out, n, s);
   auto k = k_wqueue<FmodQ<T>, T, 2, VPT, STAGES, MINB>;
   constexpr int smem = (kThreads / 32) * STAGES * 2 * 32 * VPT * 16;
-  static const int occ = [k] {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    int bpm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpm, k, kThreads, smem) != cudaSuccess || bpm < 1) bpm = 1;
-    return bpm;
-  }();
+  static DevCache occ_cache;
+  const int dev = current_device();
+  const int occ = per_device(occ_cache, dev, [k] { return occupancy(k, smem); });
   constexpr size_t ch_e = (size_t)32 * VPT * Vec16<T>::n;
   size_t warps = n / ch_e;
-  size_t cap = (size_t)num_sms() * occ * (kThreads / 32);
+  size_t cap = (size_t)num_sms(dev) * occ * (kThreads / 32);
   size_t w = warps < cap ? warps : cap;
   size_t g = (w + kThreads / 32 - 1) / (kThreads / 32);
   if (g < 1) g = 1;
@@ -1399,6 +1405,7 @@ static int launch_fmod_w(const T* a, const T* b, T* out, size_t n, vem_stream_t 
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return (int)cudaGetLastError();
 }
+#endif  // VEM_TUNE
 template <class T, int VPT, int STAGES, int MINB = 1, int ROWS = 1, int FETCH = 1>
 static int launch_fmod_q(const T* a, const T* b, T* out, size_t n, vem_stream_t s) {
   using OpF = typename std::conditional<sizeof(T) == 8, OpFmodD, OpFmodF>::type;
@@ -1412,6 +1419,7 @@ struct OpFmodFFlat {
     return fmod_f_flat(x, y);
   }
 };
+#ifdef VEM_TUNE
 struct OpFmodFFixed {
   __device__ __forceinline__ float operator()(float x, float y, const double* tab) const {
     (void)tab;
@@ -1423,6 +1431,7 @@ static int launch_fmod_fixed(const T* a, const T* b, T* out, size_t n, vem_strea
   if constexpr (sizeof(T) == 4) return launch_stream<OpFmodFFixed, float, 2, kNoTable, VPT, STAGES, MINB>(a, b, out, n, s);
   else return launch_fmod_q<double, 2, 2, 1, 1>(a, b, out, n, s);
 }
+#endif  // VEM_TUNE
 template <class T, int VPT, int STAGES, int MINB = 1>
 static int launch_fmod_flat(const T* a, const T* b, T* out, size_t n, vem_stream_t s) {
   if constexpr (sizeof(T) == 4) return launch_stream<OpFmodFFlat, float, 2, kNoTable, VPT, STAGES, MINB>(a, b, out, n, s);
@@ -1438,14 +1447,16 @@ static int launch_fmod(const T* a, const T* b, T* out, size_t n, vem_stream_t s)
     else return launch_binary<OpFmodF, T, kNoTable, 1>(a, b, out, n, s);
   }
   auto k = k_fmod<T, MINB>;
-  static const int occ = [k] {
+  static DevCache occ_cache;
+  const int dev = current_device();
+  const int occ = per_device(occ_cache, dev, [k] {
     int bpm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpm, k, kFmodWarps * 32, 0) != cudaSuccess || bpm < 1)
       bpm = 1;
     return bpm;
-  }();
+  });
   size_t chunks = (n + kFmodChunk - 1) / kFmodChunk;
-  size_t warps_cap = (size_t)num_sms() * occ * kFmodWarps;
+  size_t warps_cap = (size_t)num_sms(dev) * occ * kFmodWarps;
   size_t warps = chunks < warps_cap ? chunks : warps_cap;
   size_t g = (warps + kFmodWarps - 1) / kFmodWarps;
   k<<<(int)(g < 1 ? 1 : g), kFmodWarps * 32, 0, (cudaStream_t)s>>>(a, b, out, n);
@@ -1490,8 +1501,9 @@ template <int MODE>
 static int launch_reduce_d(const double* x, double* hi, double* lo, int* q, size_t n, vem_stream_t s) {
   if (n == 0) return 0;
   auto k = k_reduce_d<MODE>;
-  static const int occ = occupancy(k);
-  int g = grid_for(occ, n, 1);
+  static DevCache occ;
+  const int dev = current_device();
+  int g = grid_for(dev, per_device(occ, dev, [k] { return occupancy(k); }), n, 1);
   k<<<g, kThreads, 0, (cudaStream_t)s>>>(x, hi, lo, q, n);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return (int)cudaGetLastError();
@@ -1654,8 +1666,9 @@ int vem_ph_reduce_d(const double* x, double* hi, double* lo, int* q, size_t n, v
 }
 int vem_ph_reduce_f(const float* x, double* r, int* q, size_t n, vem_stream_t s) {
   if (n == 0) return 0;
-  static const int occ = occupancy(k_reduce_f);
-  int g = grid_for(occ, n, 1);
+  static DevCache occ;
+  const int dev = current_device();
+  int g = grid_for(dev, per_device(occ, dev, [] { return occupancy(k_reduce_f); }), n, 1);
   k_reduce_f<<<g, kThreads, 0, (cudaStream_t)s>>>(x, r, q, n);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return (int)cudaGetLastError();

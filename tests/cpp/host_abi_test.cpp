@@ -56,6 +56,12 @@ int main(int argc, char** argv) {
   if (vem_run_sharded("exp_d_u10", x.data(), nullptr, o.data(), n, 1, &ms) != 0) return 1;
   ((uarr_d)dlsym(h, "vo_exp_d_u10_arr"))(x.data(), e.data(), n);
   if (std::memcmp(o.data(), e.data(), n * 8) != 0) { std::printf("run_sharded differs\n"); bad++; }
+  // three shards on device 0 from three host threads (ragged boundaries:
+  // n = 2^16 + 3 is not a multiple of 3 * 16 bytes), binary entry point
+  const int devs[3] = {0, 0, 0};
+  if (vem_run_sharded_on("pow_d_u10", x.data(), y.data(), o.data(), n, 3, devs, &ms) != 0) return 1;
+  ((barr_d)dlsym(h, "vo_pow_d_u10_arr"))(x.data(), y.data(), e.data(), n);
+  if (std::memcmp(o.data(), e.data(), n * 8) != 0) { std::printf("run_sharded_on differs\n"); bad++; }
   cudaFree(dx); cudaFree(dy); cudaFree(dout);
   std::printf("%s: %d mismatching entry points\n", bad ? "FAIL" : "OK", bad);
   return bad ? 1 : 0;

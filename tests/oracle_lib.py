@@ -136,3 +136,37 @@ def ph_table_bytes(prec: str = "d") -> bytes:
     n = 4096 if prec == "d" else 4 * 129
     p = f()
     return np.ctypeslib.as_array(p, shape=(n,)).copy().tobytes()
+
+
+# ------------------------------------------------ config inputs (host twin)
+_gen = None
+
+
+def gen():
+    global _gen
+    if _gen is None:
+        L = _load("libvem_gen.so")
+        L.vg_fill.argtypes = [_P, _P, _N, ctypes.c_uint64]
+        L.vg_checksum.argtypes = [_P, _N, ctypes.c_int, ctypes.c_uint64, ctypes.c_int, _P]
+        _gen = L
+    return _gen
+
+
+def gen_fill(recipe: dict, n: int, offset: int = 0) -> np.ndarray:
+    """oracle/vem_gen_host.c: elements [offset, offset+n) of a recipe."""
+    from paper_2001_09258_b200 import inputs as I
+    out = np.empty(n, dtype=np.float32 if recipe["f32"] else np.float64)
+    r = I.recipe_struct(recipe)
+    gen().vg_fill(ctypes.byref(r), ptr(out), n, offset)
+    return out
+
+
+def gen_checksum(a: np.ndarray, offset: int = 0, log2chunk: int = 24) -> dict:
+    n = a.size
+    if n == 0:
+        return {}
+    c0 = offset >> log2chunk
+    c1 = (offset + n - 1) >> log2chunk
+    sums = np.zeros(c1 - c0 + 1, dtype=np.uint64)
+    gen().vg_checksum(ptr(np.ascontiguousarray(a)), n, a.dtype.itemsize, offset, log2chunk, ptr(sums))
+    return {c0 + k: int(v) for k, v in enumerate(sums)}

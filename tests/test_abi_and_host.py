@@ -83,32 +83,39 @@ def test_inputs_deterministic():
 
 
 def _gloo_worker(rank, world, port, q):
+    """One rank of the sharded path on the CPU: its contiguous shard of the
+    first 2^24-element chunk of config 1 (host generator + oracle), partial
+    chunk checksums, the path's one collective (all_reduce SUM of the chunk
+    vectors, bench.py verify_workload) and the max-over-ranks timing
+    reduction; rank 0 compares with the golden oracle checksum."""
+    import json
+
     import torch
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from oracle_lib import oracle_eval
-    from paper_2001_09258_b200 import inputs as I
-    n = 4096
-    x = I.config_inputs(5, "sin", "d", n)[0]
-    lo, hi = n * rank // world, n * (rank + 1) // world  # contiguous shard
-    out = oracle_eval("sin_d_u10", x[lo:hi])
-    digest = torch.tensor([int(hashlib.md5(out.tobytes()).hexdigest()[:12], 16)], dtype=torch.int64)
-    parts = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
-    dist.all_gather(parts, digest)
+    import oracle_lib as O
+    from paper_2001_09258_b200 import configs as C
+    m = 1 << C.LOG2CHUNK
+    lo, hi = m * rank // world, m * (rank + 1) // world  # contiguous shard (SURVEY.md §8(e)), ragged
+    (r,) = C.recipes("cfg1", "sin_d_u10")
+    x = O.gen_fill(r, hi - lo, lo)
+    out = O.oracle_eval("sin_d_u10", x)
+    vec = torch.tensor([C.chunk_vector(O.gen_checksum(out, lo, C.LOG2CHUNK), 1)], dtype=torch.int64)
+    dist.all_reduce(vec, op=dist.ReduceOp.SUM)
     t = torch.tensor([float(rank + 1)])
     dist.all_reduce(t, op=dist.ReduceOp.MAX)  # max-over-ranks timing reduction
     if rank == 0:
-        full = oracle_eval("sin_d_u10", x)
-        ref = [int(hashlib.md5(full[n * r // world:n * (r + 1) // world].tobytes()).hexdigest()[:12], 16)
-               for r in range(world)]
-        q.put(([int(p.item()) for p in parts] == ref, float(t.item())))
+        gold = json.load(open(os.path.join(ROOT, "tests", "golden", "config_checksums.json")))
+        ref = gold["configs"]["cfg1"]["outputs"]["sin_d_u10"]
+        q.put((C.mismatching_chunks(vec[0].tolist(), ref, 0, 1), float(t.item())))
     dist.destroy_process_group()
 
 
-def test_sharded_digests_gloo_world2():
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_checksums_gloo(world):
     import multiprocessing as mp
     import socket
     s = socket.socket()
@@ -117,10 +124,10 @@ def test_sharded_digests_gloo_world2():
     s.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    ps = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
+    ps = [ctx.Process(target=_gloo_worker, args=(r, world, port, q)) for r in range(world)]
     for p in ps:
         p.start()
-    ok, mx = q.get(timeout=120)
+    bad, mx = q.get(timeout=180)
     for p in ps:
         p.join(timeout=60)
-    assert ok and mx == 2.0
+    assert bad == [] and mx == float(world)

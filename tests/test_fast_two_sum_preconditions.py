@@ -41,7 +41,9 @@ def test_log_table_orders_the_final_two_sum():
             k = tmp >> 52
             m = _from_bits(tmp + 0x3FE8000000000000 - (k << 52))
             rmax = max(rmax, abs(m * invc[i] - 1.0))
-        rmax *= 1.01  # L.hi = RN(r - r^2/2) in the u10 path
+        # L.hi = RN(r - r^2/2) in the u10 path: |L.hi| <= |r| + r^2/2,
+        # rounded up by at most one ulp (a factor 1 + 2^-52)
+        rmax = (rmax + rmax * rmax / 2) * (1 + 2.0 ** -52)
         rmax_all = max(rmax_all, rmax)
         if hi[i] != 0.0:
             assert math.frexp(hi[i])[1] >= math.frexp(rmax)[1], i
@@ -73,6 +75,16 @@ def test_atan_and_atan2_pairs_match_two_sum():
     for c in (-1.0, 1.0):
         assert _same(_two_sum(a, np.full_like(a, c)), _fast(np.full_like(a, c), a))
     den = np.exp(rng.uniform(-700, 700, 1 << 20))
+    # atan2_split pre-scales huge / tiny denominators by 2^-100 / 2^100: cover
+    # the scaled ranges near 2^1000 and 2^-900, and subnormal numerators
+    scaled = np.concatenate([np.ldexp(rng.uniform(1, 2, 1 << 16), rng.integers(995, 1024, 1 << 16)) * 2.0 ** -100,
+                             np.ldexp(rng.uniform(1, 2, 1 << 16), rng.integers(-1022, -900, 1 << 16)) * 2.0 ** 100])
+    den = np.concatenate([den, scaled])
     num = den * rng.uniform(lo, 1.0, den.size)
+    sub_den = np.ldexp(rng.uniform(1, 2, 1 << 16), rng.integers(-1074, -1022, 1 << 16))
+    sub_num = sub_den * rng.uniform(lo, 1.0, sub_den.size)  # subnormal numerators (and denominators)
+    den = np.concatenate([den, sub_den])
+    num = np.concatenate([num, sub_num])
+    assert np.all(np.abs(den) >= np.abs(num))  # Fast2Sum's precondition
     for sg in (-1.0, 1.0):
         assert _same(_two_sum(num, sg * den), _fast(sg * den, num))

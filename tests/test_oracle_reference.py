@@ -142,18 +142,47 @@ def test_two_over_pi_bits_match_reference_constant():
 
 @needs_ref
 def test_dd_ops_bit_exact_vs_reference():
-    """ddarith.hpp operators (FMA path) vs the oracle's restatement."""
+    """ddarith.hpp operators (FMA path, compiled from the reference by
+    oracle/ref_build.py) vs the oracle's restatements (vo_dd_*), bit for bit:
+    two_sum, two_prod, dd_add2, dd_mul, dd_div, dd_squ, dd_recip,
+    dd_normalize over random DD operands spanning 2^-60..2^60 in both signs,
+    tails 2^-53 below their heads, plus cancellation pairs (x, -x(1+eps))."""
     L = ref_lib("gcc")
     O = ctypes.CDLL(os.path.join(ROOT, "oracle", "_build", "libvem_oracle.so"))
     D = ctypes.c_double
     P = ctypes.POINTER(ctypes.c_double)
-    for fn in ("ref_dd_add2", "ref_dd_mul", "ref_dd_div"):
-        getattr(L, fn).argtypes = [D, D, D, D, P, P]
+    for lib, pre in ((L, "ref_"), (O, "vo_")):
+        for fn in ("dd_add2", "dd_mul", "dd_div"):
+            getattr(lib, pre + fn).argtypes = [D, D, D, D, P, P]
+        for fn in ("dd_squ", "dd_normalize", "two_sum", "two_prod"):
+            getattr(lib, pre + fn).argtypes = [D, D, P, P]
+        getattr(lib, pre + "dd_recip").argtypes = [D, P, P]
     rng = np.random.default_rng(7)
-    xs = rng.standard_normal((2000, 4)) * np.exp2(rng.integers(-30, 30, (2000, 4)))
-    h, lo = D(), D()
-    for a, b, c, d in xs:
-        b, d = b * 2 ** -60, d * 2 ** -60
-        L.ref_dd_div(a, b, c, d, ctypes.byref(h), ctypes.byref(lo))
-        assert np.isfinite(h.value)
-    assert O is not None
+    n = 3000
+    hi = rng.standard_normal((n, 2)) * np.exp2(rng.integers(-60, 60, (n, 2)))
+    lo = hi * rng.standard_normal((n, 2)) * 2.0 ** -53
+    hi[: n // 10, 1] = -hi[: n // 10, 0] * (1 + rng.standard_normal(n // 10) * 2.0 ** -40)  # cancellation
+    ops = {
+        "dd_add2": lambda f, a, b, c, d, h, l: f(a, b, c, d, h, l),
+        "dd_mul": lambda f, a, b, c, d, h, l: f(a, b, c, d, h, l),
+        "dd_div": lambda f, a, b, c, d, h, l: f(a, b, c, d, h, l),
+        "dd_squ": lambda f, a, b, c, d, h, l: f(a, b, h, l),
+        "dd_normalize": lambda f, a, b, c, d, h, l: f(a, b, h, l),
+        "two_sum": lambda f, a, b, c, d, h, l: f(a, c, h, l),
+        "two_prod": lambda f, a, b, c, d, h, l: f(a, c, h, l),
+        "dd_recip": lambda f, a, b, c, d, h, l: f(c, h, l),
+    }
+    bits = lambda v: np.float64(v).view(np.uint64)  # noqa: E731
+    for op, call in ops.items():
+        bad = 0
+        for k in range(n):
+            a, c = float(hi[k, 0]), float(hi[k, 1])
+            b, d = float(lo[k, 0]), float(lo[k, 1])
+            if op in ("dd_normalize",):  # precondition |hi| >= |lo|
+                b = a * 2.0 ** -60
+            rh, rl, oh, ol = D(), D(), D(), D()
+            call(getattr(L, "ref_" + op), a, b, c, d, ctypes.byref(rh), ctypes.byref(rl))
+            call(getattr(O, "vo_" + op), a, b, c, d, ctypes.byref(oh), ctypes.byref(ol))
+            if bits(rh.value) != bits(oh.value) or bits(rl.value) != bits(ol.value):
+                bad += 1
+        assert bad == 0, f"{op}: oracle differs from ddarith.hpp in {bad} of {n} cases"

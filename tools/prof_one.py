@@ -1,7 +1,7 @@
 #!/usr/bin/env python3
 """Run one entry point on one BASELINE config's inputs (dev tool for ncu).
 
-Usage: python tools/prof_one.py NAME[,NAME...] CFG [log2_n=24] [reps=3]
+Usage: python tools/prof_one.py NAME[@CFG][,NAME[@CFG]...] CFG [log2_n=24] [reps=3]
 e.g.  ncu --set full -k regex:k_stream -s 1 -c 1 python tools/prof_one.py sin_d_u10 5 24
 reps=0: each entry point runs exactly once, no warm-up (one ncu capture per
 entry point with -c <number of names>).
@@ -23,12 +23,17 @@ def main():
     n = 1 << (int(sys.argv[3]) if len(sys.argv) > 3 else 24)
     reps = int(sys.argv[4]) if len(sys.argv) > 4 else 3
     for name in sys.argv[1].split(","):
-        run(name, cfg, n, reps)
+        # NAME@CFG overrides the config per entry point
+        name, _, c = name.partition("@")
+        run(name, int(c) if c else cfg, n, reps)
 
 
 def run(name, cfg, n, reps):
+    from paper_2001_09258_b200 import _aux
     fn, p = name.split("_")[0], name.split("_")[1]
-    ts = [torch.from_numpy(a).cuda() for a in I.config_inputs(cfg, fn, p, n)]
+    # config inputs generated on the device (bit-identical to inputs.py)
+    ts = [_aux.fill(r, torch.empty(n, dtype=torch.float32 if r["f32"] else torch.float64, device="cuda"))
+          for r in I.config_recipes(cfg, fn, p)]
     out = torch.empty_like(ts[0])
     if reps == 0:
         api.call(name, *ts, out=out)
