@@ -512,6 +512,173 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
   }
 }
 
+// ------------------------------------------------ trig selector kernel
+// sin / cos / tan f64 (u10, u35) with the reference's per-lane reduction
+// selector (reduction.hpp:189-206: Cody-Waite 1 / 2 below 1e14, Payne-Hanek
+// above).  Same TMA pipeline as k_stream; per tile, every warp (32 x NE
+// elements, NE = 2 VPT):
+//   0. all elements |x| < 15      -> branch-free Cody-Waite-1 bodies from
+//      registers (config 1); all elements Payne-Hanek -> branch-free Op::ph
+//      bodies, two interleaved (config 3-like inputs through the selector);
+//   1. otherwise one class per element, 3 classes: trivial (|x| < 2^-27,
+//      zeros, subnormals, Inf/NaN: closed-form result, written straight to
+//      the warp's result block), Cody-Waite (levels 1 and 2), Payne-Hanek;
+//   2. one warp scan of the packed per-lane counts (nph << 16 | ncw) places
+//      every Payne-Hanek argument in [0, nph) and every Cody-Waite argument in
+//      [nph, nph + ncw) of the warp's sorted block (shared memory), with its
+//      tile slot alongside;
+//   3. full Payne-Hanek rows of 32 run Op::ph two rows at a time
+//      (interleaved, uniform, no divergence); the boundary row and the
+//      Cody-Waite rows run the per-lane selector op();  results are scattered
+//      to their slots in the result block;
+//   4. each lane gathers its NE results (conflict-free) for the coalesced
+//      16-byte st.global.cs.
+// Registers hold one or two rows of work at a time (the arguments live in
+// shared memory between the steps), which keeps the kernel at <= 80
+// registers: 3 CTAs (24 warps) per SM.
+template <class Op, int TABLE, int VPT, int STAGES, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_trig(const double* __restrict__ a, double* __restrict__ out,
+                                                         size_t n) {
+  using V = double2;
+  constexpr int W = 2;
+  constexpr int TILE_V = kThreads * VPT;
+  constexpr uint32_t TILE_BYTES = TILE_V * 16;
+  constexpr int TILE_E = TILE_V * W;
+  constexpr int NE = VPT * W;  // elements per lane per tile
+  constexpr int WE = 32 * NE;  // elements per warp per tile
+  constexpr int NW = kThreads / 32;
+  extern __shared__ __align__(128) unsigned char dsm[];
+  __shared__ uint64_t bars[STAGES];
+  __shared__ __align__(16) double stab[TableSize<TABLE>::n];
+  __shared__ __align__(16) double s_x[NW][WE + 32];  // sorted arguments (+ a junk slot per lane)
+  __shared__ __align__(16) double s_y[NW][WE];       // results in slot order (slot = e * 32 + lane)
+  __shared__ unsigned short s_i[NW][WE + 32];        // slot of each sorted argument
+  V* buf = reinterpret_cast<V*>(dsm);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* sx = s_x[warp];
+  double* sy = s_y[warp];
+  unsigned short* si = s_i[warp];
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; s++) tma::mbar_init(&bars[s], 1);
+    tma::fence_barrier_init();
+  }
+  const double* tab = stage_table<TABLE>(stab);  // includes __syncthreads()
+  tma::griddep_wait();  // inputs / outputs may belong to the previous grid
+  tma::griddep_launch_dependents();
+  Op op;
+  const size_t ntiles = n / TILE_E;
+  const size_t G = gridDim.x;
+  const size_t my = ntiles > blockIdx.x ? (ntiles - blockIdx.x + G - 1) / G : 0;
+  uint64_t pol = 0;
+  auto issue = [&](int s, size_t tile) {
+    tma::mbar_expect_tx(&bars[s], TILE_BYTES);
+    tma::bulk_g2s(buf + (size_t)s * TILE_V, reinterpret_cast<const V*>(a) + tile * TILE_V, TILE_BYTES, &bars[s],
+                  pol);
+  };
+  if (tid == 0) {
+    pol = tma::policy_evict_first();
+    for (int s = 0; s < STAGES && (size_t)s < my; s++) issue(s, blockIdx.x + (size_t)s * G);
+  }
+  for (size_t j = 0; j < my; j++) {
+    const int s = (int)(j % STAGES);
+    tma::mbar_wait(&bars[s], (uint32_t)((j / STAGES) & 1));
+    double xe[NE];
+#pragma unroll
+    for (int v = 0; v < VPT; v++) {
+      const V t = buf[(size_t)s * TILE_V + v * kThreads + tid];
+      xe[v * W] = t.x;
+      xe[v * W + 1] = t.y;
+    }
+    __syncthreads();  // stage s fully consumed -> refill it
+    if (tid == 0 && j + STAGES < my) {
+      tma::fence_proxy_async_smem();
+      issue(s, blockIdx.x + (j + STAGES) * G);
+    }
+    V* ov = reinterpret_cast<V*>(out) + (blockIdx.x + j * G) * TILE_V;
+    // ---- 0. uniform warps
+    bool small = true;
+#pragma unroll
+    for (int e = 0; e < NE; e++) small = small && Op::is_cw1(xe[e]);
+    if (__all_sync(0xffffffffu, small)) {
+#pragma unroll
+      for (int v = 0; v < VPT; v++) __stcs(ov + v * kThreads + tid, make_double2(op.cw1(xe[v * W], tab),
+                                                                                   op.cw1(xe[v * W + 1], tab)));
+      continue;
+    }
+    // ---- 1. classes: bit e of mph / mcw
+    uint32_t mph = 0, mcw = 0;
+#pragma unroll
+    for (int e = 0; e < NE; e++) {
+      const int c = Op::cls3(xe[e]);
+      mph |= (uint32_t)(c == 2) << e;
+      mcw |= (uint32_t)(c == 1) << e;
+    }
+    if (__all_sync(0xffffffffu, mph == (1u << NE) - 1u)) {
+#pragma unroll 1
+      for (int v = 0; v < VPT; v++) {
+        const double x0 = xe[v * W], x1 = xe[v * W + 1];
+        __stcs(ov + v * kThreads + tid, make_double2(op.ph(x0, tab), op.ph(x1, tab)));
+      }
+      continue;
+    }
+    // ---- 2. placement: one scan of the packed per-lane counts
+    const int cnt = (__popc(mph) << 16) | __popc(mcw);
+    int inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    const int tot = __shfl_sync(0xffffffffu, inc, 31);
+    const int nph = tot >> 16, nall = nph + (tot & 0xffff);
+    int pph = (inc - cnt) >> 16;
+    int pcw = nph + ((inc - cnt) & 0xffff);
+#pragma unroll
+    for (int e = 0; e < NE; e++) {
+      const bool isph = (mph >> e) & 1u, iscw = (mcw >> e) & 1u;
+      const int slot = e * 32 + lane;
+      const int pos = isph ? pph : (iscw ? pcw : WE + lane);
+      sx[pos] = xe[e];
+      si[pos] = (unsigned short)slot;
+      pph += isph;
+      pcw += iscw;
+      if (!(isph || iscw)) sy[slot] = Op::trivial(xe[e]);
+    }
+    __syncwarp();
+    // ---- 3. rows
+    int r = 0;
+#pragma unroll 1
+    for (; (r + 2) * 32 <= nph; r += 2) {
+      const int ia = r * 32 + lane, ib = ia + 32;
+      const double xa = sx[ia], xb = sx[ib];
+      const int sa = si[ia], sb = si[ib];
+      const double ya = op.ph(xa, tab), yb = op.ph(xb, tab);
+      sy[sa] = ya;
+      sy[sb] = yb;
+    }
+    if ((r + 1) * 32 <= nph) {
+      const int ia = r * 32 + lane;
+      sy[si[ia]] = op.ph(sx[ia], tab);
+      r++;
+    }
+#pragma unroll 1
+    for (; r * 32 < nall; r++) {
+      const int i = r * 32 + lane;
+      if (i < nall) sy[si[i]] = op(sx[i], tab);
+    }
+    __syncwarp();
+    // ---- 4. gather + coalesced store
+#pragma unroll
+    for (int v = 0; v < VPT; v++)
+      __stcs(ov + v * kThreads + tid, make_double2(sy[(v * W) * 32 + lane], sy[(v * W + 1) * 32 + lane]));
+    __syncwarp();  // the block is rewritten by the next tile
+  }
+  // remainder (< one tile)
+  const size_t done = ntiles * TILE_E;
+  for (size_t i = done + (size_t)blockIdx.x * kThreads + tid; i < n; i += G * kThreads) out[i] = op(a[i], tab);
+}
+
 // ------------------------------------------------------- fmod: step queue
 // fmod's cost is data dependent: ceil(E/50) exact 50-bit long-division steps
 // (E = exponent gap, config 4 f64: 0 for the half of the pairs with |x| < |y|,
@@ -1069,6 +1236,11 @@ __device__ __forceinline__ bool trig_is_trivial(double x) {
   const uint32_t h = (uint32_t)__double2hiint(x) & 0x7fffffffu;
   return h < 0x3E400000u || h >= 0x7ff00000u;
 }
+// 0 = trivial, 1 = Cody-Waite (level 1 or 2, |x| <= 1e14), 2 = Payne-Hanek
+__device__ __forceinline__ int trig_class3(double x) {
+  const uint64_t ab = bits_d(x) & 0x7fffffffffffffffull;
+  return (ab < 0x3E40000000000000ull || ab >= 0x7ff0000000000000ull) ? 0 : (ab <= 0x42d6bcc41e900000ull ? 1 : 2);
+}
 #define VEM_TRIG_OP(NAME, FN, ...)                                                       \
   struct NAME {                                                                          \
     __device__ __forceinline__ double operator()(double x, const double* tab) const {   \
@@ -1081,6 +1253,7 @@ __device__ __forceinline__ bool trig_is_trivial(double x) {
       return FN<kPh>(x, reinterpret_cast<const double*>(gPhDI) __VA_ARGS__);              \
     }                                                                                    \
     __device__ __forceinline__ static int cls(double x) { return trig_class(x); }      \
+    __device__ __forceinline__ static int cls3(double x) { return trig_class3(x); }    \
     __device__ __forceinline__ static bool is_cw1(double x) { return trig_is_cw1(x); } \
     __device__ __forceinline__ static bool is_trivial(double x) { return trig_is_trivial(x); } \
     __device__ static double trivial(double x);                                          \
@@ -1362,6 +1535,25 @@ static int launch_stream(const T* a, const T* b, T* out, size_t n, vem_stream_t 
   return (int)cudaGetLastError();
 }
 
+template <class Op, int TABLE, int VPT, int STAGES, int MINB>
+static int launch_trig(const double* a, const double*, double* out, size_t n, vem_stream_t s) {
+  if (n == 0) return 0;
+  if (!(aligned16(a) && aligned16(out))) return launch_unary<Op, double, TABLE, 1>(a, out, n, s);
+  auto k = k_trig<Op, TABLE, VPT, STAGES, MINB>;
+  constexpr int smem = STAGES * kThreads * VPT * 16;
+  static DevCache occ_cache;
+  const int dev = current_device();
+  const int occ = per_device(occ_cache, dev, [k] { return occupancy(k, smem); });
+  constexpr size_t tile_e = (size_t)kThreads * VPT * 2;
+  size_t tiles = n / tile_e;
+  size_t cap = (size_t)num_sms(dev) * occ;
+  size_t g = tiles < cap ? tiles : cap;
+  if (g < 1) g = 1;
+  launch_pdl(k, (int)g, smem, (cudaStream_t)s, a, out, n);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return (int)cudaGetLastError();
+}
+
 template <class Q, class Op, class T, int NIN, int TABLE, int VPT, int STAGES, int MINB = 1, int ROWS = 1,
           int FETCH = 1>
 static int launch_queue(const T* a, const T* b, T* out, size_t n, vem_stream_t s) {
@@ -1548,6 +1740,7 @@ struct OpFmodPlain {
   }
 };
 #define VEM_STREAM launch_tuned
+#define VEM_TRIG launch_trig
 template <class T>
 static int launch_fmod_tuned(const T* a, const T* b, T* o, size_t n, vem_stream_t s) {
   using OpF = typename std::conditional<sizeof(T) == 8, OpFmodD, OpFmodF>::type;
@@ -1581,6 +1774,7 @@ static int launch_fmod_tuned(const T* a, const T* b, T* o, size_t n, vem_stream_
 #define VEM_FMOD launch_fmod_tuned
 #else
 #define VEM_STREAM launch_stream
+#define VEM_TRIG launch_trig
 #define VEM_FMOD launch_fmod
 #endif
 
@@ -1588,9 +1782,9 @@ static int launch_fmod_tuned(const T* a, const T* b, T* o, size_t n, vem_stream_
 // vectors in flight, FP64-pipe-bound ones 2 (register pressure).
 extern "C" {
 
-int vem_sin_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpSinD, double, 1, kTableDG, 4, 2, 2>(x, nullptr, y, n, s); }
-int vem_cos_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpCosD, double, 1, kTableDG, 4, 2, 2>(x, nullptr, y, n, s); }
-int vem_tan_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpTanD, double, 1, kTableDG, 4, 2, 3>(x, nullptr, y, n, s); }
+int vem_sin_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_TRIG<OpSinD, kTableDG, 4, 2, 3>(x, nullptr, y, n, s); }
+int vem_cos_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_TRIG<OpCosD, kTableDG, 4, 2, 3>(x, nullptr, y, n, s); }
+int vem_tan_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_TRIG<OpTanD, kTableDG, 4, 2, 3>(x, nullptr, y, n, s); }
 int vem_sin_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpSinDPh, double, 1, kTableDI, 4, 2, 2>(x, nullptr, y, n, s); }
 int vem_cos_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpCosDPh, double, 1, kTableDI, 4, 2, 2>(x, nullptr, y, n, s); }
 int vem_tan_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpTanDPh, double, 1, kTableDI, 4, 2, 2>(x, nullptr, y, n, s); }
@@ -1631,9 +1825,9 @@ int vem_fmod_f(const float* x, const float* y2, float* o, size_t n, vem_stream_t
 }
 
 // ---- SURVEY.md §8(f).1 additions
-int vem_sin_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpSinDU35, double, 1, kTableDG35, 4, 2, 3>(x, nullptr, y, n, s); }
-int vem_cos_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpCosDU35, double, 1, kTableDG35, 4, 2, 3>(x, nullptr, y, n, s); }
-int vem_tan_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpTanDU35, double, 1, kTableDG35, 4, 2, 3>(x, nullptr, y, n, s); }
+int vem_sin_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_TRIG<OpSinDU35, kTableDG35, 4, 2, 3>(x, nullptr, y, n, s); }
+int vem_cos_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_TRIG<OpCosDU35, kTableDG35, 4, 2, 3>(x, nullptr, y, n, s); }
+int vem_tan_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_TRIG<OpTanDU35, kTableDG35, 4, 2, 3>(x, nullptr, y, n, s); }
 int vem_atan_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpAtanDU35, double, 1, kNoTable, 2, 2>(x, nullptr, y, n, s); }
 int vem_asin_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpAsinD, double, 1, kNoTable, 2, 2>(x, nullptr, y, n, s); }
 int vem_asin_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpAsinDU35, double, 1, kNoTable, 2, 2>(x, nullptr, y, n, s); }
