@@ -170,30 +170,6 @@ __global__ void __launch_bounds__(kThreads) k_binary(const T* __restrict__ x, co
   }
 }
 
-// Ops whose per-lane work depends on a data class (the trig reduction
-// selector, reduction.hpp:189-206: CW1 / CW2 / Payne-Hanek).  For these the
-// streaming kernel regroups each warp's elements by class (warp-level
-// ballot/popcount compaction through shared memory) so that lanes of one
-// warp take the same reduction path; results are scattered back to their
-// original slots before the coalesced store.  Warps whose elements all share
-// one class skip the regrouping.
-template <class Op> struct SortsByClass {
-  static constexpr bool value = false;
-  static constexpr int classes = 1;
-};
-// ops with a branch-free Cody-Waite-level-1 body for all-small warps
-template <class Op> struct HasCw1 { static constexpr bool value = false; };
-// Leading Payne-Hanek rows evaluated as interleaved branch-free bodies
-// (Op::ph, same values as the selector for class-2 elements) when the
-// warp's sorted block starts with at least this many full class-2 rows.
-#ifndef VEM_PH_ROWS
-#define VEM_PH_ROWS 3
-#endif
-template <class Op> struct PhRows { static constexpr int value = 0; };
-// ops with a closed-form result for "trivial" inputs (trig: |x| < 2^-27 and
-// non-finite x), which the class regrouping leaves out of the sorted rows
-template <class Op> struct HasTrivial { static constexpr bool value = false; };
-
 // Ops with a split fast path (vem_math.cuh "split fast paths"): the kernel
 // evaluates a tile's elements with Op::fast (branch-free, interleavable)
 // and passes the elements it flags to Op::slow.
@@ -208,7 +184,12 @@ __device__ __noinline__ T full_op(T x, T y, const double* tab) { return Op()(x, 
 // NIN inputs (1 or 2); tiles of kThreads*VPT 16-byte vectors per input;
 // STAGES tiles in flight per CTA (see vem_stream.cuh).  Elements past the
 // last full tile are finished by a grid-stride scalar loop in the same launch.
-template <class Op, class T, int NIN, int TABLE, int VPT, int STAGES, int MINB = 1>
+// WREL: release stages per warp (tma::stage_release_last: warps drift, no
+// CTA barrier per tile -- for kernels whose warps finish tiles at different
+// times, e.g. pow with its slow paths) or with one CTA barrier after which
+// thread 0 refills at once (the shortest refill latency, for HBM-bound
+// kernels whose bytes in flight are the limit).
+template <class Op, class T, int NIN, int TABLE, int VPT, int STAGES, int MINB = 1, bool WREL = false>
 __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__ a, const T* __restrict__ b,
                                                            T* __restrict__ out, size_t n) {
   using V = typename Vec16<T>::type;
@@ -216,24 +197,20 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
   constexpr int TILE_V = kThreads * VPT;
   constexpr uint32_t TILE_BYTES = TILE_V * 16;
   constexpr int TILE_E = TILE_V * W;
-  constexpr bool kSort = SortsByClass<Op>::value;
   constexpr int NE = VPT * W;  // elements per lane per tile
+  constexpr int NW = kThreads / 32;
   extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ uint64_t bars[STAGES];
+  __shared__ uint32_t rel[STAGES];
   __shared__ __align__(16) double stab[TableSize<TABLE>::n];
-  // + 32 junk slots at the end: unplaced (trivial) elements store there
-  // unconditionally instead of branching around the store
-  __shared__ __align__(16) T wscr[kSort ? kThreads * NE + 32 : 1];
-  __shared__ __align__(16) T wscr2[kSort && NIN == 2 ? kThreads * NE + 32 : 1];
-  __shared__ unsigned short widx[kSort ? kThreads * NE + 32 : 1];
-  __shared__ int wcur[kSort ? kThreads / 32 * 8 : 1];
   V* buf = reinterpret_cast<V*>(dsm);
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31;
   if (tid == 0) {
 #pragma unroll
     for (int s = 0; s < STAGES; s++) tma::mbar_init(&bars[s], 1);
     tma::fence_barrier_init();
   }
+  if (tid < STAGES) rel[tid] = 0;
   const double* tab = stage_table<TABLE>(stab);  // includes __syncthreads()
   if constexpr (TABLE == kNoTable) __syncthreads();
   tma::griddep_wait();  // inputs / outputs may belong to the previous grid
@@ -242,7 +219,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
   const size_t ntiles = n / TILE_E;
   const size_t G = gridDim.x;
   const size_t my = ntiles > blockIdx.x ? (ntiles - blockIdx.x + G - 1) / G : 0;
-  uint64_t pol = 0;
+  const uint64_t pol = tma::policy_evict_first();
   auto issue = [&](int s, size_t tile) {
     tma::mbar_expect_tx(&bars[s], NIN * TILE_BYTES);
     tma::bulk_g2s(buf + (size_t)(s * NIN) * TILE_V, reinterpret_cast<const V*>(a) + tile * TILE_V, TILE_BYTES,
@@ -251,10 +228,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
       tma::bulk_g2s(buf + (size_t)(s * NIN + 1) * TILE_V, reinterpret_cast<const V*>(b) + tile * TILE_V,
                     TILE_BYTES, &bars[s], pol);
   };
-  if (tid == 0) {
-    pol = tma::policy_evict_first();
+  if (tid == 0)
     for (int s = 0; s < STAGES && (size_t)s < my; s++) issue(s, blockIdx.x + (size_t)s * G);
-  }
   for (size_t j = 0; j < my; j++) {
     const int s = (int)(j % STAGES);
     tma::mbar_wait(&bars[s], (uint32_t)((j / STAGES) & 1));
@@ -264,201 +239,20 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
       va[v] = buf[(size_t)(s * NIN) * TILE_V + v * kThreads + tid];
       if constexpr (NIN == 2) vb[v] = buf[(size_t)(s * NIN + 1) * TILE_V + v * kThreads + tid];
     }
-    __syncthreads();  // stage s fully consumed -> refill it
-    if (tid == 0 && j + STAGES < my) {
-      tma::fence_proxy_async_smem();
-      issue(s, blockIdx.x + (j + STAGES) * G);
+    if constexpr (WREL) {  // per-warp stage release (vem_stream.cuh)
+      __syncwarp();
+      if (lane == 0 && tma::stage_release_last(&rel[s], NW) && j + STAGES < my) {
+        tma::fence_proxy_async_smem();
+        issue(s, blockIdx.x + (j + STAGES) * G);
+      }
+    } else {  // stage s fully consumed by the CTA -> refill it
+      __syncthreads();
+      if (tid == 0 && j + STAGES < my) {
+        tma::fence_proxy_async_smem();
+        issue(s, blockIdx.x + (j + STAGES) * G);
+      }
     }
     V* ov = reinterpret_cast<V*>(out) + (blockIdx.x + j * G) * TILE_V;
-    bool done = false;
-    if constexpr (kSort) {
-      constexpr int K = SortsByClass<Op>::classes;
-      const int lane = tid & 31;
-      const unsigned lt_mask = (1u << lane) - 1u;
-      T xe[NE], ye[NE];
-      int cl[NE];
-#pragma unroll
-      for (int v = 0; v < VPT; v++)
-#pragma unroll
-        for (int k = 0; k < W; k++) {
-          xe[v * W + k] = vget(va[v], k);
-          if constexpr (NIN == 2) ye[v * W + k] = vget(vb[v], k);
-        }
-      bool same = true;
-      bool uniform = false;
-      int c_l0 = -1;
-      if constexpr (HasCw1<Op>::value) {
-        // cheap first test: every element of the warp in the CW1 range
-        bool small = true;
-#pragma unroll
-        for (int e = 0; e < NE; e++) small = small && Op::is_cw1(xe[e]);
-        if (__all_sync(0xffffffffu, small)) {
-          uniform = true;
-          c_l0 = 0;
-        }
-      }
-      if (!uniform) {
-#pragma unroll
-        for (int e = 0; e < NE; e++) {
-          if constexpr (NIN == 2) cl[e] = Op::cls(xe[e], ye[e]);
-          else cl[e] = Op::cls(xe[e]);
-          same = same && (cl[e] == cl[0]);
-        }
-        c_l0 = __shfl_sync(0xffffffffu, cl[0], 0);
-        uniform = __all_sync(0xffffffffu, same && cl[0] == c_l0);
-      }
-      bool triv[NE];
-      T tres[NE];
-#pragma unroll
-      for (int e = 0; e < NE; e++) {
-        if constexpr (HasTrivial<Op>::value) {
-          triv[e] = Op::is_trivial(xe[e]);
-          tres[e] = Op::trivial(xe[e]);
-        } else {
-          triv[e] = false;
-          tres[e] = xe[e];
-        }
-      }
-      int nplaced = 32 * NE;
-      int nph = 0;  // placed class-2 (Payne-Hanek) elements: rows [0, nph) of the block
-      auto regroup = [&]() {
-        // counting sort of the warp's 32*NE elements by class, heaviest
-        // class first: ballots per (row, class), prefix popcounts
-        T* sx = wscr + (tid >> 5) * (32 * NE);
-        T* sy = wscr2 + (tid >> 5) * (32 * NE);
-        unsigned short* si = widx + (tid >> 5) * (32 * NE);
-        if constexpr (K == 3) {
-          // trig: two ballots per row, explicit three-way positions;
-          // trivial elements (HasTrivial) are not placed: their results
-          // stay in registers and the rows past the last placed one are
-          // skipped
-          unsigned m2[NE], m1[NE], m0[NE];
-          int n2 = 0, n1 = 0;
-#pragma unroll
-          for (int e = 0; e < NE; e++) {
-            const bool pl = !triv[e];
-            m2[e] = __ballot_sync(0xffffffffu, pl && cl[e] == 2);
-            m1[e] = __ballot_sync(0xffffffffu, pl && cl[e] == 1);
-            m0[e] = HasTrivial<Op>::value ? __ballot_sync(0xffffffffu, pl && cl[e] == 0) : ~(m2[e] | m1[e]);
-            n2 += __popc(m2[e]);
-            n1 += __popc(m1[e]);
-          }
-          int a2 = 0, a1 = n2, a0 = n2 + n1;  // heaviest class first
-          // junk slot of this lane (past every warp's block), relative to sx
-          const int junk = kThreads * NE + lane - (tid >> 5) * (32 * NE);
-#pragma unroll
-          for (int e = 0; e < NE; e++) {
-            const unsigned mk = cl[e] == 2 ? m2[e] : (cl[e] == 1 ? m1[e] : m0[e]);
-            const int base = cl[e] == 2 ? a2 : (cl[e] == 1 ? a1 : a0);
-            const int pos = triv[e] ? junk : base + __popc(mk & lt_mask);
-            a2 += __popc(m2[e]);
-            a1 += __popc(m1[e]);
-            a0 += __popc(m0[e]);
-            sx[pos] = xe[e];
-            if constexpr (NIN == 2) sy[pos] = ye[e];
-            si[pos] = (unsigned short)(e * 32 + lane);
-          }
-          nplaced = a0;
-          nph = n2;
-        } else {
-          // K classes: per-warp class cursors in shared memory; lanes of one
-          // class in a row are ranked by match_any, the group's lowest lane
-          // advances the cursor
-          int* cur = wcur + (tid >> 5) * 8;
-          if (lane < K) cur[lane] = 0;
-          __syncwarp();
-          unsigned mm[NE];
-#pragma unroll
-          for (int e = 0; e < NE; e++) {
-            mm[e] = __match_any_sync(0xffffffffu, cl[e]);
-            if ((mm[e] & lt_mask) == 0u) atomicAdd(&cur[cl[e]], __popc(mm[e]));
-          }
-          __syncwarp();
-          if (lane == 0) {  // exclusive prefix, heaviest class first
-            int acc = 0;
-            for (int c = K - 1; c >= 0; c--) {
-              const int n = cur[c];
-              cur[c] = acc;
-              acc += n;
-            }
-          }
-          __syncwarp();
-#pragma unroll
-          for (int e = 0; e < NE; e++) {
-            const int pos = cur[cl[e]] + __popc(mm[e] & lt_mask);
-            __syncwarp();
-            if ((mm[e] & lt_mask) == 0u) cur[cl[e]] += __popc(mm[e]);
-            __syncwarp();
-            sx[pos] = xe[e];
-            if constexpr (NIN == 2) sy[pos] = ye[e];
-            si[pos] = (unsigned short)(e * 32 + lane);
-          }
-        }
-        __syncwarp();
-        T xs[NE], ys[NE];
-        int ids[NE];
-#pragma unroll
-        for (int r = 0; r < NE; r++) {
-          // past the last placed element a lane repeats its row's first
-          // entry (same class: no divergence); its result is not written
-          const int i = r * 32 + lane < nplaced ? r * 32 + lane : r * 32;
-          xs[r] = sx[i];
-          if constexpr (NIN == 2) ys[r] = sy[i];
-          ids[r] = r * 32 + lane < nplaced ? si[i] : -1;
-        }
-        __syncwarp();
-        int r0 = 0;
-        if constexpr (PhRows<Op>::value > 1 && PhRows<Op>::value <= NE) {
-          constexpr int P = PhRows<Op>::value;
-          if (nph >= P * 32) {  // warp-uniform: rows 0..P-1 all Payne-Hanek
-            T yp[P];
-#pragma unroll
-            for (int r = 0; r < P; r++) yp[r] = op.ph(xs[r], tab);
-#pragma unroll
-            for (int r = 0; r < P; r++) sx[ids[r]] = yp[r];
-            r0 = P;
-          }
-        }
-#pragma unroll
-        for (int r = 0; r < NE; r++) {
-          if (r >= r0 && r * 32 < nplaced) {  // warp-uniform
-            T yv;
-            if constexpr (NIN == 2) yv = op(xs[r], ys[r], tab);
-            else yv = op(xs[r], tab);
-            if (ids[r] >= 0) sx[ids[r]] = yv;
-          }
-        }
-        __syncwarp();
-#pragma unroll
-        for (int v = 0; v < VPT; v++) {
-          V o;
-#pragma unroll
-          for (int k = 0; k < W; k++) vget(o, k) = triv[v * W + k] ? tres[v * W + k] : sx[(v * W + k) * 32 + lane];
-          __stcs(ov + v * kThreads + tid, o);
-        }
-        __syncwarp();
-      };
-      if constexpr (HasCw1<Op>::value) {
-        if (uniform && c_l0 == 0) {
-          // every element of the warp takes Cody-Waite level 1: branch-free
-          // bodies, interleaved across the thread's elements
-#pragma unroll
-          for (int v = 0; v < VPT; v++) {
-            V o;
-#pragma unroll
-            for (int k = 0; k < W; k++) vget(o, k) = op.cw1(xe[v * W + k], tab);
-            __stcs(ov + v * kThreads + tid, o);
-          }
-          done = true;
-        } else if (!uniform) {
-          regroup();
-          done = true;
-        }
-      } else if (!uniform) {
-        regroup();
-        done = true;
-      }
-    }
     if constexpr (HasFast<Op>::value) {
       T res[NE];
       int code[NE];
@@ -489,9 +283,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
         for (int k = 0; k < W; k++) vget(o, k) = res[v * W + k];
         __stcs(ov + v * kThreads + tid, o);
       }
-      done = true;
-    }
-    if (!done) {
+    } else {
 #pragma unroll
       for (int v = 0; v < VPT; v++) {
         V o;
@@ -515,27 +307,31 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
 // ------------------------------------------------ trig selector kernel
 // sin / cos / tan f64 (u10, u35) with the reference's per-lane reduction
 // selector (reduction.hpp:189-206: Cody-Waite 1 / 2 below 1e14, Payne-Hanek
-// above).  Same TMA pipeline as k_stream; per tile, every warp (32 x NE
-// elements, NE = 2 VPT):
+// above).  TMA pipeline as k_stream, but stages are released per warp
+// (tma::stage_release_last): no CTA barrier per tile, warps drift by up to
+// STAGES - 1 tiles, so a warp with more Payne-Hanek work does not hold the
+// others.  Per tile, every warp (32 x NE elements, NE = 2 VPT <= 8):
 //   0. all elements |x| < 15      -> branch-free Cody-Waite-1 bodies from
 //      registers (config 1); all elements Payne-Hanek -> branch-free Op::ph
-//      bodies, two interleaved (config 3-like inputs through the selector);
-//   1. otherwise one class per element, 3 classes: trivial (|x| < 2^-27,
-//      zeros, subnormals, Inf/NaN: closed-form result, written straight to
-//      the warp's result block), Cody-Waite (levels 1 and 2), Payne-Hanek;
-//   2. one warp scan of the packed per-lane counts (nph << 16 | ncw) places
-//      every Payne-Hanek argument in [0, nph) and every Cody-Waite argument in
-//      [nph, nph + ncw) of the warp's sorted block (shared memory), with its
-//      tile slot alongside;
-//   3. full Payne-Hanek rows of 32 run Op::ph two rows at a time
-//      (interleaved, uniform, no divergence); the boundary row and the
-//      Cody-Waite rows run the per-lane selector op();  results are scattered
-//      to their slots in the result block;
-//   4. each lane gathers its NE results (conflict-free) for the coalesced
+//      bodies (config 3-like inputs through the selector);
+//   1. otherwise a class per element from its high word: Payne-Hanek (high
+//      word > that of 1e14, incl. Inf/NaN, for which Op::ph returns the
+//      canonical NaN like every other path), Cody-Waite (2^-27 <= |x| and
+//      high word <= that of 1e14; the per-lane selector decides at the
+//      boundary word), trivial (|x| < 2^-27: sin/tan x, cos 1.0, Op::tiny);
+//   2. the warp's arguments go to a shared-memory block in slot order (slot
+//      = e * 32 + lane; conflict-free), trivial ones already replaced by their
+//      result, and one warp scan of the packed per-lane counts
+//      (nph << 16 | ncw) builds the list of non-trivial slots (8 bits each),
+//      Payne-Hanek slots first;
+//   3. full Payne-Hanek rows of the list run Op::ph (two rows interleaved, no
+//      divergence); the boundary row and the Cody-Waite rows run the
+//      per-lane selector op(); each result overwrites its argument's slot;
+//   4. the block is stored in slot order: conflict-free LDS, coalesced
 //      16-byte st.global.cs.
-// Registers hold one or two rows of work at a time (the arguments live in
-// shared memory between the steps), which keeps the kernel at <= 80
-// registers: 3 CTAs (24 warps) per SM.
+// 2.25 KB of scratch per warp: with 2 x 16 KB stages the CTA needs 50 KB, so 3
+// CTAs (24 warps, <= 80 registers) leave ~70 KB of L1 for the 32 KB integer
+// Payne-Hanek table (read through L1).
 template <class Op, int TABLE, int VPT, int STAGES, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) k_trig(const double* __restrict__ a, double* __restrict__ out,
                                                          size_t n) {
@@ -547,22 +343,23 @@ __global__ void __launch_bounds__(kThreads, MINB) k_trig(const double* __restric
   constexpr int NE = VPT * W;  // elements per lane per tile
   constexpr int WE = 32 * NE;  // elements per warp per tile
   constexpr int NW = kThreads / 32;
+  static_assert(WE <= 256, "positions are kept in 8 bits");
   extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ uint64_t bars[STAGES];
+  __shared__ uint32_t rel[STAGES];
   __shared__ __align__(16) double stab[TableSize<TABLE>::n];
-  __shared__ __align__(16) double s_x[NW][WE + 32];  // sorted arguments (+ a junk slot per lane)
-  __shared__ __align__(16) double s_y[NW][WE];       // results in slot order (slot = e * 32 + lane)
-  __shared__ unsigned short s_i[NW][WE + 32];        // slot of each sorted argument
+  __shared__ __align__(16) double s_x[NW][WE];  // per warp: arguments in slot order, then results in place
+  __shared__ unsigned char s_i[NW][WE];         // per warp: non-trivial slots, Payne-Hanek first
   V* buf = reinterpret_cast<V*>(dsm);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double* sx = s_x[warp];
-  double* sy = s_y[warp];
-  unsigned short* si = s_i[warp];
+  unsigned char* si = s_i[warp];
   if (tid == 0) {
 #pragma unroll
     for (int s = 0; s < STAGES; s++) tma::mbar_init(&bars[s], 1);
     tma::fence_barrier_init();
   }
+  if (tid < STAGES) rel[tid] = 0;
   const double* tab = stage_table<TABLE>(stab);  // includes __syncthreads()
   tma::griddep_wait();  // inputs / outputs may belong to the previous grid
   tma::griddep_launch_dependents();
@@ -570,16 +367,14 @@ __global__ void __launch_bounds__(kThreads, MINB) k_trig(const double* __restric
   const size_t ntiles = n / TILE_E;
   const size_t G = gridDim.x;
   const size_t my = ntiles > blockIdx.x ? (ntiles - blockIdx.x + G - 1) / G : 0;
-  uint64_t pol = 0;
+  const uint64_t pol = tma::policy_evict_first();
   auto issue = [&](int s, size_t tile) {
     tma::mbar_expect_tx(&bars[s], TILE_BYTES);
     tma::bulk_g2s(buf + (size_t)s * TILE_V, reinterpret_cast<const V*>(a) + tile * TILE_V, TILE_BYTES, &bars[s],
                   pol);
   };
-  if (tid == 0) {
-    pol = tma::policy_evict_first();
+  if (tid == 0)
     for (int s = 0; s < STAGES && (size_t)s < my; s++) issue(s, blockIdx.x + (size_t)s * G);
-  }
   for (size_t j = 0; j < my; j++) {
     const int s = (int)(j % STAGES);
     tma::mbar_wait(&bars[s], (uint32_t)((j / STAGES) & 1));
@@ -590,8 +385,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_trig(const double* __restric
       xe[v * W] = t.x;
       xe[v * W + 1] = t.y;
     }
-    __syncthreads();  // stage s fully consumed -> refill it
-    if (tid == 0 && j + STAGES < my) {
+    __syncwarp();  // the warp's reads of stage s are done -> release it
+    if (lane == 0 && tma::stage_release_last(&rel[s], NW) && j + STAGES < my) {
       tma::fence_proxy_async_smem();
       issue(s, blockIdx.x + (j + STAGES) * G);
     }
@@ -606,23 +401,26 @@ __global__ void __launch_bounds__(kThreads, MINB) k_trig(const double* __restric
                                                                                    op.cw1(xe[v * W + 1], tab)));
       continue;
     }
-    // ---- 1. classes: bit e of mph / mcw
+    // ---- 1. classes from the high word (bit e of mph / mcw)
     uint32_t mph = 0, mcw = 0;
 #pragma unroll
     for (int e = 0; e < NE; e++) {
-      const int c = Op::cls3(xe[e]);
-      mph |= (uint32_t)(c == 2) << e;
-      mcw |= (uint32_t)(c == 1) << e;
+      const uint32_t h = (uint32_t)__double2hiint(xe[e]) & 0x7fffffffu;
+      mph |= (uint32_t)(h > 0x42D6BCC4u) << e;                        // |x| > 1e14 or non-finite
+      mcw |= (uint32_t)(h - 0x3E400000u <= 0x42D6BCC4u - 0x3E400000u) << e;  // 2^-27 <= |x| <~ 1e14
     }
     if (__all_sync(0xffffffffu, mph == (1u << NE) - 1u)) {
-#pragma unroll 1
+#pragma unroll
       for (int v = 0; v < VPT; v++) {
         const double x0 = xe[v * W], x1 = xe[v * W + 1];
         __stcs(ov + v * kThreads + tid, make_double2(op.ph(x0, tab), op.ph(x1, tab)));
       }
       continue;
     }
-    // ---- 2. placement: one scan of the packed per-lane counts
+    // ---- 2. placement: the arguments in slot order (slot = e * 32 + lane,
+    // trivial ones already replaced by their result), plus a list of the
+    // non-trivial slots, Payne-Hanek first, from one scan of the packed
+    // per-lane counts
     const int cnt = (__popc(mph) << 16) | __popc(mcw);
     int inc = cnt;
 #pragma unroll
@@ -632,46 +430,47 @@ __global__ void __launch_bounds__(kThreads, MINB) k_trig(const double* __restric
     }
     const int tot = __shfl_sync(0xffffffffu, inc, 31);
     const int nph = tot >> 16, nall = nph + (tot & 0xffff);
-    int pph = (inc - cnt) >> 16;
-    int pcw = nph + ((inc - cnt) & 0xffff);
+    const int exc = inc - cnt;
+    int pph = exc >> 16;
+    int pcw = nph + (exc & 0xffff);
 #pragma unroll
     for (int e = 0; e < NE; e++) {
       const bool isph = (mph >> e) & 1u, iscw = (mcw >> e) & 1u;
       const int slot = e * 32 + lane;
-      const int pos = isph ? pph : (iscw ? pcw : WE + lane);
-      sx[pos] = xe[e];
-      si[pos] = (unsigned short)slot;
+      sx[slot] = (isph || iscw) ? xe[e] : Op::tiny(xe[e]);
+      if (isph || iscw) si[isph ? pph : pcw] = (unsigned char)slot;
       pph += isph;
       pcw += iscw;
-      if (!(isph || iscw)) sy[slot] = Op::trivial(xe[e]);
     }
     __syncwarp();
-    // ---- 3. rows
+    // ---- 3. rows over the slot list, results in place
     int r = 0;
 #pragma unroll 1
     for (; (r + 2) * 32 <= nph; r += 2) {
-      const int ia = r * 32 + lane, ib = ia + 32;
-      const double xa = sx[ia], xb = sx[ib];
-      const int sa = si[ia], sb = si[ib];
+      const int sa = si[r * 32 + lane], sb = si[r * 32 + 32 + lane];
+      const double xa = sx[sa], xb = sx[sb];
       const double ya = op.ph(xa, tab), yb = op.ph(xb, tab);
-      sy[sa] = ya;
-      sy[sb] = yb;
+      sx[sa] = ya;
+      sx[sb] = yb;
     }
     if ((r + 1) * 32 <= nph) {
-      const int ia = r * 32 + lane;
-      sy[si[ia]] = op.ph(sx[ia], tab);
+      const int sa = si[r * 32 + lane];
+      sx[sa] = op.ph(sx[sa], tab);
       r++;
     }
 #pragma unroll 1
     for (; r * 32 < nall; r++) {
       const int i = r * 32 + lane;
-      if (i < nall) sy[si[i]] = op(sx[i], tab);
+      if (i < nall) {
+        const int sa = si[i];
+        sx[sa] = op(sx[sa], tab);
+      }
     }
     __syncwarp();
-    // ---- 4. gather + coalesced store
+    // ---- 4. coalesced store straight from the slot-order block
 #pragma unroll
     for (int v = 0; v < VPT; v++)
-      __stcs(ov + v * kThreads + tid, make_double2(sy[(v * W) * 32 + lane], sy[(v * W + 1) * 32 + lane]));
+      __stcs(ov + v * kThreads + tid, make_double2(sx[(v * W) * 32 + lane], sx[(v * W + 1) * 32 + lane]));
     __syncwarp();  // the block is rewritten by the next tile
   }
   // remainder (< one tile)
@@ -1236,11 +1035,6 @@ __device__ __forceinline__ bool trig_is_trivial(double x) {
   const uint32_t h = (uint32_t)__double2hiint(x) & 0x7fffffffu;
   return h < 0x3E400000u || h >= 0x7ff00000u;
 }
-// 0 = trivial, 1 = Cody-Waite (level 1 or 2, |x| <= 1e14), 2 = Payne-Hanek
-__device__ __forceinline__ int trig_class3(double x) {
-  const uint64_t ab = bits_d(x) & 0x7fffffffffffffffull;
-  return (ab < 0x3E40000000000000ull || ab >= 0x7ff0000000000000ull) ? 0 : (ab <= 0x42d6bcc41e900000ull ? 1 : 2);
-}
 #define VEM_TRIG_OP(NAME, FN, ...)                                                       \
   struct NAME {                                                                          \
     __device__ __forceinline__ double operator()(double x, const double* tab) const {   \
@@ -1252,18 +1046,11 @@ __device__ __forceinline__ int trig_class3(double x) {
     __device__ __forceinline__ double ph(double x, const double* tab) const {           \
       return FN<kPh>(x, reinterpret_cast<const double*>(gPhDI) __VA_ARGS__);              \
     }                                                                                    \
-    __device__ __forceinline__ static int cls(double x) { return trig_class(x); }      \
-    __device__ __forceinline__ static int cls3(double x) { return trig_class3(x); }    \
     __device__ __forceinline__ static bool is_cw1(double x) { return trig_is_cw1(x); } \
     __device__ __forceinline__ static bool is_trivial(double x) { return trig_is_trivial(x); } \
     __device__ static double trivial(double x);                                          \
-  };                                                                                     \
-  template <> struct SortsByClass<NAME> {                                                \
-    static constexpr bool value = true;                                                  \
-    static constexpr int classes = 3;                                                    \
-  };                                                                                     \
-  template <> struct HasCw1<NAME> { static constexpr bool value = true; };              \
-  template <> struct PhRows<NAME> { static constexpr int value = VEM_PH_ROWS; };
+    __device__ static double tiny(double x);                                             \
+  };
 // selector variants: PH table from global memory (L1), coefficients staged
 VEM_TRIG_OP(OpSinD, sin_d_u10, , tab)
 VEM_TRIG_OP(OpCosD, cos_d_u10, , tab)
@@ -1274,10 +1061,10 @@ VEM_TRIG_OP(OpTanDU35, tan_d_u35)
 #undef VEM_TRIG_OP
 // TINY: the result for a finite trivial x
 #define VEM_TRIG_TINY(NAME, TINY)                                                         \
-  template <> struct HasTrivial<NAME> { static constexpr bool value = true; };           \
   __device__ __forceinline__ double NAME::trivial(double x) {                              \
     return ((uint32_t)__double2hiint(x) & 0x7fffffffu) >= 0x7ff00000u ? from_bits_d(kCanonNanD) : (TINY); \
-  }
+  }                                                                                         \
+  __device__ __forceinline__ double NAME::tiny(double x) { return (TINY); }
 VEM_TRIG_TINY(OpSinD, x)
 VEM_TRIG_TINY(OpCosD, 1.0)
 VEM_TRIG_TINY(OpTanD, x)
@@ -1361,11 +1148,6 @@ struct OpFmodD {
     (void)tab;
     return fmod_d(x, y);
   }
-  __device__ __forceinline__ static int cls(double x, double y) { return fmod_class(x, y); }
-};
-template <> struct SortsByClass<OpFmodD> {
-  static constexpr bool value = true;
-  static constexpr int classes = kFmodClasses;
 };
 VEM_SPLIT_BINARY_OP(OpPowF, float, pow_f_u10(x, y, tab), (pow_fast_f<VEM_LOG1P_F_N>(x, y, cLog1pF, tab, code)),
                     full())
@@ -1376,11 +1158,6 @@ struct OpFmodF {
     (void)tab;
     return fmod_f(x, y);
   }
-  __device__ __forceinline__ static int cls(float x, float y) { return fmod_class_f(x, y); }
-};
-template <> struct SortsByClass<OpFmodF> {
-  static constexpr bool value = true;
-  static constexpr int classes = kFmodClasses;
 };
 VEM_BINARY_OP(OpAtan2D, double, ((void)tab, atan2_d_u10(x, y)))
 VEM_BINARY_OP(OpAtan2DU35, double, ((void)tab, atan2_d_u35(x, y)))
@@ -1513,14 +1290,14 @@ static int launch_binary(const T* x, const T* y2, T* out, size_t n, vem_stream_t
   return (int)cudaGetLastError();
 }
 
-template <class Op, class T, int NIN, int TABLE, int VPT, int STAGES, int MINB = 1>
+template <class Op, class T, int NIN, int TABLE, int VPT, int STAGES, int MINB = 1, bool WREL = false>
 static int launch_stream(const T* a, const T* b, T* out, size_t n, vem_stream_t s) {
   if (n == 0) return 0;
   if (!(aligned16(a) && aligned16(out) && (NIN == 1 || aligned16(b)))) {
     if constexpr (NIN == 2) return launch_binary<Op, T, TABLE, 1>(a, b, out, n, s);
     else return launch_unary<Op, T, TABLE, 1>(a, out, n, s);
   }
-  auto k = k_stream<Op, T, NIN, TABLE, VPT, STAGES, MINB>;
+  auto k = k_stream<Op, T, NIN, TABLE, VPT, STAGES, MINB, WREL>;
   constexpr int smem = STAGES * NIN * kThreads * VPT * 16;
   static DevCache occ_cache;
   const int dev = current_device();
@@ -1712,9 +1489,13 @@ using namespace vem;
 #ifdef VEM_TUNE
 static int g_tune = -1;
 extern "C" void vem_tune_set(int v) { g_tune = v; }
-template <class Op, class T, int NIN, int TAB, int VPT, int ST, int MINB = 1>
+template <class Op, class T, int NIN, int TAB, int VPT, int ST, int MINB = 1, bool WREL = false>
 static int launch_tuned(const T* a, const T* b, T* o, size_t n, vem_stream_t s) {
   switch (g_tune) {
+    case 11: return launch_stream<Op, T, NIN, TAB, VPT, ST, MINB, !WREL>(a, b, o, n, s);
+    case 12: return launch_stream<Op, T, NIN, TAB, VPT, ST + 1, MINB, WREL>(a, b, o, n, s);
+    case 13: return launch_stream<Op, T, NIN, TAB, VPT, ST + 1, MINB, !WREL>(a, b, o, n, s);
+    case 14: return launch_stream<Op, T, NIN, TAB, VPT, ST + 2, MINB, WREL>(a, b, o, n, s);
     case 0: return launch_stream<Op, T, NIN, TAB, 1, 2>(a, b, o, n, s);
     case 1: return launch_stream<Op, T, NIN, TAB, 1, 4>(a, b, o, n, s);
     case 2: return launch_stream<Op, T, NIN, TAB, 2, 2>(a, b, o, n, s);
@@ -1726,7 +1507,7 @@ static int launch_tuned(const T* a, const T* b, T* o, size_t n, vem_stream_t s) 
     case 8: return launch_stream<Op, T, NIN, TAB, VPT, ST, 4>(a, b, o, n, s);
     case 9: return launch_stream<Op, T, NIN, TAB, 4, 2, 2>(a, b, o, n, s);
     case 10: return launch_stream<Op, T, NIN, TAB, 4, 2, 3>(a, b, o, n, s);
-    default: return launch_stream<Op, T, NIN, TAB, VPT, ST, MINB>(a, b, o, n, s);
+    default: return launch_stream<Op, T, NIN, TAB, VPT, ST, MINB, WREL>(a, b, o, n, s);
   }
 }
 // fmod without regrouping or queue (every lane loops to its warp's largest
@@ -1752,7 +1533,6 @@ static int launch_fmod_tuned(const T* a, const T* b, T* o, size_t n, vem_stream_
     case 4: return launch_fmod_w<T, 2, 2, 3>(a, b, o, n, s);
     case 5: return launch_fmod_q<T, 2, 2, 1, 2>(a, b, o, n, s);
     case 6: return launch_fmod_q<T, 4, 2, 1, 1>(a, b, o, n, s);
-    case 7: return launch_stream<OpF, T, 2, kNoTable, 2, 2>(a, b, o, n, s);
     case 9: return launch_stream<OpFmodPlain<T>, T, 2, kNoTable, 2, 2>(a, b, o, n, s);
     case 10: return launch_stream<OpFmodPlain<T>, T, 2, kNoTable, 1, 2>(a, b, o, n, s);
     case 11: return launch_fmod_q<T, 2, 2, 1, 1, 2>(a, b, o, n, s);
@@ -1793,8 +1573,8 @@ int vem_exp_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return
 int vem_exp_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpExpDU35, double, 1, kNoTable, 4, 2>(x, nullptr, y, n, s); }
 int vem_log_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpLogD, double, 1, kTableLog, 4, 2, 4>(x, nullptr, y, n, s); }
 int vem_log_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpLogDU35, double, 1, kTableLog, 2, 2, 4>(x, nullptr, y, n, s); }
-int vem_pow_d_u10(const double* x, const double* y2, double* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpPowD, double, 2, kTableLog, 2, 2, 3>(x, y2, o, n, s); }
-int vem_pow_d_u35(const double* x, const double* y2, double* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpPowDU35, double, 2, kTableLog, 2, 2, 3>(x, y2, o, n, s); }
+int vem_pow_d_u10(const double* x, const double* y2, double* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpPowD, double, 2, kTableLog, 2, 2, 3, true>(x, y2, o, n, s); }
+int vem_pow_d_u35(const double* x, const double* y2, double* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpPowDU35, double, 2, kTableLog, 2, 2, 3, true>(x, y2, o, n, s); }
 int vem_fmod_d(const double* x, const double* y2, double* o, size_t n, vem_stream_t s) {
 #ifdef VEM_TUNE
   return VEM_FMOD<double>(x, y2, o, n, s);

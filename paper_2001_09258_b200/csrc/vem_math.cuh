@@ -865,23 +865,6 @@ __device__ __forceinline__ double fmod_core(double x, double y) {
   return fmod_finish(st);
 }
 __device__ __forceinline__ double fmod_d(double x, double y) { return fmod_core(x, y); }
-// Work class of a pair for the warp regrouping of k_stream (tuning build
-// variant only since the tile work queue replaced it): the number of 50-bit
-// steps from the biased exponents (subnormals counted as exponent 0; only a
-// scheduling hint, results do not depend on it), bucketed into 6 ranges.
-constexpr int kFmodClasses = 6;
-__device__ __forceinline__ int fmod_class(double x, double y) {
-  const int ex = (int)(((uint32_t)__double2hiint(x) >> 20) & 0x7ffu);
-  const int ey = (int)(((uint32_t)__double2hiint(y) >> 20) & 0x7ffu);
-  const int n = (ex - ey - 1) / 50;  // full steps after the first (<= 0: none)
-  return n <= 0 ? 0 : (n <= 3 ? 1 : (n <= 8 ? 2 : (n <= 15 ? 3 : (n <= 24 ? 4 : 5))));
-}
-__device__ __forceinline__ int fmod_class_f(float x, float y) {
-  const int ex = (int)((bits_f(x) >> 23) & 0xffu);
-  const int ey = (int)((bits_f(y) >> 23) & 0xffu);
-  const int n = (ex - ey - 1) / 50;
-  return n <= 0 ? 0 : (n >= kFmodClasses - 1 ? kFmodClasses - 1 : n);
-}
 
 // ===================================== f32 functions (binary64 internals)
 struct redf { double r; int q; };

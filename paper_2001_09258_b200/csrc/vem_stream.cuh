@@ -74,6 +74,20 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   return p;
 }
 
+// Per-warp release of a TMA stage (no CTA-wide barrier): after reading its
+// part of stage s, every warp's lane 0 adds 1 to the stage's counter
+// (acq_rel: the warp's reads, ordered before it by __syncwarp, happen before
+// the increment); the warp whose increment completes a set of `nw` learns it
+// is last and refills the stage (after fence.proxy.async).  Fast warps run
+// ahead of slow ones by up to STAGES - 1 tiles instead of waiting at a
+// barrier every tile.  The counter only grows: arrival k of a tile is the
+// last one when k % nw == nw - 1.
+__device__ __forceinline__ bool stage_release_last(uint32_t* ctr, uint32_t nw) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(smem_addr(ctr)) : "memory");
+  return (old % nw) == nw - 1;
+}
+
 // Programmatic dependent launch (the streaming kernels are launched with
 // cudaLaunchAttributeProgrammaticStreamSerialization): `wait` blocks until
 // the previous grid in the stream has completed and its memory operations

@@ -6,7 +6,9 @@ paper_2001_09258_b200/_tune/libvem_tune.so, then times every entry point
 (filtered by argv[2]) at 2^argv[1] elements for each (VPT, STAGES) variant:
  0:(1,2) 1:(1,4) 2:(2,2) 3:(2,3) 4:(2,4) 5:(4,2), -1 = the shipped choice, and
  6/7/8 = the shipped shape with __launch_bounds__ min-blocks 2/3/4, 9/10 = (4,2) with
- min-blocks 2/3.
+ min-blocks 2/3, 11 = the shipped shape with the other stage-release scheme
+ (per-warp vs CTA barrier), 12/13 = one more stage (same / other release),
+ 14 = two more stages.  VEM_TUNE_VARIANTS=-1,11,... picks the variants.
 fmod: -1 shipped step-queue kernel; 0-4 warp-private queue (VPT,STAGES[,MINB]) (2,2) (4,2) (2,3) (4,2,2) (2,2,3);
 5-6 CTA queue (VPT,STAGES,ROWS) (2,2,2) (4,2,1); 7 = the streaming kernel with
 warp step-class regrouping (2,2); 8 = the work-ring kernel; 9/10 = the
@@ -34,6 +36,8 @@ CFG = {"sin": 1, "cos": 1, "tan": 3, "atan": 5, "exp": 2, "log": 2, "pow": 2, "f
 def build_tune():
     out = os.path.join(ROOT, "paper_2001_09258_b200", "_tune")
     os.makedirs(out, exist_ok=True)
+    if os.environ.get("VEM_TUNE_PREBUILT") and os.path.exists(os.path.join(out, "libvem_tune.so")):
+        return os.path.join(out, "libvem_tune.so")
     objs = []
     for src in build.SOURCES:
         o = os.path.join(out, src.replace(".cu", ".o"))
@@ -58,10 +62,13 @@ def main():
             continue
         fn, p = name.split("_")[0], name.split("_")[1]
         cfg = 3 if name.endswith("_ph") else CFG[fn]
+        if p == "f" and cfg in (1, 5):  # binary64-only configs
+            cfg = 3 if fn in ("sin", "cos", "tan") else 6
         if os.environ.get("VEM_TUNE_CFG"):
             cfg = int(os.environ["VEM_TUNE_CFG"])
-        arrs = I.config_inputs(cfg, fn, p, n)
-        ts = [torch.from_numpy(a).cuda() for a in arrs]
+        from paper_2001_09258_b200 import _aux
+        ts = [_aux.fill(r, torch.empty(n, dtype=torch.float32 if r["f32"] else torch.float64, device="cuda"))
+              for r in I.config_recipes(cfg, fn, p)]
         out = torch.empty_like(ts[0])
         f = getattr(L, "vem_" + name)
         if len(ts) == 2:
@@ -71,7 +78,10 @@ def main():
             f.argtypes = [ctypes.c_void_p] * 2 + [ctypes.c_size_t, ctypes.c_void_p]
             call = lambda: f(ts[0].data_ptr(), out.data_ptr(), n, stream)  # noqa: E731
         res = {}
-        for v in ((0, 14, 17, 19, 20, 21, 22) if name.startswith("fmod") else (-1, 0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10)):
+        vs = os.environ.get("VEM_TUNE_VARIANTS")
+        vs = [int(v) for v in vs.split(",")] if vs else (
+            (0, 14, 17, 19, 20, 21, 22) if name.startswith("fmod") else (-1, 0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10))
+        for v in vs:
             L.vem_tune_set(v)
             for _ in range(3):
                 call()
