@@ -309,7 +309,7 @@ static red_t ph(double x_in) {
  * and the sign of x folded into the constants.  r keeps >= 70 correct bits
  * (tests check it against mpmath, worst cases included).  |x| < 1/2: r = x,
  * q = 0; non-finite x: NaN. */
-static red_t ph_int(double x) {
+static red_t ph_int192(double x) {
   const uint64_t b = bits_d(x), ab = b & 0x7fffffffffffffffull;
   red_t o;
   if (ab >= 0x7ff0000000000000ull) {
@@ -359,6 +359,53 @@ static red_t ph_int(double x) {
   ee = fma(fh, c1, ee);
   ee = fma(fl, c0, ee);
   if (b >> 63) q = -q;
+  o.hi = p;
+  o.lo = ee;
+  o.q = q & 3;
+  return o;
+}
+
+/* Two-level integer Payne-Hanek (the functions' binary64 reduction).
+ * Fast level: the top 128 bits of the 192-bit window, P = M * W128 mod 2^128
+ * (quadrant units: LSB 2^-126); the fraction's 126 bits are cut into three
+ * exactly convertible chunks c0 (53 bits, centred in integer arithmetic),
+ * c1 (53), c2 (20) and summed with one Fast2Sum (|c0| is 0 or >= 1 > c1 in
+ * units of 2^-53).  The missing M * w[0] term is < 2^-73 quadrant units, so
+ * whenever |F| >= 2^-11 the result is within 2^-62 relative; otherwise
+ * (probability ~2^-10 for random arguments) the full 192-bit form ph_int192
+ * recomputes it.  The GPU kernels (vem_math.cuh ph_int) perform the same
+ * operations in the same order. */
+static red_t ph_int(double x) {
+  const uint64_t b = bits_d(x), ab = b & 0x7fffffffffffffffull;
+  const int ue = (int)(ab >> 52) - 1023;
+  if (ab >= 0x7ff0000000000000ull || ue < VEM_PH_DI_UEMIN) return ph_int192(x);
+  const uint64_t M = (ab & 0x000fffffffffffffull) | 0x0010000000000000ull;
+  const uint64_t* w = PH_DI + 4 * (ue - VEM_PH_DI_UEMIN);
+  const unsigned __int128 u = (unsigned __int128)M * w[1];
+  const uint64_t T0 = (uint64_t)u;
+  const uint64_t T1 = M * w[2] + (uint64_t)(u >> 64);
+  const uint32_t t3 = (uint32_t)(T1 >> 32), t2 = (uint32_t)T1, t1 = (uint32_t)(T0 >> 32), t0 = (uint32_t)T0;
+  int q = (int)((t3 + 0x20000000u) >> 30);
+  const uint32_t f = t3 & 0x3fffffffu;
+  const int64_t c0 = (int64_t)(((uint64_t)f << 23) | (t2 >> 9)) - ((f >> 29) ? (1ll << 53) : 0);
+  const uint64_t c1 = ((uint64_t)(t2 & 0x1ffu) << 44) | ((uint64_t)t1 << 12) | (t0 >> 20);
+  const uint32_t c2 = t0 & 0xfffffu;
+  /* units of 2^-53 quadrants */
+  const double S0 = (double)c0;
+  const double tb = (double)c1 * 0x1p-53;
+  const double S1 = S0 + tb;
+  const double e = (tb - (S1 - S0)) + (double)c2 * 0x1p-73;
+  const double fh = S1 + e;
+  const double fl = e - (fh - S1);
+  if (fabs(fh) < 0x1p42) return ph_int192(x);
+  const double c0p = (b >> 63) ? -K_PIO2_QD0 * 0x1p-53 : K_PIO2_QD0 * 0x1p-53;
+  const double c1p = (b >> 63) ? -K_PIO2_QD1 * 0x1p-53 : K_PIO2_QD1 * 0x1p-53;
+  const double p = fh * c0p;
+  double ee = fma(fh, c0p, -p);
+  ee = fma(fh, c1p, ee);
+  ee = fma(fl, c0p, ee);
+  if (b >> 63) q = -q;
+  red_t o;
   o.hi = p;
   o.lo = ee;
   o.q = q & 3;

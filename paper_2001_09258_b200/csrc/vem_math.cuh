@@ -340,8 +340,8 @@ __device__ __forceinline__ red ph(double x_in, const double* __restrict__ tab) {
   return o;
 }
 
-// Integer Payne-Hanek for binary64 (oracle: ph_int, which documents the
-// method): 53 x 192-bit product mod 2^192 (IMAD.WIDE chains), the quadrant
+// Integer Payne-Hanek for binary64, full 192-bit window (oracle: ph_int192;
+// the slow level of ph_int below, out of line): 53 x 192-bit product mod 2^192 (IMAD.WIDE chains), the quadrant
 // from its top two bits, and the centred fraction summed straight from the
 // product's 32-bit words as an exact floating-point expansion (each word
 // converts exactly; fast two-sums, no leading-zero shifts), then times pi/2
@@ -349,7 +349,7 @@ __device__ __forceinline__ red ph(double x_in, const double* __restrict__ tab) {
 // cascaded double-double form of reduction.hpp:89-137 takes ~90 FP64
 // instructions per element; this takes ~30 and a few integer ones.
 // `tab` = gPhDI (staged or global), read as 2 x 16 bytes per element.
-__device__ __forceinline__ red ph_int(double x, const double* __restrict__ tab) {
+__device__ __noinline__ red ph_int192(double x, const double* __restrict__ tab) {
   const uint64_t b = bits_d(x), ab = b & 0x7fffffffffffffffull;
   const int ue = (int)(ab >> 52) - 1023;
   const bool small = ue < VEM_PH_DI_UEMIN;
@@ -396,6 +396,59 @@ __device__ __forceinline__ red ph_int(double x, const double* __restrict__ tab) 
   red o;
   // non-finite x: a meaningless r (the functions select the canonical NaN
   // from x itself, as the oracle's NaN r yields)
+  o.hi = small ? x : p;
+  o.lo = small ? 0.0 : ee;
+  o.q = small ? 0 : (q & 3);
+  return o;
+}
+
+// Two-level integer Payne-Hanek (oracle: ph_int, same operations in the same
+// order).  Fast level: M * (top 128 bits of the window) mod 2^128 (one
+// 64 x 64 -> 128 product and one low product), the quadrant from the top two
+// bits, the 126 fraction bits as three exactly convertible chunks (53 bits
+// centred in integer arithmetic, 53, 20) summed with one Fast2Sum, times
+// pi/2 in double-double.  Within 2^-62 relative whenever |F| >= 2^-11
+// quadrants; below that (~2^-10 of random arguments) ph_int192 recomputes.
+__device__ __forceinline__ red ph_int(double x, const double* __restrict__ tab) {
+  const uint64_t b = bits_d(x), ab = b & 0x7fffffffffffffffull;
+  const int ue = (int)(ab >> 52) - 1023;
+  int idx = ue - VEM_PH_DI_UEMIN;
+  idx = idx < 0 ? 0 : (idx > VEM_PH_DI_ENTRIES - 1 ? VEM_PH_DI_ENTRIES - 1 : idx);
+  const uint64_t M = (ab & 0x000fffffffffffffull) | 0x0010000000000000ull;
+  const ulonglong2* wt = reinterpret_cast<const ulonglong2*>(tab) + 2 * idx;
+  const uint64_t w1 = wt[0].y, w2 = wt[1].x;
+  const uint64_t T0 = M * w1;
+  const uint64_t T1 = M * w2 + __umul64hi(M, w1);
+  const uint32_t t3 = (uint32_t)(T1 >> 32), t2 = (uint32_t)T1, t1 = (uint32_t)(T0 >> 32), t0 = (uint32_t)T0;
+  int q = (int)((t3 + 0x20000000u) >> 30);
+  const uint32_t f = t3 & 0x3fffffffu;
+  // c0 = f : t2[31..9] (53 bits) minus 2^53 when the fraction is >= 1/2
+  const int c0hi = (int)((f >> 9) - ((f >> 29) << 21));
+  const uint32_t c0lo = (f << 23) | (t2 >> 9);
+  const double S0 = (double)(long long)(((uint64_t)(uint32_t)c0hi << 32) | c0lo);
+  // c1 = t2[8..0] : t1 : t0[31..20] (53 bits), c2 = t0[19..0]
+  const uint32_t c1hi = ((t2 & 0x1ffu) << 12) | (t1 >> 20);
+  const uint32_t c1lo = (t1 << 12) | (t0 >> 20);
+  const double tb = (double)(((uint64_t)c1hi << 32) | c1lo) * 0x1p-53;
+  const double S1 = S0 + tb;
+  const double e = (tb - (S1 - S0)) + (double)(t0 & 0xfffffu) * 0x1p-73;
+  const double fh = S1 + e;
+  const double fl = e - (fh - S1);
+  // |x| < 1/2 returns (x, 0, 0) below; non-finite x leaves a meaningless r
+  // (the functions select the canonical NaN from x itself)
+  const bool small = ue < VEM_PH_DI_UEMIN;
+  if (!small && ab < 0x7ff0000000000000ull && fabs(fh) < 0x1p42) return ph_int192(x, tab);
+  // r = F (pi/2) sign(x) with pi/2 * 2^-53 = C0 + C1 (units of 2^-53 above)
+  const int sx = (int)(uint32_t)(b >> 32) & (int)0x80000000u;
+  constexpr double kC0 = kPio2Qd0 * 0x1p-53, kC1 = kPio2Qd1 * 0x1p-53;
+  const double c0 = __hiloint2double(__double2hiint(kC0) ^ sx, __double2loint(kC0));
+  const double c1 = __hiloint2double(__double2hiint(kC1) ^ sx, __double2loint(kC1));
+  const double p = fh * c0;
+  double ee = fma(fh, c0, -p);
+  ee = fma(fh, c1, ee);
+  ee = fma(fl, c0, ee);
+  if (b >> 63) q = -q;
+  red o;
   o.hi = small ? x : p;
   o.lo = small ? 0.0 : ee;
   o.q = small ? 0 : (q & 3);
