@@ -524,7 +524,7 @@ __device__ __forceinline__ fmod_pend fmod_pend_setup(double x, double y) {
     p.ed = ed;
   }
   p.md = md;
-  const double rmd = 1.0 / md;  // RN(1/md): the signed step's bound (fmod_stepn_rs)
+  const double rmd = __drcp_rn(md);  // RN(1/md): the signed step's bound (fmod_stepn_rs)
   p.rmd = rmd * 0x1p50;
   // E >= 0; (E - 1) / 50 for E - 1 in [0, 2100] (and 0 for E = 0)
   p.steps = E == 0 ? 0 : (int)(((uint32_t)(E - 1) * 1311u) >> 16);
@@ -572,20 +572,37 @@ struct FmodQ {
   }
   __device__ static T eval1(T x, T y, const double*) {
     fmod_pend A = fmod_pend_setup((double)x, (double)y);
-    for (int k = 0; k < A.steps; k++) A.r = fmod_stepn50(A.r, A.md, A.rmd);
+    // the lanes of a queue row have (nearly) the same step count: four steps
+    // per trip keep the loop control off the dependent chain
+    int k = A.steps;
+#pragma unroll 1
+    for (; k >= 4; k -= 4) {
+      A.r = fmod_stepn50(A.r, A.md, A.rmd);
+      A.r = fmod_stepn50(A.r, A.md, A.rmd);
+      A.r = fmod_stepn50(A.r, A.md, A.rmd);
+      A.r = fmod_stepn50(A.r, A.md, A.rmd);
+    }
+#pragma unroll 1
+    for (; k > 0; k--) A.r = fmod_stepn50(A.r, A.md, A.rmd);
     return (T)fmod_pend_finish(A);
   }
   __device__ static void eval2(T xa, T ya, T xb, T yb, T& ra, T& rb, const double*) {
     fmod_pend A = fmod_pend_setup((double)xa, (double)ya);
     fmod_pend B = fmod_pend_setup((double)xb, (double)yb);
-    const int c = min(A.steps, B.steps);
-    int i = 0;
-    for (; i < c; i++) {
+    // two independent chains interleaved, two steps of each per trip
+    int i = min(A.steps, B.steps);
+#pragma unroll 1
+    for (; i >= 2; i -= 2) {
+      A.r = fmod_stepn50(A.r, A.md, A.rmd);
+      B.r = fmod_stepn50(B.r, B.md, B.rmd);
       A.r = fmod_stepn50(A.r, A.md, A.rmd);
       B.r = fmod_stepn50(B.r, B.md, B.rmd);
     }
-    for (int k = i; k < A.steps; k++) A.r = fmod_stepn50(A.r, A.md, A.rmd);
-    for (int k = i; k < B.steps; k++) B.r = fmod_stepn50(B.r, B.md, B.rmd);
+    const int c = min(A.steps, B.steps) - i;
+#pragma unroll 1
+    for (int k = c; k < A.steps; k++) A.r = fmod_stepn50(A.r, A.md, A.rmd);
+#pragma unroll 1
+    for (int k = c; k < B.steps; k++) B.r = fmod_stepn50(B.r, B.md, B.rmd);
     ra = (T)fmod_pend_finish(A);
     rb = (T)fmod_pend_finish(B);
   }
@@ -681,7 +698,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_queue(const T* __restrict__ 
       int k;
       if (Q::triage(xe[e], ye[e], res, k)) {
         key[e] = k;
-        rank[e] = atomicAdd(&hist[k], 1);
+        rank[e] = (int)tma::smem_atomic_inc(&hist[k]);
       }
       so[slot] = res;
     }
@@ -1548,6 +1565,10 @@ static int launch_fmod_tuned(const T* a, const T* b, T* o, size_t n, vem_stream_
     case 21: return launch_fmod_fixed<T, 2, 2, 2>(a, b, o, n, s);
     case 22: return launch_fmod_fixed<T, 1, 4>(a, b, o, n, s);
     case 8: return launch_fmod<T>(a, b, o, n, s);
+    case 23: return launch_fmod_q<T, 4, 2, 1, 2>(a, b, o, n, s);
+    case 24: return launch_fmod_q<T, 2, 3, 1, 2>(a, b, o, n, s);
+    case 25: return launch_fmod_q<T, 2, 2, 2, 2>(a, b, o, n, s);
+    case 26: return launch_fmod_q<T, 4, 2, 1, 1>(a, b, o, n, s);
     default: return launch_fmod_q<T, 2, 2, 1, 1>(a, b, o, n, s);
   }
 }

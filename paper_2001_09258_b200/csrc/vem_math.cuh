@@ -886,7 +886,7 @@ __device__ __forceinline__ bool fmod_setup(double x, double y, fmod_state& st, d
   double mn = mant_1_2(n, en), md = mant_1_2(d, ed);
   int E = en - ed;
   st.md = md;
-  const double rmd = 1.0 / md;  // RN(1/md): signed steps (fmod_stepn_rs)
+  const double rmd = __drcp_rn(md);  // RN(1/md): signed steps (fmod_stepn_rs)
   st.rmd = rmd * 0x1p50;
   st.ed = ed;
   st.x = x;

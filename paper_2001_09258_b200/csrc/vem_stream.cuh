@@ -88,6 +88,15 @@ __device__ __forceinline__ bool stage_release_last(uint32_t* ctr, uint32_t nw) {
   return (old % nw) == nw - 1;
 }
 
+// Plain shared-memory atomic increment (returns the old value).  Written as
+// PTX so the compiler does not wrap it in its warp-aggregation sequence
+// (match/popc/shuffle per call): the histogram keys of one warp mostly differ.
+__device__ __forceinline__ uint32_t smem_atomic_inc(int* p) {
+  uint32_t old;
+  asm volatile("atom.shared::cta.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(smem_addr(p)) : "memory");
+  return old;
+}
+
 // Programmatic dependent launch (the streaming kernels are launched with
 // cudaLaunchAttributeProgrammaticStreamSerialization): `wait` blocks until
 // the previous grid in the stream has completed and its memory operations
