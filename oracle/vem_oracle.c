@@ -626,25 +626,24 @@ static inline logred_t log_reduce(double a, double Eadj) {
   return o;
 }
 
-/* log1p(rh + rl) as DD: rh - rh^2/2 (exact) + rh^3 Q(rh) + rl(1 - rh) */
+/* log1p(rh + rl) as DD: rh - rh^2/2 (exact: p2 = -z/2, its error -ez/2 with
+ * ez = fma(rh, rh, -z)) + rh^3 Q(rh) + rl(1 - rh), the low terms fused */
 static inline dd_t log1p_dd(double rh, double rl, const double* c, int n) {
   double z = rh * rh;
   double Q = poly(c, n, rh);
-  double t3 = (rh * z) * Q;
-  double h2 = -0.5 * rh;
-  double p2 = rh * h2;
-  double e2 = fma(rh, h2, -p2);
-  double lo = e2 + (t3 + fma(-rl, rh, rl));
+  double p2 = -0.5 * z;
+  double ez = fma(rh, rh, -z);
+  double lo = fma(-0.5, ez, fma(rh * z, Q, fma(-rl, rh, rl)));
   dd_t S = two_sum_fast(rh, p2);
   S.lo = S.lo + lo;
   return S;
 }
 
-/* E*ln2 + logc as DD (E*LN2_H42 exact for |E| < 2^11) */
+/* E*ln2 + logc as DD: E*LN2_H42 (exact for |E| < 2^11) and logc_hi are both
+ * on the 2^-42 grid below 2^10, so their sum is exact (tools/genlogtables.py) */
 static inline dd_t eln2_logc(const logred_t* g) {
   double eh = g->E * LN2_H42;
-  dd_t H = two_sum_fast(eh, g->logc_hi);
-  H.lo = H.lo + fma(g->E, LN2_T42, g->logc_lo);
+  dd_t H = {eh + g->logc_hi, fma(g->E, LN2_T42, g->logc_lo)};
   return H;
 }
 

@@ -673,23 +673,20 @@ __device__ __forceinline__ logred log_reduce(double a, double Eadj, const double
 
 template <int N>
 __device__ __forceinline__ dd log1p_dd(double rh, double rl, const double* c) {
-  double z = rh * rh;
-  double Q = poly<N>(c, rh);
-  double t3 = (rh * z) * Q;
-  double h2 = -0.5 * rh;
-  double p2 = rh * h2;
-  double e2 = fma(rh, h2, -p2);
-  double lo = e2 + (t3 + fma(-rl, rh, rl));
+  const double z = rh * rh;
+  const double Q = poly<N>(c, rh);
+  const double p2 = -0.5 * z;  // -rh^2/2, its error -ez/2 (exact)
+  const double ez = fma(rh, rh, -z);
+  const double lo = fma(-0.5, ez, fma(rh * z, Q, fma(-rl, rh, rl)));
   dd S = two_sum_fast(rh, p2);
   S.lo = S.lo + lo;
   return S;
 }
 
+// E ln2_h42 and logc_hi lie on the 2^-42 grid below 2^10: their sum is exact
 __device__ __forceinline__ dd eln2_logc(const logred& g) {
-  double eh = g.E * ccLn2H42;
-  dd H = two_sum_fast(eh, g.logc_hi);
-  H.lo = H.lo + fma(g.E, ccLn2T42, g.logc_lo);
-  return H;
+  const double eh = g.E * ccLn2H42;
+  return dd{eh + g.logc_hi, fma(g.E, ccLn2T42, g.logc_lo)};
 }
 
 template <bool kU10, bool kAdj = true>
