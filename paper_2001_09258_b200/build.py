@@ -52,13 +52,18 @@ def _stale(lib: str = LIB, sources=SOURCES) -> bool:
     return False
 
 
-def _link(lib: str, sources, verbose: bool):
+CHECK_LIB = os.path.join(HERE, "libvem_check.so")
+
+
+def _link(lib: str, sources, verbose: bool, extra=()):
     objs = []
     bdir = os.path.join(HERE, "_build")
     os.makedirs(bdir, exist_ok=True)
     for s in sources:
         o = os.path.join(bdir, s.replace(".cu", ".o"))
-        cmd = [nvcc(), *NVCC_FLAGS, "-c", os.path.join(CSRC, s), "-o", o]
+        if extra:
+            o = o.replace(".o", "_check.o")
+        cmd = [nvcc(), *NVCC_FLAGS, *extra, "-c", os.path.join(CSRC, s), "-o", o]
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)
@@ -81,5 +86,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_check(force: bool = False, verbose: bool = False) -> str:
+    """The bounds-checked variant (-DVEM_CHECK) for the guard tests; load it
+    with VEM_LIB=<path> (paper_2001_09258_b200/_lib.py)."""
+    if force or _stale(CHECK_LIB, SOURCES):
+        _link(CHECK_LIB, SOURCES, verbose, extra=("-DVEM_CHECK",))
+    return CHECK_LIB
+
+
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    if "--check" in sys.argv:
+        print(build_check(force="--force" in sys.argv, verbose=True))
+    else:
+        print(build(force="--force" in sys.argv, verbose=True))

@@ -23,6 +23,21 @@ namespace vem {
 
 static std::atomic<uint64_t> g_launches{0};
 
+// Checked build (-DVEM_CHECK, build.py --check -> libvem_check.so): device-side
+// bounds assertions on every computed shared-memory index of the sorting
+// kernels (k_trig, k_queue) and on the queue / list counts; a violation traps
+// (the launch fails with cudaErrorLaunchFailure / illegal instruction).  This
+// stands in for compute-sanitizer, which is closed on the GPU pool; the
+// guard-band tests (tests/test_gpu_guard.py) cover the global side.
+#ifdef VEM_CHECK
+#define VEM_ASSERT(c) \
+  do {                \
+    if (!(c)) __trap(); \
+  } while (0)
+#else
+#define VEM_ASSERT(c) ((void)0)
+#endif
+
 // kTableDG: the f64 Payne-Hanek table is read from global memory (L1-resident,
 // __ldg) rather than staged: the 32 KB stage would cost occupancy on inputs
 // that never leave the Cody-Waite range.
@@ -438,6 +453,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_trig(const double* __restric
       const bool isph = (mph >> e) & 1u, iscw = (mcw >> e) & 1u;
       const int slot = e * 32 + lane;
       sx[slot] = (isph || iscw) ? xe[e] : Op::tiny(xe[e]);
+      VEM_ASSERT(!(isph || iscw) || ((isph ? pph : pcw) < WE && (isph ? pph < nph : pcw < nall)));
       if (isph || iscw) si[isph ? pph : pcw] = (unsigned char)slot;
       pph += isph;
       pcw += iscw;
@@ -448,6 +464,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_trig(const double* __restric
 #pragma unroll 1
     for (; (r + 2) * 32 <= nph; r += 2) {
       const int sa = si[r * 32 + lane], sb = si[r * 32 + 32 + lane];
+      VEM_ASSERT((r + 2) * 32 <= nph && sa < WE && sb < WE);
       const double xa = sx[sa], xb = sx[sb];
       const double ya = op.ph(xa, tab), yb = op.ph(xb, tab);
       sx[sa] = ya;
@@ -721,6 +738,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_queue(const T* __restrict__ 
       const int be = __shfl_sync(0xffffffffu, base_even, k >> 1);
       if (key[e] >= 0) {
         const int pos = ((k & 1) ? bo : be) + rank[e];
+        VEM_ASSERT(pos >= 0 && pos < Qn && Qn <= TILE_E);
         qx[pos] = xe[e];
         if constexpr (NIN == 2) qy[pos] = ye[e];
         qi[pos] = (unsigned short)(((e / W) * kThreads + tid) * W + (e % W));
@@ -741,6 +759,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_queue(const T* __restrict__ 
         const int pa = p0 + lane, ca = pa < Qn ? pa : p0;
         if constexpr (ROWS == 1) {
           const T r = Q::eval1(qx[ca], NIN == 2 ? qy[ca] : (T)0, tab);
+          VEM_ASSERT(ca >= 0 && ca < Qn && (pa >= Qn || qi[pa] < TILE_E));
           if (pa < Qn) so[qi[pa]] = r;
         } else {
           const int pb = pa + 32, cb = pb < Qn ? pb : p0;
@@ -1537,8 +1556,21 @@ struct OpFmodPlain {
     else return fmod_f(x, y);
   }
 };
+template <class Op, int TAB, int VPT, int ST, int MINB>
+static int launch_trig_tuned(const double* a, const double* b, double* o, size_t n, vem_stream_t s) {
+  switch (g_tune) {
+    case 30: return launch_trig<Op, TAB, 4, 3, 3>(a, b, o, n, s);
+    case 31: return launch_trig<Op, TAB, 4, 3, 2>(a, b, o, n, s);
+    case 32: return launch_trig<Op, TAB, 2, 3, 3>(a, b, o, n, s);
+    case 33: return launch_trig<Op, TAB, 2, 4, 3>(a, b, o, n, s);
+    case 34: return launch_trig<Op, TAB, 4, 2, 2>(a, b, o, n, s);
+    case 35: return launch_trig<Op, TAB, 2, 2, 4>(a, b, o, n, s);
+    case 36: return launch_trig<Op, TAB, 4, 4, 2>(a, b, o, n, s);
+    default: return launch_trig<Op, TAB, VPT, ST, MINB>(a, b, o, n, s);
+  }
+}
 #define VEM_STREAM launch_tuned
-#define VEM_TRIG launch_trig
+#define VEM_TRIG launch_trig_tuned
 template <class T>
 static int launch_fmod_tuned(const T* a, const T* b, T* o, size_t n, vem_stream_t s) {
   using OpF = typename std::conditional<sizeof(T) == 8, OpFmodD, OpFmodF>::type;

@@ -1,7 +1,8 @@
 """The oracle meets each function's ULP bound against MPFR 4.2.1 (320-bit),
 and matches the C99 Annex F special-value table (SPEC.md:601-609 criteria 1,
 2, 4).  Sample sizes keep the CPU suite to a few minutes; the -m slow marker
-runs 10x larger sweeps."""
+runs SPEC.md:603's sizes (10^6 points per generator incl. random bit
+patterns, 10^5 per Table-2 domain)."""
 from __future__ import annotations
 
 import math
@@ -104,14 +105,50 @@ def test_ulp_bound_vs_mpfr(name):
         assert e <= bound, f"{name}: {e:.3f} ulp > {bound} at {[a[i] for a in args]} -> {out[i]!r}"
 
 
+# SPEC.md:603 acceptance criterion 1 sizes: 10^6 random bit patterns, 10^5
+# uniform samples per Table-2 domain, 10^4 points near k pi/2 (the last is
+# test_near_multiples_of_pi_over_2, 6 x 10^4 points, in the default suite).
+N_SPEC_BITS = 10 ** 6
+N_SPEC_DOMAIN = 10 ** 5
+
+
 @pytest.mark.slow
 @pytest.mark.parametrize("name", sorted(DOMAINS))
 def test_ulp_bound_vs_mpfr_large(name):
+    """Every generator of the entry point (config domains and random bit
+    patterns) at 10^6 points."""
     fn, bound, gens = DOMAINS[name]
     for g in gens:
-        args = g(20 * N)
+        args = g(N_SPEC_BITS)
         e, i, out = _max_ulp(name, fn, *args)
         assert e <= bound, f"{name}: {e:.3f} ulp at {[a[i] for a in args]}"
+
+
+# PAPER.md Table 2 domains (PAPER.md:1194-1300), per function and accuracy
+TABLE2 = {
+    "sin": [(0.4, 0.5), (0.0, 6.28), (0.0, 1e100)], "cos": [(0.4, 0.5), (0.0, 6.28), (0.0, 1e100)],
+    "tan": [(0.4, 0.5), (0.0, 6.28), (0.0, 1e100)], "atan": [(-700.0, 700.0)], "log": [(0.0, 1e300)],
+    "exp": [(-700.0, 700.0)],
+}
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", [f"{f}_d_{a}" for f in TABLE2 for a in ("u10", "u35")] + ["pow_d_u10", "pow_d_u35"])
+def test_ulp_bound_table2_domains(name):
+    fn, acc = name.split("_")[0], name.split("_")[2]
+    bound = 1.0 if acc == "u10" else 3.5
+    if fn == "pow":
+        args = (I.uniform(41, N_SPEC_DOMAIN, -30.0, 30.0), I.uniform(42, N_SPEC_DOMAIN, -30.0, 30.0))
+        args = (np.abs(args[0]),) + args[1:]  # real results: |x| (the sign rule is tested on the Annex F grid)
+        e, i, out = _max_ulp(name, fn, *args)
+        assert e <= bound, (name, e, [a[i] for a in args])
+        return
+    for k, (lo, hi) in enumerate(TABLE2[fn]):
+        x = I.uniform(43 + k, N_SPEC_DOMAIN, lo, hi)
+        if fn == "log":
+            x = x[x > 0]
+        e, i, out = _max_ulp(name, fn, x)
+        assert e <= bound, (name, (lo, hi), e, x[i])
 
 
 def test_near_multiples_of_pi_over_2():

@@ -44,6 +44,7 @@ ENTRY = {  # kernel functor -> C-ABI entry point
     "OpPowDU35": "pow_d_u35", "OpFmodD": "fmod_d", "OpSinF": "sin_f_u10", "OpCosF": "cos_f_u10",
     "OpTanF": "tan_f_u10", "OpExpF": "exp_f_u10", "OpExpFU35": "exp_f_u35", "OpLogF": "log_f_u10",
     "OpLogFU35": "log_f_u35", "OpPowF": "pow_f_u10", "OpPowFU35": "pow_f_u35", "OpFmodF": "fmod_f", "OpFmodFFlat": "fmod_f",
+    "OpSinDU35": "sin_d_u35", "OpCosDU35": "cos_d_u35", "OpTanDU35": "tan_d_u35",
 }
 
 
@@ -96,16 +97,28 @@ def main():
             except ValueError:
                 pass
         mixes[entry_of(kname)] = c
+    stall_cols = [(i, h[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")])
+                  for i, h in enumerate(hdr) if h.startswith("smsp__average_warps_issue_stalled_")
+                  and h.endswith("_per_issue_active.ratio")]
     out = {}
     for k, r in enumerate(data):
         name = entry_of(r[kcol])
         d = {}
+        st = []
+        for i, nm in stall_cols:
+            try:
+                st.append((float(r[i]), nm))
+            except ValueError:
+                pass
+        d["stalls_per_issue"] = {nm: round(v, 2) for v, nm in sorted(st, reverse=True)[:6]}
         for key, ci in col.items():
             try:
                 d[key] = float(r[ci])
             except ValueError:
                 d[key] = r[ci]
         mb = 1e6 if units[col["dram_read_mb"]].lower().startswith("m") else (1e9 if units[col["dram_read_mb"]].lower().startswith("g") else 1.0)
+        tu = units[col["duration_us"]].lower()  # ncu picks nsecond / usecond / msecond / second
+        d["duration_us"] = d["duration_us"] * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(tu, 1.0)
         d["dram_bytes_per_elem"] = round((d["dram_read_mb"] + d["dram_write_mb"]) * mb / elems, 3)
         d["inst_per_elem"] = round(d["inst_executed"] * 32 / elems, 2)
         if name in mixes:
@@ -124,6 +137,9 @@ def main():
             f.write(f"| {n} | {d['duration_us']:.1f} | {d['dram_bytes_per_elem']} | {d['inst_per_elem']} | "
                     f"{d.get('fp64_inst_per_elem')} | {d['fp64_pipe_pct']:.1f} | {d['issue_active_pct']:.1f} | "
                     f"{d['dram_pct']:.1f} | {int(d['registers'])} |\n")
+        f.write("\nTop warp-stall reasons (cycles per issued instruction):\n\n")
+        for n, d in out.items():
+            f.write(f"- {n}: " + ", ".join(f"{k} {v}" for k, v in d.get("stalls_per_issue", {}).items()) + "\n")
         f.write("\nTop opcodes per element (thread instructions):\n\n")
         for n, d in out.items():
             f.write(f"- {n}: " + ", ".join(f"{o} {v}" for o, v in list(d.get('mix_per_elem', {}).items())[:14]) + "\n")

@@ -1,7 +1,7 @@
 #!/usr/bin/env python3
 """Run one entry point on one BASELINE config's inputs (dev tool for ncu).
 
-Usage: python tools/prof_one.py NAME[@CFG][,NAME[@CFG]...] CFG [log2_n=24] [reps=3]
+Usage: python tools/prof_one.py NAME[@CFG[@LOG2N]][,...] CFG [log2_n=24] [reps=3]
 e.g.  ncu --set full -k regex:k_stream -s 1 -c 1 python tools/prof_one.py sin_d_u10 5 24
 reps=0: each entry point runs exactly once, no warm-up (one ncu capture per
 entry point with -c <number of names>).
@@ -23,9 +23,10 @@ def main():
     n = 1 << (int(sys.argv[3]) if len(sys.argv) > 3 else 24)
     reps = int(sys.argv[4]) if len(sys.argv) > 4 else 3
     for name in sys.argv[1].split(","):
-        # NAME@CFG overrides the config per entry point
-        name, _, c = name.partition("@")
-        run(name, int(c) if c else cfg, n, reps)
+        # NAME@CFG[@LOG2N] overrides the config (and size) per entry point
+        parts = name.split("@")
+        run(parts[0], int(parts[1]) if len(parts) > 1 else cfg, 1 << int(parts[2]) if len(parts) > 2 else n, reps)
+        torch.cuda.empty_cache()
 
 
 def run(name, cfg, n, reps):
