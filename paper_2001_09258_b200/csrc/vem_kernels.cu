@@ -1624,7 +1624,7 @@ int vem_tan_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { ret
 int vem_atan_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpAtanD, double, 1, kNoTable, 2, 2>(x, nullptr, y, n, s); }
 int vem_exp_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpExpD, double, 1, kNoTable, 1, 2, 3>(x, nullptr, y, n, s); }
 int vem_exp_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpExpDU35, double, 1, kNoTable, 4, 2>(x, nullptr, y, n, s); }
-int vem_log_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpLogD, double, 1, kTableLog, 4, 2, 4>(x, nullptr, y, n, s); }
+int vem_log_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpLogD, double, 1, kTableLog, 4, 2, 4, true>(x, nullptr, y, n, s); }
 int vem_log_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpLogDU35, double, 1, kTableLog, 2, 2, 4>(x, nullptr, y, n, s); }
 int vem_pow_d_u10(const double* x, const double* y2, double* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpPowD, double, 2, kTableLog, 2, 2, 3, true>(x, y2, o, n, s); }
 int vem_pow_d_u35(const double* x, const double* y2, double* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpPowDU35, double, 2, kTableLog, 2, 2, 3, true>(x, y2, o, n, s); }

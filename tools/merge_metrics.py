@@ -27,8 +27,9 @@ def main():
                                    "stalls_per_issue": m.get("stalls_per_issue")}
         for ext in (".md", ".json"):
             src = os.path.splitext(path)[0] + ext
-            if os.path.exists(src):
-                shutil.copy(src, os.path.join(ROOT, "profiles", base + ext))
+            dst = os.path.join(ROOT, "profiles", base + ext)
+            if os.path.exists(src) and os.path.abspath(src) != os.path.abspath(dst):
+                shutil.copy(src, dst)
     json.dump(km, open(km_path, "w"), indent=1, sort_keys=True)
     print(f"merged {len(sys.argv) - 1} summaries into {km_path}")
 

@@ -116,10 +116,13 @@ def main():
                 d[key] = float(r[ci])
             except ValueError:
                 d[key] = r[ci]
-        mb = 1e6 if units[col["dram_read_mb"]].lower().startswith("m") else (1e9 if units[col["dram_read_mb"]].lower().startswith("g") else 1.0)
+        def unit_scale(u):  # ncu picks byte / Kbyte / Mbyte / Gbyte per column
+            u = u.lower()
+            return 1e9 if u.startswith("g") else 1e6 if u.startswith("m") else 1e3 if u.startswith("k") else 1.0
         tu = units[col["duration_us"]].lower()  # ncu picks nsecond / usecond / msecond / second
         d["duration_us"] = d["duration_us"] * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(tu, 1.0)
-        d["dram_bytes_per_elem"] = round((d["dram_read_mb"] + d["dram_write_mb"]) * mb / elems, 3)
+        d["dram_bytes_per_elem"] = round((d["dram_read_mb"] * unit_scale(units[col["dram_read_mb"]]) +
+                                          d["dram_write_mb"] * unit_scale(units[col["dram_write_mb"]])) / elems, 3)
         d["inst_per_elem"] = round(d["inst_executed"] * 32 / elems, 2)
         if name in mixes:
             mix = mixes[name]
