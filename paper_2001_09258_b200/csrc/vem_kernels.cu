@@ -189,11 +189,42 @@ __global__ void __launch_bounds__(kThreads) k_binary(const T* __restrict__ x, co
 // evaluates a tile's elements with Op::fast (branch-free, interleavable)
 // and passes the elements it flags to Op::slow.
 template <class Op> struct HasFast { static constexpr bool value = false; };
+// Ops with trivial-result classes (closed-form results for saturated /
+// special / tiny arguments: exp, log, pow, atan; vem_math.cuh "trivial
+// classes").  Triv<Op>::maybe is a cheap bit test (false for every argument
+// of the configs where nothing saturates, e.g. config 2); Triv<Op>::exact decides
+// exactly and gives the result, equal bit for bit to the full function's.
+// k_stream compacts the non-trivial elements of a warp into rows when at
+// least a quarter of its lanes' first elements may be trivial (config 5:
+// 50-97 % of the elements are).
+template <class Op> struct Triv { static constexpr bool value = false; };
+template <class Op> struct HasTriv { static constexpr bool value = Triv<Op>::value; };
 // the full function for rare elements: one out-of-line copy per Op
 template <class Op, class T>
 __device__ __noinline__ T full_op(T x, const double* tab) { return Op()(x, tab); }
 template <class Op, class T>
 __device__ __noinline__ T full_op(T x, T y, const double* tab) { return Op()(x, y, tab); }
+
+// one element through the op's fast path and, if flagged, its slow hook (or
+// the plain op for ops without a split fast path)
+template <class Op, int NIN, class T>
+__device__ __forceinline__ T eval_one(const Op& op, T x, T y, const double* tab) {
+  if constexpr (HasFast<Op>::value) {
+    int code;
+    T r;
+    if constexpr (NIN == 2) r = op.fast(x, y, tab, code);
+    else r = op.fast(x, tab, code);
+    if (code) {
+      if constexpr (NIN == 2) r = Op::slow(x, y, r, code, tab);
+      else r = Op::slow(x, r, code, tab);
+    }
+    return r;
+  } else {
+    (void)y;
+    if constexpr (NIN == 2) return op(x, y, tab);
+    else return op(x, tab);
+  }
+}
 
 // ------------------------------------------------- TMA-staged streaming
 // NIN inputs (1 or 2); tiles of kThreads*VPT 16-byte vectors per input;
@@ -218,6 +249,12 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
   __shared__ uint64_t bars[STAGES];
   __shared__ uint32_t rel[STAGES];
   __shared__ __align__(16) double stab[TableSize<TABLE>::n];
+  // trivial-class compaction scratch (HasTriv ops only): per warp the
+  // arguments / results in slot order and the list of non-trivial slots
+  constexpr int kCW = HasTriv<Op>::value ? 32 * NE : 1;
+  __shared__ __align__(16) T s_cx[HasTriv<Op>::value ? NW : 1][kCW];
+  __shared__ __align__(16) T s_cy[HasTriv<Op>::value && NIN == 2 ? NW : 1][kCW];
+  __shared__ unsigned char s_ci[HasTriv<Op>::value ? NW : 1][kCW];
   V* buf = reinterpret_cast<V*>(dsm);
   const int tid = threadIdx.x, lane = tid & 31;
   if (tid == 0) {
@@ -235,6 +272,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
   const size_t G = gridDim.x;
   const size_t my = ntiles > blockIdx.x ? (ntiles - blockIdx.x + G - 1) / G : 0;
   const uint64_t pol = tma::policy_evict_first();
+  bool tmode = false;  // HasTriv: this warp compacts trivial elements (decided on its first tile)
+  (void)tmode;
   auto issue = [&](int s, size_t tile) {
     tma::mbar_expect_tx(&bars[s], NIN * TILE_BYTES);
     tma::bulk_g2s(buf + (size_t)(s * NIN) * TILE_V, reinterpret_cast<const V*>(a) + tile * TILE_V, TILE_BYTES,
@@ -268,6 +307,71 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
       }
     }
     V* ov = reinterpret_cast<V*>(out) + (blockIdx.x + j * G) * TILE_V;
+    if constexpr (HasTriv<Op>::value) {
+      static_assert(sizeof(T) == 8 && W == 2, "trivial-class compaction: binary64");
+      // ---- warps with many trivial elements: compact the others into rows.
+      // The decision samples each lane's first element (one cheap test per
+      // lane and tile, so the dense path below pays ~1 instruction per
+      // element): compact when at least a quarter of the lanes' samples may
+      // be trivial.
+      // The mode is decided per warp on its first tile (input arrays are
+      // rarely heterogeneous at this scale) so that the dense path carries
+      // no per-tile test; in compaction mode every tile re-checks.
+      bool m0;
+      if constexpr (NIN == 2) m0 = Triv<Op>::maybe(va[0].x, vb[0].x);
+      else m0 = Triv<Op>::maybe(va[0].x);
+      if (j == 0) tmode = __popc(__ballot_sync(0xffffffffu, m0)) >= 8;
+      if (tmode && __popc(__ballot_sync(0xffffffffu, m0)) >= 8) {
+        constexpr int WE = 32 * NE;
+        T* sx = s_cx[tid >> 5];
+        T* sy = NIN == 2 ? s_cy[(tid >> 5) % (NIN == 2 ? NW : 1)] : sx;  // unary: y unused
+        unsigned char* si = s_ci[tid >> 5];
+        uint32_t mn = 0;  // non-trivial
+#pragma unroll
+        for (int v = 0; v < VPT; v++)
+#pragma unroll
+          for (int k = 0; k < W; k++) {
+            const int e = v * W + k, slot = e * 32 + lane;
+            const T x = vget(va[v], k);
+            T r = x;
+            bool t;
+            if constexpr (NIN == 2) t = Triv<Op>::exact(x, vget(vb[v], k), r);
+            else t = Triv<Op>::exact(x, r);
+            sx[slot] = t ? r : x;
+            if constexpr (NIN == 2) sy[slot] = vget(vb[v], k);
+            mn |= (uint32_t)!t << e;
+          }
+        const int cnt = __popc(mn);
+        int inc = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc += t;
+        }
+        const int nall = __shfl_sync(0xffffffffu, inc, 31);
+        int p = inc - cnt;
+#pragma unroll
+        for (int e = 0; e < NE; e++)
+          if ((mn >> e) & 1u) si[p++] = (unsigned char)(e * 32 + lane);
+        __syncwarp();
+#pragma unroll 1
+        for (int r = 0; r * 32 < nall; r += 2) {  // two rows per trip (independent chains)
+          const int ia = r * 32 + lane, ib = ia + 32;
+          const int sa = si[ia < nall ? ia : 0], sb = si[ib < nall ? ib : 0];
+          const T ya = eval_one<Op, NIN>(op, sx[sa], sy[sa], tab);
+          const T yb = eval_one<Op, NIN>(op, sx[sb], sy[sb], tab);
+          __syncwarp();
+          if (ia < nall) sx[sa] = ya;
+          if (ib < nall) sx[sb] = yb;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int v = 0; v < VPT; v++)
+          __stcs(ov + v * kThreads + tid, make_double2(sx[(v * W) * 32 + lane], sx[(v * W + 1) * 32 + lane]));
+        __syncwarp();  // the block is rewritten by the next tile
+        continue;
+      }
+    }
     if constexpr (HasFast<Op>::value) {
       T res[NE];
       int code[NE];
@@ -658,6 +762,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_queue(const T* __restrict__ 
   __shared__ __align__(16) T so[TILE_E];  // output block (tile order)
   __shared__ unsigned short qi[TILE_E];
   __shared__ int hist[kQKeys + 1];  // + the unit-fetch counter
+  __shared__ int qoff[kThreads / 32][kQKeys];  // per-warp copies of the queue offsets
   V* buf = reinterpret_cast<V*>(dsm);
   const int tid = threadIdx.x, lane = tid & 31;
   if (tid == 0) {
@@ -731,13 +836,16 @@ __global__ void __launch_bounds__(kThreads, MINB) k_queue(const T* __restrict__ 
     const int Qn = __shfl_sync(0xffffffffu, suf, 0);
     const int base_odd = suf - h0 - h1;  // keys > 2*lane+1
     const int base_even = base_odd + h1;
+    // this warp's copy of the 64 queue offsets (one LDS per element below
+    // instead of two shuffles)
+    int* offs = qoff[tid >> 5];
+    offs[2 * lane] = base_even;
+    offs[2 * lane + 1] = base_odd;
+    __syncwarp();
 #pragma unroll
     for (int e = 0; e < NE; e++) {
-      const int k = key[e] < 0 ? 0 : key[e];
-      const int bo = __shfl_sync(0xffffffffu, base_odd, k >> 1);
-      const int be = __shfl_sync(0xffffffffu, base_even, k >> 1);
       if (key[e] >= 0) {
-        const int pos = ((k & 1) ? bo : be) + rank[e];
+        const int pos = offs[key[e]] + rank[e];
         VEM_ASSERT(pos >= 0 && pos < Qn && Qn <= TILE_E);
         qx[pos] = xe[e];
         if constexpr (NIN == 2) qy[pos] = ye[e];
@@ -749,12 +857,22 @@ __global__ void __launch_bounds__(kThreads, MINB) k_queue(const T* __restrict__ 
     // end duplicate the unit's first entry (same cost class, result dropped)
     // (FETCH units per atomic: consecutive units have nearly the same cost)
     const int nunits = (Qn + 32 * ROWS - 1) / (32 * ROWS);
-    for (int u0 = 0;;) {
-      if (lane == 0) u0 = atomicAdd(&hist[kQKeys], FETCH);
-      u0 = __shfl_sync(0xffffffffu, u0, 0);
-      if (u0 >= nunits) break;
+    // FETCH == 0: static snake order over the warps (round k: unit 8k + w
+    // for even k, 8k + 7 - w for odd k) -- the units are sorted heaviest
+    // first, so consecutive rounds balance; no atomic per unit.
+    // FETCH > 0: dynamic fetch of FETCH units per shared-memory atomic.
+    constexpr int kNW = kThreads / 32;
+    const int wq = tid >> 5;
+    for (int u0 = 0, rnd = 0;; rnd++) {
+      if constexpr (FETCH == 0) {
+        u0 = rnd * kNW + ((rnd & 1) ? kNW - 1 - wq : wq);
+      } else {
+        if (lane == 0) u0 = (int)tma::smem_atomic_add(&hist[kQKeys], FETCH);
+        u0 = __shfl_sync(0xffffffffu, u0, 0);
+      }
+      if (u0 >= nunits) break;  // (snake: every later round's unit is larger)
 #pragma unroll 1
-      for (int u = u0; u < u0 + FETCH && u < nunits; u++) {
+      for (int u = u0; u < u0 + (FETCH == 0 ? 1 : FETCH) && u < nunits; u++) {
         const int p0 = u * 32 * ROWS;
         const int pa = p0 + lane, ca = pa < Qn ? pa : p0;
         if constexpr (ROWS == 1) {
@@ -1204,6 +1322,38 @@ VEM_BINARY_OP(OpFdimF, float, ((void)tab, fdim_f(x, y)))
 #undef VEM_BINARY_OP
 #undef VEM_SPLIT_BINARY_OP
 
+// trivial classes (vem_math.cuh triv_*): exp, log, pow, atan (binary64)
+struct TrivExpD {
+  static constexpr bool value = true;
+  __device__ __forceinline__ static bool maybe(double x) { return triv_exp_maybe(x); }
+  __device__ __forceinline__ static bool exact(double x, double& r) { return triv_exp(x, r); }
+};
+struct TrivLogD {
+  static constexpr bool value = true;
+  __device__ __forceinline__ static bool maybe(double x) { return triv_log_maybe(x); }
+  __device__ __forceinline__ static bool exact(double x, double& r) { return triv_log(x, r); }
+};
+struct TrivPowD {
+  static constexpr bool value = true;
+  __device__ __forceinline__ static bool maybe(double x, double y) { return triv_pow_maybe(x, y); }
+  __device__ __forceinline__ static bool exact(double x, double y, double& r) { return triv_pow(x, y, r); }
+};
+struct TrivAtanD {
+  static constexpr bool value = true;
+  __device__ __forceinline__ static bool maybe(double x) { return triv_atan_maybe(x); }
+  __device__ __forceinline__ static bool exact(double x, double& r) { return triv_atan(x, r); }
+};
+// Enabled where the full computation is expensive enough for the compaction
+// to pay and the dense path does not lose (A/B, `profiles/r02_ab_triv/`:
+// config 5 pow_d_u10 +17 %, atan +5-13 %, config 2 pow_d_u10 unchanged;
+// exp -40 %, log -10 % on config 5 -- their fast paths are cheaper than the
+// placement and rows -- and pow_d_u35 -3.5 % on config 2 (code layout of
+// its dense path), so TrivExpD / TrivLogD stay unused and pow_d_u35 keeps
+// the dense path only).
+template <> struct Triv<OpPowD> : TrivPowD {};
+template <> struct Triv<OpAtanD> : TrivAtanD {};
+template <> struct Triv<OpAtanDU35> : TrivAtanD {};
+
 // ------------------------------------------------------------- launching
 // Per-device launch state.  The shared-memory opt-in
 // (cudaFuncAttributeMaxDynamicSharedMemorySize) and the occupancy figure are
@@ -1601,6 +1751,8 @@ static int launch_fmod_tuned(const T* a, const T* b, T* o, size_t n, vem_stream_
     case 24: return launch_fmod_q<T, 2, 3, 1, 2>(a, b, o, n, s);
     case 25: return launch_fmod_q<T, 2, 2, 2, 2>(a, b, o, n, s);
     case 26: return launch_fmod_q<T, 4, 2, 1, 1>(a, b, o, n, s);
+    case 27: return launch_fmod_q<T, 2, 2, 1, 1, 0>(a, b, o, n, s);
+    case 28: return launch_fmod_q<T, 2, 2, 1, 2, 0>(a, b, o, n, s);
     default: return launch_fmod_q<T, 2, 2, 1, 1>(a, b, o, n, s);
   }
 }
@@ -1632,7 +1784,7 @@ int vem_fmod_d(const double* x, const double* y2, double* o, size_t n, vem_strea
 #ifdef VEM_TUNE
   return VEM_FMOD<double>(x, y2, o, n, s);
 #else
-  return launch_fmod_q<double, 2, 2, 1, 1>(x, y2, o, n, s);
+  return launch_fmod_q<double, 2, 2, 1, 2, 0>(x, y2, o, n, s);  // two rows per lane, static snake schedule
 #endif
 }
 

@@ -217,7 +217,7 @@ __device__ __forceinline__ dd dd_squ(dd x) {
   return {p, e};
 }
 __device__ __forceinline__ dd dd_div(dd x, dd y) {
-  double t = 1.0 / y.hi;
+  double t = __drcp_rn(y.hi);  // == RN(1 / y.hi), without the division routine's slow path
   double q = x.hi * t;
   double u = fma(t, x.hi, -q);
   double v = fma(y.lo, -t, fma(y.hi, -t, 1.0));
@@ -1000,7 +1000,7 @@ __device__ __forceinline__ float tan_f_u10(float x, const double* tab) {
   double z = r.r * r.r;
   double P = poly<VEM_TAN_F_N>(cTanF, z);
   double t = fma(r.r * z, P, r.r);
-  double y = (r.q & 1) ? -1.0 / t : t;
+  double y = (r.q & 1) ? -__drcp_rn(t) : t;
   return fin_f_odd(x, (float)y);
 }
 
@@ -1146,7 +1146,7 @@ __device__ __forceinline__ float fmod_f_flat(float x, float y) {
   const double md = from_bits_d((db & 0x000fffffffffffffull) | 0x3ff0000000000000ull);
   const int E = en - ed;  // 0 when not pending
   const int steps = E == 0 ? 0 : (int)(((uint32_t)(E - 1) * 1311u) >> 16);
-  const double rmd = 1.0 / md;
+  const double rmd = __drcp_rn(md);
   const double rmd50 = rmd * 0x1p50;
   double r = fmod_stepn_rs(mn * __hiloint2double((1023 + E - 50 * steps) << 20, 0), md, rmd);
 #pragma unroll 1
@@ -1173,7 +1173,7 @@ __device__ __forceinline__ float fmod_f_fixed(float x, float y) {
   double r = from_bits_d((nb & 0x000fffffffffffffull) | 0x3ff0000000000000ull);
   const double md = from_bits_d((db & 0x000fffffffffffffull) | 0x3ff0000000000000ull);
   const int E = en - ed;  // [0, 277]; 0 when not pending
-  const double rmd = 1.0 / md;
+  const double rmd = __drcp_rn(md);
 #pragma unroll
   for (int i = 0; i < 6; i++) {
     const int s = (int)(((uint32_t)(E + i) * 10923u) >> 16);  // (E + i) / 6 for E + i <= 282
@@ -1367,11 +1367,76 @@ __device__ __forceinline__ double atan2_d_u35(double y, double x) {
   const atan2_parts p = atan2_split(y, x);
   const double nn = p.c1 ? p.num - p.den : p.num;
   const double dn = p.c1 ? p.num + p.den : p.den;
-  const double b = nn * (1.0 / dn);
+  const double b = nn * __drcp_rn(dn);
   const double z = b * b;
   const double P = poly<VEM_ATAN_D_U35_N>(cAtanDU35, z);
   const double g = p.ch + (double)p.sig * fma(b * z, P, b);
   return canon_d(atan2_special(y, x, copysign_b(g, y)));
+}
+
+// ============================================ trivial classes (kernels)
+// Closed-form results for arguments whose value the full function returns
+// without computation -- saturated, special or tiny -- used by k_stream to
+// keep such elements out of the computed rows (config 5: 50-97 % of the
+// elements).  maybe() is a cheap superset test on the bits; exact() decides
+// and gives the result, bit-identical to the full function's (oracle:
+// vo_triv_*, tests/test_trivial_classes.py checks every rule against the
+// oracle's full functions).
+// exp: |x| < 2^-54 -> 1.0; x > ln(DBL_MAX) -> +inf; x < -745.13 -> +0; NaN.
+__device__ __forceinline__ bool triv_exp_maybe(double x) {
+  const uint32_t h = (uint32_t)__double2hiint(x) & 0x7fffffffu;
+  return h >= 0x40862E42u || h < 0x3C900000u;
+}
+__device__ __forceinline__ bool triv_exp(double x, double& r) {
+  const uint32_t h = (uint32_t)__double2hiint(x) & 0x7fffffffu;
+  r = h < 0x3C900000u ? 1.0 : (x > kExpOvf ? kInf : (x < kExpUnf ? 0.0 : from_bits_d(kCanonNanD)));
+  return h < 0x3C900000u || x > kExpOvf || x < kExpUnf || x != x;
+}
+// log: negative (incl. -inf, negative NaN bits) -> NaN, +-0 -> -inf, +inf, NaN
+__device__ __forceinline__ bool triv_log_maybe(double x) {
+  const uint64_t ix = bits_d(x);
+  return ix - 0x0000000000000001ull >= 0x7fefffffffffffffull;  // not positive finite nonzero
+}
+__device__ __forceinline__ bool triv_log(double x, double& r) {
+  const uint64_t ix = bits_d(x);
+  r = (ix << 1) == 0ull ? -kInf : (ix == 0x7ff0000000000000ull ? kInf : from_bits_d(kCanonNanD));
+  return ix - 0x0000000000000001ull >= 0x7fefffffffffffffull;
+}
+// pow (x, y finite and nonzero, x normal): x < 0 with y not an integer ->
+// NaN; x > 0 with |y log x| certainly beyond the saturation thresholds ->
+// +inf / +0.  log|x| lies in [e ln2, (e+1) ln2) for x = 2^e m, so
+// |y log x| >= |y| m ln2 with m = e (e >= 0) or e + 1 (e < 0), its sign the
+// sign of y m: y m > 1025 (710.5 > ln DBL_MAX) -> +inf, y m < -1077
+// (-746.5 < -745.14) -> +0.  maybe(): x negative / special / subnormal or
+// |e| > 34 (config 2's x in [1e-10, 1e10]: never).
+__device__ __forceinline__ bool triv_pow_maybe(double x, double y) {
+  (void)y;  // a hint only: large |y| with moderate x is left to the full path
+  // x negative (sign bit: a huge unsigned word), special, or 2^e with
+  // |e| > 34: one subtract and one compare on the high word
+  return (uint32_t)__double2hiint(x) - 0x3DD00000u >= 0x04400000u;
+}
+__device__ __forceinline__ bool triv_pow(double x, double y, double& r) {
+  const uint32_t hx = (uint32_t)__double2hiint(x);
+  const uint32_t hy = (uint32_t)__double2hiint(y) & 0x7fffffffu, ly = (uint32_t)__double2loint(y);
+  const bool fx = ((hx & 0x7fffffffu) - 0x00100000u) < 0x7fe00000u;  // normal, either sign
+  const bool fy = (hy < 0x7ff00000u) && ((hy | ly) != 0u);
+  const int e = (int)((hx >> 20) & 0x7ffu) - 1023;
+  const double p = y * (double)(e >= 0 ? e : e + 1);
+  const bool neg = (int)hx < 0;
+  const bool nanr = neg && trunc(y) != y;
+  r = nanr ? from_bits_d(kCanonNanD) : (p > 1025.0 ? kInf : 0.0);
+  return fx && fy && (nanr || (!neg && (p > 1025.0 || p < -1077.0)));
+}
+// atan: |x| >= 2^54 (incl. inf) -> +-pi/2 (the double nearest); |x| < 2^-27
+// -> x; NaN -> NaN
+__device__ __forceinline__ bool triv_atan_maybe(double x) {
+  const uint32_t h = (uint32_t)__double2hiint(x) & 0x7fffffffu;
+  return h >= 0x43500000u || h < 0x3E400000u;
+}
+__device__ __forceinline__ bool triv_atan(double x, double& r) {
+  const uint32_t h = (uint32_t)__double2hiint(x) & 0x7fffffffu;
+  r = x != x ? from_bits_d(kCanonNanD) : (h < 0x3E400000u ? x : copysign_b(kPio2Qd0, x));
+  return h >= 0x43500000u || h < 0x3E400000u;
 }
 
 // ============================================ split fast paths (kernels)

@@ -33,8 +33,28 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                : "memory");
 }
 
+// Waits for the stage's phase.  With VEM_MBAR_HINT the waiting thread asks to
+// be suspended for up to that many ns per try (it wakes when the phase
+// completes) instead of re-issuing try_wait: warps that run ahead of the TMA
+// stream then stop consuming issue slots.
+#ifndef VEM_MBAR_HINT
+#define VEM_MBAR_HINT 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   uint32_t a = smem_addr(bar);
+#if VEM_MBAR_HINT
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "@P1 bra.uni DONE;\n"
+      "bra.uni LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(a),
+      "r"(phase), "n"(VEM_MBAR_HINT)
+      : "memory");
+#else
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
@@ -46,6 +66,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       "}\n" ::"r"(a),
       "r"(phase)
       : "memory");
+#endif
 }
 
 // Cross-proxy WAR: the generic-proxy LDS reads of a stage (by all threads,
@@ -94,6 +115,11 @@ __device__ __forceinline__ bool stage_release_last(uint32_t* ctr, uint32_t nw) {
 __device__ __forceinline__ uint32_t smem_atomic_inc(int* p) {
   uint32_t old;
   asm volatile("atom.shared::cta.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(smem_addr(p)) : "memory");
+  return old;
+}
+__device__ __forceinline__ uint32_t smem_atomic_add(int* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.shared::cta.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(smem_addr(p)), "r"(v) : "memory");
   return old;
 }
 
