@@ -1473,26 +1473,21 @@ __device__ __forceinline__ double log_slow_d(double x, F full) {
   if (ix - 1ull < 0x000fffffffffffffull) return full();  // positive subnormal
   return (ix << 1) == 0ull ? -kInf : (ix == 0x7ff0000000000000ull ? kInf : from_bits_d(kCanonNanD));
 }
-// pow codes: bit 0 = full function, bit 1 = negative base (sign / NaN rule),
-// bit 2 = exp overflow (t > ln(DBL_MAX)), bit 3 = exp underflow to 0.  The
-// saturation tests use the high word of t with a one-ulp-of-the-word margin:
-// t in the margin gets bit 0 instead, never a wrong saturation.
+// pow code: 0 for a positive normal x with |t| < 708 (t = y log x; y = +-0
+// gives t = +-0 and the exact 1.0, inf / NaN y give |t| = inf / NaN and are
+// flagged) -- two compares per element; otherwise bit 31 set and the high
+// word of t (shifted right by one) below it, from which the slow hook
+// rebuilds the classification (saturated / negative base / special operand).
 template <int NL>
 __device__ __forceinline__ double pow_fast_d(double x, double y, const double* cl, const double* lt, int& code) {
   const uint32_t hx = (uint32_t)__double2hiint(x);
-  const uint32_t hy = (uint32_t)__double2hiint(y) & 0x7fffffffu, ly = (uint32_t)__double2loint(y);
-  const bool fx = ((hx & 0x7fffffffu) - 0x00100000u) < 0x7fe00000u;  // normal, either sign
-  const bool fy = (hy < 0x7ff00000u) && ((hy | ly) != 0u);
   const double ax = __hiloint2double((int)(hx & 0x7fffffffu), __double2loint(x));
   const dd t = dd_mul_d(log_dd<NL, false>(ax, 0.0, cl, lt), y);
   int e;
   const double R = exp_dd_core(t.hi, t.lo, lt, e);
   const uint32_t th = (uint32_t)__double2hiint(t.hi);
-  const uint32_t ht = th & 0x7fffffffu;
-  const bool neg = (int)th < 0;  // selects only: no branch between the elements' chains
-  const int sat = (!neg && ht >= 0x40862E43u) ? 4 : ((neg && ht >= 0x40874911u) ? 8 : 1);
-  const int c = (((int)hx < 0) ? 2 : 0) | ((ht >= kExpFastHi) ? sat : 0);
-  code = (fx && fy) ? c : 1;
+  const bool ok = (hx - 0x00100000u < 0x7fe00000u) && ((th & 0x7fffffffu) < kExpFastHi);
+  code = ok ? 0 : (int)((th >> 1) | 0x80000000u);
   return __hiloint2double(__double2hiint(R) + (e << 20), __double2loint(R));
 }
 // pow of a negative finite base (pow_core_d's rule on R = pow(|x|, y))
@@ -1509,21 +1504,30 @@ __device__ __forceinline__ double pow_special_x_d(double x, double y) {
   else res = (y < 0.0) ? ((yodd && x < 0.0) ? -0.0 : 0.0) : ((yodd && x < 0.0) ? -kInf : kInf);
   return (x != x) ? from_bits_d(kCanonNanD) : res;
 }
+// The saturation tests use the high word of t without its last bit, with a
+// margin: t in the margin goes to the full function, never to a wrong
+// saturation (ln DBL_MAX = 0x40862E42FEFA39EF, -ln(2^-1075) = 0x40874910D52D3052).
 template <class F>
 __device__ __forceinline__ double pow_slow_split_d(double x, double y, double r, int code, F full) {
-  if (code & 1) {
+  const uint32_t hx = (uint32_t)__double2hiint(x);
+  const uint32_t hy = (uint32_t)__double2hiint(y) & 0x7fffffffu, ly = (uint32_t)__double2loint(y);
+  const bool fx = ((hx & 0x7fffffffu) - 0x00100000u) < 0x7fe00000u;  // normal, either sign
+  const bool fy = (hy < 0x7ff00000u) && ((hy | ly) != 0u);
+  if (!(fx && fy)) {
     // x in {+-0, +-Inf, NaN} with an ordinary y: inline; everything else
-    // flagged here (subnormal x, special y, t in the saturation margin)
-    // needs the full function
-    const uint32_t hx = (uint32_t)__double2hiint(x) & 0x7fffffffu;
-    const uint32_t hy = (uint32_t)__double2hiint(y) & 0x7fffffffu, ly = (uint32_t)__double2loint(y);
-    const bool fy = (hy < 0x7ff00000u) && ((hy | ly) != 0u);
-    const bool sx = hx >= 0x7ff00000u || is_zero_bits(x);
+    // flagged here (subnormal x, special y) needs the full function
+    const bool sx = (hx & 0x7fffffffu) >= 0x7ff00000u || is_zero_bits(x);
     if (fy && sx) return pow_special_x_d(x, y);
     return full();
   }
-  r = (code & 4) ? kInf : ((code & 8) ? 0.0 : r);
-  return (code & 2) ? pow_neg_fix_d(r, y) : r;
+  const uint32_t t2 = (uint32_t)code & 0x3fffffffu;  // |t| high word >> 1
+  const bool tneg = ((uint32_t)code & 0x40000000u) != 0u;
+  if (t2 >= (kExpFastHi >> 1)) {
+    const bool sat = tneg ? (t2 >= (0x40874912u >> 1)) : (t2 >= (0x40862E44u >> 1));
+    if (!sat) return full();
+    r = tneg ? 0.0 : kInf;
+  }
+  return ((int)hx < 0) ? pow_neg_fix_d(r, y) : r;
 }
 template <int N>
 __device__ __forceinline__ float log_fast_f(float x, const double* c, const double* lt, int& code) {
