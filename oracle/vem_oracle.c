@@ -71,7 +71,6 @@ static inline float canon_f(float y) { return (y != y) ? from_bits_f(CANON_NAN_F
 
 static const double PH_D[4 * VEM_PH_D_ENTRIES] = {VEM_PH_D_INIT};
 static const uint64_t PH_DI[4 * VEM_PH_DI_ENTRIES] = {VEM_PH_DI_INIT};
-static const uint32_t PH_F[4 * VEM_PH_F_ENTRIES] = {VEM_PH_F_INIT};
 static const double LOGT_INVC[256] = {VEM_LOGT_INVC_INIT};
 static const double LOGT_HI[256] = {VEM_LOGT_HI_INIT};
 static const double LOGT_LO[256] = {VEM_LOGT_LO_INIT};
@@ -829,59 +828,45 @@ static const double C_TAN_F[] = VEM_TAN_F_ARR;
 static const double C_EXP_F[] = VEM_EXP_F_ARR;
 static const double C_EXP_F_U35[] = VEM_EXP_F_U35_ARR;
 
-/* f32 Payne-Hanek, integer form (new; the reference is double-only):
- * |x| = M*2^E, M in [2^23, 2^24); W(E) = floor((2^E*2/pi mod 4)*2^126)
- * (tools/genphtable.py).  p = M*W(E) mod 2^128 carries the quadrant in its
- * top two bits; rounding to the nearest quadrant is the +2^125 carry, and the
- * signed fraction s = p<<2 is taken in one's complement (|error| 2^-128).
- * tools/phf_margin.c proves |s| >= 2^(128-30) for every binary32 >= 1/2, so
- * the top 64 bits of |s| << clz are exact to 2^-63 relative; one RN
- * conversion and one multiply by pi/2 * 2^-(64+lz) give r.  |x| < 1/2 takes
- * r = x, q = 0 (selected, not branched: the integer work runs on a dummy M).
- * Every f32 trig lane takes this path (no selector, no divergence). */
+/* f32 Payne-Hanek in binary64 limbs (new; the reference is double-only).
+ * |x| = M*2^S, M in [2^23, 2^24); the table (tools/genphtable.py) holds
+ * V(S) = (2^S * 2/pi) mod 4 as three limbs t0 (29 bits, weights 2^1..2^-27),
+ * t1 (29 bits, ..2^-56), t2 (53 bits, ..2^-109), each divided by 2^S, so with
+ * xd = (double)x:  p0 = xd*t0 = M*a0 is exact (53 bits), n = rint(p0 + xd*t1)
+ * by the 1.5*2^52 shift (its low word carries the quadrant, two's complement
+ * for x < 0; M*a1 < 2^-3 must take part, or |f| could reach 5/8),
+ * f0 = p0 - n exact, and f = fma(xd, t2, fma(xd, t1, f0)) is the
+ * centred fraction of x*2/pi: the inner fma is exact whenever its result is
+ * below 2^-3 (the cancellation case), so f is within 2^-52 relative + 2^-85
+ * absolute (smallest |f| over all binary32: ~2^-30).  r = f * pi/2.
+ * Exponents below 2^25 use entry 0 (plain 2/pi split), so tiny x need no
+ * special case: r = x(1 + O(2^-52)).  Inf/NaN give NaN (inf - inf).  Every
+ * f32 trig lane takes this path (no selector, no divergence). */
 typedef struct { double r; int q; } redf_t;
+static const double PH_F[4 * VEM_PH_F_ENTRIES] = {VEM_PH_F_INIT};
 static redf_t ph_f(float xf) {
-  uint32_t b = bits_f(xf) & 0x7fffffffu;
-  uint32_t fe = b >> 23;
-  int small = fe < 126;
-  uint32_t idx = small ? 0 : fe - 126;
-  idx = idx > VEM_PH_F_ENTRIES - 1 ? VEM_PH_F_ENTRIES - 1 : idx;  /* inf/NaN: any entry */
-  uint32_t M = small ? 0x800000u : ((b & 0x7fffffu) | 0x800000u);
-  const uint32_t* w = PH_F + 4 * idx;
-  uint64_t t = (uint64_t)M * w[0];
-  t = (uint64_t)M * w[1] + (t >> 32);
-  uint32_t p1 = (uint32_t)t;
-  t = (uint64_t)M * w[2] + (t >> 32);
-  uint32_t p2 = (uint32_t)t;
-  uint32_t p3 = M * w[3] + (uint32_t)(t >> 32);
-  int q = (int)(((p3 + 0x20000000u) >> 30) & 3u);
-  uint32_t mask = (uint32_t)((int32_t)(p3 << 2) >> 31);
-  uint32_t u3 = p3 ^ mask, u2 = p2 ^ mask, u1 = p1 ^ mask;
-  uint32_t s3 = (u3 << 2) | (u2 >> 30);
-  int lz = s3 ? __builtin_clz(s3) : 32; /* <= 29 (phf_margin.c) */
-  int sh = lz + 2;
-  uint32_t nh = (u3 << sh) | (u2 >> (32 - sh));
-  uint32_t nl = (u2 << sh) | (u1 >> (32 - sh));
-  double d = (double)(((uint64_t)nh << 32) | nl);
-  uint32_t sgn = (mask ^ bits_f(xf)) & 0x80000000u;
-  double c = from_bits_d(((uint64_t)((0x3FF921FBu - ((uint32_t)(64 + lz) << 20)) | sgn) << 32) | 0x54442D18u);
-  double r = d * c;
-  if (bits_f(xf) >> 31) q = -q;
+  uint32_t fe = (bits_f(xf) >> 23) & 0xffu;
+  uint32_t idx = (fe > VEM_PH_F_FE0 ? fe : VEM_PH_F_FE0) - VEM_PH_F_FE0;
+  const double* t = PH_F + 4 * idx;
+  double xd = (double)xf;
+  double p0 = xd * t[0];
+  double n = fma(xd, t[1], p0) + 0x1.8p52; /* rint of the two-limb product: |f| <= 1/2 + 2^-31 */
+  double f0 = p0 - (n - 0x1.8p52);
+  double f = fma(xd, t[2], fma(xd, t[1], f0));
   redf_t o;
-  o.r = small ? (double)xf : r;
-  o.q = small ? 0 : (q & 3);
+  o.r = f * 0x1.921fb54442d18p+0;
+  o.q = (int)((uint32_t)bits_d(n) & 3u);
   return o;
 }
 
 static double sincos_core_f(double r, int cosform) {
-  /* sin: r + (r z) S(z);  cos: 1 + z (-1/2 + z C(z))  -> A + (A z) P(z) */
-  double c[5];
-  for (int i = 0; i < 4; i++) c[i] = cosform ? (i == 0 ? -0.5 : C_COS_F[i - 1]) : C_SIN_F[i];
-  c[4] = cosform ? C_COS_F[3] : 0.0;
+  /* sin: r (1 + z S(z)) (a product: -0 stays -0);  cos: 1 + z (-1/2 + z C(z)) */
   double z = r * r;
-  double P = poly(c, 5, z);
-  double A = cosform ? 1.0 : r;
-  return fma(A * z, P, A);
+  if (cosform) {
+    double c[5] = {-0.5, C_COS_F[0], C_COS_F[1], C_COS_F[2], C_COS_F[3]};
+    return fma(z, poly(c, 5, z), 1.0);
+  }
+  return r * fma(z, poly(C_SIN_F, 4, z), 1.0);
 }
 
 float vo_sin_f_u10(float x) {
@@ -1256,7 +1241,7 @@ void vo_ph_reduce_f(const float* x, double* r, int* q, size_t n) {
   }
 }
 const double* vo_ph_table_d(void) { return PH_D; }
-const uint32_t* vo_ph_table_f(void) { return PH_F; }
+const double* vo_ph_table_f(void) { return PH_F; }
 double vo_round_ta(double x) { return round_ta(x); }
 
 #define UNARY_ARR(name, T)                                             \

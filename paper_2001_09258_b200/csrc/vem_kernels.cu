@@ -38,29 +38,59 @@ static std::atomic<uint64_t> g_launches{0};
 #define VEM_ASSERT(c) ((void)0)
 #endif
 
-// kTableDG: the f64 Payne-Hanek table is read from global memory (L1-resident,
-// __ldg) rather than staged: the 32 KB stage would cost occupancy on inputs
-// that never leave the Cody-Waite range.
+// kTableDG / kTableDG35 (selector kernels): sin|cos coefficients, then the
+// integer Payne-Hanek window words w1 | w2 (kPhDIStaged doubles, 16.4 KB).
+// k_trig stages the window lazily -- the first warp of a CTA that meets a
+// Payne-Hanek element copies it (stage_ph_lazy) -- so inputs that never leave
+// the Cody-Waite range (config 1) pay nothing.
 // kTableD: the reference-algorithm PH table (reduction entry points);
-// kTableDI: the integer PH table (function kernels) + sin|cos coefficients
+// kTableDI: the integer PH window words w1 | w2 (forced-PH kernels) + sin|cos
+// coefficients
 enum TableKind { kNoTable = 0, kTableD = 1, kTableF = 2, kTableLog = 3, kTableDG = 4, kTableDG35 = 5, kTableDI = 6 };
 
 template <int TABLE>
 struct TableSize {
   static constexpr int n = TABLE == kTableD   ? 4 * VEM_PH_D_ENTRIES + kSinCosCoefN
-                           : TABLE == kTableDI ? 4 * VEM_PH_DI_ENTRIES + kSinCosCoefN
+                           : TABLE == kTableDI ? kPhDIStaged + kSinCosCoefN
                            : TABLE == kTableF ? kPhFDoubles + kSinCosCoefN
                            : TABLE == kTableLog ? kLogTabN
-                           : (TABLE == kTableDG || TABLE == kTableDG35) ? kSinCosCoefN
+                           : (TABLE == kTableDG || TABLE == kTableDG35) ? kSinCosCoefN + kPhDIStaged
                                                 : 2;
 };
 
-template <int TABLE>
+// w1 | w2 of the integer Payne-Hanek window, gPhDI records -> two arrays
+__device__ __forceinline__ void copy_ph_window(double* dst, int first, int step) {
+  unsigned long long* d = reinterpret_cast<unsigned long long*>(dst);
+  for (int i = first; i < VEM_PH_DI_ENTRIES; i += step) {
+    d[i] = __ldg(gPhDI + 4 * i + 1);
+    d[VEM_PH_DI_ENTRIES + i] = __ldg(gPhDI + 4 * i + 2);
+  }
+}
+// Lazy staging for k_trig, called by a converged warp that is about to run
+// Payne-Hanek elements.  `ready` is a CTA-shared flag (0 at kernel start).
+// Warps that find it clear copy the window themselves (concurrent copies
+// write identical values) and set it after a CTA-scope fence; a warp that
+// finds it set fences and reads.
+__device__ __forceinline__ void stage_ph_lazy(double* dst, volatile int* ready) {
+  const int lane = threadIdx.x & 31;
+  const int r = __shfl_sync(0xffffffffu, *ready, 0);
+  if (r == 0) {
+    copy_ph_window(dst, lane, 32);
+    __threadfence_block();
+    __syncwarp();
+    if (lane == 0) *ready = 1;
+  } else {
+    __threadfence_block();
+  }
+}
+
+template <int TABLE, bool LAZY_PH = false>
 __device__ __forceinline__ const double* stage_table(double* stab) {
   if constexpr (TABLE == kNoTable) {
     return nullptr;
   } else if constexpr (TABLE == kTableDG || TABLE == kTableDG35) {
     if (threadIdx.x < kSinCosCoefN) stab[threadIdx.x] = (TABLE == kTableDG ? gSinCosD : gSinCosD35)[threadIdx.x];
+    if constexpr (!LAZY_PH) copy_ph_window(stab + kSinCosCoefN, threadIdx.x, blockDim.x);
     __syncthreads();
     return stab;
   } else {
@@ -75,10 +105,17 @@ __device__ __forceinline__ const double* stage_table(double* stab) {
           stab[kSlExpHi + i] = gLogExp[kLtExpHi + i];
         }
       }
+    } else if constexpr (TABLE == kTableF) {  // replicated, skewed copies (vem_math.cuh kPhFStride*)
+      for (int i = threadIdx.x; i < 16 * VEM_PH_F_ENTRIES; i += blockDim.x) {
+        const int c = i / VEM_PH_F_ENTRIES, k = i - c * VEM_PH_F_ENTRIES;
+        if (c < 8)
+          reinterpret_cast<double2*>(stab)[c * kPhFStride01 + k] = make_double2(gPhF[4 * k], gPhF[4 * k + 1]);
+        stab[kPhFT2 + c * kPhFStride2 + k] = gPhF[4 * k + 2];
+      }
+    } else if constexpr (TABLE == kTableDI) {
+      copy_ph_window(stab, threadIdx.x, blockDim.x);
     } else {
-      const double* src = TABLE == kTableD    ? gPhD
-                          : TABLE == kTableDI ? reinterpret_cast<const double*>(gPhDI)
-                                              : reinterpret_cast<const double*>(gPhF);
+      const double* src = gPhD;
       constexpr int n2 = (TableSize<TABLE>::n - kSinCosCoefN) / 2;
       const double2* s2 = reinterpret_cast<const double2*>(src);
       double2* d2 = reinterpret_cast<double2*>(stab);
@@ -479,7 +516,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_trig(const double* __restric
     tma::fence_barrier_init();
   }
   if (tid < STAGES) rel[tid] = 0;
-  const double* tab = stage_table<TABLE>(stab);  // includes __syncthreads()
+  __shared__ int s_phready;  // the Payne-Hanek window is staged (stage_ph_lazy)
+  if (tid == 0) s_phready = 0;
+  bool have_ph = false;      // this warp has seen it staged
+  const double* tab = stage_table<TABLE, true>(stab);  // includes __syncthreads()
   tma::griddep_wait();  // inputs / outputs may belong to the previous grid
   tma::griddep_launch_dependents();
   Op op;
@@ -527,6 +567,15 @@ __global__ void __launch_bounds__(kThreads, MINB) k_trig(const double* __restric
       const uint32_t h = (uint32_t)__double2hiint(xe[e]) & 0x7fffffffu;
       mph |= (uint32_t)(h > 0x42D6BCC4u) << e;                        // |x| > 1e14 or non-finite
       mcw |= (uint32_t)(h - 0x3E400000u <= 0x42D6BCC4u - 0x3E400000u) << e;  // 2^-27 <= |x| <~ 1e14
+    }
+    if (!have_ph) {  // any element the selector may send to Payne-Hanek (boundary word included)
+      uint32_t hm = 0;
+#pragma unroll
+      for (int e = 0; e < NE; e++) hm = max(hm, (uint32_t)__double2hiint(xe[e]) & 0x7fffffffu);
+      if (__any_sync(0xffffffffu, hm >= 0x42D6BCC4u)) {
+        stage_ph_lazy(stab + kSinCosCoefN, &s_phready);
+        have_ph = true;
+      }
     }
     if (__all_sync(0xffffffffu, mph == (1u << NE) - 1u)) {
 #pragma unroll
@@ -594,9 +643,18 @@ __global__ void __launch_bounds__(kThreads, MINB) k_trig(const double* __restric
       __stcs(ov + v * kThreads + tid, make_double2(sx[(v * W) * 32 + lane], sx[(v * W + 1) * 32 + lane]));
     __syncwarp();  // the block is rewritten by the next tile
   }
-  // remainder (< one tile)
+  // remainder (< one tile): per-lane selector; a warp with a Payne-Hanek
+  // element stages the window first
   const size_t done = ntiles * TILE_E;
-  for (size_t i = done + (size_t)blockIdx.x * kThreads + tid; i < n; i += G * kThreads) out[i] = op(a[i], tab);
+  for (size_t i0 = done + (size_t)blockIdx.x * kThreads + (tid & ~31); i0 < n; i0 += G * kThreads) {
+    const size_t i = i0 + lane;
+    const double x = i < n ? a[i] : 0.0;
+    if (!have_ph && __any_sync(0xffffffffu, ((uint32_t)__double2hiint(x) & 0x7fffffffu) >= 0x42D6BCC4u)) {
+      stage_ph_lazy(stab + kSinCosCoefN, &s_phready);
+      have_ph = true;
+    }
+    if (i < n) out[i] = op(x, tab);
+  }
 }
 
 // ------------------------------------------------------- fmod: step queue
@@ -1192,20 +1250,20 @@ __device__ __forceinline__ bool trig_is_trivial(double x) {
 #define VEM_TRIG_OP(NAME, FN, ...)                                                       \
   struct NAME {                                                                          \
     __device__ __forceinline__ double operator()(double x, const double* tab) const {   \
-      return FN<kSel>(x, reinterpret_cast<const double*>(gPhDI) __VA_ARGS__);             \
+      return FN<kSel>(x, tab + kSinCosCoefN __VA_ARGS__);                                 \
     }                                                                                    \
     __device__ __forceinline__ double cw1(double x, const double* tab) const {          \
-      return FN<kCw1>(x, reinterpret_cast<const double*>(gPhDI) __VA_ARGS__);             \
+      return FN<kCw1>(x, tab + kSinCosCoefN __VA_ARGS__);                                 \
     }                                                                                    \
     __device__ __forceinline__ double ph(double x, const double* tab) const {           \
-      return FN<kPh>(x, reinterpret_cast<const double*>(gPhDI) __VA_ARGS__);              \
+      return FN<kPh>(x, tab + kSinCosCoefN __VA_ARGS__);                                  \
     }                                                                                    \
     __device__ __forceinline__ static bool is_cw1(double x) { return trig_is_cw1(x); } \
     __device__ __forceinline__ static bool is_trivial(double x) { return trig_is_trivial(x); } \
     __device__ static double trivial(double x);                                          \
     __device__ static double tiny(double x);                                             \
   };
-// selector variants: PH table from global memory (L1), coefficients staged
+// selector variants: `tab` = staged coefficients, then the PH window words
 VEM_TRIG_OP(OpSinD, sin_d_u10, , tab)
 VEM_TRIG_OP(OpCosD, cos_d_u10, , tab)
 VEM_TRIG_OP(OpTanD, tan_d_u10)
@@ -1226,8 +1284,8 @@ VEM_TRIG_TINY(OpSinDU35, x)
 VEM_TRIG_TINY(OpCosDU35, 1.0)
 VEM_TRIG_TINY(OpTanDU35, x)
 #undef VEM_TRIG_TINY
-VEM_UNARY_OP(OpSinDPh, double, (sin_d_u10<kPh>(x, tab, tab + 4 * VEM_PH_DI_ENTRIES)))
-VEM_UNARY_OP(OpCosDPh, double, (cos_d_u10<kPh>(x, tab, tab + 4 * VEM_PH_DI_ENTRIES)))
+VEM_UNARY_OP(OpSinDPh, double, (sin_d_u10<kPh>(x, tab, tab + kPhDIStaged)))
+VEM_UNARY_OP(OpCosDPh, double, (cos_d_u10<kPh>(x, tab, tab + kPhDIStaged)))
 VEM_UNARY_OP(OpTanDPh, double, (tan_d_u10<kPh>(x, tab)))
 VEM_UNARY_OP(OpAtanD, double, ((void)tab, atan_d_u10(x)))
 VEM_UNARY_OP(OpAtanDU35, double, ((void)tab, atan_d_u35(x)))
@@ -1693,6 +1751,12 @@ static int launch_tuned(const T* a, const T* b, T* o, size_t n, vem_stream_t s) 
     case 8: return launch_stream<Op, T, NIN, TAB, VPT, ST, 4>(a, b, o, n, s);
     case 9: return launch_stream<Op, T, NIN, TAB, 4, 2, 2>(a, b, o, n, s);
     case 10: return launch_stream<Op, T, NIN, TAB, 4, 2, 3>(a, b, o, n, s);
+    case 15: return launch_stream<Op, T, NIN, TAB, 2, 2, 3>(a, b, o, n, s);
+    case 16: return launch_stream<Op, T, NIN, TAB, 2, 2, 4>(a, b, o, n, s);
+    case 17: return launch_stream<Op, T, NIN, TAB, 2, 3, 4>(a, b, o, n, s);
+    case 18: return launch_stream<Op, T, NIN, TAB, 1, 2, 6>(a, b, o, n, s);
+    case 19: return launch_stream<Op, T, NIN, TAB, 1, 4, 6>(a, b, o, n, s);
+    case 20: return launch_stream<Op, T, NIN, TAB, 2, 2, 5>(a, b, o, n, s);
     default: return launch_stream<Op, T, NIN, TAB, VPT, ST, MINB, WREL>(a, b, o, n, s);
   }
 }

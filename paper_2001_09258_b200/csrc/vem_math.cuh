@@ -126,8 +126,20 @@ __constant__ double cAsinDU35[] = VEM_ASIN_D_U35_ARR;
 __device__ const double gPhD[4 * VEM_PH_D_ENTRIES] = {VEM_PH_D_INIT};
 // integer Payne-Hanek table (ph_int): [w0, w1, w2, 0] per exponent
 __device__ const unsigned long long gPhDI[4 * VEM_PH_DI_ENTRIES] = {VEM_PH_DI_INIT};
-__device__ __align__(16) const uint32_t gPhF[4 * VEM_PH_F_ENTRIES] = {VEM_PH_F_INIT};
-constexpr int kPhFDoubles = 2 * VEM_PH_F_ENTRIES;  // staged size of gPhF in doubles
+constexpr int kPhDIStaged = 2 * VEM_PH_DI_ENTRIES;  // staged w1 | w2 arrays (doubles; even: 16-byte aligned tail)
+__device__ __align__(16) const double gPhF[4 * VEM_PH_F_ENTRIES] = {VEM_PH_F_INIT};
+// Staged layout of the binary32 Payne-Hanek table: every lane of a warp reads
+// a different entry (the exponents are random), so a plain table costs ~11
+// bank-conflict wavefronts per load.  The staged copy is replicated once per
+// bank group with a one-group skew between copies -- {t0, t1} as 16-byte
+// records in 8 copies (stride 105 records = 1 mod 8), t2 as doubles in 16
+// copies (stride 113 = 1 mod 16) -- and lane L reads copy (L - entry) mod 8
+// (mod 16), so its bank group is L mod 8 (mod 16): conflict-free, 4 + 2
+// wavefronts, the minimum for 24 bytes per lane.
+constexpr int kPhFStride01 = VEM_PH_F_ENTRIES + 1, kPhFStride2 = VEM_PH_F_ENTRIES + 9;
+static_assert(kPhFStride01 % 8 == 1 && kPhFStride2 % 16 == 1, "skew of one bank group per copy");
+constexpr int kPhFT2 = 2 * 8 * kPhFStride01;                 // offset of the t2 copies (doubles)
+constexpr int kPhFDoubles = kPhFT2 + 16 * kPhFStride2;       // staged size in doubles
 // log / exp tables (tools/genlogtables.py).  Global copy: structure of
 // arrays (offsets in doubles below).  Staged shared-memory block: dense
 // 16-byte pairs where a lookup needs two values (one LDS.128, no stride
@@ -348,8 +360,9 @@ __device__ __forceinline__ red ph(double x_in, const double* __restrict__ tab) {
 // in double-double with the sign of x folded into the constant.  The
 // cascaded double-double form of reduction.hpp:89-137 takes ~90 FP64
 // instructions per element; this takes ~30 and a few integer ones.
-// `tab` = gPhDI (staged or global), read as 2 x 16 bytes per element.
-__device__ __noinline__ red ph_int192(double x, const double* __restrict__ tab) {
+// Reads the full window (w0, w1, w2) from the global table gPhDI (rare path).
+__device__ __noinline__ red ph_int192(double x) {
+  const double* __restrict__ tab = reinterpret_cast<const double*>(gPhDI);
   const uint64_t b = bits_d(x), ab = b & 0x7fffffffffffffffull;
   const int ue = (int)(ab >> 52) - 1023;
   const bool small = ue < VEM_PH_DI_UEMIN;
@@ -409,14 +422,19 @@ __device__ __noinline__ red ph_int192(double x, const double* __restrict__ tab) 
 // centred in integer arithmetic, 53, 20) summed with one Fast2Sum, times
 // pi/2 in double-double.  Within 2^-62 relative whenever |F| >= 2^-11
 // quadrants; below that (~2^-10 of random arguments) ph_int192 recomputes.
+// `tab`: the staged copy of the window's top two words as two arrays, w1 at
+// [0, ENTRIES) and w2 at [ENTRIES, 2 ENTRIES) (kPhDIStaged doubles).  The
+// lanes of a warp read random entries: 8-byte words at an 8-byte stride spread
+// over all 16 bank pairs (~5 wavefronts per load), where the 32-byte records
+// of gPhDI use 4 of them (~11).
 __device__ __forceinline__ red ph_int(double x, const double* __restrict__ tab) {
   const uint64_t b = bits_d(x), ab = b & 0x7fffffffffffffffull;
   const int ue = (int)(ab >> 52) - 1023;
   int idx = ue - VEM_PH_DI_UEMIN;
   idx = idx < 0 ? 0 : (idx > VEM_PH_DI_ENTRIES - 1 ? VEM_PH_DI_ENTRIES - 1 : idx);
   const uint64_t M = (ab & 0x000fffffffffffffull) | 0x0010000000000000ull;
-  const ulonglong2* wt = reinterpret_cast<const ulonglong2*>(tab) + 2 * idx;
-  const uint64_t w1 = wt[0].y, w2 = wt[1].x;
+  const uint64_t* wt = reinterpret_cast<const uint64_t*>(tab) + idx;
+  const uint64_t w1 = wt[0], w2 = wt[VEM_PH_DI_ENTRIES];
   const uint64_t T0 = M * w1;
   const uint64_t T1 = M * w2 + __umul64hi(M, w1);
   const uint32_t t3 = (uint32_t)(T1 >> 32), t2 = (uint32_t)T1, t1 = (uint32_t)(T0 >> 32), t0 = (uint32_t)T0;
@@ -437,7 +455,7 @@ __device__ __forceinline__ red ph_int(double x, const double* __restrict__ tab) 
   // |x| < 1/2 returns (x, 0, 0) below; non-finite x leaves a meaningless r
   // (the functions select the canonical NaN from x itself)
   const bool small = ue < VEM_PH_DI_UEMIN;
-  if (!small && ab < 0x7ff0000000000000ull && fabs(fh) < 0x1p42) return ph_int192(x, tab);
+  if (!small && ab < 0x7ff0000000000000ull && fabs(fh) < 0x1p42) return ph_int192(x);
   // r = F (pi/2) sign(x) with pi/2 * 2^-53 = C0 + C1 (units of 2^-53 above)
   const int sx = (int)(uint32_t)(b >> 32) & (int)0x80000000u;
   constexpr double kC0 = kPio2Qd0 * 0x1p-53, kC1 = kPio2Qd1 * 0x1p-53;
@@ -919,66 +937,44 @@ __device__ __forceinline__ double fmod_d(double x, double y) { return fmod_core(
 // ===================================== f32 functions (binary64 internals)
 struct redf { double r; int q; };
 
-// Final selects of the odd f32 trig functions, on the input's bits (same
-// outputs as the oracle's x == 0 / isinf / isnan chain): +-0 -> x,
-// inf/NaN -> canonical NaN, otherwise the finite result o.
-__device__ __forceinline__ float fin_f_odd(float x, float o) {
-  const uint32_t b = bits_f(x) & 0x7fffffffu;
-  o = b == 0u ? x : o;
-  return b >= 0x7f800000u ? from_bits_f(kCanonNanF) : o;
-}
+// NaN results (inf / NaN arguments: the reduction's inf - inf) -> canonical NaN
+__device__ __forceinline__ float fin_f_nan(float o) { return o != o ? from_bits_f(kCanonNanF) : o; }
 
-// oracle/vem_oracle.c ph_f: integer Payne-Hanek for binary32.  p = M*W(E)
-// mod 2^128 by three IMAD.WIDE.U32 (64-bit addend = carry chain) and one
-// IMAD; quadrant = top two bits after the +2^125 rounding carry; fraction
-// = one's-complement |p<<2|, normalised by clz (<= 29, tools/phf_margin.c),
-// top 64 bits -> one RN conversion -> one multiply by +-pi/2*2^-(64+lz).
-// FP64 work: I2F + DMUL (the binary64 formulation needed ~22 FP64 ops).
+// oracle/vem_oracle.c ph_f: binary32 Payne-Hanek in three binary64 limbs.
+// The table entry for the biased exponent (clamped below at 2^25, where no
+// bits above the quadrant need dropping) holds (2^S 2/pi mod 4) / 2^S as t0
+// (29 bits), t1 (29 bits), t2 (53 bits): xd*t0 is exact, n = rint(xd*t0 +
+// xd*t1) by the 1.5*2^52 shift carries the quadrant in its low word (two's
+// complement for x < 0), f0 = xd*t0 - n is exact and two FMAs add the lower
+// limbs (the inner one exact in the cancellation case).  8 FP64 instructions, one
+// conversion, no integer multiply, no sign / small-argument special cases
+// (tiny x: r = x(1 + O(2^-52)); +-0 stays +-0; inf/NaN -> NaN).
 __device__ __forceinline__ redf ph_f(float xf, const double* __restrict__ tab) {
-  const uint32_t xb = bits_f(xf);
-  const uint32_t b = xb & 0x7fffffffu;
-  const uint32_t fe = b >> 23;
-  const bool small = fe < 126;
-  uint32_t idx = small ? 0u : fe - 126u;
-  idx = idx > VEM_PH_F_ENTRIES - 1 ? VEM_PH_F_ENTRIES - 1 : idx;
-  const uint32_t M = small ? 0x800000u : ((b & 0x7fffffu) | 0x800000u);
-  const uint4 w = reinterpret_cast<const uint4*>(tab)[idx];
-  uint64_t t = (uint64_t)M * w.x;
-  t = (uint64_t)M * w.y + (t >> 32);
-  const uint32_t p1 = (uint32_t)t;
-  t = (uint64_t)M * w.z + (t >> 32);
-  const uint32_t p2 = (uint32_t)t;
-  const uint32_t p3 = M * w.w + (uint32_t)(t >> 32);
-  int q = (int)(((p3 + 0x20000000u) >> 30) & 3u);
-  const uint32_t mask = (uint32_t)((int32_t)(p3 << 2) >> 31);
-  const uint32_t u3 = p3 ^ mask, u2 = p2 ^ mask, u1 = p1 ^ mask;
-  const uint32_t s3 = __funnelshift_l(u2, u3, 2);
-  const int lz = __clz(s3);
-  const int sh = lz + 2;
-  const uint32_t nh = __funnelshift_l(u2, u3, sh);
-  const uint32_t nl = __funnelshift_l(u1, u2, sh);
-  const double d = __ull2double_rn(((uint64_t)nh << 32) | nl);
-  const uint32_t sgn = (mask ^ xb) & 0x80000000u;
-  const double c = __hiloint2double((int)((0x3FF921FBu - ((uint32_t)(64 + lz) << 20)) | sgn), 0x54442D18);
-  const double r = d * c;
-  if (xb >> 31) q = -q;
+  const uint32_t fe = (bits_f(xf) >> 23) & 0xffu;
+  const uint32_t idx = (fe > VEM_PH_F_FE0 ? fe : VEM_PH_F_FE0) - VEM_PH_F_FE0;
+  const uint32_t sk = threadIdx.x - idx;  // copy = (lane - entry) mod 8 / 16 (kPhFStride*: conflict-free)
+  const double2 t01 = reinterpret_cast<const double2*>(tab)[(sk & 7u) * kPhFStride01 + idx];
+  const double t2 = tab[kPhFT2 + (sk & 15u) * kPhFStride2 + idx];
+  const double xd = (double)xf;
+  const double p0 = xd * t01.x;
+  const double n = fma(xd, t01.y, p0) + 0x1.8p52;  // rint of the two-limb product: |f| <= 1/2 + 2^-31
+  const double f0 = p0 - (n - 0x1.8p52);
+  const double f = fma(xd, t2, fma(xd, t01.y, f0));
   redf o;
-  o.r = small ? (double)xf : r;
-  o.q = small ? 0 : (q & 3);
+  o.r = f * 0x1.921fb54442d18p+0;
+  o.q = __double2loint(n) & 3;
   return o;
 }
 
 // oracle: sincos_core_f.  Both forms from constant-bank coefficients and a
-// per-lane select of the result: the FP64 pipe has room in these
-// integer-reduction kernels, the shared-memory pipe does not.  Same values
-// as the selected 5-term Horner (the sin set's leading 0 is exact:
-// fma(0, z, c3) == c3; the cos form's A*z is 1.0*z == z).
+// per-lane select of the result (cheaper than selecting five coefficients).
+// sin as a product r (1 + z S(z)): -0 stays -0 without a select.
 __device__ __forceinline__ double sincos_core_f(double r, int cosform, const double* tab) {
   (void)tab;
   const double z = r * r;
   const double Ps = fma(fma(fma(cSinF[3], z, cSinF[2]), z, cSinF[1]), z, cSinF[0]);
   const double Pc = fma(fma(fma(fma(cCosF[3], z, cCosF[2]), z, cCosF[1]), z, cCosF[0]), z, -0.5);
-  const double ys = fma(r * z, Ps, r);
+  const double ys = r * fma(z, Ps, 1.0);
   const double yc = fma(z, Pc, 1.0);
   return cosform != 0 ? yc : ys;
 }
@@ -987,13 +983,13 @@ __device__ __forceinline__ float sin_f_u10(float x, const double* tab) {
   redf r = ph_f(x, tab);
   double y = sincos_core_f(r.r, r.q & 1, tab);
   y = neg_if(y, r.q & 2);
-  return fin_f_odd(x, (float)y);
+  return fin_f_nan((float)y);
 }
 __device__ __forceinline__ float cos_f_u10(float x, const double* tab) {
   redf r = ph_f(x, tab);
   double y = sincos_core_f(r.r, (r.q & 1) ^ 1, tab);
   y = neg_if(y, (r.q + 1) & 2);
-  return (bits_f(x) & 0x7fffffffu) >= 0x7f800000u ? from_bits_f(kCanonNanF) : (float)y;
+  return fin_f_nan((float)y);
 }
 __device__ __forceinline__ float tan_f_u10(float x, const double* tab) {
   redf r = ph_f(x, tab);
@@ -1001,7 +997,7 @@ __device__ __forceinline__ float tan_f_u10(float x, const double* tab) {
   double P = poly<VEM_TAN_F_N>(cTanF, z);
   double t = fma(r.r * z, P, r.r);
   double y = (r.q & 1) ? -__drcp_rn(t) : t;
-  return fin_f_odd(x, (float)y);
+  return fin_f_nan((float)y);
 }
 
 template <int N>

@@ -132,8 +132,8 @@ def reduce_ref(variant: str, kind: str, x: np.ndarray, level: int = 1, table: by
 def ph_table_bytes(prec: str = "d") -> bytes:
     L = oracle()
     f = L.vo_ph_table_d if prec == "d" else L.vo_ph_table_f
-    f.restype = ctypes.POINTER(ctypes.c_double if prec == "d" else ctypes.c_uint32)
-    n = 4096 if prec == "d" else 4 * 129
+    f.restype = ctypes.POINTER(ctypes.c_double)
+    n = 4096 if prec == "d" else 4 * 104
     p = f()
     return np.ctypeslib.as_array(p, shape=(n,)).copy().tobytes()
 

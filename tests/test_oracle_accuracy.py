@@ -292,23 +292,72 @@ def test_special_grid_runs_everywhere():
         assert out.shape == sp.shape
 
 
-def test_f32_integer_payne_hanek_margin(tmp_path):
-    """The binary32 integer Payne-Hanek (oracle ph_f, kernels ph_f) needs the
-    rounded fraction of M*W(E) to keep its leading one in the top 32-bit word
-    for EVERY binary32 >= 1/2; tools/phf_margin.c checks all 2^23 x 129
-    (mantissa, exponent) pairs exhaustively (~3 s)."""
-    import subprocess
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    exe = str(tmp_path / "phf_margin")
-    subprocess.run(["/usr/bin/gcc", "-O2", "-I", os.path.join(root, "paper_2001_09258_b200", "csrc"),
-                    os.path.join(root, "tools", "phf_margin.c"), "-o", exe], check=True)
-    out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
-    assert out.returncode == 0, out.stdout
-    assert "worst 29" in out.stdout
+def test_f32_payne_hanek_vs_mpmath():
+    """The binary32 three-limb Payne-Hanek (oracle ph_f == kernels ph_f)
+    against a 400-bit mpmath reduction: for every biased exponent, the
+    mantissas whose x*2/pi comes closest to an integer (continued-fraction
+    convergents of 2^S 2/pi, the worst cases for cancellation) plus random
+    mantissas: same quadrant (or the neighbouring one with |f| within 2^-30 of
+    1/2), |f| <= 1/2 + 2^-30, r within 2^-50 relative."""
+    import ctypes
+    import mpmath as mp
+    from fractions import Fraction
+    from oracle_lib import oracle
+    L = oracle()
+    rng = np.random.default_rng(5)
+    xs = []
+    with mp.workprec(500):
+        two_over_pi = 2 / mp.pi
+        for fe in range(100, 255):
+            S = fe - 150
+            v = two_over_pi * mp.mpf(2) ** S
+            frac = v - mp.floor(v)
+            fr = Fraction(int(mp.floor(frac * mp.mpf(2) ** 300)), 1 << 300)
+            # convergents p/q of frac(v) with q < 2^24: M = q (scaled into [2^23, 2^24) when possible)
+            h0, h1, k0, k1 = 0, 1, 1, 0
+            t = fr
+            for _ in range(40):
+                a = t.numerator // t.denominator
+                h0, h1 = h1, a * h1 + h0
+                k0, k1 = k1, a * k1 + k0
+                if k1 >= (1 << 24):
+                    break
+                for mult in (1, 2, 3):  # k1 * 2^S, renormalised by the conversion
+                    if k1 * mult < (1 << 24):
+                        xs.append(np.ldexp(np.float32(k1 * mult), S).astype(np.float32))
+                t = t - a
+                if t == 0:
+                    break
+                t = 1 / t
+            for M in rng.integers(1 << 23, 1 << 24, 40):
+                xs.append(np.ldexp(np.float32(M), S).astype(np.float32))
+    x = np.array([v for v in xs if np.isfinite(v) and v != 0], dtype=np.float32)
+    assert x.size > 8000
+    x = np.concatenate([x, -x[::7]])
+    r = np.zeros(x.size); q = np.zeros(x.size, np.int32)
+    P = ctypes.c_void_p
+    L.vo_ph_reduce_f.argtypes = [P, P, P, ctypes.c_size_t]
+    L.vo_ph_reduce_f(x.ctypes.data, r.ctypes.data, q.ctypes.data, x.size)
+    worst = 0.0
+    with mp.workprec(500):
+        for xi, ri, qi in zip(x.tolist(), r.tolist(), q.tolist()):
+            v = mp.mpf(xi) * 2 / mp.pi
+            n = mp.nint(v)
+            f = v - n
+            if (int(n) - qi) % 4 != 0:  # only legitimate next to |f| = 1/2
+                assert abs(abs(f) - mp.mpf(0.5)) < mp.mpf(2) ** -30, (xi, qi, int(n) % 4)
+                n = n + (1 if f > 0 else -1)
+                f = v - n
+                assert (int(n) - qi) % 4 == 0
+            assert abs(f) <= mp.mpf(0.5) + mp.mpf(2) ** -30
+            rt = f * mp.pi / 2
+            worst = max(worst, float(abs((mp.mpf(ri) - rt) / rt)))
+    assert worst < 2.0 ** -50, np.log2(worst)
+    assert min(abs(v) for v in r.tolist()) < 2.0 ** -28  # the near-integer cases were exercised
 
 
 def test_f32_reduction_accuracy_vs_f64_payne_hanek():
-    """r and q from the integer binary32 reduction against the double-double
+    """r and q from the binary32 reduction against the double-double
     result of the repaired reference Payne-Hanek (reduction.hpp:89-137, far
     more accurate than binary64) on the same inputs: same quadrant, r within
     2^-51 relative."""

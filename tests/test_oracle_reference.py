@@ -98,7 +98,7 @@ def test_reference_table_digests():
 def test_our_table_digests_pinned():
     d = _digests()
     assert hashlib.md5(ph_table_bytes("d")).hexdigest() == d["f64_mod4"]
-    assert hashlib.md5(ph_table_bytes("f")).hexdigest() == d["f32_int"]
+    assert hashlib.md5(ph_table_bytes("f")).hexdigest() == d["f32_fp"]
     assert len(ph_table_bytes("d")) == 32768  # SPEC.md:227 "32K bytes"
 
 

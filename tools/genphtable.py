@@ -17,13 +17,14 @@ Also emitted, for parity with the reference generator (after the one-line
 off-by-one fix), the frac-only variant whose md5 the survey pinned
 (515acbe7c5e28c4087b63b4696a730da).
 
-The f32 table (new; the reference is double-only) is a fixed-point
-one for an integer Payne-Hanek: 129 entries for E in [-24, 104] (|x| = M*2^E,
-M in [2^23, 2^24)), each W(E) = floor((2^E * 2/pi mod 4) * 2^126) as four
-little-endian 32-bit words (2064 bytes).  M*W(E) mod 2^128 then holds the
-quadrant in its top two bits and the fraction below; `tools/phf_margin.c`
-shows (exhaustively over every M and E) that the rounded fraction is never
-below 2^-30, so 126 fraction bits leave >= 70 bits of relative precision.
+The f32 table (new; the reference is double-only) serves a
+three-limb binary64 Payne-Hanek: 104 entries for the biased exponents 152..255
+(|x| = M*2^S, M in [2^23, 2^24), S = fe - 150; smaller exponents use entry 0),
+each (2^S * 2/pi mod 4) cut into a 29-bit limb (weights 2^1..2^-27: M times it
+is exact in binary64), a second 29-bit limb and a 53-bit tail, stored divided
+by 2^S as three doubles plus a zero pad (3328 bytes).  The dropped bits lie
+below 2^-109: an absolute error < 2^-85 quadrants, against a smallest reduced
+argument of ~2^-30 over all binary32 inputs (tests/test_oracle_accuracy.py).
 
 The f64 integer table (new, for the kernels' own binary64 Payne-Hanek; the
 reference-algorithm table above stays the parity anchor of vem_ph_reduce_d):
@@ -37,6 +38,7 @@ first 2560 fractional bits agree with them).
 from __future__ import annotations
 
 import hashlib
+import math
 import os
 import struct
 import sys
@@ -113,19 +115,30 @@ def table_f64_frac():
     return out
 
 
-PH_F_ENTRIES = 129
-PH_F_EMIN = -24
+PH_F_ENTRIES = 104
+PH_F_FE0 = 152  # biased exponents <= 152 share entry 0 (no bits above 2^1 to drop)
+PH_F_K = 109    # lowest kept weight 2^-109
 
 
-def table_f32_words():
-    """[w0, w1, w2, w3] per entry: floor((2^E*2/pi mod 4) * 2^126), LE words."""
+def table_f32_fp():
+    """[t0, t1, t2, 0] per entry (doubles).  |x| = M * 2^S, M in [2^23, 2^24), S
+    = fe - 150 for the biased exponent fe (entry fe - 152, fe clamped to >= 152;
+    for S < 2 the S = 2 entry applies unchanged, its limbs being relative to x).
+    V = (2^S * 2/pi) mod 4 cut at weights 2^1..2^-27 (29 bits: M * a0 is exact in
+    binary64), 2^-28..2^-56 (29 bits) and 2^-57..2^-109 (53 bits); each limb is
+    stored divided by 2^S, so that x * t_k == M * a_k with the binary32 x
+    converted to binary64."""
     out = []
+    K = PH_F_K
     for i in range(PH_F_ENTRIES):
-        E = i + PH_F_EMIN
-        sh = NBITS - E - 126  # TOP * 2^(E+126-NBITS)
-        v = (TOP >> sh) if sh >= 0 else (TOP << -sh)
-        v &= (1 << 128) - 1  # mod 4 at scale 2^126
-        out.extend((v >> (32 * k)) & 0xFFFFFFFF for k in range(4))
+        S = i + PH_F_FE0 - 150
+        v = TOP >> (NBITS - S - K)  # floor(2^S * 2/pi * 2^K)
+        v &= (1 << (K + 2)) - 1     # mod 4
+        a0 = v >> (K - 27)
+        a1 = (v >> (K - 56)) & ((1 << 29) - 1)
+        a2 = v & ((1 << (K - 56)) - 1)
+        assert a0 < (1 << 29) and a2 < (1 << 53)
+        out.extend([math.ldexp(a0, -27 - S), math.ldexp(a1, -56 - S), math.ldexp(a2, -K - S), 0.0])
     return out
 
 
@@ -165,21 +178,21 @@ def md5(limbs):
 
 
 def emit_header(path, t64, t32, tdi):
-    m32 = hashlib.md5(serialize_words(t32)).hexdigest()
+    m32 = md5(t32)
     mdi = hashlib.md5(serialize_u64(tdi)).hexdigest()
     lines = [
         "/* GENERATED by tools/genphtable.py -- do not edit.",
         " * Repaired Payne-Hanek tables (centred 2^E*2/pi mod 4, cascaded nearest",
         " * doubles); layout follows ph_table.hpp:8-15 (entry E+52, 4 limbs).",
         f" * md5(f64 table, 32768 B LE) = {md5(t64)}",
-        f" * md5(f32 table,  2064 B LE) = {m32}",
+        f" * md5(f32 table,  {8 * len(t32)} B LE) = {m32}",
         f" * md5(f64 integer table, {8 * len(tdi)} B LE) = {mdi} */",
         "#ifndef VEM_PH_TABLES_H",
         "#define VEM_PH_TABLES_H",
         "#define VEM_PH_D_ENTRIES 1024",
         "#define VEM_PH_D_EXPBIAS 52",
         f"#define VEM_PH_F_ENTRIES {PH_F_ENTRIES}",
-        f"#define VEM_PH_F_EMIN ({PH_F_EMIN})",
+        f"#define VEM_PH_F_FE0 {PH_F_FE0}",
         f'#define VEM_PH_D_MD5 "{md5(t64)}"',
         f'#define VEM_PH_F_MD5 "{m32}"',
         f"#define VEM_PH_DI_ENTRIES {PH_DI_ENTRIES}",
@@ -193,7 +206,7 @@ def emit_header(path, t64, t32, tdi):
     lines.append("")
     lines.append("#define VEM_PH_F_INIT \\")
     for i in range(0, len(t32), 4):
-        row = ", ".join(f"0x{w:08x}u" for w in t32[i:i + 4])
+        row = ", ".join(x.hex() for x in t32[i:i + 4])
         lines.append(f"  {row}, \\")
     lines.append("")
     lines.append("#define VEM_PH_DI_INIT \\")
@@ -208,19 +221,19 @@ def emit_header(path, t64, t32, tdi):
 
 def main():
     t64 = table_f64_mod4()
-    t32 = table_f32_words()
+    t32 = table_f32_fp()
     tdi = table_f64_int()
     tfr = table_f64_frac()
     print("f64 mod4 md5", md5(t64))
     print("f64 frac md5", md5(tfr))
-    m32 = hashlib.md5(serialize_words(t32)).hexdigest()
-    print("f32 int md5", m32)
+    m32 = md5(t32)
+    print("f32 fp md5", m32)
     mdi = hashlib.md5(serialize_u64(tdi)).hexdigest()
     print("f64 int md5", mdi)
     emit_header(os.path.join(ROOT, "paper_2001_09258_b200", "csrc", "vem_ph_tables.h"), t64, t32, tdi)
     os.makedirs(os.path.join(ROOT, "tests", "golden"), exist_ok=True)
     with open(os.path.join(ROOT, "tests", "golden", "ph_table_digests.txt"), "w") as f:
-        f.write(f"f64_mod4 {md5(t64)}\nf64_frac {md5(tfr)}\nf32_int {m32}\nf64_int {mdi}\n")
+        f.write(f"f64_mod4 {md5(t64)}\nf64_frac {md5(tfr)}\nf32_fp {m32}\nf64_int {mdi}\n")
 
 
 if __name__ == "__main__":

@@ -8,7 +8,7 @@ paper_2001_09258_b200/_tune/libvem_tune.so, then times every entry point
  6/7/8 = the shipped shape with __launch_bounds__ min-blocks 2/3/4, 9/10 = (4,2) with
  min-blocks 2/3, 11 = the shipped shape with the other stage-release scheme
  (per-warp vs CTA barrier), 12/13 = one more stage (same / other release),
- 14 = two more stages.  VEM_TUNE_VARIANTS=-1,11,... picks the variants.
+ 14 = two more stages, 15-20 = (VPT,STAGES,min-blocks) (2,2,3) (2,2,4) (2,3,4) (1,2,6) (1,4,6) (2,2,5).  VEM_TUNE_VARIANTS=-1,11,... picks the variants.
 fmod: -1 shipped step-queue kernel; 0-4 warp-private queue (VPT,STAGES[,MINB]) (2,2) (4,2) (2,3) (4,2,2) (2,2,3);
 5-6 CTA queue (VPT,STAGES,ROWS) (2,2,2) (4,2,1); 7 = the streaming kernel with
 warp step-class regrouping (2,2); 8 = the work-ring kernel; 9/10 = the
