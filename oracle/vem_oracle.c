@@ -383,19 +383,17 @@ static red_t ph_int(double x) {
   const unsigned __int128 u = (unsigned __int128)M * w[1];
   const uint64_t T0 = (uint64_t)u;
   const uint64_t T1 = M * w[2] + (uint64_t)(u >> 64);
-  const uint32_t t3 = (uint32_t)(T1 >> 32), t2 = (uint32_t)T1, t1 = (uint32_t)(T0 >> 32), t0 = (uint32_t)T0;
+  const uint32_t t3 = (uint32_t)(T1 >> 32), t2 = (uint32_t)T1, t1 = (uint32_t)(T0 >> 32);
   int q = (int)((t3 + 0x20000000u) >> 30);
   const uint32_t f = t3 & 0x3fffffffu;
+  /* fraction bits below 2^-73 are noise (the dropped M*w0 term): two chunks,
+   * 53 bits centred + the next 32 (weights down to 2^-85), units of 2^-53 */
   const int64_t c0 = (int64_t)(((uint64_t)f << 23) | (t2 >> 9)) - ((f >> 29) ? (1ll << 53) : 0);
-  const uint64_t c1 = ((uint64_t)(t2 & 0x1ffu) << 44) | ((uint64_t)t1 << 12) | (t0 >> 20);
-  const uint32_t c2 = t0 & 0xfffffu;
-  /* units of 2^-53 quadrants */
+  const uint32_t c1 = (t2 << 23) | (t1 >> 9);
   const double S0 = (double)c0;
-  const double tb = (double)c1 * 0x1p-53;
-  const double S1 = S0 + tb;
-  const double e = (tb - (S1 - S0)) + (double)c2 * 0x1p-73;
-  const double fh = S1 + e;
-  const double fl = e - (fh - S1);
+  const double tb = (double)c1 * 0x1p-32;
+  const double fh = S0 + tb;           /* |S0| is 0 or >= 1 > tb: Fast2Sum, exact pair */
+  const double fl = tb - (fh - S0);
   if (fabs(fh) < 0x1p42) return ph_int192(x);
   const double c0p = (b >> 63) ? -K_PIO2_QD0 * 0x1p-53 : K_PIO2_QD0 * 0x1p-53;
   const double c1p = (b >> 63) ? -K_PIO2_QD1 * 0x1p-53 : K_PIO2_QD1 * 0x1p-53;
@@ -889,7 +887,17 @@ float vo_tan_f_u10(float x) {
   double z = r.r * r.r;
   double P = poly(C_TAN_F, VEM_TAN_F_N, z);
   double t = fma(r.r * z, P, r.r);
-  double y = (r.q & 1) ? -1.0 / t : t;
+  /* -cot, branch-free: 1/|t| from a binary32 magic-constant seed (rel. error
+   * <= 0.051), three binary32 Newton steps (<= 2^-23.9 measured bound 6e-8) and
+   * one binary64 Newton step (<= 2^-47): far below the final binary32
+   * rounding.  |t| >= 2^-31 for an odd quadrant: every binary32 value normal. */
+  double ta = fabs(t);
+  float tf = (float)ta;
+  float yf = from_bits_f(0x7EF311C7u - bits_f(tf));
+  for (int i = 0; i < 3; i++) yf = fmaf(yf, fmaf(-tf, yf, 1.0f), yf);
+  double y0 = (double)yf;
+  double y1 = fma(y0, fma(-ta, y0, 1.0), y0);
+  double y = (r.q & 1) ? (t < 0.0 ? y1 : -y1) : t;
   float o = (float)y;
   o = (x == 0.0f) ? x : o;
   return canon_f(isinf(x) ? (float)NAN : (x != x ? x : o));

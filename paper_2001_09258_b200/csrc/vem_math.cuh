@@ -418,9 +418,9 @@ __device__ __noinline__ red ph_int192(double x) {
 // Two-level integer Payne-Hanek (oracle: ph_int, same operations in the same
 // order).  Fast level: M * (top 128 bits of the window) mod 2^128 (one
 // 64 x 64 -> 128 product and one low product), the quadrant from the top two
-// bits, the 126 fraction bits as three exactly convertible chunks (53 bits
-// centred in integer arithmetic, 53, 20) summed with one Fast2Sum, times
-// pi/2 in double-double.  Within 2^-62 relative whenever |F| >= 2^-11
+// bits, the top 85 fraction bits (the rest is below the dropped M*w0 term) as
+// two exactly convertible chunks (53 bits centred in integer arithmetic, 32)
+// summed with one Fast2Sum, times pi/2 in double-double.  Within 2^-62 relative whenever |F| >= 2^-11
 // quadrants; below that (~2^-10 of random arguments) ph_int192 recomputes.
 // `tab`: the staged copy of the window's top two words as two arrays, w1 at
 // [0, ENTRIES) and w2 at [ENTRIES, 2 ENTRIES) (kPhDIStaged doubles).  The
@@ -430,32 +430,33 @@ __device__ __noinline__ red ph_int192(double x) {
 __device__ __forceinline__ red ph_int(double x, const double* __restrict__ tab) {
   const uint64_t b = bits_d(x), ab = b & 0x7fffffffffffffffull;
   const int ue = (int)(ab >> 52) - 1023;
-  int idx = ue - VEM_PH_DI_UEMIN;
-  idx = idx < 0 ? 0 : (idx > VEM_PH_DI_ENTRIES - 1 ? VEM_PH_DI_ENTRIES - 1 : idx);
+  // one unsigned clamp: |x| < 1/2 (negative index) and inf/NaN read the last
+  // entry and leave through the rare path / the functions' NaN select
+  uint32_t idx = (uint32_t)(ue - VEM_PH_DI_UEMIN);
+  idx = idx > VEM_PH_DI_ENTRIES - 1 ? VEM_PH_DI_ENTRIES - 1 : idx;
   const uint64_t M = (ab & 0x000fffffffffffffull) | 0x0010000000000000ull;
   const uint64_t* wt = reinterpret_cast<const uint64_t*>(tab) + idx;
   const uint64_t w1 = wt[0], w2 = wt[VEM_PH_DI_ENTRIES];
   const uint64_t T0 = M * w1;
   const uint64_t T1 = M * w2 + __umul64hi(M, w1);
-  const uint32_t t3 = (uint32_t)(T1 >> 32), t2 = (uint32_t)T1, t1 = (uint32_t)(T0 >> 32), t0 = (uint32_t)T0;
+  const uint32_t t3 = (uint32_t)(T1 >> 32), t2 = (uint32_t)T1, t1 = (uint32_t)(T0 >> 32);
   int q = (int)((t3 + 0x20000000u) >> 30);
   const uint32_t f = t3 & 0x3fffffffu;
-  // c0 = f : t2[31..9] (53 bits) minus 2^53 when the fraction is >= 1/2
+  // fraction bits below 2^-73 are noise (the dropped M*w0 term): two chunks,
+  // c0 = f : t2[31..9] (53 bits) minus 2^53 when the fraction is >= 1/2, and
+  // c1 = t2[8..0] : t1[31..9] (32 bits, weights down to 2^-85); units of 2^-53
   const int c0hi = (int)((f >> 9) - ((f >> 29) << 21));
   const uint32_t c0lo = (f << 23) | (t2 >> 9);
   const double S0 = (double)(long long)(((uint64_t)(uint32_t)c0hi << 32) | c0lo);
-  // c1 = t2[8..0] : t1 : t0[31..20] (53 bits), c2 = t0[19..0]
-  const uint32_t c1hi = ((t2 & 0x1ffu) << 12) | (t1 >> 20);
-  const uint32_t c1lo = (t1 << 12) | (t0 >> 20);
-  const double tb = (double)(((uint64_t)c1hi << 32) | c1lo) * 0x1p-53;
-  const double S1 = S0 + tb;
-  const double e = (tb - (S1 - S0)) + (double)(t0 & 0xfffffu) * 0x1p-73;
-  const double fh = S1 + e;
-  const double fl = e - (fh - S1);
-  // |x| < 1/2 returns (x, 0, 0) below; non-finite x leaves a meaningless r
-  // (the functions select the canonical NaN from x itself)
-  const bool small = ue < VEM_PH_DI_UEMIN;
-  if (!small && ab < 0x7ff0000000000000ull && fabs(fh) < 0x1p42) return ph_int192(x);
+  const double tb = (double)__funnelshift_l(t1, t2, 23) * 0x1p-32;
+  const double fh = S0 + tb;  // |S0| is 0 or >= 1 > tb: Fast2Sum, exact pair
+  const double fl = tb - (fh - S0);
+  // rare: |F| < 2^-11 quadrants (finite x), or |x| < 1/2 (ph_int192 returns
+  // (x, 0, 0)); non-finite x leaves a meaningless r (the functions select
+  // the canonical NaN from x itself).  Tests on high words only.
+  const uint32_t hab = (uint32_t)(ab >> 32);
+  const bool fsmall = ((uint32_t)__double2hiint(fh) & 0x7fffffffu) < 0x42900000u;  // |fh| < 2^42
+  if (hab < 0x3fe00000u || (fsmall && hab < 0x7ff00000u)) return ph_int192(x);
   // r = F (pi/2) sign(x) with pi/2 * 2^-53 = C0 + C1 (units of 2^-53 above)
   const int sx = (int)(uint32_t)(b >> 32) & (int)0x80000000u;
   constexpr double kC0 = kPio2Qd0 * 0x1p-53, kC1 = kPio2Qd1 * 0x1p-53;
@@ -467,9 +468,9 @@ __device__ __forceinline__ red ph_int(double x, const double* __restrict__ tab) 
   ee = fma(fl, c0, ee);
   if (b >> 63) q = -q;
   red o;
-  o.hi = small ? x : p;
-  o.lo = small ? 0.0 : ee;
-  o.q = small ? 0 : (q & 3);
+  o.hi = p;
+  o.lo = ee;
+  o.q = q & 3;
   return o;
 }
 
@@ -996,7 +997,20 @@ __device__ __forceinline__ float tan_f_u10(float x, const double* tab) {
   double z = r.r * r.r;
   double P = poly<VEM_TAN_F_N>(cTanF, z);
   double t = fma(r.r * z, P, r.r);
-  double y = (r.q & 1) ? -__drcp_rn(t) : t;
+  // -cot, branch-free (the library reciprocals carry a slow-path branch per
+  // element, which keeps the compiler from interleaving the elements' chains):
+  // 1/|t| from a binary32 magic-constant seed (<= 0.051), three binary32 Newton
+  // steps (FP32 pipe, <= 2^-23.9) and one binary64 step (<= 2^-47)
+  const double ta = fabs(t);
+  const float tf = (float)ta;
+  float yf = from_bits_f(0x7EF311C7u - bits_f(tf));
+#pragma unroll
+  for (int i = 0; i < 3; i++) yf = fmaf(yf, fmaf(-tf, yf, 1.0f), yf);
+  const double y0 = (double)yf;
+  const double y1 = fma(y0, fma(-ta, y0, 1.0), y0);
+  // odd quadrant: -1/t = -sign(t) y1
+  const double yo = __hiloint2double(__double2hiint(y1) | (~__double2hiint(t) & (int)0x80000000u), __double2loint(y1));
+  double y = (r.q & 1) ? yo : t;
   return fin_f_nan((float)y);
 }
 
