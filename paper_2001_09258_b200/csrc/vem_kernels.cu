@@ -286,12 +286,14 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
   __shared__ uint64_t bars[STAGES];
   __shared__ uint32_t rel[STAGES];
   __shared__ __align__(16) double stab[TableSize<TABLE>::n];
-  // trivial-class compaction scratch (HasTriv ops only): per warp the
-  // arguments / results in slot order and the list of non-trivial slots
-  constexpr int kCW = HasTriv<Op>::value ? 32 * NE : 1;
-  __shared__ __align__(16) T s_cx[HasTriv<Op>::value ? NW : 1][kCW];
-  __shared__ __align__(16) T s_cy[HasTriv<Op>::value && NIN == 2 ? NW : 1][kCW];
-  __shared__ unsigned char s_ci[HasTriv<Op>::value ? NW : 1][kCW];
+  // trivial-class compaction (HasTriv ops only): per warp a stack of pending
+  // non-trivial elements (argument(s) + global element index), carried from
+  // tile to tile so that they are evaluated in full rows of 32
+  constexpr int kQGrp = NE < 4 ? NE : 4;  // elements per lane pushed between two drains
+  constexpr int kQCap = HasTriv<Op>::value ? 32 * kQGrp + 32 : 1;
+  __shared__ __align__(16) T s_qx[HasTriv<Op>::value ? NW : 1][kQCap];
+  __shared__ __align__(16) T s_qy[HasTriv<Op>::value && NIN == 2 ? NW : 1][kQCap];
+  __shared__ uint32_t s_qi[HasTriv<Op>::value ? NW : 1][kQCap];  // (CTA-local tile number) * TILE_E + offset in the tile
   V* buf = reinterpret_cast<V*>(dsm);
   const int tid = threadIdx.x, lane = tid & 31;
   if (tid == 0) {
@@ -310,7 +312,14 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
   const size_t my = ntiles > blockIdx.x ? (ntiles - blockIdx.x + G - 1) / G : 0;
   const uint64_t pol = tma::policy_evict_first();
   bool tmode = false;  // HasTriv: this warp compacts trivial elements (decided on its first tile)
+  int qn = 0;          // HasTriv: entries on this warp's stack of pending non-trivial elements
+  // stack entry -> global element index (entries hold the CTA-local tile number in 32 bits)
+  auto qelem = [&](uint32_t q) -> size_t {
+    return (blockIdx.x + (size_t)(q / (uint32_t)TILE_E) * G) * (size_t)TILE_E + (q % (uint32_t)TILE_E);
+  };
+  (void)qelem;
   (void)tmode;
+  (void)qn;
   auto issue = [&](int s, size_t tile) {
     tma::mbar_expect_tx(&bars[s], NIN * TILE_BYTES);
     tma::bulk_g2s(buf + (size_t)(s * NIN) * TILE_V, reinterpret_cast<const V*>(a) + tile * TILE_V, TILE_BYTES,
@@ -346,66 +355,84 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
     V* ov = reinterpret_cast<V*>(out) + (blockIdx.x + j * G) * TILE_V;
     if constexpr (HasTriv<Op>::value) {
       static_assert(sizeof(T) == 8 && W == 2, "trivial-class compaction: binary64");
-      // ---- warps with many trivial elements: compact the others into rows.
-      // The decision samples each lane's first element (one cheap test per
-      // lane and tile, so the dense path below pays ~1 instruction per
-      // element): compact when at least a quarter of the lanes' samples may
-      // be trivial.
-      // The mode is decided per warp on its first tile (input arrays are
-      // rarely heterogeneous at this scale) so that the dense path carries
-      // no per-tile test; in compaction mode every tile re-checks.
+      // ---- warps with many trivial elements.  The decision samples each
+      // lane's first element (one cheap test per lane and tile, so the dense
+      // path below pays ~1 instruction per element).  The mode is decided per
+      // warp on its first tile (input arrays are rarely heterogeneous at this
+      // scale) so that the dense path carries no per-tile test; in compaction
+      // mode every tile re-checks (at least a quarter of the samples).
+      // Trivial results are stored at once; the other elements are pushed on
+      // the warp's stack and evaluated 32 at a time -- full rows, whatever the
+      // tile's share of them (config 5: 4-8 %, i.e. 5-10 per warp and tile:
+      // evaluated per tile, the rows ran 5-10 active lanes of 32) -- each
+      // result stored to its own element.
       bool m0;
       if constexpr (NIN == 2) m0 = Triv<Op>::maybe(va[0].x, vb[0].x);
       else m0 = Triv<Op>::maybe(va[0].x);
-      if (j == 0) tmode = __popc(__ballot_sync(0xffffffffu, m0)) >= 8;
+      if (j == 0) tmode = __popc(__ballot_sync(0xffffffffu, m0)) >= 8 && my * (size_t)TILE_E < ((size_t)1 << 32);
       if (tmode && __popc(__ballot_sync(0xffffffffu, m0)) >= 8) {
-        constexpr int WE = 32 * NE;
-        T* sx = s_cx[tid >> 5];
-        T* sy = NIN == 2 ? s_cy[(tid >> 5) % (NIN == 2 ? NW : 1)] : sx;  // unary: y unused
-        unsigned char* si = s_ci[tid >> 5];
+        T* qx = s_qx[tid >> 5];
+        T* qy = NIN == 2 ? s_qy[(tid >> 5) % (NIN == 2 ? NW : 1)] : qx;  // unary: y unused
+        uint32_t* qi = s_qi[tid >> 5];
+        const uint32_t qbase = (uint32_t)j * (uint32_t)TILE_E;
         uint32_t mn = 0;  // non-trivial
 #pragma unroll
-        for (int v = 0; v < VPT; v++)
-#pragma unroll
-          for (int k = 0; k < W; k++) {
-            const int e = v * W + k, slot = e * 32 + lane;
-            const T x = vget(va[v], k);
-            T r = x;
-            bool t;
-            if constexpr (NIN == 2) t = Triv<Op>::exact(x, vget(vb[v], k), r);
-            else t = Triv<Op>::exact(x, r);
-            sx[slot] = t ? r : x;
-            if constexpr (NIN == 2) sy[slot] = vget(vb[v], k);
-            mn |= (uint32_t)!t << e;
+        for (int v = 0; v < VPT; v++) {
+          T r0 = va[v].x, r1 = va[v].y;
+          bool t0, t1;
+          if constexpr (NIN == 2) {
+            t0 = Triv<Op>::exact(va[v].x, vb[v].x, r0);
+            t1 = Triv<Op>::exact(va[v].y, vb[v].y, r1);
+          } else {
+            t0 = Triv<Op>::exact(va[v].x, r0);
+            t1 = Triv<Op>::exact(va[v].y, r1);
           }
-        const int cnt = __popc(mn);
-        int inc = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int t = __shfl_up_sync(0xffffffffu, inc, o);
-          if (lane >= o) inc += t;
+          mn |= ((uint32_t)!t0 | ((uint32_t)!t1 << 1)) << (v * W);
+          // one coalesced 16-byte store per vector; a non-trivial element's
+          // half is a placeholder that the same warp overwrites when it pops the
+          // element (the __syncwarp()s between the push and the pop order the
+          // two stores; separate 8-byte stores of the trivial halves measured
+          // 15 % slower: partially written sectors)
+          __stcs(ov + v * kThreads + tid, make_double2(r0, r1));
         }
-        const int nall = __shfl_sync(0xffffffffu, inc, 31);
-        int p = inc - cnt;
 #pragma unroll
-        for (int e = 0; e < NE; e++)
-          if ((mn >> e) & 1u) si[p++] = (unsigned char)(e * 32 + lane);
-        __syncwarp();
-#pragma unroll 1
-        for (int r = 0; r * 32 < nall; r += 2) {  // two rows per trip (independent chains)
-          const int ia = r * 32 + lane, ib = ia + 32;
-          const int sa = si[ia < nall ? ia : 0], sb = si[ib < nall ? ib : 0];
-          const T ya = eval_one<Op, NIN>(op, sx[sa], sy[sa], tab);
-          const T yb = eval_one<Op, NIN>(op, sx[sb], sy[sb], tab);
+        for (int g = 0; g < NE; g += kQGrp) {  // push kQGrp elements per lane, then drain full rows
+          const uint32_t mg = (mn >> g) & ((1u << kQGrp) - 1u);
+          const int cnt = __popc(mg);
+          int inc = cnt;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += t;
+          }
+          int p = qn + inc - cnt;
+          qn += __shfl_sync(0xffffffffu, inc, 31);
+          VEM_ASSERT(qn <= kQCap);
+#pragma unroll
+          for (int e = g; e < g + kQGrp; e++)
+            if ((mn >> e) & 1u) {
+              qx[p] = vget(va[e / W], e % W);
+              if constexpr (NIN == 2) qy[p] = vget(vb[e / W], e % W);
+              qi[p] = qbase + (uint32_t)(((e / W) * kThreads + tid) * W + (e % W));
+              p++;
+            }
           __syncwarp();
-          if (ia < nall) sx[sa] = ya;
-          if (ib < nall) sx[sb] = yb;
+          while (qn >= 32) {  // full rows off the top of the stack; two at a time (independent chains)
+            if (qn >= 64) {
+              const int ia = qn - 32 + lane, ib = qn - 64 + lane;
+              const T ya = eval_one<Op, NIN>(op, qx[ia], qy[ia], tab);
+              const T yb = eval_one<Op, NIN>(op, qx[ib], qy[ib], tab);
+              __stcs(out + qelem(qi[ia]), ya);
+              __stcs(out + qelem(qi[ib]), yb);
+              qn -= 64;
+            } else {
+              const int ia = qn - 32 + lane;
+              __stcs(out + qelem(qi[ia]), eval_one<Op, NIN>(op, qx[ia], qy[ia], tab));
+              qn -= 32;
+            }
+          }
+          __syncwarp();  // the popped entries are overwritten by the next pushes
         }
-        __syncwarp();
-#pragma unroll
-        for (int v = 0; v < VPT; v++)
-          __stcs(ov + v * kThreads + tid, make_double2(sx[(v * W) * 32 + lane], sx[(v * W + 1) * 32 + lane]));
-        __syncwarp();  // the block is rewritten by the next tile
         continue;
       }
     }
@@ -450,6 +477,12 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
         }
         __stcs(ov + v * kThreads + tid, o);
       }
+    }
+  }
+  if constexpr (HasTriv<Op>::value) {  // the last, partial row of the warp's stack
+    if (lane < qn) {
+      const T* qy = NIN == 2 ? s_qy[(tid >> 5) % (NIN == 2 ? NW : 1)] : s_qx[tid >> 5];
+      __stcs(out + qelem(s_qi[tid >> 5][lane]), eval_one<Op, NIN>(op, s_qx[tid >> 5][lane], qy[lane], tab));
     }
   }
   // remainder (< one tile)
