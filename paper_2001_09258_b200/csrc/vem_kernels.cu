@@ -46,7 +46,8 @@ static std::atomic<uint64_t> g_launches{0};
 // kTableD: the reference-algorithm PH table (reduction entry points);
 // kTableDI: the integer PH window words w1 | w2 (forced-PH kernels) + sin|cos
 // coefficients
-enum TableKind { kNoTable = 0, kTableD = 1, kTableF = 2, kTableLog = 3, kTableDG = 4, kTableDG35 = 5, kTableDI = 6 };
+enum TableKind { kNoTable = 0, kTableD = 1, kTableF = 2, kTableLog = 3, kTableDG = 4, kTableDG35 = 5, kTableDI = 6,
+                 kTableLogF = 7 };  // kTableLogF: the f32 log records, replicated per bank group (vem_math.cuh kRepLogF*)
 
 template <int TABLE>
 struct TableSize {
@@ -54,6 +55,7 @@ struct TableSize {
                            : TABLE == kTableDI ? kPhDIStaged + kSinCosCoefN
                            : TABLE == kTableF ? kPhFDoubles + kSinCosCoefN
                            : TABLE == kTableLog ? kLogTabN
+                           : TABLE == kTableLogF ? kRepLogFN + 128
                            : (TABLE == kTableDG || TABLE == kTableDG35) ? kSinCosCoefN + kPhDIStaged
                                                 : 2;
 };
@@ -98,13 +100,16 @@ __device__ __forceinline__ const double* stage_table(double* stab) {
       for (int i = threadIdx.x; i < 256; i += blockDim.x) {
         reinterpret_cast<double2*>(stab + kSlLogIH)[i] = make_double2(gLogExp[kLtInvc + i], gLogExp[kLtHi + i]);
         stab[kSlLogLo + i] = gLogExp[kLtLo + i];
-        reinterpret_cast<double2*>(stab + kSlLogF)[i] =
-            make_double2((double)__ldg(gLogTfInvc + i), gLogExp[kLtfHi + i]);
-        if (i < 128) {
+        if (i < 128)
           reinterpret_cast<double2*>(stab + kSlExp)[i] = make_double2(gLogExp[kLtExpHi + i], gLogExp[kLtExpLo + i]);
-          stab[kSlExpHi + i] = gLogExp[kLtExpHi + i];
-        }
       }
+    } else if constexpr (TABLE == kTableLogF) {
+      for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) {
+        const int c = i >> 8, k = i & 255;
+        reinterpret_cast<double2*>(stab)[c * kRepLogFStride + k] =
+            make_double2((double)__ldg(gLogTfInvc + k), gLogExp[kLtfHi + k]);
+      }
+      if (threadIdx.x < 128) stab[kRepLogFN + threadIdx.x] = gLogExp[kLtExpHi + threadIdx.x];
     } else if constexpr (TABLE == kTableF) {  // replicated, skewed copies (vem_math.cuh kPhFStride*)
       for (int i = threadIdx.x; i < 16 * VEM_PH_F_ENTRIES; i += blockDim.x) {
         const int c = i / VEM_PH_F_ENTRIES, k = i - c * VEM_PH_F_ENTRIES;
@@ -1359,9 +1364,10 @@ VEM_UNARY_OP(OpCosF, float, (cos_f_u10(x, tab)))
 VEM_UNARY_OP(OpTanF, float, (tan_f_u10(x, tab)))
 VEM_UNARY_OP(OpExpF, float, ((void)tab, exp_f_u10(x)))
 VEM_UNARY_OP(OpExpFU35, float, ((void)tab, exp_f_u35(x)))
+// f32 log / pow: the replicated table staging (kTableLogF)
 VEM_SPLIT_UNARY_OP(OpLogF, float, (log_f_u10(x, tab)), (log_fast_f<VEM_LOG1P_F_N>(x, cLog1pF, tab, code)), full())
-VEM_SPLIT_UNARY_OP(OpLogFU35, float, (log_f_u35(x, tab)), (log_fast_f<VEM_LOG1P_F_U35_N>(x, cLog1pFU35, tab, code)),
-                   full())
+VEM_SPLIT_UNARY_OP(OpLogFU35, float, (log_f_u35(x, tab)),
+                   (log_fast_f<VEM_LOG1P_F_U35_N>(x, cLog1pFU35, tab, code)), full())
 #undef VEM_UNARY_OP
 #undef VEM_SPLIT_UNARY_OP
 
@@ -1894,10 +1900,10 @@ int vem_cos_f_u10_ph(const float* x, float* y, size_t n, vem_stream_t s) { retur
 int vem_tan_f_u10_ph(const float* x, float* y, size_t n, vem_stream_t s) { return vem_tan_f_u10(x, y, n, s); }
 int vem_exp_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpExpF, float, 1, kNoTable, 2, 2>(x, nullptr, y, n, s); }
 int vem_exp_f_u35(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpExpFU35, float, 1, kNoTable, 1, 2>(x, nullptr, y, n, s); }
-int vem_log_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpLogF, float, 1, kTableLog, 2, 2>(x, nullptr, y, n, s); }
-int vem_log_f_u35(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpLogFU35, float, 1, kTableLog, 2, 2>(x, nullptr, y, n, s); }
-int vem_pow_f_u10(const float* x, const float* y2, float* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpPowF, float, 2, kTableLog, 2, 2, 3>(x, y2, o, n, s); }
-int vem_pow_f_u35(const float* x, const float* y2, float* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpPowFU35, float, 2, kTableLog, 2, 2, 3>(x, y2, o, n, s); }
+int vem_log_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpLogF, float, 1, kTableLogF, 2, 2>(x, nullptr, y, n, s); }
+int vem_log_f_u35(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpLogFU35, float, 1, kTableLogF, 2, 2>(x, nullptr, y, n, s); }
+int vem_pow_f_u10(const float* x, const float* y2, float* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpPowF, float, 2, kTableLogF, 2, 2, 3>(x, y2, o, n, s); }
+int vem_pow_f_u35(const float* x, const float* y2, float* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpPowFU35, float, 2, kTableLogF, 2, 2, 3>(x, y2, o, n, s); }
 int vem_fmod_f(const float* x, const float* y2, float* o, size_t n, vem_stream_t s) {
 #ifdef VEM_TUNE
   return VEM_FMOD<float>(x, y2, o, n, s);

@@ -147,12 +147,19 @@ constexpr int kPhFDoubles = kPhFT2 + 16 * kPhFStride2;       // staged size in d
 //   [kSlLogIH + 2 i] {invc, logc_hi}                 i < 256  (f64 log)
 //   [kSlLogLo + i]   logc_lo                         i < 256
 //   [kSlExp + 2 j]   {2^(j/128) hi, lo}              j < 128  (exp of pow_d)
-//   [kSlExpHi + j]   2^(j/128) hi                    j < 128  (f32 exp of pow_f)
-//   [kSlLogF + 2 i]  {(double)invc_f32, logc hi}     i < 256  (f32 log/pow)
 constexpr int kLtInvc = 0, kLtHi = 256, kLtLo = 512, kLtExpHi = 768, kLtExpLo = 896, kLtfHi = 1024;
 constexpr int kLogTabD = 1280;  // global SoA doubles (+ 256 binary32 invc)
-constexpr int kSlLogIH = 0, kSlLogLo = 512, kSlExp = 768, kSlExpHi = 1024, kSlLogF = 1152;
-constexpr int kLogTabN = 1664;  // staged doubles
+constexpr int kSlLogIH = 0, kSlLogLo = 512, kSlExp = 768;
+constexpr int kLogTabN = 1024;  // staged doubles (f64 log / pow kernels)
+// Replicated staging for the f32 log kernels (layout 1): the lanes of a warp
+// read random entries, so the plain 16-byte records cost ~7.5 bank-conflict
+// wavefronts per load (the f32 log kernels were shared-memory bound: 70 % of
+// the LSU's wavefronts at 0.78 of the HBM roofline).  8 copies of the
+// {invc, logc hi} records, one bank group of skew between copies (stride 257
+// records = 1 mod 8); lane L reads copy (L - entry) mod 8, so its bank group is
+// L mod 8: conflict-free, 4 wavefronts.
+constexpr int kRepLogFStride = 257;
+constexpr int kRepLogFN = 2 * 8 * kRepLogFStride;  // staged doubles (then 128 doubles 2^(j/128) for pow_f)
 __device__ const double gLogExp[kLogTabD] = {VEM_LOGT_INVC_INIT VEM_LOGT_HI_INIT VEM_LOGT_LO_INIT
                                                  VEM_EXPT_HI_INIT VEM_EXPT_LO_INIT VEM_LOGTF_HI_INIT};
 __device__ const float gLogTfInvc[256] = {VEM_LOGTF_INVC_INIT};
@@ -1031,6 +1038,11 @@ __device__ __forceinline__ float exp_core_f(float x, const double* c) {
 __device__ __forceinline__ float exp_f_u10(float x) { return exp_core_f<VEM_EXP_F_N>(x, cExpF); }
 __device__ __forceinline__ float exp_f_u35(float x) { return exp_core_f<VEM_EXP_F_U35_N>(x, cExpFU35); }
 
+// {invc, logc hi} of entry idx from the replicated f32 staging (kRepLogF*,
+// kTableLogF: what every f32 log / pow kernel stages)
+__device__ __forceinline__ double2 ld_logf(const double* __restrict__ lt, int idx) {
+  return reinterpret_cast<const double2*>(lt)[(int)((threadIdx.x - (uint32_t)idx) & 7u) * kRepLogFStride + idx];
+}
 template <int N>
 __device__ __forceinline__ double log_f_internal(double a, const double* c, const double* __restrict__ lt) {
   uint64_t ix = bits_d(a);
@@ -1038,7 +1050,7 @@ __device__ __forceinline__ double log_f_internal(double a, const double* c, cons
   long long k = (long long)tmp >> 52;
   int idx = (int)((tmp >> 44) & 255u);
   double m = from_bits_d(ix - ((uint64_t)k << 52));
-  const double2 ih = reinterpret_cast<const double2*>(lt + kSlLogF)[idx];  // {invc, hi}
+  const double2 ih = ld_logf(lt, idx);  // {invc, hi}
   double r = fma(m, ih.x, -1.0);  // == (double)invc_f32: exact product
   double Q = poly<N>(c, r);
   double L = fma(r * r, Q, r);
@@ -1054,7 +1066,7 @@ __device__ __forceinline__ double log_f_internal_f(float x, const double* c, con
   int k = (int)t >> 23;
   int idx = (int)((t >> 15) & 255u);
   double m = (double)from_bits_f(ux - ((uint32_t)k << 23));
-  const double2 ih = reinterpret_cast<const double2*>(lt + kSlLogF)[idx];
+  const double2 ih = ld_logf(lt, idx);
   double r = fma(m, ih.x, -1.0);
   double Q = poly<N>(c, r);
   double L = fma(r * r, Q, r);
@@ -1084,7 +1096,7 @@ __device__ __forceinline__ double exp_f_internal(double t, const double* __restr
   double r = fma(kd, -ccExpjL1, t);
   r = fma(kd, -ccExpjL2, r);
   double p = fma(r * r, fma(r, ccSixth, 0.5), r);
-  double T = lt[kSlExpHi + (k & 127)];
+  double T = lt[kRepLogFN + (k & 127)];  // f32 staging (kTableLogF): 2^(j/128) after the replicated log records
   double R = fma(T, p, T);
   return __hiloint2double(__double2hiint(R) + ((k >> 7) << 20), __double2loint(R));
 }

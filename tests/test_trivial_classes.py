@@ -100,3 +100,47 @@ def test_pow_trivial_results_equal_full_function(name):
     x2, y2 = I.config_inputs(2, "pow", "d", 100000)
     assert not triv_pow(x2, y2)[0].any()
     assert not ((hi(x2) - np.uint32(0x3DD00000)) >= np.uint32(0x04400000)).any()
+
+
+# ------------------------------------------------------------- GPU: carry-over
+def _mixed_wide(seed, n, share_dense):
+    """Wide-range arguments (mostly trivial results) with dense stretches:
+    segments of 5000-70000 elements alternate between log-uniform magnitudes
+    over the whole binary64 range and moderate ones, so warps enter and leave
+    the compaction mode and the per-warp stacks carry pending elements across
+    tiles with very different non-trivial shares."""
+    rng = np.random.default_rng(seed)
+    x = I.log_uniform(seed, n, 1e-300, 1e300, signed=True)
+    pos = 0
+    while pos < n:
+        m = int(rng.integers(5000, 70000))
+        if rng.random() < share_dense:
+            x[pos:pos + m] = np.exp(rng.uniform(-12, 12, min(m, n - pos))) * rng.choice([-1.0, 1.0], min(m, n - pos))
+        pos += m
+    x[rng.integers(0, n, 64)] = np.array([np.inf, -np.inf, np.nan, 0.0] * 16)
+    return x
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["pow_d_u10", "atan_d_u10", "atan_d_u35"])
+def test_gpu_compaction_carry_over(cuda, name):
+    """k_stream's trivial-class compaction with the per-warp carry-over stack
+    (vem_kernels.cu): mixed trivial / dense inputs, ragged sizes (partial last
+    tile, pending elements flushed at the end), misaligned buffers take the
+    plain kernel, and in place -- all bit-identical to the oracle."""
+    import torch
+    from paper_2001_09258_b200 import api
+    for n, seed, dense in ((1 << 21, 3, 0.25), ((1 << 20) + 12345, 4, 0.6), (300001, 5, 0.0), (4099, 6, 0.0)):
+        x = _mixed_wide(seed, n, dense)
+        args = [x]
+        if name.startswith("pow"):
+            y = I.uniform(seed + 100, n, -30.0, 30.0)
+            y[::97] = np.round(y[::97])  # integer exponents: negative bases are not NaN
+            args.append(y)
+        want = oracle_eval(name, *args)
+        dev = [torch.from_numpy(a).to(cuda) for a in args]
+        out = torch.empty_like(dev[0])
+        api.call(name, *dev, out=out)
+        assert _same(out.cpu().numpy(), want), (name, n, "out of place")
+        api.call(name, *dev, out=dev[0])  # in place: the stack holds its own copy of the arguments
+        assert _same(dev[0].cpu().numpy(), want), (name, n, "in place")
