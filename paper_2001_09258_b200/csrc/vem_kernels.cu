@@ -1877,9 +1877,9 @@ int vem_sin_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { ret
 int vem_cos_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpCosDPh, double, 1, kTableDI, 4, 2, 2>(x, nullptr, y, n, s); }
 int vem_tan_d_u10_ph(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpTanDPh, double, 1, kTableDI, 4, 2, 2>(x, nullptr, y, n, s); }
 int vem_atan_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpAtanD, double, 1, kNoTable, 2, 2>(x, nullptr, y, n, s); }
-int vem_exp_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpExpD, double, 1, kNoTable, 1, 2, 3>(x, nullptr, y, n, s); }
+int vem_exp_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpExpD, double, 1, kNoTable, 2, 2, 3>(x, nullptr, y, n, s); }
 int vem_exp_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpExpDU35, double, 1, kNoTable, 4, 2>(x, nullptr, y, n, s); }
-int vem_log_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpLogD, double, 1, kTableLog, 4, 2, 4, true>(x, nullptr, y, n, s); }
+int vem_log_d_u10(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpLogD, double, 1, kTableLog, 4, 2, 3, true>(x, nullptr, y, n, s); }
 int vem_log_d_u35(const double* x, double* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpLogDU35, double, 1, kTableLog, 2, 2, 4>(x, nullptr, y, n, s); }
 int vem_pow_d_u10(const double* x, const double* y2, double* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpPowD, double, 2, kTableLog, 2, 2, 3, true>(x, y2, o, n, s); }
 int vem_pow_d_u35(const double* x, const double* y2, double* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpPowDU35, double, 2, kTableLog, 2, 2, 3, true>(x, y2, o, n, s); }
@@ -1893,13 +1893,13 @@ int vem_fmod_d(const double* x, const double* y2, double* o, size_t n, vem_strea
 
 int vem_sin_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpSinF, float, 1, kTableF, 4, 2>(x, nullptr, y, n, s); }
 int vem_cos_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpCosF, float, 1, kTableF, 4, 2>(x, nullptr, y, n, s); }
-int vem_tan_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpTanF, float, 1, kTableF, 2, 2, 4>(x, nullptr, y, n, s); }
+int vem_tan_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpTanF, float, 1, kTableF, 4, 2, 2>(x, nullptr, y, n, s); }
 // every f32 trig lane takes the f32 Payne-Hanek path: the forced variants are the same kernels
 int vem_sin_f_u10_ph(const float* x, float* y, size_t n, vem_stream_t s) { return vem_sin_f_u10(x, y, n, s); }
 int vem_cos_f_u10_ph(const float* x, float* y, size_t n, vem_stream_t s) { return vem_cos_f_u10(x, y, n, s); }
 int vem_tan_f_u10_ph(const float* x, float* y, size_t n, vem_stream_t s) { return vem_tan_f_u10(x, y, n, s); }
-int vem_exp_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpExpF, float, 1, kNoTable, 2, 2>(x, nullptr, y, n, s); }
-int vem_exp_f_u35(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpExpFU35, float, 1, kNoTable, 1, 2>(x, nullptr, y, n, s); }
+int vem_exp_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpExpF, float, 1, kNoTable, 2, 2, 3>(x, nullptr, y, n, s); }
+int vem_exp_f_u35(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpExpFU35, float, 1, kNoTable, 2, 2, 3>(x, nullptr, y, n, s); }
 int vem_log_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpLogF, float, 1, kTableLogF, 2, 2>(x, nullptr, y, n, s); }
 int vem_log_f_u35(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpLogFU35, float, 1, kTableLogF, 2, 2>(x, nullptr, y, n, s); }
 int vem_pow_f_u10(const float* x, const float* y2, float* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpPowF, float, 2, kTableLogF, 2, 2, 3>(x, y2, o, n, s); }
