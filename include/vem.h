@@ -19,10 +19,11 @@
  *    canonical quiet NaN (0x7ff8000000000000 / 0x7fc00000);
  *  - reentrant from any host thread, on any device (launch state is cached
  *    per device); the Payne-Hanek tables are device constants (replace the
- *    lazy singleton ph_table(), ph_table.cpp:182-185): the binary32 table and
- *    the forced-Payne-Hanek kernels' binary64 table are staged per CTA into
- *    shared memory, the binary64 selector kernels (sin/cos/tan_d) read theirs
- *    through L1 (most of their lanes never touch it);
+ *    lazy singleton ph_table(), ph_table.cpp:182-185) staged per CTA into
+ *    shared memory in bank-conflict-aware layouts (the binary32 limbs
+ *    replicated per bank group, the binary64 window words as two 8-byte
+ *    arrays); the binary64 selector kernels (sin/cos/tan_d) stage theirs
+ *    lazily, when a CTA first meets an argument above 1e14;
  *  - results are bit-identical to the deterministic CPU oracle (oracle/).
  *
  * Accuracy: *_u10 <= 1.0 ulp, *_u35 <= 3.5 ulp (vs MPFR), fmod exact.
