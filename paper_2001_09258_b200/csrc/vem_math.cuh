@@ -680,20 +680,24 @@ struct logred { double rh, rl, E, logc_hi, logc_lo; };
 // is never -0, so the dropped "+ 0.0" cannot change a bit).
 template <bool kAdj = true>
 __device__ __forceinline__ logred log_reduce(double a, double Eadj, const double* __restrict__ lt) {
-  uint64_t ix = bits_d(a);
-  uint64_t tmp = ix - 0x3fe8000000000000ull;
-  long long k = (long long)tmp >> 52;
-  int idx = (int)((tmp >> 44) & 255u);
-  double m = from_bits_d(ix - ((uint64_t)k << 52));
-  const double2 ih = reinterpret_cast<const double2*>(lt + kSlLogIH)[idx];  // {invc, hi}
+  // bits(a) - bits(0.75): the constant's low word is 0, so everything is on
+  // the high word (same k, idx and m as the oracle's 64-bit form); the table
+  // offsets are formed in bytes (idx * 16, idx * 8) with one shift and one mask
+  const uint32_t hix = (uint32_t)__double2hiint(a);
+  const uint32_t t = hix - 0x3fe80000u;
+  const int k = (int)t >> 20;
+  const uint32_t off16 = (t >> 8) & 0xff0u;  // idx = bits 12..19 of t
+  const double m = __hiloint2double((int)(hix - (t & 0xfff00000u)), __double2loint(a));
+  const double2 ih =
+      *reinterpret_cast<const double2*>(reinterpret_cast<const char*>(lt + kSlLogIH) + off16);  // {invc, hi}
   double invc = ih.x;
   double p = m * invc;
   logred o;
   o.rl = fma(m, invc, -p);
   o.rh = p - 1.0;
-  o.E = kAdj ? (double)(int)k + Eadj : (double)(int)k;
+  o.E = kAdj ? (double)k + Eadj : (double)k;
   o.logc_hi = ih.y;
-  o.logc_lo = lt[kSlLogLo + idx];
+  o.logc_lo = *reinterpret_cast<const double*>(reinterpret_cast<const char*>(lt + kSlLogLo) + (off16 >> 1));
   return o;
 }
 
