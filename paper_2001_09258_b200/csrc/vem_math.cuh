@@ -1564,9 +1564,12 @@ template <int NL>
 __device__ __forceinline__ float pow_fast_f(float x, float y, const double* cl, const double* lt, int& code) {
   const uint32_t uy = bits_f(y);
   const bool fy = ((uy & 0x7fffffffu) - 1u) < 0x7f7fffffu;
-  code = (is_pos_normal_f(x) && fy) ? 0 : 1;
-  double t = (double)y * log_f_internal_f<NL>(x, cl, lt);
-  t = (((uint32_t)__double2hiint(t) & 0x7fffffffu) >= 0x40690000u) ? ((t > 0.0) ? 200.0 : -200.0) : t;
+  const double t = (double)y * log_f_internal_f<NL>(x, cl, lt);
+  // |t| >= 200 saturates: left to the full function (a flag instead of the
+  // clamp's three selects; the table index below is masked, so a huge or NaN
+  // t reads inside the table)
+  const bool big = ((uint32_t)__double2hiint(t) & 0x7fffffffu) >= 0x40690000u;
+  code = (is_pos_normal_f(x) && fy && !big) ? 0 : 1;
   return (float)exp_f_internal(t, lt);
 }
 
