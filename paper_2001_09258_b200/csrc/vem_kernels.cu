@@ -359,7 +359,6 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
     }
     V* ov = reinterpret_cast<V*>(out) + (blockIdx.x + j * G) * TILE_V;
     if constexpr (HasTriv<Op>::value) {
-      static_assert(sizeof(T) == 8 && W == 2, "trivial-class compaction: binary64");
       // ---- warps with many trivial elements.  The decision samples each
       // lane's first element (one cheap test per lane and tile, so the dense
       // path below pays ~1 instruction per element).  The mode is decided per
@@ -372,8 +371,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
       // evaluated per tile, the rows ran 5-10 active lanes of 32) -- each
       // result stored to its own element.
       bool m0;
-      if constexpr (NIN == 2) m0 = Triv<Op>::maybe(va[0].x, vb[0].x);
-      else m0 = Triv<Op>::maybe(va[0].x);
+      if constexpr (NIN == 2) m0 = Triv<Op>::maybe(vget(va[0], 0), vget(vb[0], 0));
+      else m0 = Triv<Op>::maybe(vget(va[0], 0));
       if (j == 0) tmode = __popc(__ballot_sync(0xffffffffu, m0)) >= 8 && my * (size_t)TILE_E < ((size_t)1 << 32);
       if (tmode && __popc(__ballot_sync(0xffffffffu, m0)) >= 8) {
         T* qx = s_qx[tid >> 5];
@@ -383,22 +382,20 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
         uint32_t mn = 0;  // non-trivial
 #pragma unroll
         for (int v = 0; v < VPT; v++) {
-          T r0 = va[v].x, r1 = va[v].y;
-          bool t0, t1;
-          if constexpr (NIN == 2) {
-            t0 = Triv<Op>::exact(va[v].x, vb[v].x, r0);
-            t1 = Triv<Op>::exact(va[v].y, vb[v].y, r1);
-          } else {
-            t0 = Triv<Op>::exact(va[v].x, r0);
-            t1 = Triv<Op>::exact(va[v].y, r1);
+          V o = va[v];  // a non-trivial element's placeholder: its own argument
+#pragma unroll
+          for (int k = 0; k < W; k++) {
+            bool t;
+            if constexpr (NIN == 2) t = Triv<Op>::exact(vget(va[v], k), vget(vb[v], k), vget(o, k));
+            else t = Triv<Op>::exact(vget(va[v], k), vget(o, k));
+            mn |= (uint32_t)!t << (v * W + k);
           }
-          mn |= ((uint32_t)!t0 | ((uint32_t)!t1 << 1)) << (v * W);
           // one coalesced 16-byte store per vector; a non-trivial element's
-          // half is a placeholder that the same warp overwrites when it pops the
+          // part is a placeholder that the same warp overwrites when it pops the
           // element (the __syncwarp()s between the push and the pop order the
-          // two stores; separate 8-byte stores of the trivial halves measured
+          // two stores; separate narrow stores of the trivial parts measured
           // 15 % slower: partially written sectors)
-          __stcs(ov + v * kThreads + tid, make_double2(r0, r1));
+          __stcs(ov + v * kThreads + tid, o);
         }
 #pragma unroll
         for (int g = 0; g < NE; g += kQGrp) {  // push kQGrp elements per lane, then drain full rows
@@ -1671,6 +1668,11 @@ struct OpFmodFFlat {
     return fmod_f_flat(x, y);
   }
 };
+// (A trivial class for fmodf -- everything but |x| > |y| > 0, half of config
+// 4's pairs -- through the carry-over stack measured slower, 260 -> 238
+// Gelem/s: with half of the elements non-trivial, their scattered 4-byte
+// stores cost more than the skipped work; the stack pays for shares of a few
+// per cent, as pow's and atan's on config 5.)
 #ifdef VEM_TUNE
 struct OpFmodFFixed {
   __device__ __forceinline__ float operator()(float x, float y, const double* tab) const {
