@@ -702,13 +702,15 @@ static double exp_dd(dd_t t) {
   double kd = rint_fma(th, VEM_EXPJ_INV, &k);
   double r1 = fma(kd, -VEM_EXPJ_L1, th);
   double r2 = fma(kd, -VEM_EXPJ_L2, tl);
-  dd_t r = two_sum_fast(r1, r2); /* |r2| <~ 2^-26; if |r1| < |r2| the error is < 2^-79 */
-  double z = r.hi * r.hi;
-  double Q = poly(C_EXPJ_D, VEM_EXPJ_D_N, r.hi);
-  double s2 = z * fma(r.hi, Q, 0.5);
-  double em1l = r.lo + fma(r.hi, r.lo, s2);
+  /* |r2| <~ 2^-26, |r| <= ln2/256: the rounding error of this sum is below
+   * 2^-61.5, i.e. 0.003 ulp of the result -- not worth a two-sum and the two
+   * operations that would carry it (round 2; the result moved by at most that) */
+  double r = r1 + r2;
+  double z = r * r;
+  double Q = poly(C_EXPJ_D, VEM_EXPJ_D_N, r);
+  double s2 = z * fma(r, Q, 0.5);
   double Th = EXPT_HI[k & 127], Tl = EXPT_LO[k & 127];
-  double u = fma(Th, r.hi, fma(Th, em1l, Tl));
+  double u = fma(Th, r, fma(Th, s2, Tl));
   double R = Th + u;
   int32_t e = k >> 7;
   if (fast) return from_bits_d(bits_d(R) + ((uint64_t)(int64_t)e << 52));
