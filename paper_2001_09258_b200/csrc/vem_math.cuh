@@ -1176,8 +1176,15 @@ __device__ __forceinline__ float fmod_f_flat(float x, float y) {
   const double rmd = __drcp_rn(md);
   const double rmd50 = rmd * 0x1p50;
   double r = fmod_stepn_rs(mn * __hiloint2double((1023 + E - 50 * steps) << 20, 0), md, rmd);
+  // warp-uniform trip count (the largest of the active lanes' counts) with the
+  // step predicated per lane: the same iterations as a per-lane loop, without
+  // its divergence bookkeeping (BSSY / BSYNC / predicated branch: more
+  // instructions per trip than the step's four)
+  const int kmax = __reduce_max_sync(__activemask(), steps);
 #pragma unroll 1
-  for (int k = 0; k < steps; k++) r = fmod_stepn50(r, md, rmd50);
+  for (int k = 0; k < kmax; k++) {
+    if (k < steps) r = fmod_stepn50(r, md, rmd50);
+  }
   r = r < 0.0 ? r + md : r;
   const float m = (float)(r * __hiloint2double(ed << 20, 0));  // r 2^(ed-1023), exact
   float res = pend ? m : (bx < by ? x : 0.0f);                 // |x| < |y| -> x; |x| == |y| -> 0
