@@ -520,9 +520,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_stream(const T* __restrict__
 //      per-lane selector op(); each result overwrites its argument's slot;
 //   4. the block is stored in slot order: conflict-free LDS, coalesced
 //      16-byte st.global.cs.
-// 2.25 KB of scratch per warp: with 2 x 16 KB stages the CTA needs 50 KB, so 3
-// CTAs (24 warps, <= 80 registers) leave ~70 KB of L1 for the 32 KB integer
-// Payne-Hanek table (read through L1).
+// 2.25 KB of scratch per warp and the lazily staged Payne-Hanek window
+// (w1 | w2, 16.4 KB): with 2 x 16 KB stages the CTA needs 68 KB, so 3 CTAs
+// (24 warps, <= 80 registers) fit.
 template <class Op, int TABLE, int VPT, int STAGES, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) k_trig(const double* __restrict__ a, double* __restrict__ out,
                                                          size_t n) {

@@ -509,7 +509,8 @@ __device__ __forceinline__ red trig_reduce(double x, const double* __restrict__ 
 }
 
 // the functions' selector (oracle: trig_reduce_fn): CW1 / CW2 as the
-// reference, the integer Payne-Hanek above 1e14; `tab` = gPhDI
+// reference, the integer Payne-Hanek above 1e14; `tab` = the staged window
+// words (kPhDIStaged)
 __device__ __forceinline__ red trig_reduce_fn(double x, const double* __restrict__ tab) {
   const int c = trig_class(x);
   red r;
@@ -553,7 +554,7 @@ __device__ __forceinline__ bool not_finite_bits(double x) {
 // kernels use it for warps whose elements are all |x| <= 15, where the
 // selector takes that path anyway: same values, no branches).
 enum RedMode { kSel = 0, kPh = 1, kCw1 = 2 };
-// `tab` is the integer Payne-Hanek table gPhDI (staged or global)
+// `tab`: the staged integer Payne-Hanek window words (w1 | w2, kPhDIStaged)
 template <int kMode>
 __device__ __forceinline__ red reduce_mode(double x, const double* tab) {
   if constexpr (kMode == kPh) return ph_int(x, tab);
