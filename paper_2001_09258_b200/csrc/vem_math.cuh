@@ -434,6 +434,11 @@ __device__ __noinline__ red ph_int192(double x) {
 // lanes of a warp read random entries: 8-byte words at an 8-byte stride spread
 // over all 16 bank pairs (~5 wavefronts per load), where the 32-byte records
 // of gPhDI use 4 of them (~11).
+// kAbs: reduce |x| (positive constants, no quadrant negation: 6 instructions
+// fewer); the caller folds the sign of x into its result -- every function
+// here is exactly odd or even in (r, q), so the values are the same bit for
+// bit as with the signed reduction (the oracle's).
+template <bool kAbs = false>
 __device__ __forceinline__ red ph_int(double x, const double* __restrict__ tab) {
   const uint64_t b = bits_d(x), ab = b & 0x7fffffffffffffffull;
   const int ue = (int)(ab >> 52) - 1023;
@@ -463,17 +468,22 @@ __device__ __forceinline__ red ph_int(double x, const double* __restrict__ tab) 
   // the canonical NaN from x itself).  Tests on high words only.
   const uint32_t hab = (uint32_t)(ab >> 32);
   const bool fsmall = ((uint32_t)__double2hiint(fh) & 0x7fffffffu) < 0x42900000u;  // |fh| < 2^42
-  if (hab < 0x3fe00000u || (fsmall && hab < 0x7ff00000u)) return ph_int192(x);
+  if (hab < 0x3fe00000u || (fsmall && hab < 0x7ff00000u)) return ph_int192(kAbs ? from_bits_d(ab) : x);
   // r = F (pi/2) sign(x) with pi/2 * 2^-53 = C0 + C1 (units of 2^-53 above)
-  const int sx = (int)(uint32_t)(b >> 32) & (int)0x80000000u;
   constexpr double kC0 = kPio2Qd0 * 0x1p-53, kC1 = kPio2Qd1 * 0x1p-53;
-  const double c0 = __hiloint2double(__double2hiint(kC0) ^ sx, __double2loint(kC0));
-  const double c1 = __hiloint2double(__double2hiint(kC1) ^ sx, __double2loint(kC1));
+  double c0 = kC0, c1 = kC1;
+  if constexpr (!kAbs) {
+    const int sx = (int)(uint32_t)(b >> 32) & (int)0x80000000u;
+    c0 = __hiloint2double(__double2hiint(kC0) ^ sx, __double2loint(kC0));
+    c1 = __hiloint2double(__double2hiint(kC1) ^ sx, __double2loint(kC1));
+  }
   const double p = fh * c0;
   double ee = fma(fh, c0, -p);
   ee = fma(fh, c1, ee);
   ee = fma(fl, c0, ee);
-  if (b >> 63) q = -q;
+  if constexpr (!kAbs) {
+    if (b >> 63) q = -q;
+  }
   red o;
   o.hi = p;
   o.lo = ee;
@@ -557,9 +567,18 @@ enum RedMode { kSel = 0, kPh = 1, kCw1 = 2 };
 // `tab`: the staged integer Payne-Hanek window words (w1 | w2, kPhDIStaged)
 template <int kMode>
 __device__ __forceinline__ red reduce_mode(double x, const double* tab) {
-  if constexpr (kMode == kPh) return ph_int(x, tab);
+  if constexpr (kMode == kPh) return ph_int<true>(x, tab);  // (r, q) of |x|: see odd_sign
   else if constexpr (kMode == kCw1) return cw1(x);
   else return trig_reduce_fn(x, tab);
+}
+// kPh reduces |x|: the odd functions (sin, tan) flip their result by the sign
+// of x, cos needs nothing.  0 for the signed reductions.
+template <int kMode>
+__device__ __forceinline__ double odd_sign(double y, double x) {
+  if constexpr (kMode == kPh)
+    return __hiloint2double(__double2hiint(y) ^ (__double2hiint(x) & (int)0x80000000u), __double2loint(y));
+  else
+    return y;
 }
 
 // NaN can only come from a non-finite input: canonicalised by an integer test
@@ -568,7 +587,7 @@ template <int kMode>
 __device__ __forceinline__ double sin_d_u10(double x, const double* tab, const double* coef) {
   red r = reduce_mode<kMode>(x, tab);
   double y = sincos_core_d(r.hi, r.lo, r.q & 1, coef);
-  y = neg_if(y, r.q & 2);
+  y = odd_sign<kMode>(neg_if(y, r.q & 2), x);
   y = is_zero_bits(x) ? x : y;
   if constexpr (kMode == kCw1) return y;  // |x| <= 15: finite
   else return not_finite_bits(x) ? from_bits_d(kCanonNanD) : y;
@@ -603,7 +622,7 @@ __device__ __forceinline__ double tan_core_d(double rh, double rl, int odd) {
 template <int kMode>
 __device__ __forceinline__ double tan_d_u10(double x, const double* tab) {
   red r = reduce_mode<kMode>(x, tab);
-  double y = tan_core_d(r.hi, r.lo, r.q & 1);
+  double y = odd_sign<kMode>(tan_core_d(r.hi, r.lo, r.q & 1), x);
   y = (fabs(x) < 0x1p-27) ? x : y;
   // finite x never gives a NaN y: the oracle's canon_d(y) is this select
   return not_finite_bits(x) ? from_bits_d(kCanonNanD) : y;
@@ -1252,7 +1271,7 @@ template <int kMode>
 __device__ __forceinline__ double sin_d_u35(double x, const double* tab, const double* coef) {
   red r = reduce_mode<kMode>(x, tab);
   double y = sincos_core_d_u35(r.hi, r.q & 1, coef);
-  y = neg_if(y, r.q & 2);
+  y = odd_sign<kMode>(neg_if(y, r.q & 2), x);
   y = is_zero_bits(x) ? x : y;
   if constexpr (kMode == kCw1) return y;
   else return not_finite_bits(x) ? from_bits_d(kCanonNanD) : y;
@@ -1278,7 +1297,7 @@ __device__ __forceinline__ double tan_core_d_u35(double rh, double rl, int odd) 
 template <int kMode>
 __device__ __forceinline__ double tan_d_u35(double x, const double* tab) {
   red r = reduce_mode<kMode>(x, tab);
-  double y = tan_core_d_u35(r.hi, r.lo, r.q & 1);
+  double y = odd_sign<kMode>(tan_core_d_u35(r.hi, r.lo, r.q & 1), x);
   y = (fabs(x) < 0x1p-27) ? x : y;
   return not_finite_bits(x) ? from_bits_d(kCanonNanD) : y;
 }
