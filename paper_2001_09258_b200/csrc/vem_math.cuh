@@ -453,12 +453,14 @@ __device__ __forceinline__ red ph_int(double x, const double* __restrict__ tab) 
   const uint64_t T1 = M * w2 + __umul64hi(M, w1);
   const uint32_t t3 = (uint32_t)(T1 >> 32), t2 = (uint32_t)T1, t1 = (uint32_t)(T0 >> 32);
   int q = (int)((t3 + 0x20000000u) >> 30);
-  const uint32_t f = t3 & 0x3fffffffu;
   // fraction bits below 2^-73 are noise (the dropped M*w0 term): two chunks,
-  // c0 = f : t2[31..9] (53 bits) minus 2^53 when the fraction is >= 1/2, and
-  // c1 = t2[8..0] : t1[31..9] (32 bits, weights down to 2^-85); units of 2^-53
-  const int c0hi = (int)((f >> 9) - ((f >> 29) << 21));
-  const uint32_t c0lo = (f << 23) | (t2 >> 9);
+  // c0 = f : t2[31..9] (f = the 30 fraction bits of t3; 53 bits) minus 2^53
+  // when the fraction is >= 1/2 -- i.e. the 53-bit field read as two's
+  // complement: its high word is t3 shifted left by 2 (the quadrant bits out)
+  // and arithmetically right by 11 -- and c1 = t2[8..0] : t1[31..9] (32 bits,
+  // weights down to 2^-85); units of 2^-53
+  const int c0hi = (int)(t3 << 2) >> 11;
+  const uint32_t c0lo = __funnelshift_l(t2, t3, 23);
   const double S0 = (double)(long long)(((uint64_t)(uint32_t)c0hi << 32) | c0lo);
   const double tb = (double)__funnelshift_l(t1, t2, 23) * 0x1p-32;
   const double fh = S0 + tb;  // |S0| is 0 or >= 1 > tb: Fast2Sum, exact pair
