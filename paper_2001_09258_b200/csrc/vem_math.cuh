@@ -462,7 +462,9 @@ __device__ __forceinline__ red ph_int(double x, const double* __restrict__ tab) 
   const int c0hi = (int)(t3 << 2) >> 11;
   const uint32_t c0lo = __funnelshift_l(t2, t3, 23);
   const double S0 = (double)(long long)(((uint64_t)(uint32_t)c0hi << 32) | c0lo);
-  const double tb = (double)__funnelshift_l(t1, t2, 23) * 0x1p-32;
+  // c1 * 2^-32 without a conversion: 2^20 + c1 2^-32 is the double with high word
+  // 0x41300000 and low word c1 (exact), minus 2^20 (exact)
+  const double tb = __hiloint2double(0x41300000, (int)__funnelshift_l(t1, t2, 23)) - 0x1p20;
   const double fh = S0 + tb;  // |S0| is 0 or >= 1 > tb: Fast2Sum, exact pair
   const double fl = tb - (fh - S0);
   // rare: |F| < 2^-11 quadrants (finite x), or |x| < 1/2 (ph_int192 returns
@@ -590,7 +592,9 @@ __device__ __forceinline__ double sin_d_u10(double x, const double* tab, const d
   red r = reduce_mode<kMode>(x, tab);
   double y = sincos_core_d(r.hi, r.lo, r.q & 1, coef);
   y = odd_sign<kMode>(neg_if(y, r.q & 2), x);
-  y = is_zero_bits(x) ? x : y;
+  // +-0 -> x; kPh: the reduction of |x| = 0 is (0, 0, 0), the core gives +0 and
+  // odd_sign the sign of x: no select needed
+  if constexpr (kMode != kPh) y = is_zero_bits(x) ? x : y;
   if constexpr (kMode == kCw1) return y;  // |x| <= 15: finite
   else return not_finite_bits(x) ? from_bits_d(kCanonNanD) : y;
 }
@@ -1274,7 +1278,7 @@ __device__ __forceinline__ double sin_d_u35(double x, const double* tab, const d
   red r = reduce_mode<kMode>(x, tab);
   double y = sincos_core_d_u35(r.hi, r.q & 1, coef);
   y = odd_sign<kMode>(neg_if(y, r.q & 2), x);
-  y = is_zero_bits(x) ? x : y;
+  if constexpr (kMode != kPh) y = is_zero_bits(x) ? x : y;  // (kPh: as sin_d_u10)
   if constexpr (kMode == kCw1) return y;
   else return not_finite_bits(x) ? from_bits_d(kCanonNanD) : y;
 }
