@@ -472,7 +472,8 @@ __device__ __forceinline__ red ph_int(double x, const double* __restrict__ tab) 
   // the canonical NaN from x itself).  Tests on high words only.
   const uint32_t hab = (uint32_t)(ab >> 32);
   const bool fsmall = ((uint32_t)__double2hiint(fh) & 0x7fffffffu) < 0x42900000u;  // |fh| < 2^42
-  if (hab < 0x3fe00000u || (fsmall && hab < 0x7ff00000u)) return ph_int192(kAbs ? from_bits_d(ab) : x);
+  // (a non-finite x with a small garbage fraction takes the rare path too: harmless)
+  if (hab < 0x3fe00000u || fsmall) return ph_int192(kAbs ? from_bits_d(ab) : x);
   // r = F (pi/2) sign(x) with pi/2 * 2^-53 = C0 + C1 (units of 2^-53 above)
   constexpr double kC0 = kPio2Qd0 * 0x1p-53, kC1 = kPio2Qd1 * 0x1p-53;
   double c0 = kC0, c1 = kC1;
