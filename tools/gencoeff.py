@@ -145,7 +145,7 @@ SPECS = {
                 "log1p(r) = r - r^2/2 + r^3*P(r), |r|<=2^-8 (table-driven log)"),
     "log1p_d_u35": (log1p3_target(), log1p3_weight(), -R_L1P, R_L1P, list(range(5)), 0,
                     "log1p(r) = r - r^2/2 + r^3*P(r), |r|<=2^-8 (u35)"),
-    "expj_d": (exp3_target(), exp3_weight(), -R_EXPJ, R_EXPJ, list(range(4)), 0,
+    "expj_d": (exp3_target(), exp3_weight(), -R_EXPJ, R_EXPJ, list(range(3)), 0,
                "exp(r) = 1 + r + r^2/2 + r^3*P(r), |r|<=ln2/256 (table-driven exp)"),
     "log1p_f": (log1p2_target(), log1p2_weight(), -R_L1P, R_L1P, list(range(3)), 0,
                 "f32 log1p(r) = r + r^2*P(r), |r|<=2^-8"),
