@@ -649,7 +649,8 @@ static double log_fast_d(double a, double Eadj, int u10) {
   dd_t H = eln2_logc(&g);
   dd_t L;
   if (u10) {
-    L = log1p_dd(g.rh, g.rl, C_LOG1P_D, VEM_LOG1P_D_N);
+    /* the 5-term set (2^-64.2): the 6-term one (2^-71.6) is for pow's double-double log */
+    L = log1p_dd(g.rh, g.rl, C_LOG1P_D_U35, VEM_LOG1P_D_U35_N);
   } else {
     double z = g.rh * g.rh;
     double Q = poly(C_LOG1P_D_U35, VEM_LOG1P_D_U35_N, g.rh);

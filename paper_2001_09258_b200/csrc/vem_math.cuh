@@ -752,7 +752,8 @@ __device__ __forceinline__ double log_fast_d(double a, double Eadj, const double
   dd H = eln2_logc(g);
   dd L;
   if (kU10) {
-    L = log1p_dd<VEM_LOG1P_D_N>(g.rh, g.rl, cLog1pD);
+    // the 5-term set (2^-64.2): the 6-term one (2^-71.6) is for pow's double-double log
+    L = log1p_dd<VEM_LOG1P_D_U35_N>(g.rh, g.rl, cLog1pDU35);
   } else {
     double z = g.rh * g.rh;
     double Q = poly<VEM_LOG1P_D_U35_N>(cLog1pDU35, g.rh);
