@@ -1904,8 +1904,8 @@ int vem_exp_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return V
 int vem_exp_f_u35(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpExpFU35, float, 1, kNoTable, 2, 2, 3>(x, nullptr, y, n, s); }
 int vem_log_f_u10(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpLogF, float, 1, kTableLogF, 2, 2>(x, nullptr, y, n, s); }
 int vem_log_f_u35(const float* x, float* y, size_t n, vem_stream_t s) { return VEM_STREAM<OpLogFU35, float, 1, kTableLogF, 2, 2>(x, nullptr, y, n, s); }
-int vem_pow_f_u10(const float* x, const float* y2, float* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpPowF, float, 2, kTableLogF, 2, 2, 3>(x, y2, o, n, s); }
-int vem_pow_f_u35(const float* x, const float* y2, float* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpPowFU35, float, 2, kTableLogF, 2, 2, 3>(x, y2, o, n, s); }
+int vem_pow_f_u10(const float* x, const float* y2, float* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpPowF, float, 2, kTableLogF, 2, 4>(x, y2, o, n, s); }
+int vem_pow_f_u35(const float* x, const float* y2, float* o, size_t n, vem_stream_t s) { return VEM_STREAM<OpPowFU35, float, 2, kTableLogF, 2, 4>(x, y2, o, n, s); }
 int vem_fmod_f(const float* x, const float* y2, float* o, size_t n, vem_stream_t s) {
 #ifdef VEM_TUNE
   return VEM_FMOD<float>(x, y2, o, n, s);
